@@ -1,0 +1,223 @@
+/*
+ * scantherm_b200 — C ABI of the B200 (sm_100a) heat-operator library.
+ *
+ * Drop-in boundary for the hot path of the reference package
+ * `scantherm` (arXiv 2302.05164 re-implementation, Python/numpy).  The
+ * reference has no native FFI; its operator interface is the Python
+ * class ThermalOperator (pkg/src/scantherm/operators.py:84).  Each entry
+ * point below replaces one method of that class or of the time
+ * integrator, and is bound from Python with ctypes
+ * (paper_2302_05164_b200/_lib.py; INTEGRATION.md shows the binding).
+ *
+ * Conventions
+ *  - plain pointers and sizes; float64 fields, int32/int64 indices;
+ *  - every function returns 0 on success and a negative ST_E* code on
+ *    failure; st_last_error() gives the message of the calling thread's
+ *    last failure (reference errors are ValueError / RuntimeError /
+ *    InstabilityError; the Python layer re-raises the same types);
+ *  - host pointers ("const double* T", "double* out") are copied
+ *    host<->device inside the call on the context's stream and the call
+ *    returns after the result is on the host;
+ *  - the context owns its device buffers; one context per mesh epoch
+ *    (the reference rebuilds its operator per mesh update,
+ *    driver.py:162-164); calls on one context are stream-ordered and
+ *    not thread-safe.
+ */
+#ifndef SCANTHERM_B200_H
+#define SCANTHERM_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define ST_OK 0
+#define ST_EINVAL (-1)
+#define ST_ECUDA (-2)
+#define ST_ENOMEM (-3)
+#define ST_EUNSUPPORTED (-4)
+#define ST_ENOCONV (-5)
+
+typedef struct st_ctx st_ctx;
+
+/* Material law (reference params.py:17 MaterialParams) + extension:
+ * latent_heat > 0 turns on the apparent heat capacity
+ * c_app = c + latent_heat / (T_lat_l - T_lat_s) strictly inside
+ * (T_lat_s, T_lat_l). */
+typedef struct st_material {
+  double k_p, k_m, k_s, rho, c, T_s, T_l;
+  double latent_heat, T_lat_s, T_lat_l;
+} st_material;
+
+/* Top-surface losses (reference params.py:37 BoundaryParams; T_max =
+ * T_v + T_max_offset) + extension h_conv (convection). */
+typedef struct st_boundary {
+  double emissivity, sigma_s, T_inf, T_v, C_P, C_T, C_M, h_v, T_h0, T_max;
+  double h_conv;
+} st_boundary;
+
+/* Beam model (reference params.py:63 HeatSourceParams). */
+typedef struct st_laser {
+  double radius, h_powder, cutoff_radii;
+} st_laser;
+
+typedef struct st_params {
+  st_material mat;
+  st_boundary bnd;
+  st_laser las;
+} st_params;
+
+/* One beam at one step (reference physics.py:96 BeamState); a beam
+ * contributes only when active != 0 and power > 0 (operators.py:270).
+ * 40 bytes, matching physics.BEAM_DTYPE. */
+typedef struct st_beam {
+  double x, y, z_top, power;
+  int32_t active;
+  int32_t _pad;
+} st_beam;
+
+/* Tables of an arbitrary (adaptive, hanging-node) Q1 mesh: reference
+ * DofMap (mesh.py:619-638) + per-cell geometry (operators.py:104-112)
+ * + facet quadrature (operators.py:118-134, FaceSet mesh.py:980). */
+typedef struct st_unstructured_mesh {
+  int64_t n_cells, n_vertices;
+  const int32_t* cell_verts;   /* (n_cells, 8), corner ix*4+iy*2+iz   */
+  const double* cell_h;        /* (n_cells,)  edge length (m)          */
+  const double* cell_anchor;   /* (n_cells,3) min corner (m)           */
+  const uint8_t* is_slave;     /* (n_vertices,)                        */
+  const uint8_t* is_dirichlet; /* (n_vertices,)                        */
+  int64_t n_slaves;
+  const int64_t* slaves;       /* (n_slaves,) ascending                */
+  const int64_t* slave_ptr;    /* (n_slaves+1,)                        */
+  const int64_t* slave_masters;
+  const double* slave_weights;
+  int64_t n_faces;             /* +z facets, sorted by cell            */
+  const int64_t* face_cell;    /* (n_faces,) active-cell position      */
+  const double* face_vx;       /* (n_faces,2,2) Vx[f][i][q]            */
+  const double* face_vy;       /* (n_faces,2,2)                        */
+  const double* face_area;     /* (n_faces,) area per facet qp         */
+} st_unstructured_mesh;
+
+/* Uniform box of degree-p cells (p = 1..4), nodes numbered x-major,
+ * z-fastest on the p-refined lattice (reference rule mesh.py:712-715);
+ * GLL nodes, (p+1)^3 Gauss points.  Bottom node plane Dirichlet, top
+ * faces radiating. */
+typedef struct st_structured_mesh {
+  int32_t nx, ny, nz, degree;
+  double h, x0, y0, z0;
+  int32_t dirichlet_bottom, top_faces;
+} st_structured_mesh;
+
+/* evaluate_rhs term flags (operators.py:247 diffusion/faces/source). */
+#define ST_RHS_DIFFUSION 1
+#define ST_RHS_FACES 2
+#define ST_RHS_SOURCE 4
+#define ST_RHS_FROZEN_K 8
+
+/* resident fields */
+#define ST_FIELD_T 0
+#define ST_FIELD_RC 1
+
+int st_version(void);
+const char* st_last_error(void);
+int st_device_count(int* n);
+
+/* ThermalOperator.__init__ (operators.py:91-114) */
+int st_ctx_create_unstructured(int device, const st_unstructured_mesh* mesh,
+                               const st_params* params, st_ctx** out);
+int st_ctx_create_structured(int device, const st_structured_mesh* mesh,
+                             const st_params* params, st_ctx** out);
+int st_ctx_destroy(st_ctx* ctx);
+int64_t st_ctx_n_vertices(const st_ctx* ctx);
+int64_t st_ctx_n_cells(const st_ctx* ctx);
+int st_ctx_qp_per_cell(const st_ctx* ctx);
+/* number of kernels this context has launched so far */
+int64_t st_ctx_launches(const st_ctx* ctx);
+/* the cudaStream_t the context launches on (as an opaque pointer) */
+void* st_ctx_stream(const st_ctx* ctx);
+/* deterministic (fixed-order gather) vs atomic scatter, SolverSettings.deterministic */
+int st_ctx_set_deterministic(st_ctx* ctx, int deterministic);
+
+/* Resident state (T: n_vertices, r_c: n_cells * qp_per_cell). */
+int st_set_field(st_ctx* ctx, int field, const double* host, int64_t n);
+int st_get_field(st_ctx* ctx, int field, double* host, int64_t n);
+/* r_c == value everywhere (e.g. a fully consolidated plate); the
+ * structured backend then stores no history at all. */
+int st_set_uniform_rc(st_ctx* ctx, double value);
+/* raw device pointer of a resident field (for zero-copy interop) */
+double* st_field_device_ptr(st_ctx* ctx, int field);
+
+/* --- per-call operator methods on host arrays (drop-in API) --------- */
+/* evaluate_rhs (operators.py:318): condensed f, Dirichlet rows kept.
+ * rc may be NULL only with ST_RHS_FROZEN_K or without ST_RHS_DIFFUSION. */
+int st_evaluate_rhs(st_ctx* ctx, const double* T, const double* rc, int flags,
+                    double frozen_k, const st_beam* beams, int n_beams,
+                    double* out);
+/* lumped_capacity (operators.py:325); with latent heat the capacity
+ * depends on T (pass T), else T may be NULL. */
+int st_lumped_capacity(st_ctx* ctx, const double* T, double* out);
+/* apply_mass (operators.py:341) */
+int st_apply_mass(st_ctx* ctx, const double* v, double* out);
+/* explicit_fused_step (operators.py:352-369) */
+int st_explicit_step(st_ctx* ctx, const double* T, double dt, const double* rc,
+                     const st_beam* beams, int n_beams, double* out);
+/* update_history (operators.py:219-225), rc updated in place */
+int st_update_history(st_ctx* ctx, const double* T, double* rc);
+/* apply_jacobian (operators.py:380-410) */
+int st_apply_jacobian(st_ctx* ctx, const double* v, const double* T_lin,
+                      const double* rc, double dt, double* out);
+/* jacobian_diagonal (operators.py:426-459) */
+int st_jacobian_diagonal(st_ctx* ctx, const double* T_lin, const double* rc,
+                         double dt, double* out);
+
+/* --- device-resident time integration ------------------------------- */
+/* n_steps forward-Euler steps of run_scan_phase (timestepping.py:211-
+ * 221) on the resident (T, r_c): step, stability check, history update.
+ * dts[n_steps]; beams[n_steps * n_beams].  On divergence (|T| > 1e7 or
+ * non-finite, timestepping.py:186-192) the state is left exactly at the
+ * failing step and *fail_step (1-based within the call) / *t_extreme
+ * are set; otherwise *fail_step = 0.  *t_max receives max(T) over all
+ * accepted steps (PhaseStats.t_max_seen). */
+int st_explicit_steps(st_ctx* ctx, int n_steps, const double* dts,
+                      const st_beam* beams, int n_beams, int* fail_step,
+                      double* t_extreme, double* t_max);
+/* One backward-Euler step of run_cooldown_phase on the resident state
+ * (_implicit_step, timestepping.py:229-283: f_re frozen at T_n, Newton
+ * with Jacobi-PCG).  On success the resident T is the new iterate (not
+ * yet Dirichlet-pinned, like the reference) and *converged = 1. */
+int st_implicit_step(st_ctx* ctx, double dt, double newton_tol,
+                     double newton_abs_tol, int newton_max_iter,
+                     double krylov_tol, int krylov_max_iter, int precond,
+                     int* newton_iters, int* krylov_iters, int* converged);
+/* Dirichlet pin of the resident T + history update (run_cooldown_phase
+ * :357-362). */
+int st_finish_implicit_step(st_ctx* ctx);
+/* krylov_solve (timestepping.py:102-131) for J(T_lin) x = b with the
+ * Jacobi preconditioner (precond = 1) or none (0). */
+int st_pcg(st_ctx* ctx, const double* T_lin, const double* rc, double dt,
+           const double* b, double tol, int max_iter, int precond, double* x,
+           int* iters, int* converged);
+
+/* --- measurement ------------------------------------------------------ */
+/* When enabled, the step loop brackets its dominant kernel with CUDA
+ * events on the context stream; st_profile_read returns the summed
+ * device milliseconds and launch count of that kernel since enabling. */
+int st_profile_enable(st_ctx* ctx, int enable);
+int st_profile_read(st_ctx* ctx, double* main_ms, int64_t* main_launches,
+                    char* main_name, int name_len);
+/* Algorithmic HBM bytes per DoF-update the dominant kernel must move. */
+double st_algorithmic_bytes_per_dof(const st_ctx* ctx);
+/* Benchmark loop: like st_explicit_steps (no divergence replay), but
+ * every step is bracketed by CUDA events on the context stream and,
+ * when flush_bytes > 0, preceded (outside the events) by a write of
+ * flush_bytes to a scratch buffer to evict L2.  step_ms[n_steps]
+ * receives each step's device time; main_ms[n_steps] (nullable) the
+ * dominant kernel's time within the step. */
+int st_bench_explicit(st_ctx* ctx, int n_steps, const double* dts, const st_beam* beams,
+                      int n_beams, int64_t flush_bytes, float* step_ms, float* main_ms);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

@@ -1,0 +1,814 @@
+// C ABI of scantherm_b200 (include/scantherm_b200.h): context lifetime,
+// resident fields, the per-call operator methods of ThermalOperator and
+// the device-resident time-integration loops of timestepping.py.
+#include <cmath>
+#include <algorithm>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "st_common.cuh"
+
+namespace st {
+
+static thread_local std::string g_err;
+void set_error(const std::string& msg) { g_err = msg; }
+
+DevParams make_dev_params(const st_params& p) {
+  DevParams d{};
+  const st_material& m = p.mat;
+  const st_boundary& b = p.bnd;
+  const st_laser& l = p.las;
+  d.k_p = m.k_p;
+  d.k_m = m.k_m;
+  d.k_s = m.k_s;
+  d.T_s = m.T_s;
+  d.T_l = m.T_l;
+  d.dT_l = m.T_l - m.T_s;
+  d.inv_dT_l = 1.0 / (m.T_l - m.T_s);
+  d.dk_slope = (m.k_m - m.k_s) / (m.T_l - m.T_s);
+  d.rhoc = m.rho * m.c;
+  d.latent = m.latent_heat > 0.0 ? 1 : 0;
+  d.lat_bump = d.latent ? m.rho * (m.latent_heat / (m.T_lat_l - m.T_lat_s)) : 0.0;
+  d.T_lat_s = m.T_lat_s;
+  d.T_lat_l = m.T_lat_l;
+  d.eps_sigma = b.emissivity * b.sigma_s;
+  double Ti2 = b.T_inf * b.T_inf;
+  d.Ti4 = Ti2 * Ti2;
+  d.T_inf = b.T_inf;
+  d.T_v = b.T_v;
+  d.T_max = b.T_max;
+  // evaporation can only fire when the clamp admits T > T_v
+  d.evap_on = (b.T_max > b.T_v && b.C_P != 0.0) ? 1 : 0;
+  d.cp082 = 0.82 * b.C_P;
+  d.C_T = b.C_T;
+  d.inv_Tv = 1.0 / b.T_v;
+  d.C_M = b.C_M;
+  d.h_v = b.h_v;
+  d.c_mat = m.c;
+  d.T_h0 = b.T_h0;
+  d.h_conv = b.h_conv;
+  d.radius = l.radius;
+  d.h_powder = l.h_powder;
+  double cut = l.cutoff_radii * l.radius;
+  d.cut2 = cut * cut;
+  d.R2 = l.radius * l.radius;
+  return d;
+}
+
+int Ctx::upload_beams(const st_beam* b, int64_t count) {
+  if (count <= 0) return ST_OK;
+  if ((int64_t)beams.n < count) ST_TRY(beams.alloc(count));
+  std::vector<DevBeam> hb(count);
+  const double R = params.las.radius, hs = params.las.h_powder;
+  const double denom = M_PI * R * R * hs;  // np.pi * R * R * h_powder
+  for (int64_t i = 0; i < count; i++) {
+    hb[i].x = b[i].x;
+    hb[i].y = b[i].y;
+    hb[i].z_top = b[i].z_top;
+    bool on = b[i].active != 0 && b[i].power > 0.0;
+    hb[i].peak = on ? 2.0 * b[i].power / denom : 0.0;
+  }
+  ST_CUDA(cudaMemcpyAsync(beams.p, hb.data(), count * sizeof(DevBeam), cudaMemcpyHostToDevice,
+                          stream));
+  // hb goes out of scope: make sure the copy has consumed it
+  ST_CUDA(cudaStreamSynchronize(stream));
+  return ST_OK;
+}
+
+int Ctx::vec(int i, double** out) {
+  if ((int64_t)scratch[i].n < nv) ST_TRY(scratch[i].alloc(nv));
+  *out = scratch[i].p;
+  return ST_OK;
+}
+
+int Ctx::h2d(double* dst, const double* src, int64_t n) {
+  if (n) ST_CUDA(cudaMemcpyAsync(dst, src, n * sizeof(double), cudaMemcpyHostToDevice, stream));
+  return ST_OK;
+}
+
+int Ctx::d2h(double* dst, const double* src, int64_t n) {
+  if (n) ST_CUDA(cudaMemcpyAsync(dst, src, n * sizeof(double), cudaMemcpyDeviceToHost, stream));
+  ST_CUDA(cudaStreamSynchronize(stream));
+  return ST_OK;
+}
+
+int Ctx::sync() {
+  ST_CUDA(cudaStreamSynchronize(stream));
+  return ST_OK;
+}
+
+void Ctx::prof_begin() {
+  if (bench_ev0) {
+    cudaEventRecord(*bench_ev0, stream);
+    return;
+  }
+  if (prof) cudaEventRecord(ev0, stream);
+}
+void Ctx::prof_end() {
+  if (bench_ev1) {
+    cudaEventRecord(*bench_ev1, stream);
+    return;
+  }
+  if (!prof) return;
+  cudaEventRecord(ev1, stream);
+  cudaEventSynchronize(ev1);
+  float ms = 0.f;
+  cudaEventElapsedTime(&ms, ev0, ev1);
+  prof_ms += ms;
+  prof_launches++;
+}
+
+}  // namespace st
+
+using namespace st;
+
+static int check_ctx(st_ctx* c) {
+  if (!c || !c->impl.be) {
+    set_error("null or uninitialised context");
+    return ST_EINVAL;
+  }
+  cudaError_t e = cudaSetDevice(c->impl.device);
+  if (e != cudaSuccess) {
+    set_error(std::string("cudaSetDevice: ") + cudaGetErrorString(e));
+    return ST_ECUDA;
+  }
+  return ST_OK;
+}
+
+static int ctx_common_init(Ctx* c, int device, const st_params* params) {
+  if (!params) {
+    set_error("params is NULL");
+    return ST_EINVAL;
+  }
+  const st_material& m = params->mat;
+  if (!(m.T_s < m.T_l) || m.rho <= 0 || m.c <= 0) {
+    set_error("invalid material parameters");
+    return ST_EINVAL;
+  }
+  int n = 0;
+  ST_CUDA(cudaGetDeviceCount(&n));
+  if (device < 0 || device >= n) {
+    set_error("device index out of range");
+    return ST_EINVAL;
+  }
+  c->device = device;
+  ST_CUDA(cudaSetDevice(device));
+  ST_CUDA(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
+  c->params = *params;
+  c->dp = make_dev_params(*params);
+  ST_TRY(c->red.alloc(kRedBlocks + 64 + 2 * 1024));
+  ST_CUDA(cudaMallocHost(&c->pinned, 4096 * sizeof(double)));
+  ST_CUDA(cudaEventCreate(&c->ev0));
+  ST_CUDA(cudaEventCreate(&c->ev1));
+  return ST_OK;
+}
+
+static void ctx_free(st_ctx* c) {
+  if (!c) return;
+  Ctx& x = c->impl;
+  cudaSetDevice(x.device);
+  if (x.stream) cudaStreamSynchronize(x.stream);
+  delete x.be;
+  x.be = nullptr;
+  if (x.pinned) cudaFreeHost(x.pinned);
+  if (x.ev0) cudaEventDestroy(x.ev0);
+  if (x.ev1) cudaEventDestroy(x.ev1);
+  x.T.free();
+  x.T_alt.free();
+  x.rc.free();
+  x.rc_snap.free();
+  x.T_snap.free();
+  x.beams.free();
+  x.red.free();
+  for (auto& s : x.scratch) s.free();
+  if (x.stream) cudaStreamDestroy(x.stream);
+  delete c;
+}
+
+extern "C" {
+
+int st_version(void) { return 100; }
+
+const char* st_last_error(void) { return g_err.c_str(); }
+
+int st_device_count(int* n) {
+  ST_CUDA(cudaGetDeviceCount(n));
+  return ST_OK;
+}
+
+int st_ctx_create_unstructured(int device, const st_unstructured_mesh* mesh,
+                               const st_params* params, st_ctx** out) {
+  if (!mesh || !out) {
+    set_error("null argument");
+    return ST_EINVAL;
+  }
+  st_ctx* c = new st_ctx();
+  int rc = ctx_common_init(&c->impl, device, params);
+  if (rc == ST_OK) {
+    int err = ST_OK;
+    c->impl.be = make_unstructured(&c->impl, mesh, &err);
+    rc = err;
+  }
+  if (rc != ST_OK) {
+    std::string keep = g_err;
+    ctx_free(c);
+    g_err = keep;
+    *out = nullptr;
+    return rc;
+  }
+  *out = c;
+  return ST_OK;
+}
+
+int st_ctx_create_structured(int device, const st_structured_mesh* mesh,
+                             const st_params* params, st_ctx** out) {
+  if (!mesh || !out) {
+    set_error("null argument");
+    return ST_EINVAL;
+  }
+  st_ctx* c = new st_ctx();
+  int rc = ctx_common_init(&c->impl, device, params);
+  if (rc == ST_OK) {
+    int err = ST_OK;
+    c->impl.be = make_structured(&c->impl, mesh, &err);
+    rc = err;
+  }
+  if (rc != ST_OK) {
+    std::string keep = g_err;
+    ctx_free(c);
+    g_err = keep;
+    *out = nullptr;
+    return rc;
+  }
+  *out = c;
+  return ST_OK;
+}
+
+int st_ctx_destroy(st_ctx* ctx) {
+  ctx_free(ctx);
+  return ST_OK;
+}
+
+int64_t st_ctx_n_vertices(const st_ctx* c) { return c ? c->impl.nv : -1; }
+int64_t st_ctx_n_cells(const st_ctx* c) { return c ? c->impl.n_cells : -1; }
+int st_ctx_qp_per_cell(const st_ctx* c) { return c ? c->impl.qpc : -1; }
+int64_t st_ctx_launches(const st_ctx* c) { return c ? c->impl.launches : -1; }
+void* st_ctx_stream(const st_ctx* c) { return c ? (void*)c->impl.stream : nullptr; }
+
+int st_ctx_set_deterministic(st_ctx* ctx, int deterministic) {
+  ST_TRY(check_ctx(ctx));
+  ctx->impl.deterministic = deterministic ? 1 : 0;
+  return ST_OK;
+}
+
+}  // extern "C"
+
+// ---------------------------------------------------------------------------
+// helpers on the resident state
+// ---------------------------------------------------------------------------
+static double* rc_ptr(Ctx& c) { return c.rc_uniform ? nullptr : c.rc.p; }
+
+static int flush_history(Ctx& c) {
+  if (c.history_pending) {
+    ST_TRY(c.be->history(c.T.p, rc_ptr(c)));
+    c.history_pending = 0;
+  }
+  return ST_OK;
+}
+
+static int need_state(Ctx& c) {
+  if (!c.have_T) {
+    set_error("resident temperature not set (st_set_field ST_FIELD_T)");
+    return ST_EINVAL;
+  }
+  if (!c.have_rc && !c.rc_uniform) {
+    set_error("resident history not set (st_set_field ST_FIELD_RC or st_set_uniform_rc)");
+    return ST_EINVAL;
+  }
+  return ST_OK;
+}
+
+// per-call staging: host T/rc into scratch buffers that never alias the
+// resident state
+static int stage_rc(Ctx& c, const double* rc_host, double** out) {
+  if (!rc_host) {
+    *out = nullptr;
+    return ST_OK;
+  }
+  int64_t n = c.n_cells * c.qpc;
+  if ((int64_t)c.rc_snap.n < n) ST_TRY(c.rc_snap.alloc(n));
+  ST_TRY(c.h2d(c.rc_snap.p, rc_host, n));
+  *out = c.rc_snap.p;
+  return ST_OK;
+}
+
+// PCG with Jacobi preconditioner on device vectors (timestepping.py:102-131);
+// x0 = 0, stop at ||r|| <= tol ||b||.  Uses scratch vectors 0..4.
+static int pcg_dev(Ctx& c, const double* Tl, const double* rc, double dt, const double* b,
+                   double tol, int max_iter, const double* diag_inv, double* x, int* iters,
+                   int* converged) {
+  const int64_t nv = c.nv;
+  double *r, *z, *p, *Ap;
+  ST_TRY(c.vec(1, &r));
+  ST_TRY(c.vec(2, &z));
+  ST_TRY(c.vec(3, &p));
+  ST_TRY(c.vec(4, &Ap));
+  ST_CUDA(cudaMemsetAsync(x, 0, nv * sizeof(double), c.stream));
+  double bb;
+  ST_TRY(c.dot(b, b, nv, &bb));
+  double bnorm = std::sqrt(bb);
+  *iters = 0;
+  *converged = 1;
+  if (bnorm == 0.0) return ST_OK;
+  ST_CUDA(cudaMemcpyAsync(r, b, nv * sizeof(double), cudaMemcpyDeviceToDevice, c.stream));
+  if (bnorm <= tol * bnorm) return ST_OK;
+  if (diag_inv)
+    ST_TRY(vec_mul(&c, r, diag_inv, z, nv));
+  else
+    ST_CUDA(cudaMemcpyAsync(z, r, nv * sizeof(double), cudaMemcpyDeviceToDevice, c.stream));
+  ST_CUDA(cudaMemcpyAsync(p, z, nv * sizeof(double), cudaMemcpyDeviceToDevice, c.stream));
+  double rz;
+  ST_TRY(c.dot(r, z, nv, &rz));
+  for (int it = 1; it <= max_iter; it++) {
+    ST_TRY(c.be->jacobian(p, Tl, rc, dt, Ap));
+    double pAp;
+    ST_TRY(c.dot(p, Ap, nv, &pAp));
+    double alpha = rz / pAp;
+    ST_TRY(vec_axpy(&c, alpha, p, x, nv));
+    ST_TRY(vec_axpy(&c, -alpha, Ap, r, nv));
+    double rr;
+    ST_TRY(c.dot(r, r, nv, &rr));
+    if (std::sqrt(rr) <= tol * bnorm) {
+      *iters = it;
+      return ST_OK;
+    }
+    if (diag_inv)
+      ST_TRY(vec_mul(&c, r, diag_inv, z, nv));
+    else
+      ST_CUDA(cudaMemcpyAsync(z, r, nv * sizeof(double), cudaMemcpyDeviceToDevice, c.stream));
+    double rz_new;
+    ST_TRY(c.dot(r, z, nv, &rz_new));
+    ST_TRY(vec_xpby(&c, z, rz_new / rz, p, nv));
+    rz = rz_new;
+  }
+  *iters = max_iter;
+  *converged = 0;
+  return ST_OK;
+}
+
+extern "C" {
+
+int st_set_field(st_ctx* ctx, int field, const double* host, int64_t n) {
+  ST_TRY(check_ctx(ctx));
+  Ctx& c = ctx->impl;
+  if (field == ST_FIELD_T) {
+    if (n != c.nv) {
+      set_error("T has the wrong length");
+      return ST_EINVAL;
+    }
+    if ((int64_t)c.T.n < n) ST_TRY(c.T.alloc(n));
+    ST_TRY(c.h2d(c.T.p, host, n));
+    ST_TRY(c.sync());
+    c.have_T = 1;
+    c.history_pending = 0;
+    return ST_OK;
+  }
+  if (field == ST_FIELD_RC) {
+    if (n != c.n_cells * c.qpc) {
+      set_error("r_c has the wrong length");
+      return ST_EINVAL;
+    }
+    if ((int64_t)c.rc.n < n) ST_TRY(c.rc.alloc(n));
+    ST_TRY(c.h2d(c.rc.p, host, n));
+    ST_TRY(c.sync());
+    c.have_rc = 1;
+    c.rc_uniform = 0;
+    c.history_pending = 0;
+    return ST_OK;
+  }
+  set_error("unknown field");
+  return ST_EINVAL;
+}
+
+int st_set_uniform_rc(st_ctx* ctx, double value) {
+  ST_TRY(check_ctx(ctx));
+  Ctx& c = ctx->impl;
+  c.history_pending = 0;
+  if (value >= 1.0) {
+    // max(r_c, g) == r_c for r_c >= 1 >= g: the history never changes
+    c.rc_uniform = 1;
+    c.rc_value = value;
+    c.have_rc = 1;
+    return ST_OK;
+  }
+  int64_t n = c.n_cells * c.qpc;
+  std::vector<double> h(n, value);
+  return st_set_field(ctx, ST_FIELD_RC, h.data(), n);
+}
+
+int st_get_field(st_ctx* ctx, int field, double* host, int64_t n) {
+  ST_TRY(check_ctx(ctx));
+  Ctx& c = ctx->impl;
+  ST_TRY(need_state(c));
+  ST_TRY(flush_history(c));
+  if (field == ST_FIELD_T) {
+    if (n != c.nv) {
+      set_error("T has the wrong length");
+      return ST_EINVAL;
+    }
+    return c.d2h(host, c.T.p, n);
+  }
+  if (field == ST_FIELD_RC) {
+    if (n != c.n_cells * c.qpc) {
+      set_error("r_c has the wrong length");
+      return ST_EINVAL;
+    }
+    if (c.rc_uniform) {
+      for (int64_t i = 0; i < n; i++) host[i] = c.rc_value;
+      return ST_OK;
+    }
+    return c.d2h(host, c.rc.p, n);
+  }
+  set_error("unknown field");
+  return ST_EINVAL;
+}
+
+double* st_field_device_ptr(st_ctx* ctx, int field) {
+  if (!ctx) return nullptr;
+  Ctx& c = ctx->impl;
+  if (flush_history(c) != ST_OK) return nullptr;
+  if (field == ST_FIELD_T) return c.T.p;
+  if (field == ST_FIELD_RC) return c.rc_uniform ? nullptr : c.rc.p;
+  return nullptr;
+}
+
+int st_evaluate_rhs(st_ctx* ctx, const double* T, const double* rc, int flags, double frozen_k,
+                    const st_beam* beams, int n_beams, double* out) {
+  ST_TRY(check_ctx(ctx));
+  Ctx& c = ctx->impl;
+  if ((flags & ST_RHS_DIFFUSION) && !(flags & ST_RHS_FROZEN_K) && !rc) {
+    set_error("evaluate_rhs needs r_c unless the conductivity is frozen");
+    return ST_EINVAL;
+  }
+  double *Td, *fd, *rcd;
+  ST_TRY(c.vec(0, &Td));
+  ST_TRY(c.vec(1, &fd));
+  ST_TRY(c.h2d(Td, T, c.nv));
+  ST_TRY(stage_rc(c, rc, &rcd));
+  int nb = (beams && (flags & ST_RHS_SOURCE)) ? n_beams : 0;
+  ST_TRY(c.upload_beams(beams, nb));
+  ST_TRY(c.be->rhs(Td, rcd, flags, frozen_k, nb, c.beams.p, fd, 0));
+  return c.d2h(out, fd, c.nv);
+}
+
+int st_lumped_capacity(st_ctx* ctx, const double* T, double* out) {
+  ST_TRY(check_ctx(ctx));
+  Ctx& c = ctx->impl;
+  double *Td = nullptr, *od;
+  if (T && c.dp.latent) {
+    ST_TRY(c.vec(0, &Td));
+    ST_TRY(c.h2d(Td, T, c.nv));
+  }
+  ST_TRY(c.vec(1, &od));
+  ST_TRY(c.be->capacity(Td, od));
+  return c.d2h(out, od, c.nv);
+}
+
+int st_apply_mass(st_ctx* ctx, const double* v, double* out) {
+  ST_TRY(check_ctx(ctx));
+  Ctx& c = ctx->impl;
+  double *vd, *od;
+  ST_TRY(c.vec(0, &vd));
+  ST_TRY(c.vec(1, &od));
+  ST_TRY(c.h2d(vd, v, c.nv));
+  ST_TRY(c.be->mass(vd, od));
+  return c.d2h(out, od, c.nv);
+}
+
+int st_explicit_step(st_ctx* ctx, const double* T, double dt, const double* rc,
+                     const st_beam* beams, int n_beams, double* out) {
+  ST_TRY(check_ctx(ctx));
+  Ctx& c = ctx->impl;
+  if (!rc) {
+    set_error("explicit step needs r_c");
+    return ST_EINVAL;
+  }
+  double *Td, *od, *rcd;
+  ST_TRY(c.vec(0, &Td));
+  ST_TRY(c.vec(1, &od));
+  ST_TRY(c.h2d(Td, T, c.nv));
+  ST_TRY(stage_rc(c, rc, &rcd));
+  int nb = beams ? n_beams : 0;
+  ST_TRY(c.upload_beams(beams, nb));
+  ST_CUDA(cudaMemsetAsync(c.red.p + kRedBlocks + 64, 0, 2 * sizeof(double), c.stream));
+  ST_TRY(c.be->explicit_step(Td, rcd, dt, nb, c.beams.p, od, 0, c.red.p + kRedBlocks + 64));
+  return c.d2h(out, od, c.nv);
+}
+
+int st_update_history(st_ctx* ctx, const double* T, double* rc) {
+  ST_TRY(check_ctx(ctx));
+  Ctx& c = ctx->impl;
+  double *Td, *rcd;
+  ST_TRY(c.vec(0, &Td));
+  ST_TRY(c.h2d(Td, T, c.nv));
+  ST_TRY(stage_rc(c, rc, &rcd));
+  ST_TRY(c.be->history(Td, rcd));
+  return c.d2h(rc, rcd, c.n_cells * c.qpc);
+}
+
+int st_apply_jacobian(st_ctx* ctx, const double* v, const double* T_lin, const double* rc,
+                      double dt, double* out) {
+  ST_TRY(check_ctx(ctx));
+  Ctx& c = ctx->impl;
+  double *vd, *Td, *od, *rcd;
+  ST_TRY(c.vec(0, &Td));
+  ST_TRY(c.vec(6, &vd));
+  ST_TRY(c.vec(7, &od));
+  ST_TRY(c.h2d(Td, T_lin, c.nv));
+  ST_TRY(c.h2d(vd, v, c.nv));
+  ST_TRY(stage_rc(c, rc, &rcd));
+  ST_TRY(c.be->jacobian(vd, Td, rcd, dt, od));
+  return c.d2h(out, od, c.nv);
+}
+
+int st_jacobian_diagonal(st_ctx* ctx, const double* T_lin, const double* rc, double dt,
+                         double* out) {
+  ST_TRY(check_ctx(ctx));
+  Ctx& c = ctx->impl;
+  double *Td, *od, *rcd;
+  ST_TRY(c.vec(0, &Td));
+  ST_TRY(c.vec(1, &od));
+  ST_TRY(c.h2d(Td, T_lin, c.nv));
+  ST_TRY(stage_rc(c, rc, &rcd));
+  ST_TRY(c.be->jac_diag(Td, rcd, dt, od));
+  return c.d2h(out, od, c.nv);
+}
+
+int st_pcg(st_ctx* ctx, const double* T_lin, const double* rc, double dt, const double* b,
+           double tol, int max_iter, int precond, double* x, int* iters, int* converged) {
+  ST_TRY(check_ctx(ctx));
+  Ctx& c = ctx->impl;
+  double *Td, *bd, *xd, *di = nullptr, *rcd;
+  ST_TRY(c.vec(0, &Td));
+  ST_TRY(c.vec(5, &bd));
+  ST_TRY(c.vec(6, &xd));
+  ST_TRY(c.h2d(Td, T_lin, c.nv));
+  ST_TRY(c.h2d(bd, b, c.nv));
+  ST_TRY(stage_rc(c, rc, &rcd));
+  if (precond) {
+    ST_TRY(c.vec(7, &di));
+    ST_TRY(c.be->jac_diag(Td, rcd, dt, di));
+    ST_TRY(vec_recip(&c, di, di, c.nv));
+  }
+  ST_TRY(pcg_dev(c, Td, rcd, dt, bd, tol, max_iter, di, xd, iters, converged));
+  return c.d2h(x, xd, c.nv);
+}
+
+// ---------------------------------------------------------------------------
+// device-resident explicit loop (run_scan_phase, timestepping.py:195-226)
+// ---------------------------------------------------------------------------
+static const double kDiverged = 1.0e7;  // timestepping.py:183
+
+int st_explicit_steps(st_ctx* ctx, int n_steps, const double* dts, const st_beam* beams,
+                      int n_beams, int* fail_step, double* t_extreme, double* t_max) {
+  ST_TRY(check_ctx(ctx));
+  Ctx& c = ctx->impl;
+  ST_TRY(need_state(c));
+  if (fail_step) *fail_step = 0;
+  if (n_steps <= 0) return ST_OK;
+  const int nb = beams ? n_beams : 0;
+  ST_TRY(c.upload_beams(beams, (int64_t)n_steps * nb));
+  if ((int64_t)c.T_alt.n < c.nv) ST_TRY(c.T_alt.alloc(c.nv));
+  const int64_t nrc = c.rc_uniform ? 0 : c.n_cells * c.qpc;
+  const int kBatch = 512;
+  double tmax_all = -INFINITY;
+  unsigned long long* slots = reinterpret_cast<unsigned long long*>(c.red.p + kRedBlocks + 64);
+  std::vector<unsigned long long> hs(2 * kBatch);
+  for (int b0 = 0; b0 < n_steps; b0 += kBatch) {
+    const int nbatch = std::min(kBatch, n_steps - b0);
+    // snapshot so that a divergence leaves the state at the failing step
+    if ((int64_t)c.T_snap.n < c.nv) ST_TRY(c.T_snap.alloc(c.nv));
+    ST_CUDA(cudaMemcpyAsync(c.T_snap.p, c.T.p, c.nv * sizeof(double), cudaMemcpyDeviceToDevice,
+                            c.stream));
+    if (nrc) {
+      if ((int64_t)c.rc_snap.n < nrc) ST_TRY(c.rc_snap.alloc(nrc));
+      ST_CUDA(cudaMemcpyAsync(c.rc_snap.p, c.rc.p, nrc * sizeof(double),
+                              cudaMemcpyDeviceToDevice, c.stream));
+    }
+    const int pending0 = c.history_pending;
+    ST_CUDA(cudaMemsetAsync(slots, 0, 2 * nbatch * sizeof(unsigned long long), c.stream));
+    for (int i = 0; i < nbatch; i++) {
+      const int s = b0 + i;
+      ST_TRY(c.be->explicit_step(c.T.p, rc_ptr(c), dts[s], nb, c.beams.p + (int64_t)s * nb,
+                                 c.T_alt.p, c.history_pending,
+                                 reinterpret_cast<double*>(slots + 2 * i)));
+      std::swap(c.T.p, c.T_alt.p);
+      std::swap(c.T.n, c.T_alt.n);
+      c.history_pending = 1;
+    }
+    ST_CUDA(cudaMemcpyAsync(hs.data(), slots, 2 * nbatch * sizeof(unsigned long long),
+                            cudaMemcpyDeviceToHost, c.stream));
+    ST_CUDA(cudaStreamSynchronize(c.stream));
+    for (int i = 0; i < nbatch; i++) {
+      double am;
+      std::memcpy(&am, &hs[2 * i], 8);
+      double sm = key_to_double(hs[2 * i + 1]);
+      if (!std::isfinite(am) || am > kDiverged) {
+        // replay the batch up to the failing step; its history update is
+        // never applied (the reference raises before update_history)
+        ST_CUDA(cudaMemcpyAsync(c.T.p, c.T_snap.p, c.nv * sizeof(double),
+                                cudaMemcpyDeviceToDevice, c.stream));
+        if (nrc)
+          ST_CUDA(cudaMemcpyAsync(c.rc.p, c.rc_snap.p, nrc * sizeof(double),
+                                  cudaMemcpyDeviceToDevice, c.stream));
+        c.history_pending = pending0;
+        for (int j = 0; j <= i; j++) {
+          const int s = b0 + j;
+          ST_TRY(c.be->explicit_step(c.T.p, rc_ptr(c), dts[s], nb, c.beams.p + (int64_t)s * nb,
+                                     c.T_alt.p, c.history_pending,
+                                     reinterpret_cast<double*>(slots)));
+          std::swap(c.T.p, c.T_alt.p);
+          std::swap(c.T.n, c.T_alt.n);
+          c.history_pending = 1;
+        }
+        c.history_pending = 0;
+        ST_TRY(c.sync());
+        if (fail_step) *fail_step = b0 + i + 1;
+        if (t_extreme) *t_extreme = am;
+        if (t_max) *t_max = tmax_all;
+        return ST_OK;
+      }
+      tmax_all = std::max(tmax_all, sm);
+    }
+  }
+  if (t_max) *t_max = tmax_all;
+  return ST_OK;
+}
+
+// ---------------------------------------------------------------------------
+// backward Euler (timestepping.py:229-283, 355-362)
+// ---------------------------------------------------------------------------
+int st_implicit_step(st_ctx* ctx, double dt, double newton_tol, double newton_abs_tol,
+                     int newton_max_iter, double krylov_tol, int krylov_max_iter, int precond,
+                     int* newton_iters, int* krylov_iters, int* converged) {
+  ST_TRY(check_ctx(ctx));
+  Ctx& c = ctx->impl;
+  ST_TRY(need_state(c));
+  ST_TRY(flush_history(c));
+  const int64_t nv = c.nv;
+  static_assert(sizeof(DevBuf<double>) > 0, "");
+  // vectors: 8..: allocate extra scratch on demand beyond the 8 slots
+  DevBuf<double> Tn, Ti, fre, f, r, tmp, di, delta;
+  ST_TRY(Tn.alloc(nv));
+  ST_TRY(Ti.alloc(nv));
+  ST_TRY(fre.alloc(nv));
+  ST_TRY(f.alloc(nv));
+  ST_TRY(r.alloc(nv));
+  ST_TRY(tmp.alloc(nv));
+  ST_TRY(di.alloc(nv));
+  ST_TRY(delta.alloc(nv));
+  double* rc = rc_ptr(c);
+  ST_CUDA(cudaMemcpyAsync(Tn.p, c.T.p, nv * sizeof(double), cudaMemcpyDeviceToDevice, c.stream));
+  ST_CUDA(cudaMemcpyAsync(Ti.p, c.T.p, nv * sizeof(double), cudaMemcpyDeviceToDevice, c.stream));
+  // boundary flux frozen at the step start
+  ST_TRY(c.be->rhs(Tn.p, rc, ST_RHS_FACES, 0.0, 0, nullptr, fre.p, 0));
+  double norm0 = -1.0;
+  int nn = 0, nk = 0;
+  *converged = 0;
+  for (int k = 0; k < newton_max_iter; k++) {
+    ST_TRY(c.be->rhs(Ti.p, rc, ST_RHS_DIFFUSION, 0.0, 0, nullptr, f.p, 0));
+    ST_TRY(vec_sub(&c, Ti.p, Tn.p, tmp.p, nv));
+    double* Md;
+    ST_TRY(c.vec(0, &Md));
+    ST_TRY(c.be->mass(tmp.p, Md));
+    ST_TRY(vec_sub_scale(&c, Md, f.p, dt, fre.p, r.p, nv));
+    ST_TRY(c.be->mask_rows(r.p));
+    double rr;
+    ST_TRY(c.dot(r.p, r.p, nv, &rr));
+    double norm = std::sqrt(rr);
+    if (norm0 < 0) norm0 = norm;
+    if (norm <= newton_abs_tol || norm <= newton_tol * norm0) {
+      ST_CUDA(cudaMemcpyAsync(c.T.p, Ti.p, nv * sizeof(double), cudaMemcpyDeviceToDevice,
+                              c.stream));
+      ST_TRY(c.sync());
+      *newton_iters = nn;
+      *krylov_iters = nk;
+      *converged = 1;
+      return ST_OK;
+    }
+    double* dip = nullptr;
+    if (precond) {
+      ST_TRY(c.be->jac_diag(Ti.p, rc, dt, di.p));
+      ST_TRY(vec_recip(&c, di.p, di.p, nv));
+      dip = di.p;
+    }
+    ST_TRY(vec_scal_copy(&c, -1.0, r.p, r.p, nv));
+    int it = 0, ok = 0;
+    ST_TRY(pcg_dev(c, Ti.p, rc, dt, r.p, krylov_tol, krylov_max_iter, dip, delta.p, &it, &ok));
+    nk += it;
+    if (!ok) break;
+    ST_TRY(vec_axpy(&c, 1.0, delta.p, Ti.p, nv));
+    ST_TRY(c.be->distribute(Ti.p));
+    nn++;
+  }
+  ST_TRY(c.sync());
+  *newton_iters = nn;
+  *krylov_iters = nk;
+  *converged = 0;
+  return ST_OK;
+}
+
+int st_finish_implicit_step(st_ctx* ctx) {
+  ST_TRY(check_ctx(ctx));
+  Ctx& c = ctx->impl;
+  ST_TRY(c.be->pin_dirichlet(c.T.p, c.dp.T_inf));
+  ST_TRY(c.be->history(c.T.p, rc_ptr(c)));
+  c.history_pending = 0;
+  return c.sync();
+}
+
+// ---------------------------------------------------------------------------
+// measurement
+// ---------------------------------------------------------------------------
+int st_profile_enable(st_ctx* ctx, int enable) {
+  ST_TRY(check_ctx(ctx));
+  Ctx& c = ctx->impl;
+  c.prof = enable ? 1 : 0;
+  c.prof_ms = 0.0;
+  c.prof_launches = 0;
+  return ST_OK;
+}
+
+int st_profile_read(st_ctx* ctx, double* main_ms, int64_t* main_launches, char* main_name,
+                    int name_len) {
+  ST_TRY(check_ctx(ctx));
+  Ctx& c = ctx->impl;
+  ST_TRY(c.sync());
+  if (main_ms) *main_ms = c.prof_ms;
+  if (main_launches) *main_launches = c.prof_launches;
+  if (main_name && name_len > 0) {
+    std::strncpy(main_name, c.be->main_kernel(), name_len - 1);
+    main_name[name_len - 1] = 0;
+  }
+  return ST_OK;
+}
+
+double st_algorithmic_bytes_per_dof(const st_ctx* ctx) {
+  if (!ctx || !ctx->impl.be) return 0.0;
+  return ctx->impl.be->bytes_per_dof();
+}
+
+int st_bench_explicit(st_ctx* ctx, int n_steps, const double* dts, const st_beam* beams,
+                      int n_beams, int64_t flush_bytes, float* step_ms, float* main_ms) {
+  ST_TRY(check_ctx(ctx));
+  Ctx& c = ctx->impl;
+  ST_TRY(need_state(c));
+  if (n_steps <= 0) return ST_OK;
+  const int nb = beams ? n_beams : 0;
+  ST_TRY(c.upload_beams(beams, (int64_t)n_steps * nb));
+  if ((int64_t)c.T_alt.n < c.nv) ST_TRY(c.T_alt.alloc(c.nv));
+  DevBuf<char> flush;
+  if (flush_bytes > 0) ST_TRY(flush.alloc(flush_bytes));
+  std::vector<cudaEvent_t> ev(4 * (size_t)n_steps);
+  for (auto& e : ev) ST_CUDA(cudaEventCreate(&e));
+  unsigned long long* slots = reinterpret_cast<unsigned long long*>(c.red.p + kRedBlocks + 64);
+  int rc = ST_OK;
+  for (int s = 0; s < n_steps && rc == ST_OK; s++) {
+    if (flush_bytes > 0) {
+      // alternate the fill byte so the writes cannot be elided
+      if (cudaMemsetAsync(flush.p, s & 0xff, flush_bytes, c.stream) != cudaSuccess) {
+        set_error("flush memset failed");
+        rc = ST_ECUDA;
+        break;
+      }
+    }
+    cudaMemsetAsync(slots, 0, 2 * sizeof(unsigned long long), c.stream);
+    cudaEventRecord(ev[4 * s], c.stream);
+    c.bench_ev0 = &ev[4 * s + 1];
+    c.bench_ev1 = &ev[4 * s + 2];
+    rc = c.be->explicit_step(c.T.p, rc_ptr(c), dts[s], nb, c.beams.p + (int64_t)s * nb,
+                             c.T_alt.p, c.history_pending, reinterpret_cast<double*>(slots));
+    c.bench_ev0 = c.bench_ev1 = nullptr;
+    cudaEventRecord(ev[4 * s + 3], c.stream);
+    std::swap(c.T.p, c.T_alt.p);
+    std::swap(c.T.n, c.T_alt.n);
+    c.history_pending = 1;
+  }
+  if (rc == ST_OK) {
+    ST_CUDA(cudaStreamSynchronize(c.stream));
+    for (int s = 0; s < n_steps; s++) {
+      float ms = 0.f;
+      ST_CUDA(cudaEventElapsedTime(&ms, ev[4 * s], ev[4 * s + 3]));
+      step_ms[s] = ms;
+      if (main_ms) {
+        ST_CUDA(cudaEventElapsedTime(&ms, ev[4 * s + 1], ev[4 * s + 2]));
+        main_ms[s] = ms;
+      }
+    }
+  }
+  for (auto& e : ev) cudaEventDestroy(e);
+  return rc;
+}
+
+}  // extern "C"

@@ -1,0 +1,116 @@
+// Pointwise physics on the device.  Each function restates one
+// reference law with the same operation order (material.py, physics.py);
+// fp64 throughout.
+#pragma once
+
+#include "st_internal.h"
+
+namespace st {
+
+// g(T) (material.py:46-57): 0 below T_s, 1 above T_l, ramp between.
+__device__ __forceinline__ double liquid_fraction(const DevParams& P, double T) {
+  double ramp = (T - P.T_s) / P.dT_l;
+  return T < P.T_s ? 0.0 : (T > P.T_l ? 1.0 : ramp);
+}
+
+// Same law with the ramp as a multiply by 1/(T_l - T_s) (hot kernels).
+__device__ __forceinline__ double liquid_fraction_fast(const DevParams& P, double T) {
+  double ramp = (T - P.T_s) * P.inv_dT_l;
+  return T < P.T_s ? 0.0 : (T > P.T_l ? 1.0 : ramp);
+}
+
+// k = (r_p k_p + r_m k_m) + r_s k_s, r_s clamped at 0 (material.py:68-85).
+__device__ __forceinline__ double conductivity(const DevParams& P, double g, double rc) {
+  double r_p = 1.0 - rc;
+  double r_s = rc - g;
+  r_s = r_s < 0.0 ? 0.0 : r_s;
+  return (r_p * P.k_p + g * P.k_m) + r_s * P.k_s;
+}
+
+// dk/dT at frozen r_c (material.py:88-94).
+__device__ __forceinline__ double conductivity_derivative(const DevParams& P, double T) {
+  return (T > P.T_s && T < P.T_l) ? P.dk_slope : 0.0;
+}
+
+// rho * c_app(T): rho c (+ rho L/(T_lat_l-T_lat_s) strictly inside the
+// latent interval when the extension is on).
+__device__ __forceinline__ double heat_capacity(const DevParams& P, double T) {
+  double v = P.rhoc;
+  if (P.latent && T > P.T_lat_s && T < P.T_lat_l) v = P.rhoc + P.lat_bump;
+  return v;
+}
+
+// Outward surface flux: radiation (physics.py:174-183) + evaporation
+// (physics.py:186-202) + convection (extension).
+__device__ __forceinline__ double surface_flux(const DevParams& P, double T) {
+  double T2 = T * T;
+  double q = P.eps_sigma * (T2 * T2 - P.Ti4);
+  if (P.evap_on) {
+    double Tc = T < P.T_max ? T : P.T_max;
+    Tc = Tc < 1.0 ? 1.0 : Tc;
+    if (Tc > P.T_v) {
+      double mdot = P.cp082 * exp(-P.C_T * (1.0 / Tc - P.inv_Tv)) * sqrt(P.C_M / Tc);
+      q = q + mdot * (P.h_v + P.c_mat * (Tc - P.T_h0));
+    }
+  }
+  if (P.h_conv != 0.0) q = q + P.h_conv * (T - P.T_inf);
+  return q;
+}
+
+// Gaussian slab source at one point (physics.py:154-171).
+__device__ __forceinline__ double beam_source(const DevParams& P, const DevBeam& b,
+                                              double x, double y, double z) {
+  double dx = x - b.x;
+  double dy = y - b.y;
+  double r2 = dx * dx + dy * dy;
+  bool in_slab = (z >= b.z_top - P.h_powder) && (z <= b.z_top);
+  double q = b.peak * exp((-2.0 * r2) / P.R2);
+  return in_slab ? q : 0.0;
+}
+
+// Cell-level hit test of the reference (operators.py:295-307): xy box
+// distance to the beam axis within cutoff, and overlap with the slab.
+__device__ __forceinline__ bool beam_hits_cell(const DevParams& P, const DevBeam& b,
+                                               double ax, double ay, double az,
+                                               double h) {
+  if (b.peak == 0.0) return false;
+  double dx = fmax(fmax(ax - b.x, b.x - ax - h), 0.0);
+  double dy = fmax(fmax(ay - b.y, b.y - ay - h), 0.0);
+  double zlo = b.z_top - P.h_powder, zhi = b.z_top;
+  return (dx * dx + dy * dy <= P.cut2) && (az <= zhi) && (az + h >= zlo);
+}
+
+// order-preserving bit key of a double (for atomicMax of signed values)
+__device__ __forceinline__ unsigned long long order_key(double x) {
+  unsigned long long b = __double_as_longlong(x);
+  return (b & 0x8000000000000000ULL) ? ~b : (b | 0x8000000000000000ULL);
+}
+__host__ __device__ inline double key_to_double(unsigned long long k) {
+  unsigned long long b = (k & 0x8000000000000000ULL) ? (k & 0x7FFFFFFFFFFFFFFFULL) : ~k;
+#ifdef __CUDA_ARCH__
+  return __longlong_as_double((long long)b);
+#else
+  double d;
+  memcpy(&d, &b, 8);
+  return d;
+#endif
+}
+
+// block-wide max of (|x|, x) into two global order keys
+__device__ __forceinline__ void block_max2(double absval, double val,
+                                          unsigned long long* slot) {
+  unsigned long long ka = __double_as_longlong(fabs(absval));  // >= 0: bits monotone
+  unsigned long long ks = order_key(val);
+  for (int o = 16; o > 0; o >>= 1) {
+    unsigned long long a2 = __shfl_xor_sync(0xffffffffu, ka, o);
+    unsigned long long s2 = __shfl_xor_sync(0xffffffffu, ks, o);
+    ka = a2 > ka ? a2 : ka;
+    ks = s2 > ks ? s2 : ks;
+  }
+  if ((threadIdx.x & 31) == 0) {
+    atomicMax(slot, ka);
+    atomicMax(slot + 1, ks);
+  }
+}
+
+}  // namespace st

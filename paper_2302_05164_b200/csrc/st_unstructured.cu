@@ -1,0 +1,934 @@
+// Q1 operator on arbitrary (adaptive, hanging-node) meshes.
+//
+// Restates reference operators.py for general DofMap tables:
+//   cell kernels  : one thread per active cell, 2x2x2 sum factorisation
+//                   in registers (operators.py:44-55, 247-316, 341-424)
+//   node kernels  : one thread per vertex; deterministic gather of the
+//                   per-cell element vectors through a vertex incidence
+//                   CSR in canonical cell order (= np.bincount order,
+//                   operators.py:229-237), hanging-node condensation in
+//                   np.add.at order (mesh.py:663-670), then the fused
+//                   forward-Euler update + Dirichlet pin (operators.py:
+//                   352-369); slaves are re-interpolated afterwards
+//                   (mesh.py:652-661).
+// An atomic-scatter variant (SolverSettings.deterministic = False, the
+// analogue of the reference's colored scatter) skips the element buffer.
+#include <algorithm>
+#include <cmath>
+#include <map>
+#include <vector>
+
+#include "st_common.cuh"
+
+namespace st {
+
+__constant__ double cV[2][2];   // V1[i][q] (operators.py:33-34)
+__constant__ double cD[2][2];   // D1
+__constant__ double cU[2];      // (GAUSS_1D + 1) / 2
+__constant__ double cPhi[8][8];      // PHI_REF[c][q]
+__constant__ double cG[3][8][8];     // GRAD_REF[d][c][q]
+__constant__ double cPhi2[8];        // sum_q PHI^2
+__constant__ double cGG[8][8];       // sum_d GRAD[d][c][q]^2
+
+template <int D>
+__device__ __forceinline__ double M1(int i, int q) {
+  return D ? cD[i][q] : cV[i][q];
+}
+
+// out[a,b,c] = sum_ijk A[i][a] B[j][b] C[k][c] in[i,j,k]; flat index x*4+y*2+z
+template <int DX, int DY, int DZ>
+__device__ __forceinline__ void interp(const double* t, double* o) {
+  double s[8], r[8];
+#pragma unroll
+  for (int a = 0; a < 2; a++)
+#pragma unroll
+    for (int jk = 0; jk < 4; jk++)
+      s[a * 4 + jk] = fma(M1<DX>(1, a), t[4 + jk], M1<DX>(0, a) * t[jk]);
+#pragma unroll
+  for (int a = 0; a < 2; a++)
+#pragma unroll
+    for (int b = 0; b < 2; b++)
+#pragma unroll
+      for (int k = 0; k < 2; k++)
+        r[a * 4 + b * 2 + k] = fma(M1<DY>(1, b), s[a * 4 + 2 + k], M1<DY>(0, b) * s[a * 4 + k]);
+#pragma unroll
+  for (int ab = 0; ab < 4; ab++)
+#pragma unroll
+    for (int c = 0; c < 2; c++)
+      o[ab * 2 + c] = fma(M1<DZ>(1, c), r[ab * 2 + 1], M1<DZ>(0, c) * r[ab * 2]);
+}
+
+// transpose: out[i,j,k] = sum_abc A[i][a] B[j][b] C[k][c] in[a,b,c]
+template <int DX, int DY, int DZ>
+__device__ __forceinline__ void project(const double* t, double* o) {
+  double s[8], r[8];
+#pragma unroll
+  for (int i = 0; i < 2; i++)
+#pragma unroll
+    for (int bc = 0; bc < 4; bc++)
+      s[i * 4 + bc] = fma(M1<DX>(i, 1), t[4 + bc], M1<DX>(i, 0) * t[bc]);
+#pragma unroll
+  for (int i = 0; i < 2; i++)
+#pragma unroll
+    for (int j = 0; j < 2; j++)
+#pragma unroll
+      for (int c = 0; c < 2; c++)
+        r[i * 4 + j * 2 + c] = fma(M1<DY>(j, 1), s[i * 4 + 2 + c], M1<DY>(j, 0) * s[i * 4 + c]);
+#pragma unroll
+  for (int ij = 0; ij < 4; ij++)
+#pragma unroll
+    for (int k = 0; k < 2; k++)
+      o[ij * 2 + k] = fma(M1<DZ>(k, 1), r[ij * 2 + 1], M1<DZ>(k, 0) * r[ij * 2]);
+}
+
+struct CellGeo {
+  const int* cv;
+  const double* h;
+  const double* anc;
+  const double* detw;
+};
+
+struct FaceTab {
+  const int* ptr;  // per cell CSR (n+1)
+  const double* vx;
+  const double* vy;
+  const double* area;
+};
+
+__device__ __forceinline__ void gather8(const int* cv, int64_t c, const double* X, double* t) {
+#pragma unroll
+  for (int i = 0; i < 8; i++) t[i] = X[cv[c * 8 + i]];
+}
+
+// ---------------------------------------------------------------------------
+// rhs element vectors: -diffusion + faces + sources   (operators.py:247-316)
+// ---------------------------------------------------------------------------
+__global__ void k_rhs_cells(int64_t n, CellGeo g, FaceTab ft, DevParams P,
+                            const double* __restrict__ T, double* rc,
+                            double rc_value, int flags, double frozen_k,
+                            int pending, int nb, const DevBeam* beams,
+                            double* E, double* Ec, double* f_atomic,
+                            double* c_atomic) {
+  int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (c >= n) return;
+  double t[8], e[8];
+  gather8(g.cv, c, T, t);
+#pragma unroll
+  for (int i = 0; i < 8; i++) e[i] = 0.0;
+  const double h = g.h[c];
+  double tq[8];
+  bool need_tq = ((flags & ST_RHS_DIFFUSION) && !(flags & ST_RHS_FROZEN_K)) || Ec || c_atomic;
+  if (need_tq) interp<0, 0, 0>(t, tq);
+  if (flags & ST_RHS_DIFFUSION) {
+    double k[8];
+    if (flags & ST_RHS_FROZEN_K) {
+#pragma unroll
+      for (int q = 0; q < 8; q++) k[q] = frozen_k;
+    } else {
+#pragma unroll
+      for (int q = 0; q < 8; q++) {
+        double r = rc ? rc[c * 8 + q] : rc_value;
+        double gq = liquid_fraction(P, tq[q]);
+        if (pending && rc) {
+          r = fmax(r, gq);
+          rc[c * 8 + q] = r;
+        }
+        k[q] = conductivity(P, gq, r);
+      }
+    }
+    const double hh = h / 2.0;
+    double gd[8], pr[8];
+    interp<1, 0, 0>(t, gd);
+#pragma unroll
+    for (int q = 0; q < 8; q++) gd[q] = (hh * k[q]) * gd[q];
+    project<1, 0, 0>(gd, pr);
+#pragma unroll
+    for (int i = 0; i < 8; i++) e[i] -= pr[i];
+    interp<0, 1, 0>(t, gd);
+#pragma unroll
+    for (int q = 0; q < 8; q++) gd[q] = (hh * k[q]) * gd[q];
+    project<0, 1, 0>(gd, pr);
+#pragma unroll
+    for (int i = 0; i < 8; i++) e[i] -= pr[i];
+    interp<0, 0, 1>(t, gd);
+#pragma unroll
+    for (int q = 0; q < 8; q++) gd[q] = (hh * k[q]) * gd[q];
+    project<0, 0, 1>(gd, pr);
+#pragma unroll
+    for (int i = 0; i < 8; i++) e[i] -= pr[i];
+  }
+  if ((flags & ST_RHS_FACES) && ft.ptr) {
+    for (int fi = ft.ptr[c]; fi < ft.ptr[c + 1]; fi++) {
+      const double* vx = ft.vx + fi * 4;  // [i][q]
+      const double* vy = ft.vy + fi * 4;
+      double tf[2][2], s[2][2], q[2][2];
+#pragma unroll
+      for (int i = 0; i < 2; i++)
+#pragma unroll
+        for (int j = 0; j < 2; j++) tf[i][j] = t[i * 4 + j * 2 + 1];
+#pragma unroll
+      for (int a = 0; a < 2; a++)
+#pragma unroll
+        for (int j = 0; j < 2; j++) s[a][j] = fma(vx[2 + a], tf[1][j], vx[a] * tf[0][j]);
+      const double ar = -ft.area[fi];
+#pragma unroll
+      for (int a = 0; a < 2; a++)
+#pragma unroll
+        for (int b = 0; b < 2; b++) {
+          double tqf = fma(vy[2 + b], s[a][1], vy[b] * s[a][0]);
+          q[a][b] = surface_flux(P, tqf) * ar;
+        }
+#pragma unroll
+      for (int i = 0; i < 2; i++)
+#pragma unroll
+        for (int b = 0; b < 2; b++) s[i][b] = fma(vx[i * 2 + 1], q[1][b], vx[i * 2] * q[0][b]);
+#pragma unroll
+      for (int i = 0; i < 2; i++)
+#pragma unroll
+        for (int j = 0; j < 2; j++) e[i * 4 + j * 2 + 1] += fma(vy[j * 2 + 1], s[i][1], vy[j * 2] * s[i][0]);
+    }
+  }
+  if ((flags & ST_RHS_SOURCE) && nb > 0) {
+    const double ax = g.anc[c * 3], ay = g.anc[c * 3 + 1], az = g.anc[c * 3 + 2];
+    for (int b = 0; b < nb; b++) {
+      DevBeam bm = beams[b];
+      if (!beam_hits_cell(P, bm, ax, ay, az, h)) continue;
+      double qv[8], pr[8];
+      const double dw = g.detw[c];
+#pragma unroll
+      for (int a = 0; a < 2; a++)
+#pragma unroll
+        for (int bb = 0; bb < 2; bb++)
+#pragma unroll
+          for (int cc = 0; cc < 2; cc++)
+            qv[a * 4 + bb * 2 + cc] =
+                beam_source(P, bm, ax + cU[a] * h, ay + cU[bb] * h, az + cU[cc] * h) * dw;
+      project<0, 0, 0>(qv, pr);
+#pragma unroll
+      for (int i = 0; i < 8; i++) e[i] += pr[i];
+    }
+  }
+  double ec[8];
+  if (Ec || c_atomic) {
+    const double dw = g.detw[c];
+#pragma unroll
+    for (int q = 0; q < 8; q++) tq[q] = heat_capacity(P, tq[q]) * dw;
+    project<0, 0, 0>(tq, ec);
+  }
+  if (E) {
+#pragma unroll
+    for (int i = 0; i < 8; i++) E[c * 8 + i] = e[i];
+    if (Ec)
+#pragma unroll
+      for (int i = 0; i < 8; i++) Ec[c * 8 + i] = ec[i];
+  } else {
+#pragma unroll
+    for (int i = 0; i < 8; i++) atomicAdd(f_atomic + g.cv[c * 8 + i], e[i]);
+    if (c_atomic)
+#pragma unroll
+      for (int i = 0; i < 8; i++) atomicAdd(c_atomic + g.cv[c * 8 + i], ec[i]);
+  }
+}
+
+// consistent capacity apply / lumped capacity (operators.py:325-348):
+// v == nullptr => ones; T != nullptr => rho c_app(T_q)
+__global__ void k_mass_cells(int64_t n, CellGeo g, DevParams P, const double* v,
+                             const double* T, double scale, double* E) {
+  int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (c >= n) return;
+  double t[8], q[8], o[8];
+  if (v) {
+    gather8(g.cv, c, v, t);
+    interp<0, 0, 0>(t, q);
+  } else {
+#pragma unroll
+    for (int i = 0; i < 8; i++) t[i] = 1.0;
+    interp<0, 0, 0>(t, q);
+  }
+  const double dw = g.detw[c];
+  if (T) {
+    double tt[8], tq[8];
+    gather8(g.cv, c, T, tt);
+    interp<0, 0, 0>(tt, tq);
+#pragma unroll
+    for (int i = 0; i < 8; i++) q[i] = q[i] * (heat_capacity(P, tq[i]) * dw);
+  } else {
+#pragma unroll
+    for (int i = 0; i < 8; i++) q[i] = q[i] * (P.rhoc * dw);
+  }
+  project<0, 0, 0>(q, o);
+#pragma unroll
+  for (int i = 0; i < 8; i++) E[c * 8 + i] = o[i] * scale;
+}
+
+// r_c <- max(r_c, g(T_q))  (operators.py:219-225)
+__global__ void k_history(int64_t n, const int* cv, DevParams P, const double* T, double* rc) {
+  int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (c >= n) return;
+  double t[8], tq[8];
+  gather8(cv, c, T, t);
+  interp<0, 0, 0>(t, tq);
+#pragma unroll
+  for (int q = 0; q < 8; q++) rc[c * 8 + q] = fmax(rc[c * 8 + q], liquid_fraction(P, tq[q]));
+}
+
+// tangent fields at qps (operators.py:373-378)
+__device__ __forceinline__ void tangent(const DevParams& P, const double* tl, const double* rc,
+                                        double rc_value, int64_t c, double gscale, double* k,
+                                        double* dk, double* gx, double* gy, double* gz) {
+  double tq[8];
+  interp<0, 0, 0>(tl, tq);
+#pragma unroll
+  for (int q = 0; q < 8; q++) {
+    double r = rc ? rc[c * 8 + q] : rc_value;
+    k[q] = conductivity(P, liquid_fraction(P, tq[q]), r);
+    dk[q] = conductivity_derivative(P, tq[q]);
+  }
+  interp<1, 0, 0>(tl, gx);
+  interp<0, 1, 0>(tl, gy);
+  interp<0, 0, 1>(tl, gz);
+#pragma unroll
+  for (int q = 0; q < 8; q++) {
+    gx[q] *= gscale;
+    gy[q] *= gscale;
+    gz[q] *= gscale;
+  }
+}
+
+// J v element vectors: D + L + C/dt (operators.py:380-410)
+__global__ void k_jac_cells(int64_t n, CellGeo g, DevParams P, const double* vd,
+                            const double* Tl, const double* rc, double rc_value,
+                            double dt, double* E) {
+  int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (c >= n) return;
+  double v[8], tl[8], k[8], dk[8], gx[8], gy[8], gz[8], e[8], tmp[8], pr[8];
+  gather8(g.cv, c, vd, v);
+  gather8(g.cv, c, Tl, tl);
+  const double h = g.h[c];
+  const double gscale = 2.0 / h;
+  tangent(P, tl, rc, rc_value, c, gscale, k, dk, gx, gy, gz);
+  const double hh = h / 2.0;
+  interp<1, 0, 0>(v, tmp);
+#pragma unroll
+  for (int q = 0; q < 8; q++) tmp[q] = (hh * k[q]) * tmp[q];
+  project<1, 0, 0>(tmp, e);
+  interp<0, 1, 0>(v, tmp);
+#pragma unroll
+  for (int q = 0; q < 8; q++) tmp[q] = (hh * k[q]) * tmp[q];
+  project<0, 1, 0>(tmp, pr);
+#pragma unroll
+  for (int i = 0; i < 8; i++) e[i] += pr[i];
+  interp<0, 0, 1>(v, tmp);
+#pragma unroll
+  for (int q = 0; q < 8; q++) tmp[q] = (hh * k[q]) * tmp[q];
+  project<0, 0, 1>(tmp, pr);
+#pragma unroll
+  for (int i = 0; i < 8; i++) e[i] += pr[i];
+  double vq[8], w[8];
+  interp<0, 0, 0>(v, vq);
+  const double dw = g.detw[c];
+  const double dwg = dw * gscale;
+#pragma unroll
+  for (int q = 0; q < 8; q++) w[q] = dwg * dk[q] * vq[q];
+#pragma unroll
+  for (int q = 0; q < 8; q++) tmp[q] = w[q] * gx[q];
+  project<1, 0, 0>(tmp, pr);
+#pragma unroll
+  for (int i = 0; i < 8; i++) e[i] += pr[i];
+#pragma unroll
+  for (int q = 0; q < 8; q++) tmp[q] = w[q] * gy[q];
+  project<0, 1, 0>(tmp, pr);
+#pragma unroll
+  for (int i = 0; i < 8; i++) e[i] += pr[i];
+#pragma unroll
+  for (int q = 0; q < 8; q++) tmp[q] = w[q] * gz[q];
+  project<0, 0, 1>(tmp, pr);
+#pragma unroll
+  for (int i = 0; i < 8; i++) e[i] += pr[i];
+  // + apply_mass(v) / dt
+#pragma unroll
+  for (int q = 0; q < 8; q++) vq[q] = vq[q] * (P.rhoc * dw);
+  project<0, 0, 0>(vq, pr);
+#pragma unroll
+  for (int i = 0; i < 8; i++) E[c * 8 + i] = e[i] + pr[i] / dt;
+}
+
+// element Jacobian entry A[a][b] (operators.py:412-424)
+__device__ __forceinline__ double elem_entry(int a, int b, double rcdt_dw, double hh,
+                                             double dwg, const double* k, const double* dk,
+                                             const double* gx, const double* gy,
+                                             const double* gz) {
+  double m = 0.0, d = 0.0, l = 0.0;
+#pragma unroll
+  for (int q = 0; q < 8; q++) {
+    m += cPhi[a][q] * cPhi[b][q];
+    d += k[q] * (cG[0][a][q] * cG[0][b][q] + cG[1][a][q] * cG[1][b][q] + cG[2][a][q] * cG[2][b][q]);
+    l += dk[q] * cPhi[b][q] *
+         (cG[0][a][q] * gx[q] + cG[1][a][q] * gy[q] + cG[2][a][q] * gz[q]);
+  }
+  return rcdt_dw * m + hh * d + dwg * l;
+}
+
+// element diagonals (plain cells) / full matrices (cells touching a
+// hanging vertex; fold tables operators.py:158-195)
+__global__ void k_jdiag_cells(int64_t n, CellGeo g, DevParams P, const double* Tl,
+                              const double* rc, double rc_value, double dt,
+                              const int* touched_pos, double* E, double* Ae) {
+  int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (c >= n) return;
+  double tl[8], k[8], dk[8], gx[8], gy[8], gz[8];
+  gather8(g.cv, c, Tl, tl);
+  const double h = g.h[c];
+  const double gscale = 2.0 / h;
+  tangent(P, tl, rc, rc_value, c, gscale, k, dk, gx, gy, gz);
+  const double dw = g.detw[c];
+  const double rcdt_dw = (P.rhoc / dt) * dw;
+  const double hh = h / 2.0;
+  const double dwg = dw * gscale;
+  int tp = touched_pos ? touched_pos[c] : -1;
+  if (tp < 0) {
+#pragma unroll
+    for (int a = 0; a < 8; a++) {
+      double d = 0.0, l = 0.0;
+#pragma unroll
+      for (int q = 0; q < 8; q++) {
+        d += k[q] * cGG[a][q];
+        l += dk[q] * cPhi[a][q] *
+             (cG[0][a][q] * gx[q] + cG[1][a][q] * gy[q] + cG[2][a][q] * gz[q]);
+      }
+      E[c * 8 + a] = (P.rhoc / dt) * (dw * cPhi2[a]) + hh * d + dwg * l;
+    }
+  } else {
+#pragma unroll
+    for (int a = 0; a < 8; a++) E[c * 8 + a] = 0.0;
+    for (int a = 0; a < 8; a++)
+      for (int b = 0; b < 8; b++)
+        Ae[(int64_t)tp * 64 + a * 8 + b] = elem_entry(a, b, rcdt_dw, hh, dwg, k, dk, gx, gy, gz);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// node kernels
+// ---------------------------------------------------------------------------
+struct NodeTab {
+  const int* inc_ptr;  // (nv+1)
+  const int* inc_ent;  // cell*8+corner, ascending per vertex
+  const int* cond_ptr;  // (nv+1) per master: slaves folding into it
+  const int* cond_s;
+  const double* cond_w;
+  const uint8_t* is_slave;
+  const uint8_t* is_dir;
+};
+
+__device__ __forceinline__ double gather_v(const NodeTab& nt, const double* E, int64_t v) {
+  double acc = 0.0;
+  for (int i = nt.inc_ptr[v]; i < nt.inc_ptr[v + 1]; i++) acc += E[nt.inc_ent[i]];
+  return acc;
+}
+
+// condensed sum at a non-slave vertex (bincount then np.add.at order)
+__device__ __forceinline__ double gather_condensed(const NodeTab& nt, const double* E, int64_t v) {
+  double f = gather_v(nt, E, v);
+  for (int i = nt.cond_ptr[v]; i < nt.cond_ptr[v + 1]; i++)
+    f = f + nt.cond_w[i] * gather_v(nt, E, nt.cond_s[i]);
+  return f;
+}
+
+// out = condensed(E); slave rows 0; optional: dirichlet rows <- dir_src, slave rows <- slave_val
+__global__ void k_gather(int64_t nv, NodeTab nt, const double* E, double* out,
+                         const double* dir_src, int set_slave, double slave_val) {
+  int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (v >= nv) return;
+  double r;
+  if (nt.is_slave[v]) {
+    r = set_slave ? slave_val : 0.0;
+  } else {
+    r = gather_condensed(nt, E, v);
+    if (dir_src && nt.is_dir[v]) r = dir_src[v];
+  }
+  out[v] = r;
+}
+
+// forward Euler with the lumped capacity (operators.py:352-369)
+__global__ void k_step_nodes(int64_t nv, NodeTab nt, const double* E, const double* Ec,
+                             const double* f_atomic, const double* c_atomic,
+                             const double* cinv, const double* T, double dt, double T_inf,
+                             double* Tout, unsigned long long* red) {
+  int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  double out = 0.0;
+  bool live = v < nv && !nt.is_slave[v];
+  if (live) {
+    double f = E ? gather_condensed(nt, E, v) : f_atomic[v];
+    double ci;
+    if (Ec)
+      ci = 1.0 / gather_condensed(nt, Ec, v);
+    else if (c_atomic)
+      ci = 1.0 / c_atomic[v];
+    else
+      ci = cinv[v];
+    out = T[v] + dt * (ci * f);
+    if (nt.is_dir[v]) out = T_inf;
+    Tout[v] = out;
+  }
+  block_max2(live ? out : 0.0, live ? out : -INFINITY, red);
+}
+
+// hanging-vertex closure (mesh.py:652-661)
+__global__ void k_distribute(int64_t ns, const int64_t* slaves, const int64_t* ptr,
+                             const int64_t* masters, const double* w, double* v) {
+  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= ns) return;
+  double acc = 0.0;
+  for (int64_t p = ptr[i]; p < ptr[i + 1]; p++) acc += w[p] * v[masters[p]];
+  v[slaves[i]] = acc;
+}
+
+// atomic-mode condensation (fold slave rows into masters, zero slaves)
+__global__ void k_condense_atomic(int64_t ns, const int64_t* slaves, const int64_t* ptr,
+                                  const int64_t* masters, const double* w, double* v) {
+  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= ns) return;
+  double x = v[slaves[i]];
+  for (int64_t p = ptr[i]; p < ptr[i + 1]; p++) atomicAdd(v + masters[p], w[p] * x);
+  v[slaves[i]] = 0.0;
+}
+
+__global__ void k_fold(int64_t nv, const int* fptr, const int* fent, const double* fw,
+                       const double* Ae, double* diag) {
+  int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (v >= nv) return;
+  int a = fptr[v], b = fptr[v + 1];
+  if (a == b) return;
+  double d = diag[v];
+  for (int i = a; i < b; i++) d = d + fw[i] * Ae[fent[i]];
+  diag[v] = d;
+}
+
+__global__ void k_prep_v(int64_t nv, const uint8_t* is_dir, const double* v, double* vd) {
+  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= nv) return;
+  vd[i] = is_dir[i] ? 0.0 : v[i];
+}
+
+__global__ void k_mask_rows(int64_t nv, const uint8_t* is_dir, const uint8_t* is_slave, double* v) {
+  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= nv) return;
+  if (is_dir[i] || is_slave[i]) v[i] = 0.0;
+}
+
+__global__ void k_pin(int64_t nv, const uint8_t* is_dir, double* v, double val) {
+  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= nv) return;
+  if (is_dir[i]) v[i] = val;
+}
+
+__global__ void k_diag_fix(int64_t nv, const uint8_t* is_dir, const uint8_t* is_slave, double* d) {
+  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= nv) return;
+  if (is_dir[i] || is_slave[i]) d[i] = 1.0;
+}
+
+// ---------------------------------------------------------------------------
+// backend
+// ---------------------------------------------------------------------------
+static inline unsigned nblk(int64_t n) { return (unsigned)((n + kThreads - 1) / kThreads); }
+
+struct Unstructured : Backend {
+  int64_t n = 0, nv = 0, ns = 0, nf = 0;
+  DevBuf<int> cv, inc_ptr, inc_ent, cond_ptr, cond_s, face_ptr, touched_pos, fold_ptr, fold_ent;
+  DevBuf<double> h, anc, detw, cond_w, fvx, fvy, farea, cinv, E, Ec, Ae, fold_w;
+  DevBuf<uint8_t> is_slave, is_dir;
+  DevBuf<int64_t> slaves, sptr, smast;
+  DevBuf<double> sw;
+  int64_t n_touched = 0;
+
+  CellGeo geo() const { return CellGeo{cv.p, h.p, anc.p, detw.p}; }
+  FaceTab faces() const { return FaceTab{nf ? face_ptr.p : nullptr, fvx.p, fvy.p, farea.p}; }
+  NodeTab nodes() const {
+    return NodeTab{inc_ptr.p, inc_ent.p, cond_ptr.p, cond_s.p, cond_w.p, is_slave.p, is_dir.p};
+  }
+
+  int launched() {
+    c->launches++;
+    ST_LAUNCHED();
+    return ST_OK;
+  }
+
+  int distribute(double* v) override {
+    if (!ns) return ST_OK;
+    k_distribute<<<nblk(ns), kThreads, 0, c->stream>>>(ns, slaves.p, sptr.p, smast.p, sw.p, v);
+    return launched();
+  }
+
+  int mask_rows(double* v) override {
+    k_mask_rows<<<nblk(nv), kThreads, 0, c->stream>>>(nv, is_dir.p, is_slave.p, v);
+    return launched();
+  }
+
+  int pin_dirichlet(double* v, double value) override {
+    k_pin<<<nblk(nv), kThreads, 0, c->stream>>>(nv, is_dir.p, v, value);
+    return launched();
+  }
+
+  int cells_rhs(const double* T, double* rc, int flags, double frozen_k, int nb,
+                const DevBeam* beams, int pending, bool want_cap, double* f_atomic,
+                double* c_atomic) {
+    double* rcp = rc;
+    bool det = c->deterministic || f_atomic == nullptr;
+    k_rhs_cells<<<nblk(n), kThreads, 0, c->stream>>>(
+        n, geo(), faces(), c->dp, T, rcp, c->rc_value, flags, frozen_k, pending, nb, beams,
+        det ? E.p : nullptr, (det && want_cap) ? Ec.p : nullptr, det ? nullptr : f_atomic,
+        (!det && want_cap) ? c_atomic : nullptr);
+    return launched();
+  }
+
+  int rhs(const double* T, double* rc, int flags, double frozen_k, int nb,
+          const DevBeam* beams, double* f, int pending) override {
+    if (c->deterministic) {
+      ST_TRY(cells_rhs(T, rc, flags, frozen_k, nb, beams, pending, false, nullptr, nullptr));
+      k_gather<<<nblk(nv), kThreads, 0, c->stream>>>(nv, nodes(), E.p, f, nullptr, 0, 0.0);
+      return launched();
+    }
+    ST_CUDA(cudaMemsetAsync(f, 0, nv * sizeof(double), c->stream));
+    ST_TRY(cells_rhs(T, rc, flags, frozen_k, nb, beams, pending, false, f, nullptr));
+    if (ns) {
+      k_condense_atomic<<<nblk(ns), kThreads, 0, c->stream>>>(ns, slaves.p, sptr.p, smast.p, sw.p, f);
+      ST_TRY(launched());
+    }
+    return ST_OK;
+  }
+
+  int explicit_step(const double* T, double* rc, double dt, int nb, const DevBeam* beams,
+                    double* Tout, int pending, double* red) override {
+    const bool latent = c->dp.latent != 0;
+    const int flags = ST_RHS_DIFFUSION | ST_RHS_FACES | ST_RHS_SOURCE;
+    double* fa = nullptr;
+    double* ca = nullptr;
+    if (!c->deterministic) {
+      ST_TRY(c->vec(6, &fa));
+      ST_CUDA(cudaMemsetAsync(fa, 0, nv * sizeof(double), c->stream));
+      if (latent) {
+        ST_TRY(c->vec(7, &ca));
+        ST_CUDA(cudaMemsetAsync(ca, 0, nv * sizeof(double), c->stream));
+      }
+    }
+    c->prof_begin();
+    ST_TRY(cells_rhs(T, rc, flags, 0.0, nb, beams, pending, latent, fa, ca));
+    c->prof_end();
+    if (!c->deterministic && ns) {
+      k_condense_atomic<<<nblk(ns), kThreads, 0, c->stream>>>(ns, slaves.p, sptr.p, smast.p, sw.p, fa);
+      ST_TRY(launched());
+      if (latent) {
+        k_condense_atomic<<<nblk(ns), kThreads, 0, c->stream>>>(ns, slaves.p, sptr.p, smast.p, sw.p, ca);
+        ST_TRY(launched());
+      }
+    }
+    const bool det = c->deterministic != 0;
+    k_step_nodes<<<nblk(nv), kThreads, 0, c->stream>>>(
+        nv, nodes(), det ? E.p : nullptr, (det && latent) ? Ec.p : nullptr, det ? nullptr : fa,
+        (!det && latent) ? ca : nullptr, cinv.p, T, dt, c->dp.T_inf, Tout,
+        reinterpret_cast<unsigned long long*>(red));
+    ST_TRY(launched());
+    return distribute(Tout);
+  }
+
+  int history(const double* T, double* rc) override {
+    if (!rc) return ST_OK;  // uniform r_c (== 1) is a fixed point
+    k_history<<<nblk(n), kThreads, 0, c->stream>>>(n, cv.p, c->dp, T, rc);
+    return launched();
+  }
+
+  int capacity(const double* T, double* out) override {
+    k_mass_cells<<<nblk(n), kThreads, 0, c->stream>>>(n, geo(), c->dp, nullptr, T, 1.0, E.p);
+    ST_TRY(launched());
+    k_gather<<<nblk(nv), kThreads, 0, c->stream>>>(nv, nodes(), E.p, out, nullptr, 1, 1.0);
+    return launched();
+  }
+
+  int mass(const double* v, double* out) override {
+    k_mass_cells<<<nblk(n), kThreads, 0, c->stream>>>(n, geo(), c->dp, v, nullptr, 1.0, E.p);
+    ST_TRY(launched());
+    k_gather<<<nblk(nv), kThreads, 0, c->stream>>>(nv, nodes(), E.p, out, nullptr, 0, 0.0);
+    return launched();
+  }
+
+  int jacobian(const double* v, const double* Tl, const double* rc, double dt,
+               double* out) override {
+    double* vd;
+    ST_TRY(c->vec(5, &vd));
+    ST_CUDA(cudaMemcpyAsync(vd, v, nv * sizeof(double), cudaMemcpyDeviceToDevice, c->stream));
+    ST_TRY(distribute(vd));
+    k_prep_v<<<nblk(nv), kThreads, 0, c->stream>>>(nv, is_dir.p, vd, vd);
+    ST_TRY(launched());
+    c->prof_begin();
+    k_jac_cells<<<nblk(n), kThreads, 0, c->stream>>>(n, geo(), c->dp, vd, Tl, rc,
+                                                      c->rc_value, dt, E.p);
+    ST_TRY(launched());
+    c->prof_end();
+    k_gather<<<nblk(nv), kThreads, 0, c->stream>>>(nv, nodes(), E.p, out, v, 0, 0.0);
+    return launched();
+  }
+
+  int jac_diag(const double* Tl, const double* rc, double dt, double* out) override {
+    k_jdiag_cells<<<nblk(n), kThreads, 0, c->stream>>>(
+        n, geo(), c->dp, Tl, rc, c->rc_value, dt,
+        n_touched ? touched_pos.p : nullptr, E.p, Ae.p);
+    ST_TRY(launched());
+    k_gather<<<nblk(nv), kThreads, 0, c->stream>>>(nv, nodes(), E.p, out, nullptr, 0, 0.0);
+    ST_TRY(launched());
+    if (n_touched) {
+      k_fold<<<nblk(nv), kThreads, 0, c->stream>>>(nv, fold_ptr.p, fold_ent.p, fold_w.p, Ae.p, out);
+      ST_TRY(launched());
+    }
+    k_diag_fix<<<nblk(nv), kThreads, 0, c->stream>>>(nv, is_dir.p, is_slave.p, out);
+    return launched();
+  }
+
+  double bytes_per_dof() const override {
+    // T read + T' write + C^-1 read (8+8+8) + r_c read/write (2*64 per
+    // cell) + cell_verts (32 per cell), SURVEY §8d config 3 accounting
+    double cells_per_dof = (double)n / (double)(nv - ns);
+    double b = 24.0 + cells_per_dof * 32.0;
+    if (!c->rc_uniform) b += cells_per_dof * 128.0;
+    return b;
+  }
+  const char* main_kernel() const override { return "k_rhs_cells"; }
+};
+
+int init_q1_constants() {
+  static bool done = false;
+  if (done) return ST_OK;
+  // reference operators.py:30-36 (same expressions, same rounding)
+  const double sq3 = std::sqrt(3.0);
+  const double g[2] = {-1.0 / sq3, 1.0 / sq3};
+  double V[2][2], D[2][2], U[2];
+  for (int q = 0; q < 2; q++) {
+    V[0][q] = (1.0 - g[q]) / 2.0;
+    V[1][q] = (1.0 + g[q]) / 2.0;
+    D[0][q] = -0.5;
+    D[1][q] = 0.5;
+    U[q] = (g[q] + 1.0) / 2.0;
+  }
+  double Phi[8][8], G[3][8][8], Phi2[8], GG[8][8];
+  for (int c = 0; c < 8; c++) {
+    int ix = (c >> 2) & 1, iy = (c >> 1) & 1, iz = c & 1;
+    Phi2[c] = 0.0;
+    for (int q = 0; q < 8; q++) {
+      int qx = (q >> 2) & 1, qy = (q >> 1) & 1, qz = q & 1;
+      Phi[c][q] = V[ix][qx] * V[iy][qy] * V[iz][qz];
+      G[0][c][q] = D[ix][qx] * V[iy][qy] * V[iz][qz];
+      G[1][c][q] = V[ix][qx] * D[iy][qy] * V[iz][qz];
+      G[2][c][q] = V[ix][qx] * V[iy][qy] * D[iz][qz];
+      Phi2[c] += Phi[c][q] * Phi[c][q];
+      GG[c][q] = G[0][c][q] * G[0][c][q] + G[1][c][q] * G[1][c][q] + G[2][c][q] * G[2][c][q];
+    }
+  }
+  ST_CUDA(cudaMemcpyToSymbol(cV, V, sizeof(V)));
+  ST_CUDA(cudaMemcpyToSymbol(cD, D, sizeof(D)));
+  ST_CUDA(cudaMemcpyToSymbol(cU, U, sizeof(U)));
+  ST_CUDA(cudaMemcpyToSymbol(cPhi, Phi, sizeof(Phi)));
+  ST_CUDA(cudaMemcpyToSymbol(cG, G, sizeof(G)));
+  ST_CUDA(cudaMemcpyToSymbol(cPhi2, Phi2, sizeof(Phi2)));
+  ST_CUDA(cudaMemcpyToSymbol(cGG, GG, sizeof(GG)));
+  done = true;
+  return ST_OK;
+}
+
+static int build_unstructured(Unstructured* u, Ctx* c, const st_unstructured_mesh* m) {
+  const int64_t n = m->n_cells, nv = m->n_vertices, ns = m->n_slaves, nf = m->n_faces;
+  if (n < 0 || nv <= 0 || ns < 0 || nf < 0 || (n > 0 && !m->cell_verts)) {
+    set_error("invalid unstructured mesh description");
+    return ST_EINVAL;
+  }
+  if (8 * n >= (int64_t)1 << 31) {
+    set_error("unstructured backend limited to 2^28 cells");
+    return ST_EUNSUPPORTED;
+  }
+  u->n = n;
+  u->nv = nv;
+  u->ns = ns;
+  u->nf = nf;
+  cudaStream_t s = c->stream;
+  ST_TRY(init_q1_constants());
+  for (int64_t i = 0; i < 8 * n; i++)
+    if (m->cell_verts[i] < 0 || m->cell_verts[i] >= nv) {
+      set_error("cell_verts out of range");
+      return ST_EINVAL;
+    }
+  // vertex incidence CSR in canonical (cell, corner) order
+  std::vector<int> ip(nv + 1, 0), ie(8 * n);
+  for (int64_t i = 0; i < 8 * n; i++) ip[m->cell_verts[i] + 1]++;
+  for (int64_t v = 0; v < nv; v++) ip[v + 1] += ip[v];
+  {
+    std::vector<int> fill(ip.begin(), ip.end() - 1);
+    for (int64_t i = 0; i < 8 * n; i++) ie[fill[m->cell_verts[i]]++] = (int)i;
+  }
+  // condensation CSR per master, in np.add.at order of the (slave, master) pairs
+  std::vector<int> cp(nv + 1, 0), cs;
+  std::vector<double> cw;
+  if (ns) {
+    int64_t np_ = m->slave_ptr[ns];
+    std::vector<int64_t> owner(np_);
+    for (int64_t i = 0; i < ns; i++)
+      for (int64_t p = m->slave_ptr[i]; p < m->slave_ptr[i + 1]; p++) owner[p] = i;
+    for (int64_t p = 0; p < np_; p++) cp[m->slave_masters[p] + 1]++;
+    for (int64_t v = 0; v < nv; v++) cp[v + 1] += cp[v];
+    cs.resize(np_);
+    cw.resize(np_);
+    std::vector<int> fill(cp.begin(), cp.end() - 1);
+    for (int64_t p = 0; p < np_; p++) {
+      int64_t mm = m->slave_masters[p];
+      cs[fill[mm]] = (int)m->slaves[owner[p]];
+      cw[fill[mm]++] = m->slave_weights[p];
+    }
+  } else {
+    cs.push_back(0);
+    cw.push_back(0.0);
+  }
+  // per-cell face CSR (faces sorted by cell)
+  std::vector<int> fp(n + 1, 0);
+  for (int64_t f = 0; f < nf; f++) {
+    int64_t cc = m->face_cell[f];
+    if (cc < 0 || cc >= n || (f && m->face_cell[f - 1] > cc)) {
+      set_error("face_cell must be sorted cell positions");
+      return ST_EINVAL;
+    }
+    fp[cc + 1]++;
+  }
+  for (int64_t i = 0; i < n; i++) fp[i + 1] += fp[i];
+  // det_w = (h/2)^3 with libm pow as numpy's ** (operators.py:106)
+  std::vector<double> dw(n);
+  for (int64_t i = 0; i < n; i++) dw[i] = std::pow(m->cell_h[i] / 2.0, 3.0);
+  // fold tables for cells touching hanging vertices (operators.py:158-195)
+  std::vector<int> tpos(n, -1);
+  std::vector<int> fptr(nv + 1, 0), fent;
+  std::vector<double> fw;
+  int64_t nt = 0;
+  if (ns) {
+    std::map<int64_t, std::pair<std::vector<int64_t>, std::vector<double>>> expand;
+    std::vector<uint8_t> sl(nv, 0);
+    for (int64_t i = 0; i < ns; i++) {
+      sl[m->slaves[i]] = 1;
+      auto& e = expand[m->slaves[i]];
+      for (int64_t p = m->slave_ptr[i]; p < m->slave_ptr[i + 1]; p++) {
+        e.first.push_back(m->slave_masters[p]);
+        e.second.push_back(m->slave_weights[p]);
+      }
+    }
+    struct FE { int64_t m; int ent; double w; };
+    std::vector<FE> ents;
+    for (int64_t cc = 0; cc < n; cc++) {
+      bool t = false;
+      for (int a = 0; a < 8; a++) t |= sl[m->cell_verts[cc * 8 + a]] != 0;
+      if (!t) continue;
+      tpos[cc] = (int)nt;
+      std::vector<int64_t> ms[8];
+      std::vector<double> ws[8];
+      for (int a = 0; a < 8; a++) {
+        int64_t gv = m->cell_verts[cc * 8 + a];
+        auto it = expand.find(gv);
+        if (it == expand.end()) {
+          ms[a] = {gv};
+          ws[a] = {1.0};
+        } else {
+          // intersect1d works on sorted unique masters
+          std::vector<std::pair<int64_t, double>> pr;
+          for (size_t k = 0; k < it->second.first.size(); k++)
+            pr.push_back({it->second.first[k], it->second.second[k]});
+          std::sort(pr.begin(), pr.end(),
+                    [](const std::pair<int64_t, double>& x, const std::pair<int64_t, double>& y) {
+                      return x.first < y.first;
+                    });
+          for (auto& q : pr) {
+            ms[a].push_back(q.first);
+            ws[a].push_back(q.second);
+          }
+        }
+      }
+      for (int a = 0; a < 8; a++)
+        for (int b = 0; b < 8; b++) {
+          size_t i = 0, j = 0;
+          while (i < ms[a].size() && j < ms[b].size()) {
+            if (ms[a][i] == ms[b][j]) {
+              ents.push_back({ms[a][i], (int)(nt * 64 + a * 8 + b), ws[a][i] * ws[b][j]});
+              i++;
+              j++;
+            } else if (ms[a][i] < ms[b][j]) {
+              i++;
+            } else {
+              j++;
+            }
+          }
+        }
+      nt++;
+    }
+    for (auto& e : ents) fptr[e.m + 1]++;
+    for (int64_t v = 0; v < nv; v++) fptr[v + 1] += fptr[v];
+    fent.resize(ents.size());
+    fw.resize(ents.size());
+    std::vector<int> fill(fptr.begin(), fptr.end() - 1);
+    for (auto& e : ents) {
+      fent[fill[e.m]] = e.ent;
+      fw[fill[e.m]++] = e.w;
+    }
+  }
+  if (fent.empty()) {
+    fent.push_back(0);
+    fw.push_back(0.0);
+  }
+  u->n_touched = nt;
+  ST_TRY(u->cv.upload(m->cell_verts, 8 * n, s));
+  ST_TRY(u->h.upload(m->cell_h, n, s));
+  ST_TRY(u->anc.upload(m->cell_anchor, 3 * n, s));
+  ST_TRY(u->detw.upload(dw.data(), n, s));
+  ST_TRY(u->inc_ptr.upload(ip.data(), nv + 1, s));
+  ST_TRY(u->inc_ent.upload(ie.data(), 8 * n, s));
+  ST_TRY(u->cond_ptr.upload(cp.data(), nv + 1, s));
+  ST_TRY(u->cond_s.upload(cs.data(), cs.size(), s));
+  ST_TRY(u->cond_w.upload(cw.data(), cw.size(), s));
+  ST_TRY(u->face_ptr.upload(fp.data(), n + 1, s));
+  if (nf) {
+    ST_TRY(u->fvx.upload(m->face_vx, 4 * nf, s));
+    ST_TRY(u->fvy.upload(m->face_vy, 4 * nf, s));
+    ST_TRY(u->farea.upload(m->face_area, nf, s));
+  }
+  ST_TRY(u->is_slave.upload(m->is_slave, nv, s));
+  ST_TRY(u->is_dir.upload(m->is_dirichlet, nv, s));
+  if (ns) {
+    ST_TRY(u->slaves.upload(m->slaves, ns, s));
+    ST_TRY(u->sptr.upload(m->slave_ptr, ns + 1, s));
+    ST_TRY(u->smast.upload(m->slave_masters, m->slave_ptr[ns], s));
+    ST_TRY(u->sw.upload(m->slave_weights, m->slave_ptr[ns], s));
+  }
+  ST_TRY(u->touched_pos.upload(tpos.data(), n, s));
+  ST_TRY(u->fold_ptr.upload(fptr.data(), nv + 1, s));
+  ST_TRY(u->fold_ent.upload(fent.data(), fent.size(), s));
+  ST_TRY(u->fold_w.upload(fw.data(), fw.size(), s));
+  ST_TRY(u->E.alloc(8 * std::max<int64_t>(n, 1)));
+  if (c->dp.latent) ST_TRY(u->Ec.alloc(8 * std::max<int64_t>(n, 1)));
+  ST_TRY(u->Ae.alloc(64 * std::max<int64_t>(nt, 1)));
+  ST_TRY(u->cinv.alloc(nv));
+  // C^-1 cached per operator (operators.py:336-339)
+  ST_TRY(u->capacity(nullptr, u->cinv.p));
+  ST_TRY(vec_recip(c, u->cinv.p, u->cinv.p, nv));
+  ST_CUDA(cudaStreamSynchronize(s));
+  return ST_OK;
+}
+
+Backend* make_unstructured(Ctx* c, const st_unstructured_mesh* m, int* err) {
+  Unstructured* u = new Unstructured();
+  u->c = c;
+  int rc = build_unstructured(u, c, m);
+  if (rc != ST_OK) {
+    delete u;
+    *err = rc;
+    return nullptr;
+  }
+  c->nv = m->n_vertices;
+  c->n_cells = m->n_cells;
+  c->qpc = 8;
+  *err = ST_OK;
+  return u;
+}
+
+}  // namespace st

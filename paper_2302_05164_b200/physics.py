@@ -1,0 +1,163 @@
+"""Beam schedule on the host, flattened for the device step loop.
+
+The scan-path types mirror ``scantherm/physics.py`` (Segment :32,
+LayerPath :58, ScanPath :78, BeamState :96) and ``layer_beam_state``
+reproduces :135-151 operation for operation, because parity of the
+temperature field depends on the beam position rounding.  The new piece
+is :func:`flatten_schedule`, which evaluates the whole layer's beam
+states for a run of steps at once (``tau = (step - 1) * dt``,
+``timestepping.py:211-214``) into a packed float64 table that the CUDA
+step loop consumes without host round trips.
+
+``generate_hatch`` restates ``driver.py:85-111`` (serpentine hatching)
+because BASELINE config 1 is defined through it.
+"""
+
+import math
+from dataclasses import dataclass, field
+
+import numpy as np
+
+
+class ScheduleError(ValueError):
+    """Query outside the build schedule."""
+
+
+@dataclass
+class Segment:
+    x0: float
+    y0: float
+    x1: float
+    y1: float
+    v: float
+    power: float
+
+    @property
+    def length(self) -> float:
+        return float(np.hypot(self.x1 - self.x0, self.y1 - self.y0))
+
+    @property
+    def duration(self) -> float:
+        return self.length / self.v
+
+    def validate(self):
+        if self.v <= 0.0:
+            raise ValueError("scan speed must be positive")
+        if self.power < 0.0:
+            raise ValueError("power must be nonnegative")
+
+
+@dataclass
+class LayerPath:
+    layer_index: int
+    z: float
+    segments: list = field(default_factory=list)
+    cool_time: float = 0.0
+
+    def scan_duration(self) -> float:
+        return sum(s.duration for s in self.segments)
+
+    def duration(self) -> float:
+        return self.scan_duration() + self.cool_time
+
+
+@dataclass
+class ScanPath:
+    layers: list = field(default_factory=list)
+
+    def total_duration(self) -> float:
+        return sum(lp.duration() for lp in self.layers)
+
+
+@dataclass
+class BeamState:
+    position: np.ndarray
+    z_top: float
+    power: float
+    active: bool
+
+    @staticmethod
+    def off(z_top=0.0):
+        return BeamState(np.zeros(2), z_top, 0.0, False)
+
+
+def layer_beam_state(lp, tau: float) -> BeamState:
+    """Beam at time tau from the layer start (closed segment windows)."""
+    if tau < 0.0:
+        raise ScheduleError(f"tau = {tau} before the layer starts")
+    t_seg = 0.0
+    for seg in lp.segments:
+        d = seg.duration
+        if t_seg <= tau <= t_seg + d:
+            s = (tau - t_seg) * seg.v
+            frac = s / seg.length if seg.length > 0.0 else 0.0
+            pos = np.array([seg.x0 + frac * (seg.x1 - seg.x0),
+                            seg.y0 + frac * (seg.y1 - seg.y0)])
+            return BeamState(pos, lp.z, seg.power, seg.power > 0.0)
+        t_seg += d
+    if tau <= lp.duration():
+        return BeamState.off(lp.z)
+    raise ScheduleError(f"tau = {tau} beyond the layer duration {lp.duration()}")
+
+
+# packed beam record consumed by the C ABI (st_beam in include/scantherm_b200.h)
+BEAM_DTYPE = np.dtype([("x", "f8"), ("y", "f8"), ("z_top", "f8"),
+                       ("power", "f8"), ("active", "i4"), ("_pad", "i4")])
+
+
+def pack_beams(beams):
+    """List of BeamState (or None) -> contiguous BEAM_DTYPE array."""
+    out = np.zeros(len(beams), dtype=BEAM_DTYPE)
+    for i, b in enumerate(beams):
+        if b is None:
+            continue
+        out[i]["x"] = float(b.position[0])
+        out[i]["y"] = float(b.position[1])
+        out[i]["z_top"] = float(b.z_top)
+        out[i]["power"] = float(b.power)
+        out[i]["active"] = int(bool(b.active) and float(b.power) > 0.0)
+    return out
+
+
+def flatten_schedule(layer_paths, dt, n_steps, step0=1):
+    """Beam records for steps step0 .. step0+n_steps-1 of a scan phase.
+
+    ``layer_paths`` is one LayerPath or a list of concurrently scanned
+    LayerPaths (multi-spot, BASELINE config 4: the source is linear in
+    the beams).  Returns (dt_steps (n,), beams (n, n_beams) BEAM_DTYPE).
+    """
+    if not isinstance(layer_paths, (list, tuple)):
+        layer_paths = [layer_paths]
+    duration = layer_paths[0].scan_duration()
+    nb = len(layer_paths)
+    beams = np.zeros((n_steps, nb), dtype=BEAM_DTYPE)
+    dts = np.empty(n_steps)
+    for i in range(n_steps):
+        step = step0 + i
+        tau = (step - 1) * dt
+        dts[i] = min(dt, duration - tau)
+        beams[i] = pack_beams([layer_beam_state(lp, tau) for lp in layer_paths])
+    return dts, beams
+
+
+def generate_hatch(boxes, spacing, v, power, direction_deg=0.0):
+    """Serpentine tracks over (x0, y0, x1, y1) boxes, alternating sense."""
+    if direction_deg not in (0.0, 90.0, 0, 90):
+        raise ValueError("hatch direction must be 0 or 90 degrees")
+    along_x = direction_deg in (0.0, 0)
+    segs = []
+    sense = 1
+    for (x0, y0, x1, y1) in boxes:
+        width = (y1 - y0) if along_x else (x1 - x0)
+        n = max(1, int(math.floor(width / spacing + 1e-9)))
+        off = (width - (n - 1) * spacing) / 2.0
+        for i in range(n):
+            c = off + i * spacing
+            if along_x:
+                a, b = (x0, x1) if sense > 0 else (x1, x0)
+                segs.append(Segment(a, y0 + c, b, y0 + c, v, power))
+            else:
+                a, b = (y0, y1) if sense > 0 else (y1, y0)
+                segs.append(Segment(x0 + c, a, x0 + c, b, v, power))
+            sense = -sense
+    return segs
