@@ -49,7 +49,8 @@ def workload_config0(n_steps):
     params = st.ProcessParams(mat, bnd, las, st.MeshParams(h_coarse=h, n_refine=0, h_powder=h))
     T0 = 300.0 + np.random.default_rng(0).uniform(0.0, 1.0, box.n_vertices)
     dt = 1e-6
-    lp = st.LayerPath(0, 0.0, [st.Segment(0.0, 1e-3, n_steps * dt, 1e-3, 1.0, 70.0)], 0.0)
+    # the beam crosses the plate: 2 mm at 1 m/s = 2000 steps of 1 us
+    lp = st.LayerPath(0, 0.0, [st.Segment(0.0, 1e-3, 2e-3, 1e-3, 1.0, 70.0)], 0.0)
     return dict(name="config0_q1_64x64x32", box=box, params=params, T0=T0, rc=1.0,
                 dt=dt, paths=[lp], degree=1, dofs=box.n_dofs,
                 cfg={"mesh": "64x64x32 Q1", "dofs": box.n_dofs, "dt": dt,

@@ -168,8 +168,10 @@ def test_instability_is_reported_at_the_failing_step():
     op = st.ThermalOperator(forest, dm, params, st.SolverSettings())
     hist = st.initial_history(forest)
     state = st.SimulationState(forest, dm, op, T0.copy(), hist)
+    # a 20 mm virtual track: 20 steps of 1 ms, ~20x the stability bound
+    lp = st.LayerPath(0, 0.0, [st.Segment(0.0, 1e-3, 2e-2, 1e-3, 1.0, 70.0)], 0.0)
     with pytest.raises(st.InstabilityError) as ei:
-        st.run_scan_phase(state, lp, 5e-5)   # far above the stability bound
+        st.run_scan_phase(state, lp, 1e-3)
     e = ei.value
     assert e.step >= 1 and not (np.isfinite(e.t_extreme) and e.t_extreme <= 1e7)
     # the reported state is the diverged one
