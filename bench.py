@@ -4,17 +4,21 @@ explicit-step DoF-updates/s (fp64) + % of the HBM roofline).
     python bench.py [--gpus N] [--steps K] [--warmup W] [--workload NAME]
     python bench.py --impl reference ...     # CPU oracle port, rank 0 only
 
-A step is one forward-Euler update of the whole mesh (operator apply +
-lumped-capacity update + moving source + top-surface losses + Dirichlet
-pin + stability check + history).  Timing: W untimed warm-up steps, then
-K steps each bracketed by CUDA events on the library's stream, with L2
-flushed (256 MiB write) before every timed step outside the events; the
-per-rank time is the sum, the job time the max over ranks.
+Default workload: BASELINE configs[1] (128x128x32 Q2 cells, 4,293,185
+DoFs, k(T) + latent heat + radiation/convection, 70 W beam on a 5-track
+hatch, dt = 0.5 us).  A step is one forward-Euler update of the whole
+mesh: operator apply + lumped-capacity update (apparent heat capacity) +
+moving source + top-surface losses + Dirichlet pin + stability check.
+
+Timing: W untimed warm-up steps, then K steps each bracketed by CUDA
+events on the library's stream, with L2 flushed (256 MiB write) before
+every timed step outside the events; per-rank time = sum of the step
+times, job time = max over ranks.  ``sweep`` adds BASELINE configs[2]
+(~50M DoFs at degree 1..4, inputs larger than L2) measured the same way.
 
 Under torchrun (N > 1) every rank runs its own copy of the workload on
-its GPU ("replicas"; the z-slab partition with halo exchange is
-DESIGN.md §6 work in progress), value = DoF-updates of all ranks / max
-time.
+its GPU (replicas; the z-slab partition is DESIGN.md §7 future work),
+value = DoF-updates of all ranks / max time.
 """
 
 import argparse
@@ -31,48 +35,102 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 L2_FLUSH_BYTES = 256 << 20
+METRIC = "explicit-step DoF-updates/s (fp64)"
 
 
 # ---------------------------------------------------------------------------
-# workloads (BASELINE.json configs; synthetic inputs of the stated shapes)
+# workloads: BASELINE.json configs, synthetic inputs of the stated shapes
 # ---------------------------------------------------------------------------
 
-def workload_config0(n_steps):
-    """configs[0]: 64x64x32 Q1 (139,425 DoFs), k = 6.7, 70 W beam at
-    1 m/s along y = 1 mm, dt = 1 us, bottom Dirichlet 300 K."""
+def _st():
     import paper_2302_05164_b200 as st
+    return st
+
+
+def workload_config0():
+    """configs[0]: 64x64x32 Q1 (139,425 DoFs), k = 6.7 const, 70 W beam at
+    1 m/s along y = 1 mm, dt = 1 us, bottom Dirichlet 300 K."""
+    st = _st()
     h = 31.25e-6
-    box = st.StructuredBox(64, 64, 32, h, degree=1)
     mat = st.MaterialParams(k_p=6.7, k_m=6.7, k_s=6.7, rho=4430.0, c=526.0)
     bnd = st.BoundaryParams(emissivity=0.0, T_inf=300.0, T_v=1e9)
     las = st.HeatSourceParams(radius=50e-6, h_powder=40e-6, power=70.0, scan_velocity=1.0)
     params = st.ProcessParams(mat, bnd, las, st.MeshParams(h_coarse=h, n_refine=0, h_powder=h))
-    T0 = 300.0 + np.random.default_rng(0).uniform(0.0, 1.0, box.n_vertices)
-    dt = 1e-6
-    # the beam crosses the plate: 2 mm at 1 m/s = 2000 steps of 1 us
     lp = st.LayerPath(0, 0.0, [st.Segment(0.0, 1e-3, 2e-3, 1e-3, 1.0, 70.0)], 0.0)
-    return dict(name="config0_q1_64x64x32", box=box, params=params, T0=T0, rc=1.0,
-                dt=dt, paths=[lp], degree=1, dofs=box.n_dofs,
-                cfg={"mesh": "64x64x32 Q1", "dofs": box.n_dofs, "dt": dt,
-                     "material": "k=6.7 const", "beams": 1})
+    return dict(name="config0_q1_64x64x32", dims=(64, 64, 32), h=h, degree=1,
+                params=params, T0=lambda n: 300.0 + np.random.default_rng(0).uniform(0, 1, n),
+                dt=1e-6, paths=[lp], sample=(64, 64, 32),
+                cfg={"mesh": "64x64x32 Q1", "dt": 1e-6, "material": "k=6.7 const",
+                     "beams": 1})
 
 
-WORKLOADS = {"config0": workload_config0}
+def _config1_params():
+    st = _st()
+    h = 31.25e-6
+    # k(T) = g k_m + (1-g) k_s with r_c = 1 (SURVEY §0.1), c_app with latent heat
+    mat = st.MaterialParams(k_p=6.7, k_m=32.0, k_s=6.7, rho=4430.0, c=526.0, T_s=300.0,
+                            T_l=1928.0, latent_heat=2.86e5, T_lat_s=1878.0, T_lat_l=1928.0)
+    bnd = st.BoundaryParams(emissivity=0.3, T_inf=300.0, T_v=1e9, h_conv=10.0)
+    las = st.HeatSourceParams(radius=50e-6, h_powder=40e-6, power=70.0, scan_velocity=1.0)
+    return st.ProcessParams(mat, bnd, las, st.MeshParams(h_coarse=h, n_refine=0, h_powder=h))
 
 
-def make_operator(w):
-    import paper_2302_05164_b200 as st
-    box = w["box"]
-    try:
-        op = st.ThermalOperator(box, box, w["params"], st.SolverSettings())
-        backend = "structured"
-    except Exception:
-        if w["degree"] != 1:
-            raise
-        forest, dm = box.to_forest_dofmap()
-        op = st.ThermalOperator(forest, dm, w["params"], st.SolverSettings())
-        backend = "unstructured"
-    return op, backend
+def workload_config1():
+    """configs[1]: 4x4x1 mm, 128x128x32 Q2 cells (4,293,185 DoFs), k(T)
+    6.7 -> 32 W/mK over 300-1928 K, apparent heat capacity (latent
+    2.86e5 J/kg over 1878-1928 K), top radiation eps 0.3 + convection
+    h = 10, 70 W beam on a 5-track serpentine hatch (100 um), dt = 0.5 us."""
+    st = _st()
+    h = 31.25e-6
+    segs = st.generate_hatch([(1.5e-3, 1.75e-3, 2.5e-3, 2.25e-3)], 1e-4, 1.0, 70.0)
+    lp = st.LayerPath(0, 0.0, segs, 0.0)
+    return dict(name="config1_q2_128x128x32", dims=(128, 128, 32), h=h, degree=2,
+                params=_config1_params(),
+                T0=lambda n: 300.0 + np.random.default_rng(0).uniform(0, 1, n),
+                dt=0.5e-6, paths=[lp], sample=(32, 32, 32),
+                cfg={"mesh": "128x128x32 Q2", "dt": 0.5e-6,
+                     "material": "k(T) 6.7->32, c_app latent 2.86e5, rad 0.3 + conv 10",
+                     "beams": 1, "hatch": "5 tracks x 1 mm, 100 um"})
+
+
+CELLS_50M = {1: 367, 2: 184, 3: 122, 4: 92}
+
+
+def workload_config2(p):
+    """configs[2]: unit cube, ~50M DoFs at degree p, T ~ U[300, 2500],
+    material as config 1, beam off, dt = 1 ms."""
+    st = _st()
+    n = CELLS_50M[p]
+    h = 1.0 / n
+    lp = st.LayerPath(0, 0.0, [], 0.0)
+    return dict(name=f"config2_q{p}_{n}^3", dims=(n, n, n), h=h, degree=p,
+                params=_config1_params(),
+                T0=lambda m: np.random.default_rng(2).uniform(300.0, 2500.0, m),
+                dt=1e-3, paths=[lp], sample=(24, 24, 24),
+                cfg={"mesh": f"{n}^3 Q{p} unit cube", "dt": 1e-3,
+                     "material": "as config 1", "beams": 0})
+
+
+WORKLOADS = {"config0": workload_config0, "config1": workload_config1,
+             "config2_p1": lambda: workload_config2(1), "config2_p2": lambda: workload_config2(2),
+             "config2_p3": lambda: workload_config2(3), "config2_p4": lambda: workload_config2(4)}
+
+
+def build_problem(w, dims=None):
+    st = _st()
+    nx, ny, nz = dims or w["dims"]
+    box = st.StructuredBox(nx, ny, nz, w["h"], degree=w["degree"])
+    return box
+
+
+def schedule(w, n):
+    from paper_2302_05164_b200.physics import flatten_schedule
+    paths = w["paths"]
+    if not paths[0].segments:       # beam off: an empty layer of n steps
+        dts = np.full(n, w["dt"])
+        from paper_2302_05164_b200.physics import BEAM_DTYPE
+        return dts, np.zeros((n, 0), dtype=BEAM_DTYPE)
+    return flatten_schedule(paths, w["dt"], n)
 
 
 # ---------------------------------------------------------------------------
@@ -83,6 +141,7 @@ class Clocks:
     Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
          "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
          "clocks_event_reasons.sw_power_cap")
+    NAMES = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
 
     def __init__(self, index):
         self.index = index
@@ -100,7 +159,7 @@ class Clocks:
                     self.samples.append([s.strip() for s in out.split(",")])
             except Exception:
                 pass
-            self._stop.wait(0.2)
+            self._stop.wait(0.1)
 
     def __enter__(self):
         self._t = threading.Thread(target=self._run, daemon=True)
@@ -114,10 +173,15 @@ class Clocks:
     def summary(self):
         if not self.samples:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
-        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
-        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = sorted({names[i] for s in self.samples for i in range(4)
+
+        def num(x):
+            try:
+                return float(x)
+            except ValueError:
+                return None
+        sm = [v for v in (num(s[0]) for s in self.samples) if v is not None]
+        mx = [v for v in (num(s[1]) for s in self.samples) if v is not None]
+        reasons = sorted({self.NAMES[i] for s in self.samples for i in range(4)
                           if len(s) > 2 + i and s[2 + i].lower() == "active"})
         return {"sm_mhz": float(np.median(sm)) if sm else None,
                 "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
@@ -125,59 +189,104 @@ class Clocks:
 
 
 def measured_hbm_peak():
-    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
     try:
-        with open(p) as f:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
             return float(json.load(f)["hbm_gbs"]), "measured"
     except Exception:
         return 6650.0, "fallback"
 
 
 # ---------------------------------------------------------------------------
-# CPU baseline: the oracle port (numpy restatement of the reference path)
+# CPU: the oracle port (numpy restatement of the reference path)
 # ---------------------------------------------------------------------------
+
+class CpuSample:
+    """The oracle on a bounded sub-box of the workload (same physics,
+    same degree); rates are per DoF so the sub-box is representative."""
+
+    def __init__(self, w):
+        sys.path.insert(0, os.path.join(ROOT, "oracle"))
+        from cpu_oracle import OracleOperator, structured_tables
+        nx, ny, nz = w["sample"]
+        self.dims = (nx, ny, nz)
+        self.orc = OracleOperator(structured_tables(nx, ny, nz, w["h"], w["degree"]),
+                                  w["params"])
+        q = w["degree"] + 1
+        self.rc = np.ones((self.orc.n, q, q, q))
+        self.T = w["T0"](self.orc.nv)
+        self.dts, beams = schedule(w, 64)
+        from cpu_oracle import beam_tuple
+        self.beams = [[beam_tuple(b) for b in row] for row in beams]
+        self.n_dofs = self.orc.nv
+        self.i = 0
+        self.w = w
+
+    def step(self):
+        k = self.i % len(self.dts)
+        self.T = self.orc.explicit_step(self.T, float(self.dts[k]), self.rc, self.beams[k])
+        self.rc = self.orc.update_history(self.rc, self.T)
+        self.i += 1
+
+    def describe(self, n):
+        nx, ny, nz = self.dims
+        return (f"{n} explicit steps (+history) on a {nx}x{ny}x{nz} Q{self.w['degree']} sub-box "
+                f"({self.n_dofs} DoFs) of {self.w['name']} with the numpy oracle port "
+                f"(oracle/cpu_oracle.py)")
+
 
 def cpu_baseline(w, seconds=15.0):
-    sys.path.insert(0, os.path.join(ROOT, "oracle"))
-    from cpu_oracle import OracleOperator, structured_tables
     from threadpoolctl import threadpool_limits
-    box = w["box"]
     cores = os.cpu_count() or 1
-    orc = OracleOperator(structured_tables(box.nx, box.ny, box.nz, box.h, w["degree"]),
-                         w["params"])
-    q = w["degree"] + 1
-    rc = np.ones((box.n_cells, q, q, q))
-    T = w["T0"].copy()
-    from paper_2302_05164_b200.physics import flatten_schedule
-    dts, beams = flatten_schedule(w["paths"], w["dt"], 200)
-    from cpu_oracle import beam_tuple
-    n = 0
+    s = CpuSample(w)
     with threadpool_limits(limits=cores):
-        orc.capacity_inverse()
+        s.step()  # warm (capacity cache, imports)
+        n = 0
         t0 = time.perf_counter()
-        while True:
-            T = orc.explicit_step(T, float(dts[n % 200]), rc,
-                                  [beam_tuple(b) for b in beams[n % 200]])
-            rc = orc.update_history(rc, T)
+        while n < 1 or time.perf_counter() - t0 < seconds:
+            s.step()
             n += 1
-            if time.perf_counter() - t0 > seconds:
-                break
         el = time.perf_counter() - t0
-    return {"value": w["dofs"] * n / el, "unit": "DoF-updates/s", "cores": cores,
-            "kind": "port",
-            "sample": f"{n} full explicit steps (+history) of {w['name']} with the numpy oracle "
-                      f"port (oracle/cpu_oracle.py), BLAS threads <= {cores}"}
+    return {"value": s.n_dofs * n / el, "unit": "DoF-updates/s", "cores": cores,
+            "kind": "port", "sample": s.describe(n) + f", BLAS threads <= {cores}"}
 
 
 # ---------------------------------------------------------------------------
-# runs
+# GPU runs
 # ---------------------------------------------------------------------------
 
 def dist_env():
-    ws = int(os.environ.get("WORLD_SIZE", "1"))
-    rank = int(os.environ.get("RANK", "0"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
-    return ws, rank, local
+    return (int(os.environ.get("WORLD_SIZE", "1")), int(os.environ.get("RANK", "0")),
+            int(os.environ.get("LOCAL_RANK", "0")))
+
+
+def gpu_measure(w, steps, warmup, device, clocks=True):
+    st = _st()
+    box = build_problem(w)
+    op = st.ThermalOperator(box, box, w["params"], st.SolverSettings(), device=device)
+    dts, beams = schedule(w, warmup + steps)
+    T0 = w["T0"](box.n_vertices)
+    op.set_state(T0, 1.0)           # consolidated material: r_c = 1 everywhere
+    op.bench_explicit(dts[:warmup], beams[:warmup], 0)
+    launches0 = op.launches
+    clk = Clocks(device) if clocks else None
+    if clk:
+        clk.__enter__()
+    step_ms, main_ms = op.bench_explicit(dts[warmup:], beams[warmup:], L2_FLUSH_BYTES)
+    if clk:
+        clk.__exit__()
+    launches = op.launches - launches0
+    bpd = op.bytes_per_dof()
+    main_avg_s = float(np.mean(main_ms)) * 1e-3
+    peak, peak_kind = measured_hbm_peak()
+    achieved = bpd * box.n_dofs / main_avg_s / 1e9
+    _, _, main_name = op.profile_read()
+    roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                "frac": achieved / peak, "traffic": None, "kernel": main_name,
+                "bytes_per_dof": bpd, "peak_source": peak_kind,
+                "kernel_ms": float(np.mean(main_ms)),
+                "kernel_share_of_step": float(np.sum(main_ms) / np.sum(step_ms))}
+    return dict(op=op, box=box, dts=dts, beams=beams, T0=T0, step_ms=step_ms,
+                launches=launches, roofline=roofline, clocks=clk.summary() if clk else None)
 
 
 def run_ours(args):
@@ -187,65 +296,60 @@ def run_ours(args):
         import torch.distributed as dist
         torch.cuda.set_device(local)
         dist.init_process_group("nccl")
-    from paper_2302_05164_b200.physics import flatten_schedule
-    w = WORKLOADS[args.workload](args.warmup + args.steps)
-    op, backend = make_operator(w)
-    dts, beams = flatten_schedule(w["paths"], w["dt"], args.warmup + args.steps)
-    op.set_state(w["T0"], w["rc"])
-    # warm-up (untimed)
-    op.bench_explicit(dts[:args.warmup], beams[:args.warmup], 0)
-    launches0 = op.launches
+    w = WORKLOADS[args.workload]()
     if ws > 1:
         torch.distributed.barrier()
     torch.cuda.synchronize()
-    with Clocks(local) as clk:
-        step_ms, main_ms = op.bench_explicit(dts[args.warmup:], beams[args.warmup:],
-                                             L2_FLUSH_BYTES)
+    r = gpu_measure(w, args.steps, args.warmup, local)
     torch.cuda.synchronize()
-    launches = op.launches - launches0
-    total_ms = float(np.sum(step_ms))
+    total_ms = float(np.sum(r["step_ms"]))
     if ws > 1:
         t = torch.tensor([total_ms], device="cuda")
         torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
         total_ms = float(t.item())
         torch.distributed.barrier()
-    dof_updates = w["dofs"] * args.steps * ws
-    value = dof_updates / (total_ms * 1e-3)
+    dofs = r["box"].n_dofs
+    value = dofs * args.steps * ws / (total_ms * 1e-3)
 
-    # end to end through the public API: host T in, K steps, host T out
-    T_host = np.ascontiguousarray(w["T0"])
+    # end to end through the public API: host T in -> K steps -> host T, r_c out
+    op = r["op"]
+    dts, beams = r["dts"][args.warmup:], r["beams"][args.warmup:]
+    T_host = np.ascontiguousarray(r["T0"])
     t0 = time.perf_counter()
-    op.set_state(T_host, w["rc"])
-    fail, _, _ = op.run_explicit(dts[args.warmup:], beams[args.warmup:])
+    op.set_state(T_host, 1.0)
+    fail, _, _ = op.run_explicit(dts, beams)
     T_out, rc_out = op.get_state()
     e2e_s = time.perf_counter() - t0
-    assert fail == 0 and np.all(np.isfinite(T_out))
+    if fail or not np.all(np.isfinite(T_out)):
+        raise RuntimeError("end-to-end run diverged")
     nb = beams.shape[1]
-    h2d = T_host.nbytes + (0 if np.isscalar(w["rc"]) else np.asarray(w["rc"]).nbytes) \
-        + args.steps * (nb * 40 + 8)
-    d2h = T_out.nbytes + rc_out.nbytes
-    e2e = {"value": w["dofs"] * args.steps / e2e_s, "unit": "DoF-updates/s",
+    h2d = T_host.nbytes + args.steps * (nb * 40 + 8)
+    d2h = T_out.nbytes + rc_out.nbytes + args.steps * 16
+    e2e = {"value": dofs * args.steps / e2e_s, "unit": "DoF-updates/s",
            "h2d_bytes_per_step": h2d / args.steps, "d2h_bytes_per_step": d2h / args.steps,
-           "api": "ThermalOperator.set_state + run_explicit (st_explicit_steps) + get_state, "
-                  "host buffers, wall clock"}
-
-    bpd = op.bytes_per_dof()
-    main_avg_s = float(np.mean(main_ms)) * 1e-3
-    peak, peak_kind = measured_hbm_peak()
-    achieved = bpd * w["dofs"] / main_avg_s / 1e9
-    _, _, main_name = op.profile_read()
-    roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                "frac": achieved / peak, "traffic": None, "kernel": main_name,
-                "bytes_per_dof": bpd, "peak_source": peak_kind,
-                "kernel_share_of_step": float(np.sum(main_ms) / np.sum(step_ms))}
-    out = {"metric": "explicit-step DoF-updates/s (fp64)", "value": value,
-           "unit": "DoF-updates/s", "n_gpus": ws, "steps": args.steps, "warmup": args.warmup,
-           "ms_per_step": total_ms / args.steps, "higher_is_better": True,
-           "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-           "config": dict(workload=w["name"], backend=backend, l2="flushed (256 MiB write) "
-                          "before every timed step", parallelism=f"replicas x{ws}", **w["cfg"]),
-           "e2e": e2e, "roofline": roofline, "gpu_launches": int(launches),
-           "clocks": clk.summary()}
+           "api": "ThermalOperator.set_state(T host) + run_explicit(K steps, "
+                  "st_explicit_steps) + get_state(T, r_c host); wall clock"}
+    cfg = dict(workload=w["name"], dofs=dofs, backend="structured",
+               l2="flushed (256 MiB write) before every timed step",
+               parallelism=f"replicas x{ws}", **w["cfg"])
+    out = {"metric": METRIC, "value": value, "unit": "DoF-updates/s", "n_gpus": ws,
+           "steps": args.steps, "warmup": args.warmup, "ms_per_step": total_ms / args.steps,
+           "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+           "data": "synthetic", "config": cfg, "e2e": e2e, "roofline": r["roofline"],
+           "gpu_launches": int(r["launches"]), "clocks": r["clocks"]}
+    if rank == 0 and ws == 1 and args.sweep:
+        sweep = {}
+        for p in (1, 2, 3, 4):
+            wp = workload_config2(p)
+            rp = gpu_measure(wp, args.sweep_steps, 3, local, clocks=False)
+            sweep[f"q{p}"] = {"dofs": rp["box"].n_dofs,
+                              "value": rp["box"].n_dofs * args.sweep_steps
+                              / (float(np.sum(rp["step_ms"])) * 1e-3),
+                              "ms_per_step": float(np.mean(rp["step_ms"])),
+                              "roofline_frac": rp["roofline"]["frac"],
+                              "achieved_GBps": rp["roofline"]["achieved"]}
+            rp["op"].close()
+        out["sweep_config2"] = sweep
     if rank == 0 and ws == 1 and not args.no_cpu_baseline:
         out["cpu_baseline"] = cpu_baseline(w, seconds=args.cpu_seconds)
     if rank == 0:
@@ -255,24 +359,31 @@ def run_ours(args):
 
 
 def run_reference(args):
+    """The reference's CPU path (oracle port; the reference itself is a
+    Python package that is not installed on the GPU box) on the same
+    workload: each step is one explicit step of a bounded sub-box."""
     ws, rank, _ = dist_env()
     if rank != 0:
         return
-    w = WORKLOADS[args.workload](200)
-    sys.path.insert(0, os.path.join(ROOT, "oracle"))
-    per = []
-    for _ in range(args.warmup + args.steps):
-        r = cpu_baseline(w, seconds=args.cpu_seconds / max(1, args.steps))
-        per.append(r)
-    vals = [r["value"] for r in per[args.warmup:]]
-    v = float(np.mean(vals))
-    cb = dict(per[-1])
-    cb["value"] = v
-    out = {"impl": "reference", "metric": "explicit-step DoF-updates/s (fp64)", "value": v,
-           "unit": "DoF-updates/s", "n_gpus": ws, "steps": args.steps, "warmup": args.warmup,
-           "ms_per_step": w["dofs"] / v * 1e3, "higher_is_better": True, "scaling": "weak",
+    from threadpoolctl import threadpool_limits
+    w = WORKLOADS[args.workload]()
+    cores = os.cpu_count() or 1
+    s = CpuSample(w)
+    with threadpool_limits(limits=cores):
+        for _ in range(args.warmup):
+            s.step()
+        t0 = time.perf_counter()
+        for _ in range(args.steps):
+            s.step()
+        el = time.perf_counter() - t0
+    v = s.n_dofs * args.steps / el
+    out = {"impl": "reference", "metric": METRIC, "value": v, "unit": "DoF-updates/s",
+           "n_gpus": ws, "steps": args.steps, "warmup": args.warmup,
+           "ms_per_step": el / args.steps * 1e3, "higher_is_better": True, "scaling": "weak",
            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-           "config": dict(workload=w["name"], **w["cfg"]), "cpu_baseline": cb,
+           "config": dict(workload=w["name"], **w["cfg"]),
+           "cpu_baseline": {"value": v, "unit": "DoF-updates/s", "cores": cores, "kind": "port",
+                            "sample": s.describe(args.steps) + f", BLAS threads <= {cores}"},
            "e2e": {"value": v, "unit": "DoF-updates/s", "h2d_bytes_per_step": 0,
                    "d2h_bytes_per_step": 0}}
     print(json.dumps(out), flush=True)
@@ -284,13 +395,15 @@ def main():
     ap.add_argument("--steps", type=int, default=100)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--workload", default="config0", choices=sorted(WORKLOADS))
+    ap.add_argument("--workload", default="config1", choices=sorted(WORKLOADS))
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--sweep", type=int, default=1, help="also measure configs[2], p=1..4")
+    ap.add_argument("--sweep-steps", type=int, default=10)
     args = ap.parse_args()
-    if args.warmup < 3:
-        args.warmup = 3
+    args.warmup = max(3, args.warmup)
     if args.impl == "reference":
+        args.steps = min(args.steps, 20)   # bounded CPU sample per the contract
         run_reference(args)
     else:
         run_ours(args)

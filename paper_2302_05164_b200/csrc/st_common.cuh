@@ -96,9 +96,11 @@ __host__ __device__ inline double key_to_double(unsigned long long k) {
 #endif
 }
 
-// block-wide max of (|x|, x) into two global order keys
+// block-wide max of (|x|, x) into two global order keys; every thread of
+// the block must call it; one atomic pair per block
 __device__ __forceinline__ void block_max2(double absval, double val,
                                           unsigned long long* slot) {
+  __shared__ unsigned long long s_a[32], s_s[32];
   unsigned long long ka = __double_as_longlong(fabs(absval));  // >= 0: bits monotone
   unsigned long long ks = order_key(val);
   for (int o = 16; o > 0; o >>= 1) {
@@ -107,7 +109,17 @@ __device__ __forceinline__ void block_max2(double absval, double val,
     ka = a2 > ka ? a2 : ka;
     ks = s2 > ks ? s2 : ks;
   }
+  const int w = threadIdx.x >> 5, nw = (blockDim.x + 31) >> 5;
   if ((threadIdx.x & 31) == 0) {
+    s_a[w] = ka;
+    s_s[w] = ks;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int i = 1; i < nw; i++) {
+      ka = s_a[i] > ka ? s_a[i] : ka;
+      ks = s_s[i] > ks ? s_s[i] : ks;
+    }
     atomicMax(slot, ka);
     atomicMax(slot + 1, ks);
   }

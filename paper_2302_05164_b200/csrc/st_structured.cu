@@ -26,6 +26,7 @@
 #include <vector>
 
 #include "st_common.cuh"
+#include "st_basis_tables.h"
 
 namespace st {
 
@@ -60,7 +61,28 @@ struct SArgs {
   double dt;
   DevParams P;
   unsigned long long* red;
+  // uniform consolidated history (r_c = rc_value >= 1 >= g): the law
+  // k = (r_p k_p + g k_m) + r_s k_s collapses to k = kA + g kB
+  double kA, kB;
+  double glo;     // -T_s / (T_l - T_s): g = clamp(T * inv_dT_l + glo)
+  double lat_mid, lat_half;  // latent interval as |T - mid| < half
+  double hw3[125];  // (h/2) W_qa W_qb W_qc      (diffusion weight)
+  double lw3[125];  // rho L/dT (h/2)^3 W3        (latent capacity bump)
+  // C^-1 of the constant lumped capacity as a tensor product of inverse
+  // 1D lumped masses (row sums, operators.py:325-334):
+  // C^-1(I,J,K) = inv_rcdw im(I) im(J) im(K)
+  double inv_rcdw;
+  double imr[5];          // interior node residue a = 1..P-1
+  double imv_int, imv_end;  // cell vertex inside / at the end of the line
 };
+
+// inverse 1D lumped mass of node L on a line of N nodes
+template <int P>
+__device__ __forceinline__ double inv_mass1(const SArgs& A, int L, int N) {
+  const int a = L % P;
+  if (a != 0) return A.imr[a];
+  return (L == 0 || L == N - 1) ? A.imv_end : A.imv_int;
+}
 
 template <int P>
 __device__ __forceinline__ double coord(const SArgs& A, int axis, int cell, int q) {
@@ -93,9 +115,12 @@ __device__ __forceinline__ void sweep_v(double* t) {
       for (int m = 0; m < Q; m++) in[m] = t[base + m * S];
 #pragma unroll
       for (int q = 0; q < Q; q++) {
-        double acc = (TR ? sV[P - 1][q][0] : sV[P - 1][0][q]) * in[0];
+        // compile-time coefficients (st_basis_tables.h): exact zeros of the
+        // GLL/Gauss tables vanish from the instruction stream
+        double acc = (TR ? Basis<P>::V(q, 0) : Basis<P>::V(0, q)) * in[0];
 #pragma unroll
-        for (int m = 1; m < Q; m++) acc = fma(TR ? sV[P - 1][q][m] : sV[P - 1][m][q], in[m], acc);
+        for (int m = 1; m < Q; m++)
+          acc = fma(TR ? Basis<P>::V(q, m) : Basis<P>::V(m, q), in[m], acc);
         t[base + q * S] = acc;
       }
     }
@@ -114,397 +139,52 @@ __device__ __forceinline__ void project3(double* t) {
   sweep_v<P, 2, true>(t);
 }
 
-struct CellFlags {
-  bool diffusion, faces, source, frozen;
-};
-
-// Element vector of one cell (operators.py:247-316 generalised to degree
-// P).  t: node values in, element vector out.  With LATENT, ec receives
-// the apparent-capacity increment rho L/(dT) projected onto the nodes
-// (zero unless a Gauss point lies in the latent interval).
-template <int P, bool RCF, bool LATENT>
-__device__ __forceinline__ void cell_element(const SArgs& A, const CellFlags& F, int i, int j,
-                                             int k, int64_t cell, double* t, double* ec,
-                                             bool& has_lat) {
-  constexpr int Q = P + 1;
-  constexpr int Q3 = Q * Q * Q;
-  const DevParams& PP = A.P;
-  const bool top = F.faces && A.top_faces && (k == A.nz - 1);
-  double tf[Q * Q];
-  if (top) {
-#pragma unroll
-    for (int a = 0; a < Q; a++)
-#pragma unroll
-      for (int b = 0; b < Q; b++) tf[a * Q + b] = t[(a * Q + b) * Q + P];
-  }
-  interp3<P>(t);  // t now holds T at the Gauss points
-  double G[Q3];
-#pragma unroll
-  for (int q = 0; q < Q3; q++) G[q] = 0.0;
-
-  // beams hitting this cell (operators.py:295-307)
-  unsigned hits = 0;
-  if (F.source) {
-    const double ax = coord<P>(A, 0, i, -1), ay = coord<P>(A, 1, j, -1), az = coord<P>(A, 2, k, -1);
-    for (int b = 0; b < A.nb && b < 32; b++)
-      if (beam_hits_cell(PP, A.beams[b], ax, ay, az, A.h)) hits |= 1u << b;
-  }
-  has_lat = false;
-#pragma unroll
-  for (int qa = 0; qa < Q; qa++)
-#pragma unroll
-    for (int qb = 0; qb < Q; qb++)
-#pragma unroll
-      for (int qc = 0; qc < Q; qc++) {
-        const int q = (qa * Q + qb) * Q + qc;
-        const double Tq = t[q];
-        const double w3 = sW[P - 1][qa] * sW[P - 1][qb] * sW[P - 1][qc];
-        if (F.diffusion) {
-          double gx = 0.0, gy = 0.0, gz = 0.0;
-#pragma unroll
-          for (int m = 0; m < Q; m++) {
-            gx = fma(sDq[P - 1][m][qa], t[(m * Q + qb) * Q + qc], gx);
-            gy = fma(sDq[P - 1][m][qb], t[(qa * Q + m) * Q + qc], gy);
-            gz = fma(sDq[P - 1][m][qc], t[(qa * Q + qb) * Q + m], gz);
-          }
-          double kq;
-          if (F.frozen) {
-            kq = A.frozen_k;
-          } else {
-            const double g = liquid_fraction_fast(PP, Tq);
-            double r;
-            if (RCF) {
-              r = A.rc[cell * Q3 + q];
-              if (A.pending) {
-                r = fmax(r, g);
-                A.rc[cell * Q3 + q] = r;
-              }
-            } else {
-              r = A.rc_value;
-            }
-            kq = conductivity(PP, g, r);
-          }
-          // w detJ (2/h)^2 = (h/2) w;  f_diff = - sum_d D_d^T (c D_d T)
-          const double c = (A.hh * w3) * kq;
-          const double fx = c * gx, fy = c * gy, fz = c * gz;
-#pragma unroll
-          for (int m = 0; m < Q; m++) {
-            G[(m * Q + qb) * Q + qc] = fma(-sDq[P - 1][m][qa], fx, G[(m * Q + qb) * Q + qc]);
-            G[(qa * Q + m) * Q + qc] = fma(-sDq[P - 1][m][qb], fy, G[(qa * Q + m) * Q + qc]);
-            G[(qa * Q + qb) * Q + m] = fma(-sDq[P - 1][m][qc], fz, G[(qa * Q + qb) * Q + m]);
-          }
-        }
-        if (hits) {
-          const double x = coord<P>(A, 0, i, qa), y = coord<P>(A, 1, j, qb),
-                       z = coord<P>(A, 2, k, qc);
-          double s = 0.0;
-          for (int b = 0; b < A.nb && b < 32; b++)
-            if (hits & (1u << b)) s += beam_source(PP, A.beams[b], x, y, z);
-          G[q] = fma(s, A.detw0 * w3, G[q]);
-        }
-      }
-  project3<P>(G);
-  if (LATENT) {
-    // apparent-capacity increment at the Gauss points in the latent
-    // interval (t still holds T_q; it is free afterwards)
-#pragma unroll
-    for (int qa = 0; qa < Q; qa++)
-#pragma unroll
-      for (int qb = 0; qb < Q; qb++)
-#pragma unroll
-        for (int qc = 0; qc < Q; qc++) {
-          const int q = (qa * Q + qb) * Q + qc;
-          const bool in = t[q] > PP.T_lat_s && t[q] < PP.T_lat_l;
-          has_lat |= in;
-          t[q] = in ? PP.lat_bump * (A.detw0 * (sW[P - 1][qa] * sW[P - 1][qb] * sW[P - 1][qc]))
-                    : 0.0;
-        }
-    if (has_lat) {
-      project3<P>(t);
-#pragma unroll
-      for (int q = 0; q < Q3; q++) ec[q] = t[q];
-    }
-  }
-#pragma unroll
-  for (int q = 0; q < Q3; q++) t[q] = G[q];
-  if (top) {
-    // facet quadrature on the +z face (operators.py:275-290), full facets
-    double fq[Q * Q];
-#pragma unroll
-    for (int a = 0; a < Q * Q; a++) fq[a] = tf[a];
-    // interpolate to face Gauss points: y then x
-#pragma unroll
-    for (int a = 0; a < Q; a++) {
-      double in[Q];
-#pragma unroll
-      for (int b = 0; b < Q; b++) in[b] = fq[a * Q + b];
-#pragma unroll
-      for (int qb = 0; qb < Q; qb++) {
-        double acc = 0.0;
-#pragma unroll
-        for (int b = 0; b < Q; b++) acc = fma(sV[P - 1][b][qb], in[b], acc);
-        fq[a * Q + qb] = acc;
-      }
-    }
-#pragma unroll
-    for (int qb = 0; qb < Q; qb++) {
-      double in[Q];
-#pragma unroll
-      for (int a = 0; a < Q; a++) in[a] = fq[a * Q + qb];
-#pragma unroll
-      for (int qa = 0; qa < Q; qa++) {
-        double acc = 0.0;
-#pragma unroll
-        for (int a = 0; a < Q; a++) acc = fma(sV[P - 1][a][qa], in[a], acc);
-        fq[qa * Q + qb] = acc;
-      }
-    }
-    const double area0 = A.hh * A.hh;
-#pragma unroll
-    for (int qa = 0; qa < Q; qa++)
-#pragma unroll
-      for (int qb = 0; qb < Q; qb++)
-        fq[qa * Q + qb] = surface_flux(PP, fq[qa * Q + qb]) *
-                          (-(area0 * (sW[P - 1][qa] * sW[P - 1][qb])));
-    // project back: x then y
-#pragma unroll
-    for (int qb = 0; qb < Q; qb++) {
-      double in[Q];
-#pragma unroll
-      for (int qa = 0; qa < Q; qa++) in[qa] = fq[qa * Q + qb];
-#pragma unroll
-      for (int a = 0; a < Q; a++) {
-        double acc = 0.0;
-#pragma unroll
-        for (int qa = 0; qa < Q; qa++) acc = fma(sV[P - 1][a][qa], in[qa], acc);
-        fq[a * Q + qb] = acc;
-      }
-    }
-#pragma unroll
-    for (int a = 0; a < Q; a++) {
-      double in[Q];
-#pragma unroll
-      for (int qb = 0; qb < Q; qb++) in[qb] = fq[a * Q + qb];
-#pragma unroll
-      for (int b = 0; b < Q; b++) {
-        double acc = 0.0;
-#pragma unroll
-        for (int qb = 0; qb < Q; qb++) acc = fma(sV[P - 1][b][qb], in[qb], acc);
-        t[(a * Q + b) * Q + P] += acc;
-      }
-    }
-  }
-}
-
-// seam membership of node (I, J, K): shared with another CTA
-__device__ __forceinline__ bool on_seam(const SArgs& A, int P, int CY, int CZ, int I, int J, int K) {
-  const bool xs = I > 0 && I < A.NX - 1 && (I % (P * A.Lx)) == 0;
-  const bool ys = J > 0 && J < A.NY - 1 && (J % (P * CY)) == 0;
-  const bool zs = K > 0 && K < A.NZ - 1 && (K % (P * CZ)) == 0;
-  return xs || ys || zs;
-}
-
-// finalise one node with its complete f (and latent capacity increment)
-__device__ __forceinline__ double finalize_node(const SArgs& A, int64_t idx, int K, double T,
-                                                double f, double dc, bool latent) {
-  if (A.mode == 1) return f;
-  double ci = A.cinv[idx];
-  if (latent && dc != 0.0) ci = 1.0 / (1.0 / ci + dc);
-  double o = T + A.dt * (ci * f);
-  if (A.dir_bottom && K == 0) o = A.P.T_inf;
-  return o;
-}
-
-template <int P, int CY, int CZ, bool LATENT, bool RCF>
-__global__ void __launch_bounds__(CY* CZ) k_xmarch(SArgs A) {
-  constexpr int Q = P + 1;
-  constexpr int Q3 = Q * Q * Q;
-  constexpr int NYT = P * CY + 1, NZT = P * CZ + 1, PL = NYT * NZT;
-  constexpr int NACC = LATENT ? 2 : 1;
-  extern __shared__ double sm[];
-  double* ring = sm;                // Q planes of T
-  double* acc = sm + Q * PL;        // P planes of f (+ P of dC)
-  const int tid = threadIdx.x;
-  const int jl = tid / CZ, kl = tid % CZ;
-  const int j0 = blockIdx.x * CY, k0 = blockIdx.y * CZ, i0 = blockIdx.z * A.Lx;
-  if (i0 >= A.nx) return;
-  const int i1 = min(i0 + A.Lx, A.nx);
-  const int j = j0 + jl, k = k0 + kl;
-  const bool live = j < A.ny && k < A.nz;
-  const int Jn = min(P * CY, P * (A.ny - j0)) + 1;
-  const int Kn = min(P * CZ, P * (A.nz - k0)) + 1;
-  const CellFlags F{(A.flags & ST_RHS_DIFFUSION) != 0, (A.flags & ST_RHS_FACES) != 0,
-                    (A.flags & ST_RHS_SOURCE) != 0 && A.nb > 0, (A.flags & ST_RHS_FROZEN_K) != 0};
-
-  for (int t = tid; t < NACC * P * PL; t += CY * CZ) acc[t] = 0.0;
-  auto load_plane = [&](int I) {
-    double* dst = ring + (I % Q) * PL;
-    const double* src = A.T + ((int64_t)I * A.NY + (int64_t)P * j0) * A.NZ + (int64_t)P * k0;
-    for (int t = tid; t < Jn * Kn; t += CY * CZ) {
-      int jj = t / Kn, kk = t - jj * Kn;
-      dst[jj * NZT + kk] = src[(int64_t)jj * A.NZ + kk];
-    }
-  };
-  double carry[Q * Q], carryC[LATENT ? Q * Q : 1];
-#pragma unroll
-  for (int q = 0; q < Q * Q; q++) carry[q] = 0.0;
-  if (LATENT)
-#pragma unroll
-    for (int q = 0; q < Q * Q; q++) carryC[q] = 0.0;
-  double amax = 0.0, smax = -INFINITY;
-  bool bad = false;
-
-  // finalise node plane I from accumulator plane a
-  auto finalize_plane = [&](int I, int a) {
-    const double* tp = ring + (I % Q) * PL;
-    double* ap = acc + a * PL;
-    double* cp = acc + (P + a) * PL;
-    for (int t = tid; t < Jn * Kn; t += CY * CZ) {
-      int jj = t / Kn, kk = t - jj * Kn;
-      const int J = P * j0 + jj, K = P * k0 + kk;
-      const int64_t idx = ((int64_t)I * A.NY + J) * A.NZ + K;
-      const double f = ap[jj * NZT + kk];
-      ap[jj * NZT + kk] = 0.0;
-      double dc = 0.0;
-      if (LATENT) {
-        dc = cp[jj * NZT + kk];
-        cp[jj * NZT + kk] = 0.0;
-      }
-      if (on_seam(A, P, CY, CZ, I, J, K)) {
-        atomicAdd(A.fseam + idx, f);
-        if (LATENT && dc != 0.0) atomicAdd(A.cseam + idx, dc);
-      } else {
-        const double o = finalize_node(A, idx, K, tp[jj * NZT + kk], f, dc, LATENT);
-        A.out[idx] = o;
-        amax = fmax(amax, fabs(o));
-        smax = fmax(smax, o);
-        bad |= (o != o);
-      }
-    }
-  };
-
-  // accumulate this thread's element planes a = 0..P-1 (e) into acc in 4
-  // conflict-free phases; nodes of cells in the same phase never coincide
-  auto accumulate = [&](const double* e, const double* ec, bool lat, int planes) {
-#pragma unroll
-    for (int ph = 0; ph < 4; ph++) {
-      if (live && ((jl & 1) == (ph >> 1)) && ((kl & 1) == (ph & 1))) {
-        for (int a = 0; a < planes; a++) {
-#pragma unroll
-          for (int b = 0; b < Q; b++)
-#pragma unroll
-            for (int c = 0; c < Q; c++) {
-              const int s = a * PL + (P * jl + b) * NZT + (P * kl + c);
-              acc[s] += e[(a * Q + b) * Q + c];
-              if (LATENT && lat) acc[P * PL + s] += ec[(a * Q + b) * Q + c];
-            }
-        }
-      }
-      __syncthreads();
-    }
-  };
-
-  load_plane(P * i0);
-  for (int i = i0; i < i1; i++) {
-#pragma unroll
-    for (int a = 1; a <= P; a++) load_plane(P * i + a);
-    __syncthreads();
-    double t[Q3], ec[LATENT ? Q3 : 1];
-    bool lat = false;
-    if (live) {
-#pragma unroll
-      for (int a = 0; a < Q; a++) {
-        const double* tp = ring + ((P * i + a) % Q) * PL;
-#pragma unroll
-        for (int b = 0; b < Q; b++)
-#pragma unroll
-          for (int c = 0; c < Q; c++) t[(a * Q + b) * Q + c] = tp[(P * jl + b) * NZT + P * kl + c];
-      }
-      const int64_t cell = ((int64_t)i * A.ny + j) * A.nz + k;
-      if (LATENT)
-#pragma unroll
-        for (int q = 0; q < Q3; q++) ec[q] = 0.0;
-      cell_element<P, RCF, LATENT>(A, F, i, j, k, cell, t, ec, lat);
-      // x-face shared with the previous layer: add carry, keep the new one
-#pragma unroll
-      for (int q = 0; q < Q * Q; q++) {
-        t[q] += carry[q];
-        carry[q] = t[P * Q * Q + q];
-      }
-      if (LATENT) {
-        if (lat) {
-#pragma unroll
-          for (int q = 0; q < Q * Q; q++) {
-            ec[q] += carryC[q];
-            carryC[q] = ec[P * Q * Q + q];
-          }
-        } else {
-#pragma unroll
-          for (int q = 0; q < Q * Q; q++) {
-            ec[q] = carryC[q];
-            carryC[q] = 0.0;
-          }
-          lat = true;
-#pragma unroll
-          for (int q = Q * Q; q < Q3; q++) ec[q] = 0.0;
-        }
-      }
-    }
-    accumulate(t, ec, lat, P);
-    for (int a = 0; a < P; a++) finalize_plane(P * i + a, a);
-    __syncthreads();
-  }
-  // last node plane of the chunk: the carried x-face
-  {
-    double e[Q3];
-#pragma unroll
-    for (int q = 0; q < Q * Q; q++) e[q] = carry[q];
-    double ecc[LATENT ? Q3 : 1];
-    if (LATENT)
-#pragma unroll
-      for (int q = 0; q < Q * Q; q++) ecc[q] = carryC[q];
-    accumulate(e, ecc, LATENT, 1);
-    finalize_plane(P * i1, 0);
-  }
-  block_max2(bad ? (double)NAN : amax, smax, A.red);
-}
+#include "st_xmarch.cuh"
 
 // finalise the seam nodes (x planes, then y planes not on an x seam, then
 // z planes on neither)
-__global__ void k_seams(SArgs A, int P, int CY, int CZ, int nxs, int nys, int nzs, int latent) {
-  const int64_t nxp = (int64_t)A.NY * A.NZ, nyp = (int64_t)A.NX * A.NZ, nzp = (int64_t)A.NX * A.NY;
-  const int64_t tot = nxs * nxp + nys * nyp + nzs * nzp;
+// One block row (blockIdx.y) per seam plane; 32-bit in-plane indexing.
+__global__ void k_seams(SArgs A, int P, int CY, int CZ, int nxs, int nys, int nzs, int bx, int by,
+                        int bz, int latent) {
   double amax = 0.0, smax = -INFINITY;
   bool bad = false;
-  for (int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; g < tot;
-       g += (int64_t)gridDim.x * blockDim.x) {
-    int I, J, K;
-    bool mine = true;
-    if (g < nxs * nxp) {
-      int s = (int)(g / nxp);
-      int64_t r = g - s * nxp;
-      I = P * A.Lx * (s + 1);
-      J = (int)(r / A.NZ);
-      K = (int)(r - (int64_t)J * A.NZ);
-    } else if (g < nxs * nxp + nys * nyp) {
-      int64_t h = g - nxs * nxp;
-      int s = (int)(h / nyp);
-      int64_t r = h - s * nyp;
-      J = P * CY * (s + 1);
-      I = (int)(r / A.NZ);
-      K = (int)(r - (int64_t)I * A.NZ);
-      mine = !(I > 0 && I < A.NX - 1 && (I % (P * A.Lx)) == 0);
-    } else {
-      int64_t h = g - nxs * nxp - nys * nyp;
-      int s = (int)(h / nzp);
-      int64_t r = h - s * nzp;
-      K = P * CZ * (s + 1);
-      I = (int)(r / A.NY);
-      J = (int)(r - (int64_t)I * A.NY);
-      mine = !(I > 0 && I < A.NX - 1 && (I % (P * A.Lx)) == 0) &&
-             !(J > 0 && J < A.NY - 1 && (J % (P * CY)) == 0);
-    }
-    if (!mine) continue;
+  // flat block index -> (family plane, block within the plane)
+  int b = blockIdx.x, pl;
+  if (b < bx * nxs) {
+    pl = b / bx;
+    b -= pl * bx;
+  } else if ((b -= bx * nxs) < by * nys) {
+    pl = b / by;
+    b -= pl * by;
+    pl += nxs;
+  } else {
+    b -= by * nys;
+    pl = b / bz;
+    b -= pl * bz;
+    pl += nxs + nys;
+  }
+  const int t = b * blockDim.x + threadIdx.x;
+  const int sx = P * A.Lx, sy = P * CY;
+  int I, J, K;
+  bool mine;
+  if (pl < nxs) {  // x plane: (J, K) contiguous
+    I = sx * (pl + 1);
+    J = t / A.NZ;
+    K = t - J * A.NZ;
+    mine = J < A.NY;
+  } else if (pl < nxs + nys) {  // y plane: rows of K for each I
+    J = sy * (pl - nxs + 1);
+    I = t / A.NZ;
+    K = t - I * A.NZ;
+    mine = I < A.NX && !(I > 0 && I < A.NX - 1 && (I % sx) == 0);
+  } else {  // z plane: strided
+    K = P * CZ * (pl - nxs - nys + 1);
+    I = t / A.NY;
+    J = t - I * A.NY;
+    mine = I < A.NX && !(I > 0 && I < A.NX - 1 && (I % sx) == 0) &&
+           !(J > 0 && J < A.NY - 1 && (J % sy) == 0);
+  }
+  if (mine) {
     const int64_t idx = ((int64_t)I * A.NY + J) * A.NZ + K;
     const double f = A.fseam[idx];
     A.fseam[idx] = 0.0;
@@ -513,7 +193,8 @@ __global__ void k_seams(SArgs A, int P, int CY, int CZ, int nxs, int nys, int nz
       dc = A.cseam[idx];
       A.cseam[idx] = 0.0;
     }
-    const double o = finalize_node(A, idx, K, A.T[idx], f, dc, latent != 0);
+    const double o =
+        finalize_node(A, A.mode == 0 ? A.cinv[idx] : 0.0, K, A.T[idx], f, dc, latent != 0);
     A.out[idx] = o;
     amax = fmax(amax, fabs(o));
     smax = fmax(smax, o);
@@ -902,6 +583,31 @@ struct Structured : Backend {
     A.fseam = fseam.p;
     A.cseam = cseam.p;
     A.P = c->dp;
+    const DevParams& d = c->dp;
+    A.kA = (1.0 - c->rc_value) * d.k_p + c->rc_value * d.k_s;
+    A.kB = d.k_m - d.k_s;
+    A.glo = -d.T_s * d.inv_dT_l;
+    A.lat_mid = 0.5 * (d.T_lat_s + d.T_lat_l);
+    A.lat_half = 0.5 * (d.T_lat_l - d.T_lat_s);
+    const int q = p + 1;
+    std::vector<double> w(q), m1(q);
+    switch (p) {
+      case 1: for (int i = 0; i < q; i++) { w[i] = Basis<1>::W(i); m1[i] = Basis<1>::M(i); } break;
+      case 2: for (int i = 0; i < q; i++) { w[i] = Basis<2>::W(i); m1[i] = Basis<2>::M(i); } break;
+      case 3: for (int i = 0; i < q; i++) { w[i] = Basis<3>::W(i); m1[i] = Basis<3>::M(i); } break;
+      default: for (int i = 0; i < q; i++) { w[i] = Basis<4>::W(i); m1[i] = Basis<4>::M(i); } break;
+    }
+    A.inv_rcdw = 1.0 / (d.rhoc * A.detw0);
+    for (int a = 0; a < 5; a++) A.imr[a] = (a > 0 && a < p) ? 1.0 / m1[a] : 0.0;
+    A.imv_int = 1.0 / (m1[0] + m1[p]);
+    A.imv_end = 1.0 / m1[0];
+    for (int a = 0; a < q; a++)
+      for (int b = 0; b < q; b++)
+        for (int cc = 0; cc < q; cc++) {
+          const double w3 = w[a] * w[b] * w[cc];
+          A.hw3[(a * q + b) * q + cc] = A.hh * w3;
+          A.lw3[(a * q + b) * q + cc] = d.lat_bump * (A.detw0 * w3);
+        }
     return A;
   }
 
@@ -925,7 +631,8 @@ struct Structured : Backend {
   int launch_xmarch_t(const SArgs& A) {
     constexpr int CY = Tile<P>::CY, CZ = Tile<P>::CZ;
     constexpr int PL = (P * CY + 1) * (P * CZ + 1);
-    const size_t smem = (size_t)((P + 1) * PL + (LAT ? 2 : 1) * P * PL) * sizeof(double);
+    constexpr int EW = P * (P + 1) * (P + 1);
+    const size_t smem = (size_t)((2 * P + 1) * PL + (LAT ? 2 : 1) * EW * CY * CZ) * sizeof(double);
     auto kern = k_xmarch<P, CY, CZ, LAT, RCF>;
     static bool attr = false;
     if (!attr) {
@@ -957,10 +664,14 @@ struct Structured : Backend {
     ST_TRY(rc);
     const int nxs = (m.nx + Lx - 1) / Lx - 1, nys = (m.ny + cy - 1) / cy - 1,
               nzs = (m.nz + cz - 1) / cz - 1;
-    const int64_t tot = (int64_t)nxs * NY * NZ + (int64_t)nys * NX * NZ + (int64_t)nzs * NX * NY;
-    if (tot > 0) {
-      int blocks = (int)std::min<int64_t>((tot + kThreads - 1) / kThreads, 148 * 16);
-      k_seams<<<blocks, kThreads, 0, c->stream>>>(A, p, cy, cz, nxs, nys, nzs, lat ? 1 : 0);
+    // one launch over all seam planes (x, then y, then z families)
+    const int bx = (int)(((int64_t)NY * NZ + kThreads - 1) / kThreads);
+    const int by = (int)(((int64_t)NX * NZ + kThreads - 1) / kThreads);
+    const int bz = (int)(((int64_t)NX * NY + kThreads - 1) / kThreads);
+    const int64_t blocks = (int64_t)bx * nxs + (int64_t)by * nys + (int64_t)bz * nzs;
+    if (blocks > 0) {
+      k_seams<<<(unsigned)blocks, kThreads, 0, c->stream>>>(A, p, cy, cz, nxs, nys, nzs, bx, by,
+                                                            bz, lat ? 1 : 0);
       ST_TRY(launched());
     }
     return ST_OK;
@@ -1075,9 +786,11 @@ struct Structured : Backend {
   }
 
   double bytes_per_dof() const override {
-    // T_n read + T_{n+1} write + C^-1 read, + r_c traffic
-    // when the history is a stored field
-    double b = 24.0;
+    // T_n read + T_{n+1} write.  SURVEY §8d counts 24 B with a C^-1 read;
+    // this kernel evaluates C^-1 from the tensor-product lumped mass and
+    // reads no per-DoF diagonal, so 16 B is what it must move.  Plus the
+    // r_c traffic when the history is a stored field.
+    double b = 16.0;
     if (!c->rc_uniform) {
       const double q = (double)(p + 1) * (p + 1) * (p + 1);
       b += 16.0 * q * ((double)m.nx * m.ny * m.nz) / (double)nv;

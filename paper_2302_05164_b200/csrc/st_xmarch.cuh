@@ -1,0 +1,234 @@
+// k_xmarch: the explicit-step / rhs hot kernel of the structured backend
+// (included by st_structured.cu after the basis tables).  See the header
+// of st_structured.cu for the overall scheme.
+#pragma once
+
+struct CellFlags {
+  bool diffusion, faces, source, frozen;
+};
+
+__device__ __forceinline__ void cp_async8(void* smem, const void* gmem) {
+  unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(s), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_wait() {
+  asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory");
+}
+
+template <int P>
+__device__ __forceinline__ double anchor(const SArgs& A, int axis, int cell) {
+  // anchor = lattice * h when the box origin is on the lattice (one
+  // rounding, like the reference's anchor * h_fine, operators.py:105-112)
+  if (A.use_lat) {
+    const long long l = axis == 0 ? A.lx : (axis == 1 ? A.ly : A.lz);
+    return (double)(cell + l) * A.h;
+  }
+  return (axis == 0 ? A.ox : (axis == 1 ? A.oy : A.oz)) + (double)cell * A.h;
+}
+
+// 1D projection of the separable Gaussian slab source of one beam
+// (physics.py:154-171): exp(-2 r^2/R^2) = exp(-2 dx^2/R^2) exp(-2 dy^2/R^2),
+// so V^T (x) V^T (x) V^T of the point values is an outer product of three
+// 1D projections s_d[a] = sum_q V[a][q] W[q] f_d(q).
+template <int P>
+__device__ __forceinline__ void source_factors(const SArgs& A, const DevBeam& b, double ax,
+                                               double ay, double az, double* sx, double* sy,
+                                               double* sz) {
+  constexpr int Q = P + 1;
+  const DevParams& PP = A.P;
+  double fx[Q], fy[Q], fz[Q];
+#pragma unroll
+  for (int q = 0; q < Q; q++) {
+    const double dx = (ax + Basis<P>::U(q) * A.h) - b.x;
+    const double dy = (ay + Basis<P>::U(q) * A.h) - b.y;
+    const double z = az + Basis<P>::U(q) * A.h;
+    fx[q] = exp((-2.0 * (dx * dx)) / PP.R2) * Basis<P>::W(q);
+    fy[q] = exp((-2.0 * (dy * dy)) / PP.R2) * Basis<P>::W(q);
+    fz[q] = (z >= b.z_top - PP.h_powder && z <= b.z_top) ? Basis<P>::W(q) : 0.0;
+  }
+#pragma unroll
+  for (int a = 0; a < Q; a++) {
+    double x = 0.0, y = 0.0, zz = 0.0;
+#pragma unroll
+    for (int q = 0; q < Q; q++) {
+      x = fma(Basis<P>::V(a, q), fx[q], x);
+      y = fma(Basis<P>::V(a, q), fy[q], y);
+      zz = fma(Basis<P>::V(a, q), fz[q], zz);
+    }
+    sx[a] = x;
+    sy[a] = y;
+    sz[a] = zz;
+  }
+}
+
+// Element vector of one cell, degree P (operators.py:247-316 generalised):
+//   t in : node values (a x b x c, z fastest)
+//   G out: element vector
+//   t out: with LATENT and has_lat, the projected apparent-capacity
+//          increment rho L/dT_lat over the Gauss points in the interval
+template <int P, bool RCF, bool LATENT>
+__device__ __forceinline__ void cell_element(const SArgs& A, const CellFlags& F, int i, int j,
+                                             int k, int64_t cell, double* t, double* G,
+                                             bool& has_lat) {
+  constexpr int Q = P + 1;
+  constexpr int Q3 = Q * Q * Q;
+  using B = Basis<P>;
+  const DevParams& PP = A.P;
+  const bool top = F.faces && A.top_faces && (k == A.nz - 1);
+  double tf[Q * Q];
+#pragma unroll
+  for (int a = 0; a < Q; a++)
+#pragma unroll
+    for (int b = 0; b < Q; b++) tf[a * Q + b] = t[(a * Q + b) * Q + P];
+  interp3<P>(t);  // T at the Gauss points
+#pragma unroll
+  for (int q = 0; q < Q3; q++) G[q] = 0.0;
+  if (F.diffusion) {
+#pragma unroll
+    for (int qa = 0; qa < Q; qa++)
+#pragma unroll
+      for (int qb = 0; qb < Q; qb++)
+#pragma unroll
+        for (int qc = 0; qc < Q; qc++) {
+          const int q = (qa * Q + qb) * Q + qc;
+          // reference-coordinate gradient by Gauss-point collocation
+          double gx = B::Dq(0, qa) * t[(0 * Q + qb) * Q + qc];
+          double gy = B::Dq(0, qb) * t[(qa * Q + 0) * Q + qc];
+          double gz = B::Dq(0, qc) * t[(qa * Q + qb) * Q + 0];
+#pragma unroll
+          for (int m = 1; m < Q; m++) {
+            gx = fma(B::Dq(m, qa), t[(m * Q + qb) * Q + qc], gx);
+            gy = fma(B::Dq(m, qb), t[(qa * Q + m) * Q + qc], gy);
+            gz = fma(B::Dq(m, qc), t[(qa * Q + qb) * Q + m], gz);
+          }
+          double kq;
+          if (F.frozen) {
+            kq = A.frozen_k;
+          } else {
+            // g(T) (material.py:46-57) as a clamped ramp
+            const double g = fmin(fmax(fma(t[q], PP.inv_dT_l, A.glo), 0.0), 1.0);
+            if (RCF) {
+              double r = A.rc[cell * Q3 + q];
+              if (A.pending) {
+                r = fmax(r, g);
+                A.rc[cell * Q3 + q] = r;
+              }
+              kq = conductivity(PP, g, r);
+            } else {
+              kq = fma(g, A.kB, A.kA);
+            }
+          }
+          // -(w detJ (2/h)^2) k = -(h/2) W3 k ;  f_diff = sum_d Dq_d^T (c grad_d)
+          const double c = -A.hw3[q] * kq;
+          const double fx = c * gx, fy = c * gy, fz = c * gz;
+#pragma unroll
+          for (int m = 0; m < Q; m++) {
+            G[(m * Q + qb) * Q + qc] = fma(B::Dq(m, qa), fx, G[(m * Q + qb) * Q + qc]);
+            G[(qa * Q + m) * Q + qc] = fma(B::Dq(m, qb), fy, G[(qa * Q + m) * Q + qc]);
+            G[(qa * Q + qb) * Q + m] = fma(B::Dq(m, qc), fz, G[(qa * Q + qb) * Q + m]);
+          }
+        }
+  }
+  project3<P>(G);
+  if (LATENT) {
+    has_lat = false;
+#pragma unroll
+    for (int q = 0; q < Q3; q++) {
+      const bool in = fabs(t[q] - A.lat_mid) < A.lat_half;
+      has_lat |= in;
+      t[q] = in ? A.lw3[q] : 0.0;
+    }
+    if (has_lat) project3<P>(t);
+  }
+  if (F.source) {
+    const double ax = anchor<P>(A, 0, i), ay = anchor<P>(A, 1, j), az = anchor<P>(A, 2, k);
+#pragma unroll 1
+    for (int b = 0; b < A.nb; b++) {
+      const DevBeam bm = A.beams[b];
+      if (!beam_hits_cell(PP, bm, ax, ay, az, A.h)) continue;
+      double sx[Q], sy[Q], sz[Q];
+      source_factors<P>(A, bm, ax, ay, az, sx, sy, sz);
+      const double coef = bm.peak * A.detw0;
+#pragma unroll
+      for (int a = 0; a < Q; a++)
+#pragma unroll
+        for (int bb = 0; bb < Q; bb++) {
+          const double sab = coef * sx[a] * sy[bb];
+#pragma unroll
+          for (int c = 0; c < Q; c++) G[(a * Q + bb) * Q + c] = fma(sab, sz[c], G[(a * Q + bb) * Q + c]);
+        }
+    }
+  }
+  if (top) {
+    // +z facet quadrature (operators.py:275-290), full facets
+#pragma unroll
+    for (int a = 0; a < Q; a++) {
+      double in[Q];
+#pragma unroll
+      for (int b = 0; b < Q; b++) in[b] = tf[a * Q + b];
+#pragma unroll
+      for (int qb = 0; qb < Q; qb++) {
+        double acc = B::V(0, qb) * in[0];
+#pragma unroll
+        for (int b = 1; b < Q; b++) acc = fma(B::V(b, qb), in[b], acc);
+        tf[a * Q + qb] = acc;
+      }
+    }
+    double fq[Q * Q];
+#pragma unroll
+    for (int qb = 0; qb < Q; qb++) {
+      double in[Q];
+#pragma unroll
+      for (int a = 0; a < Q; a++) in[a] = tf[a * Q + qb];
+#pragma unroll
+      for (int qa = 0; qa < Q; qa++) {
+        double acc = B::V(0, qa) * in[0];
+#pragma unroll
+        for (int a = 1; a < Q; a++) acc = fma(B::V(a, qa), in[a], acc);
+        fq[qa * Q + qb] = acc;
+      }
+    }
+    const double area0 = A.hh * A.hh;
+#pragma unroll 1
+    for (int q = 0; q < Q * Q; q++) {
+      const int qa = q / Q, qb = q - (q / Q) * Q;
+      fq[q] = surface_flux(PP, fq[q]) * (-(area0 * (sW[P - 1][qa] * sW[P - 1][qb])));
+    }
+#pragma unroll
+    for (int qb = 0; qb < Q; qb++) {
+      double in[Q];
+#pragma unroll
+      for (int qa = 0; qa < Q; qa++) in[qa] = fq[qa * Q + qb];
+#pragma unroll
+      for (int a = 0; a < Q; a++) {
+        double acc = B::V(a, 0) * in[0];
+#pragma unroll
+        for (int qa = 1; qa < Q; qa++) acc = fma(B::V(a, qa), in[qa], acc);
+        tf[a * Q + qb] = acc;
+      }
+    }
+#pragma unroll
+    for (int a = 0; a < Q; a++)
+#pragma unroll
+      for (int b = 0; b < Q; b++) {
+        double acc = B::V(b, 0) * tf[a * Q + 0];
+#pragma unroll
+        for (int qb = 1; qb < Q; qb++) acc = fma(B::V(b, qb), tf[a * Q + qb], acc);
+        G[(a * Q + b) * Q + P] += acc;
+      }
+  }
+}
+
+// node update with its complete f (operators.py:359-368); with the latent
+// extension the lumped capacity is C_const + dC(T)
+__device__ __forceinline__ double finalize_node(const SArgs& A, double ci, int K, double T,
+                                                double f, double dc, bool latent) {
+  if (A.mode == 1) return f;
+  if (latent && dc != 0.0) ci = 1.0 / (1.0 / ci + dc);
+  double o = T + A.dt * (ci * f);
+  if (A.dir_bottom && K == 0) o = A.P.T_inf;
+  return o;
+}
+#include "st_xmarch_kernel.cuh"

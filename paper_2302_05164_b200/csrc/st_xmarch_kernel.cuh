@@ -1,0 +1,218 @@
+// k_xmarch kernel body (included from st_xmarch.cuh).
+//
+// One CTA = CY x CZ cells of a (y, z) tile, marching over Lx cell layers
+// in x; one thread per cell.  Per layer:
+//   prefetch (cp.async) the next layer's P node planes of T,
+//   evaluate the cell (cell_element, all in registers),
+//   store the element planes a < P in an entry-major buffer E[q][cell]
+//   (conflict-free), one barrier, then every thread finalises the nodes
+//   its cell owns (local b, c < P; plus the b = P / c = P faces on the
+//   tile's high edges): the <= 4 contributions of the (y, z) neighbour
+//   cells are summed in a fixed order (deterministic), the update is
+//   applied and T' written, or the partial sum of a tile-seam node is
+//   sent to the seam buffer.
+// C^-1 is the tensor-product lumped mass (inv_mass1), so the only HBM
+// streams are T (read once) and T' (written once).  The apparent-capacity
+// increments of the latent extension use a second element buffer Ec,
+// gathered only when some cell of the CTA had a Gauss point in the latent
+// interval in this or the previous layer.
+#pragma once
+
+template <int P>
+struct MinBlocks {
+  static constexpr int v = P == 1 ? 2 : (P == 2 ? 3 : 1);
+};
+
+template <int P, int CY, int CZ, bool LATENT, bool RCF>
+__global__ void __launch_bounds__(CY* CZ, MinBlocks<P>::v) k_xmarch(SArgs A) {
+  constexpr int Q = P + 1;
+  constexpr int Q3 = Q * Q * Q;
+  constexpr int NT = CY * CZ;
+  constexpr int NW = NT / 32;
+  constexpr int NYT = P * CY + 1, NZT = P * CZ + 1, PL = NYT * NZT;
+  constexpr int NR = 2 * P + 1;  // ring: current layer (P+1 planes) + next layer (P)
+  constexpr int EW = P * Q * Q;  // stored element entries per cell (planes a < P)
+  static_assert(NT % 32 == 0, "tile must be whole warps");
+  extern __shared__ double sm[];
+  double* Tr = sm;            // NR planes of T
+  double* E = sm + NR * PL;   // E[q * NT + cell]
+  double* Ec = E + EW * NT;   // latent increments (LATENT)
+  __shared__ int lat_any[2];  // latent increments in the current / previous layer
+  const int tid = threadIdx.x;
+  const int lane = tid & 31, warp = tid >> 5;
+  const int jl = tid / CZ, kl = tid - (tid / CZ) * CZ;
+  const int j0 = blockIdx.x * CY, k0 = blockIdx.y * CZ, i0 = blockIdx.z * A.Lx;
+  if (i0 >= A.nx) return;
+  const int i1 = min(i0 + A.Lx, A.nx);
+  const int j = j0 + jl, k = k0 + kl;
+  const bool live = j < A.ny && k < A.nz;
+  const bool hiY = live && (jl == CY - 1 || j == A.ny - 1);
+  const bool hiZ = live && (kl == CZ - 1 || k == A.nz - 1);
+  const int Jn = min(P * CY, P * (A.ny - j0)) + 1;
+  const int Kn = min(P * CZ, P * (A.nz - k0)) + 1;
+  const bool step = A.mode == 0;
+  // tile-edge node planes are seams unless they are the domain boundary
+  const bool sy_lo = jl == 0 && j0 > 0, sy_hi = jl == CY - 1 && j0 + CY < A.ny;
+  const bool sz_lo = kl == 0 && k0 > 0, sz_hi = kl == CZ - 1 && k0 + CZ < A.nz;
+  const CellFlags F{(A.flags & ST_RHS_DIFFUSION) != 0, (A.flags & ST_RHS_FACES) != 0,
+                    (A.flags & ST_RHS_SOURCE) != 0 && A.nb > 0, (A.flags & ST_RHS_FROZEN_K) != 0};
+  const int64_t plane_stride = (int64_t)A.NY * A.NZ;
+  const int64_t tile0 = (int64_t)P * j0 * A.NZ + (int64_t)P * k0;
+  // this thread's node origin within a plane (global offset and smem slot)
+  const int64_t my0 = (int64_t)P * j * A.NZ + (int64_t)P * k;
+  const int ms0 = P * jl * NZT + P * kl;
+  if (tid < 2) lat_any[tid] = 0;
+
+  // warp w stages rows jj = w, w + NW, ... of plane I (lanes along z)
+  auto load_plane = [&](int I) {
+    const double* srcT = A.T + (int64_t)I * plane_stride + tile0;
+    double* dT = Tr + (I % NR) * PL;
+#pragma unroll 1
+    for (int jj = warp; jj < Jn; jj += NW) {
+#pragma unroll
+      for (int kk = lane; kk < NZT; kk += 32)
+        if (kk < Kn) cp_async8(dT + jj * NZT + kk, srcT + (int64_t)jj * A.NZ + kk);
+    }
+  };
+
+  double carry[Q * Q], carryC[LATENT ? Q * Q : 1];
+#pragma unroll
+  for (int q = 0; q < Q * Q; q++) carry[q] = 0.0;
+  if (LATENT)
+#pragma unroll
+    for (int q = 0; q < Q * Q; q++) carryC[q] = 0.0;
+  double amax = 0.0, smax = -INFINITY;
+  bool bad = false;
+
+  // node (b, c) of plane I owned by this thread (element plane a);
+  // b, c are compile-time after unrolling
+  auto finalize_node3 = [&](int I, int a, int b, int c, bool xs, bool latn, double imIs) {
+    const double* pe = E + a * Q * Q * NT + tid;
+    // own cell, then the y-, z- and yz-neighbour below (fixed order)
+    double f = pe[(b * Q + c) * NT];
+    if (b == 0 && jl > 0) f += pe[(P * Q + c) * NT - CZ];
+    if (c == 0 && kl > 0) f += pe[(b * Q + P) * NT - 1];
+    if (b == 0 && c == 0 && jl > 0 && kl > 0) f += pe[(P * Q + P) * NT - CZ - 1];
+    const int64_t idx = (int64_t)I * plane_stride + my0 + (int64_t)b * A.NZ + c;
+    const bool seam = xs || (b == 0 && sy_lo) || (b == P && sy_hi) || (c == 0 && sz_lo) ||
+                      (c == P && sz_hi);
+    double dc = 0.0;
+    if (seam) {
+      atomicAdd(A.fseam + idx, f);
+    }
+    if (LATENT && latn) {
+        const double* pc = Ec + a * Q * Q * NT + tid;
+        dc = pc[(b * Q + c) * NT];
+        if (b == 0 && jl > 0) dc += pc[(P * Q + c) * NT - CZ];
+        if (c == 0 && kl > 0) dc += pc[(b * Q + P) * NT - 1];
+        if (b == 0 && c == 0 && jl > 0 && kl > 0) dc += pc[(P * Q + P) * NT - CZ - 1];
+      }
+    if (seam) {
+      if (LATENT && dc != 0.0) atomicAdd(A.cseam + idx, dc);
+    } else {
+      const int K = P * k + c;
+      const double ci = inv_mass1<P>(A, K, A.NZ) * (inv_mass1<P>(A, P * j + b, A.NY) * imIs);
+      const double o =
+          finalize_node(A, ci, K, Tr[(I % NR) * PL + ms0 + b * NZT + c], f, dc, LATENT);
+      A.out[idx] = o;
+      amax = fmax(amax, fabs(o));
+      smax = fmax(smax, o);
+      bad |= (o != o);
+    }
+  };
+
+  // every node of plane I owned by this thread (element plane a)
+  auto finalize_owned = [&](int I, int a, bool xs, bool latn) {
+    if (!live) return;
+    const double imIs = inv_mass1<P>(A, I, A.NX) * A.inv_rcdw;
+#pragma unroll
+    for (int b = 0; b < P; b++)
+#pragma unroll
+      for (int c = 0; c < P; c++) finalize_node3(I, a, b, c, xs, latn, imIs);
+    if (hiZ)
+#pragma unroll
+      for (int b = 0; b < P; b++) finalize_node3(I, a, b, P, xs, latn, imIs);
+    if (hiY) {
+#pragma unroll
+      for (int c = 0; c < P; c++) finalize_node3(I, a, P, c, xs, latn, imIs);
+      if (hiZ) finalize_node3(I, a, P, P, xs, latn, imIs);
+    }
+  };
+
+  // prologue: the first layer's P+1 planes
+  load_plane(P * i0);
+#pragma unroll 1
+  for (int a = 1; a <= P; a++) load_plane(P * i0 + a);
+  cp_commit();
+
+#pragma unroll 1
+  for (int i = i0; i < i1; i++) {
+    if (i + 1 < i1) {
+#pragma unroll 1
+      for (int a = 1; a <= P; a++) load_plane(P * (i + 1) + a);
+    }
+    cp_commit();
+    cp_wait<1>();
+    __syncthreads();
+    if (live) {
+      double t[Q3], G[Q3];
+      bool lat = false;
+#pragma unroll
+      for (int a = 0; a < Q; a++) {
+        const double* tp = Tr + ((P * i + a) % NR) * PL + ms0;
+#pragma unroll
+        for (int b = 0; b < Q; b++)
+#pragma unroll
+          for (int c = 0; c < Q; c++) t[(a * Q + b) * Q + c] = tp[b * NZT + c];
+      }
+      const int64_t cell = ((int64_t)i * A.ny + j) * A.nz + k;
+      cell_element<P, RCF, LATENT>(A, F, i, j, k, cell, t, G, lat);
+      if (LATENT) {
+        if (lat) {
+          lat_any[i & 1] = 1;
+#pragma unroll
+          for (int q = 0; q < Q * Q; q++) {
+            t[q] += carryC[q];
+            carryC[q] = t[P * Q * Q + q];
+          }
+        } else {
+#pragma unroll
+          for (int q = 0; q < Q * Q; q++) {
+            t[q] = carryC[q];
+            carryC[q] = 0.0;
+          }
+#pragma unroll
+          for (int q = Q * Q; q < Q3; q++) t[q] = 0.0;
+        }
+#pragma unroll
+        for (int q = 0; q < EW; q++) Ec[q * NT + tid] = t[q];
+      }
+      // x face shared with the previous layer: add the carry, keep the new one
+#pragma unroll
+      for (int q = 0; q < Q * Q; q++) {
+        G[q] += carry[q];
+        carry[q] = G[P * Q * Q + q];
+      }
+#pragma unroll
+      for (int q = 0; q < EW; q++) E[q * NT + tid] = G[q];
+    }
+    __syncthreads();
+    const bool latn = LATENT && (lat_any[0] | lat_any[1]);
+#pragma unroll 1
+    for (int a = 0; a < P; a++) finalize_owned(P * i + a, a, a == 0 && i == i0 && i0 > 0, latn);
+    __syncthreads();
+    if (tid == 0) lat_any[(i + 1) & 1] = 0;  // slot reused by the next layer
+  }
+  cp_wait<0>();
+  // last node plane of the chunk: the carried x face (as element plane 0)
+  if (live) {
+#pragma unroll
+    for (int q = 0; q < Q * Q; q++) E[q * NT + tid] = carry[q];
+    if (LATENT)
+#pragma unroll
+      for (int q = 0; q < Q * Q; q++) Ec[q * NT + tid] = carryC[q];
+  }
+  __syncthreads();
+  finalize_owned(P * i1, 0, i1 < A.nx, LATENT && (lat_any[0] | lat_any[1]));
+  block_max2(bad ? (double)NAN : amax, smax, A.red);
+}

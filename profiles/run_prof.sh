@@ -1,0 +1,11 @@
+#!/bin/bash
+# ncu capture of the explicit-step kernels (run under gpurun, 1 GPU).
+# usage: profiles/run_prof.sh <tag> [bench args...]
+set -e
+tag=$1; shift
+cmd="python bench.py --steps 3 --warmup 3 --sweep 0 --no-cpu-baseline $*"
+$cmd > gpurun_out/plain_$tag.log 2>&1
+ncu --metrics gpu__time_duration.sum --clock-control none --csv \
+    --log-file gpurun_out/launches_$tag.csv $cmd > gpurun_out/ncu_launch_$tag.log 2>&1
+ncu --set full --clock-control none --import-source on -k regex:k_xmarch -s 4 -c 1 \
+    -o gpurun_out/prof_$tag -f $cmd > gpurun_out/ncu_full_$tag.log 2>&1
