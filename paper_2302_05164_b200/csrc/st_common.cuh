@@ -120,8 +120,11 @@ __device__ __forceinline__ void block_max2(double absval, double val,
       ka = s_a[i] > ka ? s_a[i] : ka;
       ks = s_s[i] > ks ? s_s[i] : ks;
     }
-    atomicMax(slot, ka);
-    atomicMax(slot + 1, ks);
+    // same-address atomics serialise in L2: only blocks that raise the
+    // running maximum issue one (the slot only ever grows)
+    const volatile unsigned long long* vs = slot;
+    if (ka > vs[0]) atomicMax(slot, ka);
+    if (ks > vs[1]) atomicMax(slot + 1, ks);
   }
 }
 

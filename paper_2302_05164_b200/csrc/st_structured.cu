@@ -141,60 +141,72 @@ __device__ __forceinline__ void project3(double* t) {
 
 #include "st_xmarch.cuh"
 
-// finalise the seam nodes (x planes, then y planes not on an x seam, then
-// z planes on neither)
-// One block row (blockIdx.y) per seam plane; 32-bit in-plane indexing.
+// inverse 1D lumped mass, runtime degree (seam kernel)
+__device__ __forceinline__ double inv_mass1_rt(const SArgs& A, int P, int L, int N) {
+  const int a = L % P;
+  if (a != 0) return A.imr[a];
+  return (L == 0 || L == N - 1) ? A.imv_end : A.imv_int;
+}
+
+// Finalise the seam nodes: x planes, then y planes not on an x seam, then
+// z planes on neither.  A flat "virtual block" index (one block row per
+// plane, 32-bit in-plane indexing) is walked grid-stride by a small grid.
 __global__ void k_seams(SArgs A, int P, int CY, int CZ, int nxs, int nys, int nzs, int bx, int by,
                         int bz, int latent) {
   double amax = 0.0, smax = -INFINITY;
   bool bad = false;
-  // flat block index -> (family plane, block within the plane)
-  int b = blockIdx.x, pl;
-  if (b < bx * nxs) {
-    pl = b / bx;
-    b -= pl * bx;
-  } else if ((b -= bx * nxs) < by * nys) {
-    pl = b / by;
-    b -= pl * by;
-    pl += nxs;
-  } else {
-    b -= by * nys;
-    pl = b / bz;
-    b -= pl * bz;
-    pl += nxs + nys;
-  }
-  const int t = b * blockDim.x + threadIdx.x;
+  const int nvb = bx * nxs + by * nys + bz * nzs;
   const int sx = P * A.Lx, sy = P * CY;
-  int I, J, K;
-  bool mine;
-  if (pl < nxs) {  // x plane: (J, K) contiguous
-    I = sx * (pl + 1);
-    J = t / A.NZ;
-    K = t - J * A.NZ;
-    mine = J < A.NY;
-  } else if (pl < nxs + nys) {  // y plane: rows of K for each I
-    J = sy * (pl - nxs + 1);
-    I = t / A.NZ;
-    K = t - I * A.NZ;
-    mine = I < A.NX && !(I > 0 && I < A.NX - 1 && (I % sx) == 0);
-  } else {  // z plane: strided
-    K = P * CZ * (pl - nxs - nys + 1);
-    I = t / A.NY;
-    J = t - I * A.NY;
-    mine = I < A.NX && !(I > 0 && I < A.NX - 1 && (I % sx) == 0) &&
-           !(J > 0 && J < A.NY - 1 && (J % sy) == 0);
-  }
-  if (mine) {
+#pragma unroll 1
+  for (int vb = blockIdx.x; vb < nvb; vb += gridDim.x) {
+    int b = vb, pl;
+    if (b < bx * nxs) {
+      pl = b / bx;
+      b -= pl * bx;
+    } else if ((b -= bx * nxs) < by * nys) {
+      pl = b / by;
+      b -= pl * by;
+      pl += nxs;
+    } else {
+      b -= by * nys;
+      pl = b / bz;
+      b -= pl * bz;
+      pl += nxs + nys;
+    }
+    const int t = b * blockDim.x + threadIdx.x;
+    int I, J, K;
+    bool mine;
+    if (pl < nxs) {  // x plane: (J, K) contiguous
+      I = sx * (pl + 1);
+      J = t / A.NZ;
+      K = t - J * A.NZ;
+      mine = J < A.NY;
+    } else if (pl < nxs + nys) {  // y plane: rows of K for each I
+      J = sy * (pl - nxs + 1);
+      I = t / A.NZ;
+      K = t - I * A.NZ;
+      mine = I < A.NX && !(I > 0 && I < A.NX - 1 && (I % sx) == 0);
+    } else {  // z plane: strided
+      K = P * CZ * (pl - nxs - nys + 1);
+      I = t / A.NY;
+      J = t - I * A.NY;
+      mine = I < A.NX && !(I > 0 && I < A.NX - 1 && (I % sx) == 0) &&
+             !(J > 0 && J < A.NY - 1 && (J % sy) == 0);
+    }
+    if (!mine) continue;
     const int64_t idx = ((int64_t)I * A.NY + J) * A.NZ + K;
     const double f = A.fseam[idx];
-    A.fseam[idx] = 0.0;
+    const double T = A.T[idx];
     double dc = 0.0;
     if (latent) {
       dc = A.cseam[idx];
       A.cseam[idx] = 0.0;
     }
-    const double o =
-        finalize_node(A, A.mode == 0 ? A.cinv[idx] : 0.0, K, A.T[idx], f, dc, latent != 0);
+    A.fseam[idx] = 0.0;
+    // the same C^-1 as the hot kernel (tensor-product lumped mass)
+    const double ci = inv_mass1_rt(A, P, K, A.NZ) *
+                      (inv_mass1_rt(A, P, J, A.NY) * (inv_mass1_rt(A, P, I, A.NX) * A.inv_rcdw));
+    const double o = finalize_node(A, ci, K, T, f, dc, latent != 0);
     A.out[idx] = o;
     amax = fmax(amax, fabs(o));
     smax = fmax(smax, o);
@@ -627,9 +639,8 @@ struct Structured : Backend {
     return A;
   }
 
-  template <int P, bool LAT, bool RCF>
+  template <int P, int CY, int CZ, bool LAT, bool RCF>
   int launch_xmarch_t(const SArgs& A) {
-    constexpr int CY = Tile<P>::CY, CZ = Tile<P>::CZ;
     constexpr int PL = (P * CY + 1) * (P * CZ + 1);
     constexpr int EW = P * (P + 1) * (P + 1);
     const size_t smem = (size_t)((2 * P + 1) * PL + (LAT ? 2 : 1) * EW * CY * CZ) * sizeof(double);
@@ -644,10 +655,18 @@ struct Structured : Backend {
     return launched();
   }
 
+  template <int P, int CY, int CZ>
+  int launch_tile(const SArgs& A, bool lat, bool rcf) {
+    if (lat)
+      return rcf ? launch_xmarch_t<P, CY, CZ, true, true>(A)
+                 : launch_xmarch_t<P, CY, CZ, true, false>(A);
+    return rcf ? launch_xmarch_t<P, CY, CZ, false, true>(A)
+               : launch_xmarch_t<P, CY, CZ, false, false>(A);
+  }
+
   template <int P>
   int launch_xmarch_p(const SArgs& A, bool lat, bool rcf) {
-    if (lat) return rcf ? launch_xmarch_t<P, true, true>(A) : launch_xmarch_t<P, true, false>(A);
-    return rcf ? launch_xmarch_t<P, false, true>(A) : launch_xmarch_t<P, false, false>(A);
+    return launch_tile<P, Tile<P>::CY, Tile<P>::CZ>(A, lat, rcf);
   }
 
   int xmarch(SArgs& A, bool rcf) {
@@ -670,8 +689,9 @@ struct Structured : Backend {
     const int bz = (int)(((int64_t)NX * NY + kThreads - 1) / kThreads);
     const int64_t blocks = (int64_t)bx * nxs + (int64_t)by * nys + (int64_t)bz * nzs;
     if (blocks > 0) {
-      k_seams<<<(unsigned)blocks, kThreads, 0, c->stream>>>(A, p, cy, cz, nxs, nys, nzs, bx, by,
-                                                            bz, lat ? 1 : 0);
+      const unsigned grid = (unsigned)std::min<int64_t>(blocks, 4 * 148);
+      k_seams<<<grid, kThreads, 0, c->stream>>>(A, p, cy, cz, nxs, nys, nzs, bx, by, bz,
+                                                lat ? 1 : 0);
       ST_TRY(launched());
     }
     return ST_OK;
