@@ -107,6 +107,11 @@ typedef struct st_structured_mesh {
   int32_t nx, ny, nz, degree;
   double h, x0, y0, z0;
   int32_t dirichlet_bottom, top_faces;
+  /* x-slab of a larger box (multi-GPU): global index of local node plane
+   * 0 and the global node-plane count (gNX = 0: not a slab); iface_lo /
+   * iface_hi mark local node planes 0 / NX-1 as rank interfaces whose
+   * partial sums are exchanged between st_explicit_step_begin/_end. */
+  int32_t gx0, gNX, iface_lo, iface_hi;
 } st_structured_mesh;
 
 /* evaluate_rhs term flags (operators.py:247 diffusion/faces/source). */
@@ -198,6 +203,22 @@ int st_finish_implicit_step(st_ctx* ctx);
 int st_pcg(st_ctx* ctx, const double* T_lin, const double* rc, double dt,
            const double* b, double tol, int max_iter, int precond, double* x,
            int* iters, int* converged);
+
+/* --- multi-GPU slabs (structured backend) ------------------------------ */
+/* One explicit step split around the rank-interface exchange: _begin runs
+ * the cell sweep on the resident state leaving the interface planes as
+ * partial sums; st_iface_partials gives the device pointers of this
+ * rank's partial f (and latent dC, or NULL) on local plane 0 (side 0) or
+ * NX-1 (side 1), NY*NZ doubles each; _end adds the neighbours' partials
+ * (device pointers, NULL where there is no neighbour) in the fixed order
+ * low rank + high rank, finalises all seams and commits the step. */
+int st_explicit_step_begin(st_ctx* ctx, double dt, const st_beam* beams, int n_beams);
+int st_iface_partials(st_ctx* ctx, int side, double** f_plane, double** c_plane,
+                      int64_t* n);
+int st_explicit_step_end(st_ctx* ctx, const double* recv_lo_f, const double* recv_lo_c,
+                         const double* recv_hi_f, const double* recv_hi_c);
+/* max |T| and max T over the steps committed since the last call */
+int st_step_maxima(st_ctx* ctx, double* absmax, double* tmax);
 
 /* --- measurement ------------------------------------------------------ */
 /* When enabled, the step loop brackets its dominant kernel with CUDA

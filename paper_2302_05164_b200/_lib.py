@@ -69,7 +69,9 @@ class StStructuredMesh(ctypes.Structure):
                 ("nz", ctypes.c_int32), ("degree", ctypes.c_int32),
                 ("h", ctypes.c_double), ("x0", ctypes.c_double),
                 ("y0", ctypes.c_double), ("z0", ctypes.c_double),
-                ("dirichlet_bottom", ctypes.c_int32), ("top_faces", ctypes.c_int32)]
+                ("dirichlet_bottom", ctypes.c_int32), ("top_faces", ctypes.c_int32),
+                ("gx0", ctypes.c_int32), ("gNX", ctypes.c_int32),
+                ("iface_lo", ctypes.c_int32), ("iface_hi", ctypes.c_int32)]
 
 
 # (name, restype, argtypes) for every symbol of include/scantherm_b200.h
@@ -120,6 +122,12 @@ SIGNATURES = [
     ("st_profile_read", ctypes.c_int,
      [_VP, _dp, _i64p, ctypes.c_char_p, ctypes.c_int]),
     ("st_algorithmic_bytes_per_dof", ctypes.c_double, [_VP]),
+    ("st_explicit_step_begin", ctypes.c_int,
+     [_VP, ctypes.c_double, ctypes.POINTER(StBeam), ctypes.c_int]),
+    ("st_iface_partials", ctypes.c_int,
+     [_VP, ctypes.c_int, ctypes.POINTER(_dp), ctypes.POINTER(_dp), _i64p]),
+    ("st_explicit_step_end", ctypes.c_int, [_VP, _VP, _VP, _VP, _VP]),
+    ("st_step_maxima", ctypes.c_int, [_VP, _dp, _dp]),
     ("st_bench_explicit", ctypes.c_int,
      [_VP, ctypes.c_int, _dp, ctypes.POINTER(StBeam), ctypes.c_int, ctypes.c_int64,
       ctypes.POINTER(ctypes.c_float), ctypes.POINTER(ctypes.c_float)]),

@@ -158,6 +158,7 @@ static int ctx_common_init(Ctx* c, int device, const st_params* params) {
   c->params = *params;
   c->dp = make_dev_params(*params);
   ST_TRY(c->red.alloc(kRedBlocks + 64 + 2 * 1024));
+  ST_CUDA(cudaMemsetAsync(c->red.p, 0, c->red.n * sizeof(double), c->stream));
   ST_CUDA(cudaMallocHost(&c->pinned, 4096 * sizeof(double)));
   ST_CUDA(cudaEventCreate(&c->ev0));
   ST_CUDA(cudaEventCreate(&c->ev1));
@@ -757,6 +758,54 @@ int st_profile_read(st_ctx* ctx, double* main_ms, int64_t* main_launches, char* 
 double st_algorithmic_bytes_per_dof(const st_ctx* ctx) {
   if (!ctx || !ctx->impl.be) return 0.0;
   return ctx->impl.be->bytes_per_dof();
+}
+
+// ---------------------------------------------------------------------------
+// multi-GPU slab step
+// ---------------------------------------------------------------------------
+static unsigned long long* split_slot(Ctx& c) {
+  return reinterpret_cast<unsigned long long*>(c.red.p + kRedBlocks + 64 + 2 * 1020);
+}
+
+int st_explicit_step_begin(st_ctx* ctx, double dt, const st_beam* beams, int n_beams) {
+  ST_TRY(check_ctx(ctx));
+  Ctx& c = ctx->impl;
+  ST_TRY(need_state(c));
+  const int nb = beams ? n_beams : 0;
+  ST_TRY(c.upload_beams(beams, nb));
+  if ((int64_t)c.T_alt.n < c.nv) ST_TRY(c.T_alt.alloc(c.nv));
+  return c.be->step_begin(c.T.p, rc_ptr(c), dt, nb, c.beams.p, c.T_alt.p, c.history_pending,
+                          reinterpret_cast<double*>(split_slot(c)));
+}
+
+int st_iface_partials(st_ctx* ctx, int side, double** f_plane, double** c_plane, int64_t* n) {
+  ST_TRY(check_ctx(ctx));
+  return ctx->impl.be->iface_ptrs(side, f_plane, c_plane, n);
+}
+
+int st_explicit_step_end(st_ctx* ctx, const double* recv_lo_f, const double* recv_lo_c,
+                         const double* recv_hi_f, const double* recv_hi_c) {
+  ST_TRY(check_ctx(ctx));
+  Ctx& c = ctx->impl;
+  ST_TRY(c.be->step_end(recv_lo_f, recv_lo_c, recv_hi_f, recv_hi_c));
+  std::swap(c.T.p, c.T_alt.p);
+  std::swap(c.T.n, c.T_alt.n);
+  c.history_pending = 1;
+  return ST_OK;
+}
+
+int st_step_maxima(st_ctx* ctx, double* absmax, double* tmax) {
+  ST_TRY(check_ctx(ctx));
+  Ctx& c = ctx->impl;
+  unsigned long long h[2];
+  ST_CUDA(cudaMemcpyAsync(h, split_slot(c), sizeof(h), cudaMemcpyDeviceToHost, c.stream));
+  ST_CUDA(cudaStreamSynchronize(c.stream));
+  ST_CUDA(cudaMemsetAsync(split_slot(c), 0, sizeof(h), c.stream));
+  double am;
+  std::memcpy(&am, &h[0], 8);
+  if (absmax) *absmax = am;
+  if (tmax) *tmax = key_to_double(h[1]);
+  return ST_OK;
 }
 
 int st_bench_explicit(st_ctx* ctx, int n_steps, const double* dts, const st_beam* beams,

@@ -130,6 +130,24 @@ struct Backend {
   virtual int pin_dirichlet(double* v, double value) = 0;
   virtual double bytes_per_dof() const = 0;
   virtual const char* main_kernel() const = 0;
+  // multi-GPU slab step (structured backend only)
+  virtual int step_begin(const double* T, double* rc, double dt, int nb, const DevBeam* beams,
+                         double* Tout, int pending, double* red) {
+    (void)T, (void)rc, (void)dt, (void)nb, (void)beams, (void)Tout, (void)pending, (void)red;
+    set_error("split steps need the structured backend");
+    return ST_EUNSUPPORTED;
+  }
+  virtual int step_end(const double* lo_f, const double* lo_c, const double* hi_f,
+                       const double* hi_c) {
+    (void)lo_f, (void)lo_c, (void)hi_f, (void)hi_c;
+    set_error("split steps need the structured backend");
+    return ST_EUNSUPPORTED;
+  }
+  virtual int iface_ptrs(int side, double** f, double** c, int64_t* n) {
+    (void)side, (void)f, (void)c, (void)n;
+    set_error("interfaces need the structured backend");
+    return ST_EUNSUPPORTED;
+  }
 };
 
 Backend* make_unstructured(Ctx* c, const st_unstructured_mesh* m, int* err);

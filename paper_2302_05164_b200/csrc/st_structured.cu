@@ -74,7 +74,15 @@ struct SArgs {
   double inv_rcdw;
   double imr[5];          // interior node residue a = 1..P-1
   double imv_int, imv_end;  // cell vertex inside / at the end of the line
+  // x-slab of a larger box: global plane offset / count, rank interfaces
+  int gI0, gNX, iface_lo, iface_hi;
 };
+
+// x seam: chunk boundary inside the slab, or a rank interface
+__device__ __forceinline__ bool x_seam(const SArgs& A, int P, int I) {
+  return (I > 0 && I < A.NX - 1 && (I % (P * A.Lx)) == 0) || (I == 0 && A.iface_lo) ||
+         (I == A.NX - 1 && A.iface_hi);
+}
 
 // inverse 1D lumped mass of node L on a line of N nodes
 template <int P>
@@ -157,6 +165,7 @@ __global__ void k_seams(SArgs A, int P, int CY, int CZ, int nxs, int nys, int nz
   bool bad = false;
   const int nvb = bx * nxs + by * nys + bz * nzs;
   const int sx = P * A.Lx, sy = P * CY;
+  const int nchunk = nxs - A.iface_lo - A.iface_hi;  // chunk-boundary x planes
 #pragma unroll 1
   for (int vb = blockIdx.x; vb < nvb; vb += gridDim.x) {
     int b = vb, pl;
@@ -176,8 +185,13 @@ __global__ void k_seams(SArgs A, int P, int CY, int CZ, int nxs, int nys, int nz
     const int t = b * blockDim.x + threadIdx.x;
     int I, J, K;
     bool mine;
-    if (pl < nxs) {  // x plane: (J, K) contiguous
-      I = sx * (pl + 1);
+    if (pl < nxs) {  // x plane: (J, K) contiguous; interfaces first / last
+      if (A.iface_lo && pl == 0)
+        I = 0;
+      else if (pl - A.iface_lo < nchunk)
+        I = sx * (pl - A.iface_lo + 1);
+      else
+        I = A.NX - 1;
       J = t / A.NZ;
       K = t - J * A.NZ;
       mine = J < A.NY;
@@ -185,13 +199,12 @@ __global__ void k_seams(SArgs A, int P, int CY, int CZ, int nxs, int nys, int nz
       J = sy * (pl - nxs + 1);
       I = t / A.NZ;
       K = t - I * A.NZ;
-      mine = I < A.NX && !(I > 0 && I < A.NX - 1 && (I % sx) == 0);
+      mine = I < A.NX && !x_seam(A, P, I);
     } else {  // z plane: strided
       K = P * CZ * (pl - nxs - nys + 1);
       I = t / A.NY;
       J = t - I * A.NY;
-      mine = I < A.NX && !(I > 0 && I < A.NX - 1 && (I % sx) == 0) &&
-             !(J > 0 && J < A.NY - 1 && (J % sy) == 0);
+      mine = I < A.NX && !x_seam(A, P, I) && !(J > 0 && J < A.NY - 1 && (J % sy) == 0);
     }
     if (!mine) continue;
     const int64_t idx = ((int64_t)I * A.NY + J) * A.NZ + K;
@@ -205,7 +218,8 @@ __global__ void k_seams(SArgs A, int P, int CY, int CZ, int nxs, int nys, int nz
     A.fseam[idx] = 0.0;
     // the same C^-1 as the hot kernel (tensor-product lumped mass)
     const double ci = inv_mass1_rt(A, P, K, A.NZ) *
-                      (inv_mass1_rt(A, P, J, A.NY) * (inv_mass1_rt(A, P, I, A.NX) * A.inv_rcdw));
+                      (inv_mass1_rt(A, P, J, A.NY) *
+                       (inv_mass1_rt(A, P, I + A.gI0, A.gNX) * A.inv_rcdw));
     const double o = finalize_node(A, ci, K, T, f, dc, latent != 0);
     A.out[idx] = o;
     amax = fmax(amax, fabs(o));
@@ -213,6 +227,14 @@ __global__ void k_seams(SArgs A, int P, int CY, int CZ, int nxs, int nys, int nz
     bad |= (o != o);
   }
   block_max2(bad ? (double)NAN : amax, smax, A.red);
+}
+
+// rank-interface plane: own partial + neighbour partial in the fixed order
+// low rank + high rank, so both ranks obtain bitwise the same sum
+__global__ void k_iface_add(double* own, const double* recv, int64_t n, int own_is_low) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  own[i] = own_is_low ? own[i] + recv[i] : recv[i] + own[i];
 }
 
 // ---------------------------------------------------------------------------
@@ -613,6 +635,10 @@ struct Structured : Backend {
     for (int a = 0; a < 5; a++) A.imr[a] = (a > 0 && a < p) ? 1.0 / m1[a] : 0.0;
     A.imv_int = 1.0 / (m1[0] + m1[p]);
     A.imv_end = 1.0 / m1[0];
+    A.gI0 = m.gNX > 0 ? m.gx0 : 0;
+    A.gNX = m.gNX > 0 ? m.gNX : NX;
+    A.iface_lo = m.iface_lo ? 1 : 0;
+    A.iface_hi = m.iface_hi ? 1 : 0;
     for (int a = 0; a < q; a++)
       for (int b = 0; b < q; b++)
         for (int cc = 0; cc < q; cc++) {
@@ -669,20 +695,11 @@ struct Structured : Backend {
     return launch_tile<P, Tile<P>::CY, Tile<P>::CZ>(A, lat, rcf);
   }
 
-  int xmarch(SArgs& A, bool rcf) {
+  int seams(SArgs& A) {
     const bool lat = c->dp.latent != 0 && A.mode == 0;
-    c->prof_begin();
-    int rc;
-    switch (p) {
-      case 1: rc = launch_xmarch_p<1>(A, lat, rcf); break;
-      case 2: rc = launch_xmarch_p<2>(A, lat, rcf); break;
-      case 3: rc = launch_xmarch_p<3>(A, lat, rcf); break;
-      default: rc = launch_xmarch_p<4>(A, lat, rcf); break;
-    }
-    c->prof_end();
-    ST_TRY(rc);
-    const int nxs = (m.nx + Lx - 1) / Lx - 1, nys = (m.ny + cy - 1) / cy - 1,
-              nzs = (m.nz + cz - 1) / cz - 1;
+    // x planes: chunk boundaries + rank interfaces (x_seam order)
+    const int nxs = (m.nx + Lx - 1) / Lx - 1 + A.iface_lo + A.iface_hi;
+    const int nys = (m.ny + cy - 1) / cy - 1, nzs = (m.nz + cz - 1) / cz - 1;
     // one launch over all seam planes (x, then y, then z families)
     const int bx = (int)(((int64_t)NY * NZ + kThreads - 1) / kThreads);
     const int by = (int)(((int64_t)NX * NZ + kThreads - 1) / kThreads);
@@ -695,6 +712,84 @@ struct Structured : Backend {
       ST_TRY(launched());
     }
     return ST_OK;
+  }
+
+  int xmarch(SArgs& A, bool rcf, bool with_seams = true) {
+    const bool lat = c->dp.latent != 0 && A.mode == 0;
+    c->prof_begin();
+    int rc;
+    switch (p) {
+      case 1: rc = launch_xmarch_p<1>(A, lat, rcf); break;
+      case 2: rc = launch_xmarch_p<2>(A, lat, rcf); break;
+      case 3: rc = launch_xmarch_p<3>(A, lat, rcf); break;
+      default: rc = launch_xmarch_p<4>(A, lat, rcf); break;
+    }
+    c->prof_end();
+    ST_TRY(rc);
+    return with_seams ? seams(A) : ST_OK;
+  }
+
+  // --- multi-GPU slab step (rank interfaces exchanged between the halves)
+  SArgs split{};
+  bool split_open = false;
+
+  int step_begin(const double* T, double* rc, double dt, int nb, const DevBeam* beams,
+                 double* Tout, int pending, double* red) override {
+    SArgs A = sargs();
+    A.mode = 0;
+    A.flags = ST_RHS_DIFFUSION | ST_RHS_FACES | ST_RHS_SOURCE;
+    A.T = T;
+    A.out = Tout;
+    A.rc = rc;
+    A.pending = pending;
+    A.nb = nb;
+    A.beams = beams;
+    A.dt = dt;
+    A.red = reinterpret_cast<unsigned long long*>(red);
+    ST_TRY(xmarch(A, rc != nullptr, false));
+    split = A;
+    split_open = true;
+    return ST_OK;
+  }
+
+  int iface_ptrs(int side, double** f, double** cp, int64_t* n) override {
+    const int64_t plane = (int64_t)NY * NZ;
+    const int64_t off = side == 0 ? 0 : (int64_t)(NX - 1) * plane;
+    *f = fseam.p + off;
+    *cp = c->dp.latent ? cseam.p + off : nullptr;
+    *n = plane;
+    return ST_OK;
+  }
+
+  int step_end(const double* lo_f, const double* lo_c, const double* hi_f,
+               const double* hi_c) override {
+    if (!split_open) {
+      set_error("st_explicit_step_end without st_explicit_step_begin");
+      return ST_EINVAL;
+    }
+    const int64_t plane = (int64_t)NY * NZ;
+    const unsigned blocks = (unsigned)((plane + kThreads - 1) / kThreads);
+    auto add = [&](double* own, const double* recv, int own_is_low) -> int {
+      if (!own || !recv) return ST_OK;
+      k_iface_add<<<blocks, kThreads, 0, c->stream>>>(own, recv, plane, own_is_low);
+      return launched();
+    };
+    // plane 0 is shared with the lower rank (its partial comes first),
+    // plane NX-1 with the upper rank (ours comes first)
+    double *f0, *c0, *f1, *c1;
+    int64_t n;
+    iface_ptrs(0, &f0, &c0, &n);
+    iface_ptrs(1, &f1, &c1, &n);
+    if (m.iface_lo) {
+      ST_TRY(add(f0, lo_f, 0));
+      ST_TRY(add(c0, lo_c, 0));
+    }
+    if (m.iface_hi) {
+      ST_TRY(add(f1, hi_f, 1));
+      ST_TRY(add(c1, hi_c, 1));
+    }
+    split_open = false;
+    return seams(split);
   }
 
   int rhs(const double* T, double* rc, int flags, double frozen_k, int nb,

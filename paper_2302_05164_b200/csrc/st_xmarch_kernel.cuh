@@ -124,7 +124,7 @@ __global__ void __launch_bounds__(CY* CZ, MinBlocks<P>::v) k_xmarch(SArgs A) {
   // every node of plane I owned by this thread (element plane a)
   auto finalize_owned = [&](int I, int a, bool xs, bool latn) {
     if (!live) return;
-    const double imIs = inv_mass1<P>(A, I, A.NX) * A.inv_rcdw;
+    const double imIs = inv_mass1<P>(A, I + A.gI0, A.gNX) * A.inv_rcdw;
 #pragma unroll
     for (int b = 0; b < P; b++)
 #pragma unroll
@@ -199,7 +199,7 @@ __global__ void __launch_bounds__(CY* CZ, MinBlocks<P>::v) k_xmarch(SArgs A) {
     __syncthreads();
     const bool latn = LATENT && (lat_any[0] | lat_any[1]);
 #pragma unroll 1
-    for (int a = 0; a < P; a++) finalize_owned(P * i + a, a, a == 0 && i == i0 && i0 > 0, latn);
+    for (int a = 0; a < P; a++) finalize_owned(P * i + a, a, a == 0 && i == i0 && (i0 > 0 || A.iface_lo), latn);
     __syncthreads();
     if (tid == 0) lat_any[(i + 1) & 1] = 0;  // slot reused by the next layer
   }
@@ -213,6 +213,6 @@ __global__ void __launch_bounds__(CY* CZ, MinBlocks<P>::v) k_xmarch(SArgs A) {
       for (int q = 0; q < Q * Q; q++) Ec[q * NT + tid] = carryC[q];
   }
   __syncthreads();
-  finalize_owned(P * i1, 0, i1 < A.nx, LATENT && (lat_any[0] | lat_any[1]));
+  finalize_owned(P * i1, 0, i1 < A.nx || A.iface_hi, LATENT && (lat_any[0] | lat_any[1]));
   block_max2(bad ? (double)NAN : amax, smax, A.red);
 }

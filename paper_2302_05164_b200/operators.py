@@ -69,7 +69,10 @@ class ThermalOperator:
             m = _lib.StStructuredMesh(forest.nx, forest.ny, forest.nz, forest.degree,
                                       forest.h, forest.origin[0], forest.origin[1],
                                       forest.origin[2], int(forest.dirichlet_bottom),
-                                      int(forest.top_faces))
+                                      int(forest.top_faces), int(getattr(forest, "gx0", 0)),
+                                      int(getattr(forest, "gNX", 0)),
+                                      int(bool(getattr(forest, "iface_lo", False))),
+                                      int(bool(getattr(forest, "iface_hi", False))))
             _lib.check(self._lib.st_ctx_create_structured(
                 device, ctypes.byref(m), ctypes.byref(pst), ctypes.byref(self._ctx)),
                 "st_ctx_create_structured")
