@@ -16,9 +16,11 @@ every timed step outside the events; per-rank time = sum of the step
 times, job time = max over ranks.  ``sweep`` adds BASELINE configs[2]
 (~50M DoFs at degree 1..4, inputs larger than L2) measured the same way.
 
-Under torchrun (N > 1) every rank runs its own copy of the workload on
-its GPU (replicas; the z-slab partition is DESIGN.md §7 future work),
-value = DoF-updates of all ranks / max time.
+Under torchrun (N > 1) the global box is the workload box repeated N
+times along x and split into x-slabs, one per GPU (weak scaling); every
+step exchanges the rank-interface partial sums over NCCL on the
+library's stream (paper_2302_05164_b200/distributed.py).  value = DoF-
+updates of the whole box / max over ranks of the summed step times.
 """
 
 import argparse
@@ -289,13 +291,96 @@ def gpu_measure(w, steps, warmup, device, clocks=True):
                 launches=launches, roofline=roofline, clocks=clk.summary() if clk else None)
 
 
+def run_slabs(args):
+    """N > 1: the global box is the workload box repeated N times along x
+    (weak scaling, one workload-sized x-slab per GPU); every step exchanges
+    the rank-interface partial sums over NCCL on the library's stream."""
+    import torch
+    import torch.distributed as dist
+    from paper_2302_05164_b200.distributed import (GpuSlabStepper, SlabBox, SlabDriver,
+                                                   partition, torch_exchange)
+    st = _st()
+    ws, rank, local = dist_env()
+    torch.cuda.set_device(local)
+    dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    w = WORKLOADS[args.workload]()
+    nx, ny, nz = w["dims"]
+    glob = st.StructuredBox(nx * ws, ny, nz, w["h"], degree=w["degree"])
+    c0, c1 = partition(glob.nx, ws)[rank]
+    box = SlabBox(glob, c0, c1, rank, ws)
+    op = st.ThermalOperator(box, box, w["params"], st.SolverSettings(), device=local)
+    T0 = w["T0"](glob.n_vertices)
+    op.set_state(box.local_of(T0), 1.0)
+    stepper = GpuSlabStepper(op)
+    drv = SlabDriver(stepper, torch_exchange(rank, ws))
+    dts, beams = schedule(w, args.warmup + args.steps)
+    flush = torch.empty(L2_FLUSH_BYTES // 8, dtype=torch.float64, device="cuda")
+    evs = []
+    with torch.cuda.stream(stepper.stream):
+        for i in range(args.warmup):
+            drv.step(float(dts[i]), beams[i])
+        torch.cuda.synchronize()
+        dist.barrier()
+        launches0 = op.launches
+        clk = Clocks(local)
+        clk.__enter__()
+        for i in range(args.warmup, args.warmup + args.steps):
+            flush.fill_(float(i))
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            drv.step(float(dts[i]), beams[i])
+            e1.record()
+            evs.append((e0, e1))
+        torch.cuda.synchronize()
+        clk.__exit__()
+    launches = op.launches - launches0
+    total_ms = sum(a.elapsed_time(b) for a, b in evs)
+    t = torch.tensor([total_ms], device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    total_ms = float(t.item())
+    # end to end: host slab in -> K split steps with the exchange -> host out
+    T_host = box.local_of(T0)
+    dist.barrier()
+    t0 = time.perf_counter()
+    op.set_state(T_host, 1.0)
+    with torch.cuda.stream(stepper.stream):
+        for i in range(args.warmup, args.warmup + args.steps):
+            drv.step(float(dts[i]), beams[i])
+    T_out, rc_out = op.get_state()
+    e2e_s = torch.tensor([time.perf_counter() - t0], device="cuda")
+    dist.all_reduce(e2e_s, op=dist.ReduceOp.MAX)
+    nb = beams.shape[1]
+    e2e = {"value": glob.n_dofs * args.steps / float(e2e_s.item()), "unit": "DoF-updates/s",
+           "h2d_bytes_per_step": (T_host.nbytes + args.steps * nb * 40) / args.steps,
+           "d2h_bytes_per_step": (T_out.nbytes + rc_out.nbytes) / args.steps,
+           "api": "per rank: set_state + split steps (NCCL exchange) + get_state; max over ranks"}
+    am, _ = stepper.maxima()
+    amt = torch.tensor([am], device="cuda")
+    dist.all_reduce(amt, op=dist.ReduceOp.MAX)
+    if not np.isfinite(amt.item()) or amt.item() > 1e7:
+        raise RuntimeError("slab run diverged")
+    dofs_total = glob.n_dofs
+    value = dofs_total * args.steps / (total_ms * 1e-3)
+    dist.barrier()
+    if rank == 0:
+        out = {"metric": METRIC, "value": value, "unit": "DoF-updates/s", "n_gpus": ws,
+               "steps": args.steps, "warmup": args.warmup,
+               "ms_per_step": total_ms / args.steps, "higher_is_better": True,
+               "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+               "config": dict(workload=w["name"] + f"_x{ws}", dofs=dofs_total,
+                              backend="structured x-slabs",
+                              parallelism=f"x-slab dp{ws}, NCCL partial-sum interface exchange",
+                              l2="flushed (256 MiB write) before every timed step", **w["cfg"]),
+               "e2e": e2e, "gpu_launches": int(launches), "clocks": clk.summary()}
+        print(json.dumps(out), flush=True)
+    dist.destroy_process_group()
+
+
 def run_ours(args):
     import torch
     ws, rank, local = dist_env()
     if ws > 1:
-        import torch.distributed as dist
-        torch.cuda.set_device(local)
-        dist.init_process_group("nccl")
+        return run_slabs(args)
     w = WORKLOADS[args.workload]()
     if ws > 1:
         torch.distributed.barrier()
