@@ -54,8 +54,17 @@ struct SArgs {
   double* rc;
   double rc_value;
   int pending;
+  // seam partial sums: 8 slot arrays of nv doubles (slot = x side + 2 y
+  // side + 4 z side of the writing CTA), plain stores, no clearing
   double* fseam;
   double* cseam;
+  int64_t snv;
+  // rank interfaces: own pre-summed plane (packed after the sweep) and the
+  // neighbour's, per side (0: local plane 0, 1: local plane NX-1)
+  double* ipf[2];
+  double* ipc[2];
+  const double* irf[2];
+  const double* irc[2];
   int nb;
   const DevBeam* beams;
   double dt;
@@ -208,14 +217,30 @@ __global__ void k_seams(SArgs A, int P, int CY, int CZ, int nxs, int nys, int nz
     }
     if (!mine) continue;
     const int64_t idx = ((int64_t)I * A.NY + J) * A.NZ + K;
-    const double f = A.fseam[idx];
     const double T = A.T[idx];
-    double dc = 0.0;
-    if (latent) {
-      dc = A.cseam[idx];
-      A.cseam[idx] = 0.0;
+    const bool xs = x_seam(A, P, I);
+    const bool ys = J > 0 && J < A.NY - 1 && (J % sy) == 0;
+    const bool zs = K > 0 && K < A.NZ - 1 && (K % (P * CZ)) == 0;
+    // fixed order: x side outermost, then z side, then y side
+    double f = 0.0, dc = 0.0;
+    for (int xb = 0; xb <= (xs ? 1 : 0); xb++) {
+      double sf_ = 0.0, sc_ = 0.0;
+      const int side = (I == 0 && A.iface_lo) ? 0 : ((I == A.NX - 1 && A.iface_hi) ? 1 : -1);
+      const bool remote = side >= 0 && xb == (side == 0 ? 0 : 1);
+      if (remote) {
+        sf_ = A.irf[side][(int64_t)J * A.NZ + K];
+        if (latent) sc_ = A.irc[side][(int64_t)J * A.NZ + K];
+      } else {
+        for (int zb = 0; zb <= (zs ? 1 : 0); zb++)
+          for (int yb = 0; yb <= (ys ? 1 : 0); yb++) {
+            const int64_t so = (int64_t)(xb + 2 * yb + 4 * zb) * A.snv + idx;
+            sf_ += A.fseam[so];
+            if (latent) sc_ += A.cseam[so];
+          }
+      }
+      f += sf_;
+      dc += sc_;
     }
-    A.fseam[idx] = 0.0;
     // the same C^-1 as the hot kernel (tensor-product lumped mass)
     const double ci = inv_mass1_rt(A, P, K, A.NZ) *
                       (inv_mass1_rt(A, P, J, A.NY) *
@@ -229,12 +254,27 @@ __global__ void k_seams(SArgs A, int P, int CY, int CZ, int nxs, int nys, int nz
   block_max2(bad ? (double)NAN : amax, smax, A.red);
 }
 
-// rank-interface plane: own partial + neighbour partial in the fixed order
-// low rank + high rank, so both ranks obtain bitwise the same sum
-__global__ void k_iface_add(double* own, const double* recv, int64_t n, int own_is_low) {
-  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (i >= n) return;
-  own[i] = own_is_low ? own[i] + recv[i] : recv[i] + own[i];
+// rank interface: this rank's pre-summed seam partials on local plane 0
+// (it is the high x side there) or NX-1 (low side), in the same z-then-y
+// slot order k_seams uses, so both ranks add bitwise the same numbers
+__global__ void k_iface_pack(SArgs A, int P, int CY, int CZ, int side, int latent) {
+  const int64_t plane = (int64_t)A.NY * A.NZ;
+  const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (t >= plane) return;
+  const int J = (int)(t / A.NZ), K = (int)(t - (int64_t)J * A.NZ);
+  const int I = side == 0 ? 0 : A.NX - 1, xb = side == 0 ? 1 : 0;
+  const bool ys = J > 0 && J < A.NY - 1 && (J % (P * CY)) == 0;
+  const bool zs = K > 0 && K < A.NZ - 1 && (K % (P * CZ)) == 0;
+  const int64_t idx = (int64_t)I * plane + t;
+  double sf_ = 0.0, sc_ = 0.0;
+  for (int zb = 0; zb <= (zs ? 1 : 0); zb++)
+    for (int yb = 0; yb <= (ys ? 1 : 0); yb++) {
+      const int64_t so = (int64_t)(xb + 2 * yb + 4 * zb) * A.snv + idx;
+      sf_ += A.fseam[so];
+      if (latent) sc_ += A.cseam[so];
+    }
+  A.ipf[side][t] = sf_;
+  if (latent) A.ipc[side][t] = sc_;
 }
 
 // ---------------------------------------------------------------------------
@@ -582,7 +622,7 @@ struct Structured : Backend {
   int Lx = 1, cy = 8, cz = 8;
   int use_lat = 0;
   long long lx = 0, ly = 0, lz = 0;
-  DevBuf<double> cinv, fseam, cseam;
+  DevBuf<double> cinv, fseam, cseam, packf[2], packc[2];
   int64_t nv = 0;
 
   int launched() {
@@ -616,6 +656,13 @@ struct Structured : Backend {
     A.rc_value = c->rc_value;
     A.fseam = fseam.p;
     A.cseam = cseam.p;
+    A.snv = nv;
+    for (int sd = 0; sd < 2; sd++) {
+      A.ipf[sd] = packf[sd].p;
+      A.ipc[sd] = packc[sd].p;
+      A.irf[sd] = nullptr;
+      A.irc[sd] = nullptr;
+    }
     A.P = c->dp;
     const DevParams& d = c->dp;
     A.kA = (1.0 - c->rc_value) * d.k_p + c->rc_value * d.k_s;
@@ -747,17 +794,23 @@ struct Structured : Backend {
     A.dt = dt;
     A.red = reinterpret_cast<unsigned long long*>(red);
     ST_TRY(xmarch(A, rc != nullptr, false));
+    const bool lat = c->dp.latent != 0;
+    const int64_t plane = (int64_t)NY * NZ;
+    for (int sd = 0; sd < 2; sd++) {
+      if (!(sd == 0 ? m.iface_lo : m.iface_hi)) continue;
+      k_iface_pack<<<(unsigned)((plane + kThreads - 1) / kThreads), kThreads, 0, c->stream>>>(
+          A, p, cy, cz, sd, lat ? 1 : 0);
+      ST_TRY(launched());
+    }
     split = A;
     split_open = true;
     return ST_OK;
   }
 
   int iface_ptrs(int side, double** f, double** cp, int64_t* n) override {
-    const int64_t plane = (int64_t)NY * NZ;
-    const int64_t off = side == 0 ? 0 : (int64_t)(NX - 1) * plane;
-    *f = fseam.p + off;
-    *cp = c->dp.latent ? cseam.p + off : nullptr;
-    *n = plane;
+    *f = packf[side].p;
+    *cp = c->dp.latent ? packc[side].p : nullptr;
+    *n = (int64_t)NY * NZ;
     return ST_OK;
   }
 
@@ -767,26 +820,13 @@ struct Structured : Backend {
       set_error("st_explicit_step_end without st_explicit_step_begin");
       return ST_EINVAL;
     }
-    const int64_t plane = (int64_t)NY * NZ;
-    const unsigned blocks = (unsigned)((plane + kThreads - 1) / kThreads);
-    auto add = [&](double* own, const double* recv, int own_is_low) -> int {
-      if (!own || !recv) return ST_OK;
-      k_iface_add<<<blocks, kThreads, 0, c->stream>>>(own, recv, plane, own_is_low);
-      return launched();
-    };
-    // plane 0 is shared with the lower rank (its partial comes first),
-    // plane NX-1 with the upper rank (ours comes first)
-    double *f0, *c0, *f1, *c1;
-    int64_t n;
-    iface_ptrs(0, &f0, &c0, &n);
-    iface_ptrs(1, &f1, &c1, &n);
-    if (m.iface_lo) {
-      ST_TRY(add(f0, lo_f, 0));
-      ST_TRY(add(c0, lo_c, 0));
-    }
-    if (m.iface_hi) {
-      ST_TRY(add(f1, hi_f, 1));
-      ST_TRY(add(c1, hi_c, 1));
+    split.irf[0] = lo_f;
+    split.irc[0] = lo_c;
+    split.irf[1] = hi_f;
+    split.irc[1] = hi_c;
+    if ((m.iface_lo && !lo_f) || (m.iface_hi && !hi_f)) {
+      set_error("missing neighbour partials for a rank interface");
+      return ST_EINVAL;
     }
     split_open = false;
     return seams(split);
@@ -967,13 +1007,19 @@ Backend* make_structured(Ctx* c, const st_structured_mesh* m, int* err) {
   c->n_cells = (int64_t)m->nx * m->ny * m->nz;
   c->qpc = (s->p + 1) * (s->p + 1) * (s->p + 1);
   rc = s->cinv.alloc(s->nv);
-  if (rc == ST_OK) rc = s->fseam.alloc(s->nv);
-  if (rc == ST_OK && c->dp.latent) rc = s->cseam.alloc(s->nv);
-  if (rc == ST_OK && cudaMemsetAsync(s->fseam.p, 0, s->nv * sizeof(double), c->stream) != cudaSuccess)
+  if (rc == ST_OK) rc = s->fseam.alloc(8 * s->nv);
+  if (rc == ST_OK && c->dp.latent) rc = s->cseam.alloc(8 * s->nv);
+  if (rc == ST_OK &&
+      cudaMemsetAsync(s->fseam.p, 0, 8 * s->nv * sizeof(double), c->stream) != cudaSuccess)
     rc = ST_ECUDA;
   if (rc == ST_OK && c->dp.latent &&
-      cudaMemsetAsync(s->cseam.p, 0, s->nv * sizeof(double), c->stream) != cudaSuccess)
+      cudaMemsetAsync(s->cseam.p, 0, 8 * s->nv * sizeof(double), c->stream) != cudaSuccess)
     rc = ST_ECUDA;
+  for (int sd = 0; sd < 2 && rc == ST_OK; sd++) {
+    if (!(sd == 0 ? m->iface_lo : m->iface_hi)) continue;
+    rc = s->packf[sd].alloc((size_t)s->NY * s->NZ);
+    if (rc == ST_OK && c->dp.latent) rc = s->packc[sd].alloc((size_t)s->NY * s->NZ);
+  }
   if (rc == ST_OK) {
     const double rc_detw = c->dp.rhoc * std::pow(m->h / 2.0, 3.0);
     const unsigned blocks = (unsigned)((s->nv + 255) / 256);

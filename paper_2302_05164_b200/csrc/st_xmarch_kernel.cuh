@@ -86,7 +86,9 @@ __global__ void __launch_bounds__(CY* CZ, MinBlocks<P>::v) k_xmarch(SArgs A) {
 
   // node (b, c) of plane I owned by this thread (element plane a);
   // b, c are compile-time after unrolling
-  auto finalize_node3 = [&](int I, int a, int b, int c, bool xs, bool latn, double imIs) {
+  // xc: 0 = not an x seam, 1 = x seam with this CTA on the low side (the
+  // chunk's last plane), 2 = on the high side (the chunk's first plane)
+  auto finalize_node3 = [&](int I, int a, int b, int c, int xc, bool latn, double imIs) {
     const double* pe = E + a * Q * Q * NT + tid;
     // own cell, then the y-, z- and yz-neighbour below (fixed order)
     double f = pe[(b * Q + c) * NT];
@@ -94,12 +96,9 @@ __global__ void __launch_bounds__(CY* CZ, MinBlocks<P>::v) k_xmarch(SArgs A) {
     if (c == 0 && kl > 0) f += pe[(b * Q + P) * NT - 1];
     if (b == 0 && c == 0 && jl > 0 && kl > 0) f += pe[(P * Q + P) * NT - CZ - 1];
     const int64_t idx = (int64_t)I * plane_stride + my0 + (int64_t)b * A.NZ + c;
-    const bool seam = xs || (b == 0 && sy_lo) || (b == P && sy_hi) || (c == 0 && sz_lo) ||
+    const bool seam = xc || (b == 0 && sy_lo) || (b == P && sy_hi) || (c == 0 && sz_lo) ||
                       (c == P && sz_hi);
     double dc = 0.0;
-    if (seam) {
-      atomicAdd(A.fseam + idx, f);
-    }
     if (LATENT && latn) {
         const double* pc = Ec + a * Q * Q * NT + tid;
         dc = pc[(b * Q + c) * NT];
@@ -108,7 +107,11 @@ __global__ void __launch_bounds__(CY* CZ, MinBlocks<P>::v) k_xmarch(SArgs A) {
         if (b == 0 && c == 0 && jl > 0 && kl > 0) dc += pc[(P * Q + P) * NT - CZ - 1];
       }
     if (seam) {
-      if (LATENT && dc != 0.0) atomicAdd(A.cseam + idx, dc);
+      // this CTA's partial goes to its own slot (side code per seam axis)
+      const int slot = (xc == 2 ? 1 : 0) + ((b == 0 && sy_lo) ? 2 : 0) + ((c == 0 && sz_lo) ? 4 : 0);
+      const int64_t so = (int64_t)slot * A.snv + idx;
+      A.fseam[so] = f;
+      if (LATENT) A.cseam[so] = dc;
     } else {
       const int K = P * k + c;
       const double ci = inv_mass1<P>(A, K, A.NZ) * (inv_mass1<P>(A, P * j + b, A.NY) * imIs);
@@ -122,7 +125,7 @@ __global__ void __launch_bounds__(CY* CZ, MinBlocks<P>::v) k_xmarch(SArgs A) {
   };
 
   // every node of plane I owned by this thread (element plane a)
-  auto finalize_owned = [&](int I, int a, bool xs, bool latn) {
+  auto finalize_owned = [&](int I, int a, int xs, bool latn) {
     if (!live) return;
     const double imIs = inv_mass1<P>(A, I + A.gI0, A.gNX) * A.inv_rcdw;
 #pragma unroll
@@ -199,7 +202,8 @@ __global__ void __launch_bounds__(CY* CZ, MinBlocks<P>::v) k_xmarch(SArgs A) {
     __syncthreads();
     const bool latn = LATENT && (lat_any[0] | lat_any[1]);
 #pragma unroll 1
-    for (int a = 0; a < P; a++) finalize_owned(P * i + a, a, a == 0 && i == i0 && (i0 > 0 || A.iface_lo), latn);
+    for (int a = 0; a < P; a++)
+      finalize_owned(P * i + a, a, (a == 0 && i == i0 && (i0 > 0 || A.iface_lo)) ? 2 : 0, latn);
     __syncthreads();
     if (tid == 0) lat_any[(i + 1) & 1] = 0;  // slot reused by the next layer
   }
@@ -213,6 +217,7 @@ __global__ void __launch_bounds__(CY* CZ, MinBlocks<P>::v) k_xmarch(SArgs A) {
       for (int q = 0; q < Q * Q; q++) Ec[q * NT + tid] = carryC[q];
   }
   __syncthreads();
-  finalize_owned(P * i1, 0, i1 < A.nx || A.iface_hi, LATENT && (lat_any[0] | lat_any[1]));
+  finalize_owned(P * i1, 0, (i1 < A.nx || A.iface_hi) ? 1 : 0,
+                 LATENT && (lat_any[0] | lat_any[1]));
   block_max2(bad ? (double)NAN : amax, smax, A.red);
 }

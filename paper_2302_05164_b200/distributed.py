@@ -159,7 +159,9 @@ class GpuSlabStepper:
         self.stream = torch.cuda.ExternalStream(op.stream_ptr())
         lib = op._lib
         self._planes = {}
-        for side in (0, 1):
+        box = op.forest
+        self.sides = [s for s, on in ((0, box.iface_lo), (1, box.iface_hi)) if on]
+        for side in self.sides:
             f = ctypes.POINTER(ctypes.c_double)()
             c = ctypes.POINTER(ctypes.c_double)()
             n = ctypes.c_int64()
@@ -171,8 +173,6 @@ class GpuSlabStepper:
             tf = torch.as_tensor(_CudaPlane(fp, n.value), device="cuda")
             tc = torch.as_tensor(_CudaPlane(cp, n.value), device="cuda") if cp else None
             self._planes[side] = Partials(tf, tc)
-        box = op.forest
-        self.sides = [s for s, on in ((0, box.iface_lo), (1, box.iface_hi)) if on]
 
     def begin(self, dt, beams):
         from . import _lib
