@@ -7,6 +7,13 @@
 
 namespace st {
 
+// select-based max / clamp: two compares and selects instead of the
+// NaN-propagating fmax/fmin sequences (a NaN state is caught separately by
+// the divergence flag, so NaN semantics do not matter here)
+__device__ __forceinline__ double dmax(double a, double b) { return a > b ? a : b; }
+__device__ __forceinline__ double clamp01(double x) { return x < 0.0 ? 0.0 : (x > 1.0 ? 1.0 : x); }
+
+
 // g(T) (material.py:46-57): 0 below T_s, 1 above T_l, ramp between.
 __device__ __forceinline__ double liquid_fraction(const DevParams& P, double T) {
   double ramp = (T - P.T_s) / P.dT_l;

@@ -245,7 +245,7 @@ __global__ void k_seams(SArgs A, int P, int CY, int CZ, int nxs, int nys, int nz
     const double ci = inv_mass1_rt(A, P, K, A.NZ) *
                       (inv_mass1_rt(A, P, J, A.NY) *
                        (inv_mass1_rt(A, P, I + A.gI0, A.gNX) * A.inv_rcdw));
-    const double o = finalize_node(A, ci, K, T, f, dc, latent != 0);
+    const double o = finalize_node(A, ci, K == 0, T, f, dc, latent != 0);
     A.out[idx] = o;
     amax = fmax(amax, fabs(o));
     smax = fmax(smax, o);

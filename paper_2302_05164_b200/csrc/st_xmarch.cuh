@@ -2,6 +2,8 @@
 // (included by st_structured.cu after the basis tables).  See the header
 // of st_structured.cu for the overall scheme.
 #pragma once
+#include <type_traits>
+#include <utility>
 
 struct CellFlags {
   bool diffusion, faces, source, frozen;
@@ -68,20 +70,17 @@ __device__ __forceinline__ void source_factors(const SArgs& A, const DevBeam& b,
 //   G out: element vector
 //   t out: with LATENT and has_lat, the projected apparent-capacity
 //          increment rho L/dT_lat over the Gauss points in the interval
-template <int P, bool RCF, bool LATENT>
+//   node(a, b, c): re-reads a node value (top facet; keeps t's copy out of
+//          the register budget)
+template <int P, bool RCF, bool LATENT, class NodeF>
 __device__ __forceinline__ void cell_element(const SArgs& A, const CellFlags& F, int i, int j,
                                              int k, int64_t cell, double* t, double* G,
-                                             bool& has_lat) {
+                                             bool& has_lat, const NodeF& node) {
   constexpr int Q = P + 1;
   constexpr int Q3 = Q * Q * Q;
   using B = Basis<P>;
   const DevParams& PP = A.P;
   const bool top = F.faces && A.top_faces && (k == A.nz - 1);
-  double tf[Q * Q];
-#pragma unroll
-  for (int a = 0; a < Q; a++)
-#pragma unroll
-    for (int b = 0; b < Q; b++) tf[a * Q + b] = t[(a * Q + b) * Q + P];
   interp3<P>(t);  // T at the Gauss points
 #pragma unroll
   for (int q = 0; q < Q3; q++) G[q] = 0.0;
@@ -108,11 +107,11 @@ __device__ __forceinline__ void cell_element(const SArgs& A, const CellFlags& F,
             kq = A.frozen_k;
           } else {
             // g(T) (material.py:46-57) as a clamped ramp
-            const double g = fmin(fmax(fma(t[q], PP.inv_dT_l, A.glo), 0.0), 1.0);
+            const double g = clamp01(fma(t[q], PP.inv_dT_l, A.glo));
             if (RCF) {
               double r = A.rc[cell * Q3 + q];
               if (A.pending) {
-                r = fmax(r, g);
+                r = dmax(r, g);
                 A.rc[cell * Q3 + q] = r;
               }
               kq = conductivity(PP, g, r);
@@ -163,6 +162,11 @@ __device__ __forceinline__ void cell_element(const SArgs& A, const CellFlags& F,
   }
   if (top) {
     // +z facet quadrature (operators.py:275-290), full facets
+    double tf[Q * Q];
+#pragma unroll
+    for (int a = 0; a < Q; a++)
+#pragma unroll
+      for (int b = 0; b < Q; b++) tf[a * Q + b] = node(a, b, P);
 #pragma unroll
     for (int a = 0; a < Q; a++) {
       double in[Q];
@@ -223,12 +227,24 @@ __device__ __forceinline__ void cell_element(const SArgs& A, const CellFlags& F,
 
 // node update with its complete f (operators.py:359-368); with the latent
 // extension the lumped capacity is C_const + dC(T)
-__device__ __forceinline__ double finalize_node(const SArgs& A, double ci, int K, double T,
+__device__ __forceinline__ double finalize_node(const SArgs& A, double ci, bool bottom, double T,
                                                 double f, double dc, bool latent) {
   if (A.mode == 1) return f;
   if (latent && dc != 0.0) ci = 1.0 / (1.0 / ci + dc);
   double o = T + A.dt * (ci * f);
-  if (A.dir_bottom && K == 0) o = A.P.T_inf;
+  if (A.dir_bottom && bottom) o = A.P.T_inf;
   return o;
+}
+
+// compile-time loops (node offsets inside a cell become immediates)
+template <int N>
+using IC = std::integral_constant<int, N>;
+template <class F, int... I>
+__device__ __forceinline__ void static_for_(F&& f, std::integer_sequence<int, I...>) {
+  (f(IC<I>{}), ...);
+}
+template <int N, class F>
+__device__ __forceinline__ void static_for(F&& f) {
+  static_for_(f, std::make_integer_sequence<int, N>{});
 }
 #include "st_xmarch_kernel.cuh"

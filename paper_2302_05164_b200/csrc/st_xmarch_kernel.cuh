@@ -63,17 +63,27 @@ __global__ void __launch_bounds__(CY* CZ, MinBlocks<P>::v) k_xmarch(SArgs A) {
   const int ms0 = P * jl * NZT + P * kl;
   if (tid < 2) lat_any[tid] = 0;
 
-  // warp w stages rows jj = w, w + NW, ... of plane I (lanes along z)
-  auto load_plane = [&](int I) {
-    const double* srcT = A.T + (int64_t)I * plane_stride + tile0;
-    double* dT = Tr + (I % NR) * PL;
+  // stage planes Ib .. Ib+n-1: thread tid copies tile entries e = tid,
+  // tid + NT, ... (row r = e / NZT of the tile, column e % NZT)
+  auto load_planes = [&](int Ib, int n) {
 #pragma unroll 1
-    for (int jj = warp; jj < Jn; jj += NW) {
+    for (int pa = 0; pa < n; pa++) {
+      const double* srcT = A.T + (int64_t)(Ib + pa) * plane_stride + tile0;
+      double* dT = Tr + ((Ib + pa) % NR) * PL;
 #pragma unroll
-      for (int kk = lane; kk < NZT; kk += 32)
-        if (kk < Kn) cp_async8(dT + jj * NZT + kk, srcT + (int64_t)jj * A.NZ + kk);
+      for (int e0 = 0; e0 < PL; e0 += NT) {
+        const int e = e0 + tid;
+        const int r = e / NZT, cc = e - (e / NZT) * NZT;
+        if ((e0 + NT <= PL || e < PL) && r < Jn && cc < Kn)
+          cp_async8(dT + e, srcT + r * A.NZ + cc);
+      }
     }
   };
+
+  // 1D lumped inverse-mass factors of this thread's cell corners in y and
+  // z (fixed over the march); interior residues are A.imr[b]
+  const double my_0 = inv_mass1<P>(A, P * j, A.NY), my_P = inv_mass1<P>(A, P * j + P, A.NY);
+  const double mz_0 = inv_mass1<P>(A, P * k, A.NZ), mz_P = inv_mass1<P>(A, P * k + P, A.NZ);
 
   double carry[Q * Q], carryC[LATENT ? Q * Q : 1];
 #pragma unroll
@@ -84,76 +94,72 @@ __global__ void __launch_bounds__(CY* CZ, MinBlocks<P>::v) k_xmarch(SArgs A) {
   double amax = 0.0, smax = -INFINITY;
   bool bad = false;
 
-  // node (b, c) of plane I owned by this thread (element plane a);
-  // b, c are compile-time after unrolling
-  // xc: 0 = not an x seam, 1 = x seam with this CTA on the low side (the
-  // chunk's last plane), 2 = on the high side (the chunk's first plane)
-  auto finalize_node3 = [&](int I, int a, int b, int c, int xc, bool latn, double imIs) {
-    const double* pe = E + a * Q * Q * NT + tid;
+  // node (b, c) of plane I owned by this thread (element plane a at pe);
+  // b, c are compile-time.  xc: 0 = not an x seam, 1 = x seam with this CTA
+  // on the low side (the chunk's last plane), 2 = on the high side (the
+  // chunk's first plane)
+  auto finalize_node3 = [&](auto bb, auto cc, const double* pe, const double* pc,
+                            const double* tpl, int64_t g0, int xc, bool latn, double imIs) {
+    constexpr int b = decltype(bb)::value, c = decltype(cc)::value;
     // own cell, then the y-, z- and yz-neighbour below (fixed order)
     double f = pe[(b * Q + c) * NT];
     if (b == 0 && jl > 0) f += pe[(P * Q + c) * NT - CZ];
     if (c == 0 && kl > 0) f += pe[(b * Q + P) * NT - 1];
     if (b == 0 && c == 0 && jl > 0 && kl > 0) f += pe[(P * Q + P) * NT - CZ - 1];
-    const int64_t idx = (int64_t)I * plane_stride + my0 + (int64_t)b * A.NZ + c;
-    const bool seam = xc || (b == 0 && sy_lo) || (b == P && sy_hi) || (c == 0 && sz_lo) ||
-                      (c == P && sz_hi);
+    const int64_t idx = g0 + b * A.NZ + c;
+    const bool ys_lo = b == 0 && sy_lo, zs_lo = c == 0 && sz_lo;
+    const bool seam = xc || ys_lo || (b == P && sy_hi) || zs_lo || (c == P && sz_hi);
     double dc = 0.0;
     if (LATENT && latn) {
-        const double* pc = Ec + a * Q * Q * NT + tid;
-        dc = pc[(b * Q + c) * NT];
-        if (b == 0 && jl > 0) dc += pc[(P * Q + c) * NT - CZ];
-        if (c == 0 && kl > 0) dc += pc[(b * Q + P) * NT - 1];
-        if (b == 0 && c == 0 && jl > 0 && kl > 0) dc += pc[(P * Q + P) * NT - CZ - 1];
-      }
+      dc = pc[(b * Q + c) * NT];
+      if (b == 0 && jl > 0) dc += pc[(P * Q + c) * NT - CZ];
+      if (c == 0 && kl > 0) dc += pc[(b * Q + P) * NT - 1];
+      if (b == 0 && c == 0 && jl > 0 && kl > 0) dc += pc[(P * Q + P) * NT - CZ - 1];
+    }
     if (seam) {
       // this CTA's partial goes to its own slot (side code per seam axis)
-      const int slot = (xc == 2 ? 1 : 0) + ((b == 0 && sy_lo) ? 2 : 0) + ((c == 0 && sz_lo) ? 4 : 0);
+      const int slot = (xc == 2 ? 1 : 0) + (ys_lo ? 2 : 0) + (zs_lo ? 4 : 0);
       const int64_t so = (int64_t)slot * A.snv + idx;
       A.fseam[so] = f;
       if (LATENT) A.cseam[so] = dc;
     } else {
-      const int K = P * k + c;
-      const double ci = inv_mass1<P>(A, K, A.NZ) * (inv_mass1<P>(A, P * j + b, A.NY) * imIs);
-      const double o =
-          finalize_node(A, ci, K, Tr[(I % NR) * PL + ms0 + b * NZT + c], f, dc, LATENT);
+      const double mzc = c == 0 ? mz_0 : (c == P ? mz_P : A.imr[c]);
+      const double myb = b == 0 ? my_0 : (b == P ? my_P : A.imr[b]);
+      const double ci = mzc * (myb * imIs);
+      const double o = finalize_node(A, ci, c == 0 && k == 0, tpl[b * NZT + c], f, dc, LATENT);
       A.out[idx] = o;
-      amax = fmax(amax, fabs(o));
-      smax = fmax(smax, o);
+      amax = dmax(amax, fabs(o));
+      smax = dmax(smax, o);
       bad |= (o != o);
     }
   };
 
   // every node of plane I owned by this thread (element plane a)
-  auto finalize_owned = [&](int I, int a, int xs, bool latn) {
+  auto finalize_owned = [&](int I, int a, int xc, bool latn) {
     if (!live) return;
     const double imIs = inv_mass1<P>(A, I + A.gI0, A.gNX) * A.inv_rcdw;
-#pragma unroll
-    for (int b = 0; b < P; b++)
-#pragma unroll
-      for (int c = 0; c < P; c++) finalize_node3(I, a, b, c, xs, latn, imIs);
+    const double* pe = E + a * Q * Q * NT + tid;
+    const double* pc = Ec + a * Q * Q * NT + tid;
+    const double* tpl = Tr + (I % NR) * PL + ms0;
+    const int64_t g0 = (int64_t)I * plane_stride + my0;
+    static_for<P>([&](auto bb) {
+      static_for<P>([&](auto cc) { finalize_node3(bb, cc, pe, pc, tpl, g0, xc, latn, imIs); });
+    });
     if (hiZ)
-#pragma unroll
-      for (int b = 0; b < P; b++) finalize_node3(I, a, b, P, xs, latn, imIs);
+      static_for<P>([&](auto bb) { finalize_node3(bb, IC<P>{}, pe, pc, tpl, g0, xc, latn, imIs); });
     if (hiY) {
-#pragma unroll
-      for (int c = 0; c < P; c++) finalize_node3(I, a, P, c, xs, latn, imIs);
-      if (hiZ) finalize_node3(I, a, P, P, xs, latn, imIs);
+      static_for<P>([&](auto cc) { finalize_node3(IC<P>{}, cc, pe, pc, tpl, g0, xc, latn, imIs); });
+      if (hiZ) finalize_node3(IC<P>{}, IC<P>{}, pe, pc, tpl, g0, xc, latn, imIs);
     }
   };
 
   // prologue: the first layer's P+1 planes
-  load_plane(P * i0);
-#pragma unroll 1
-  for (int a = 1; a <= P; a++) load_plane(P * i0 + a);
+  load_planes(P * i0, P + 1);
   cp_commit();
 
 #pragma unroll 1
   for (int i = i0; i < i1; i++) {
-    if (i + 1 < i1) {
-#pragma unroll 1
-      for (int a = 1; a <= P; a++) load_plane(P * (i + 1) + a);
-    }
+    if (i + 1 < i1) load_planes(P * (i + 1) + 1, P);
     cp_commit();
     cp_wait<1>();
     __syncthreads();
@@ -169,7 +175,10 @@ __global__ void __launch_bounds__(CY* CZ, MinBlocks<P>::v) k_xmarch(SArgs A) {
           for (int c = 0; c < Q; c++) t[(a * Q + b) * Q + c] = tp[b * NZT + c];
       }
       const int64_t cell = ((int64_t)i * A.ny + j) * A.nz + k;
-      cell_element<P, RCF, LATENT>(A, F, i, j, k, cell, t, G, lat);
+      const int ib = P * i;
+      cell_element<P, RCF, LATENT>(A, F, i, j, k, cell, t, G, lat, [&](int a, int b, int c) {
+        return Tr[((ib + a) % NR) * PL + ms0 + b * NZT + c];
+      });
       if (LATENT) {
         if (lat) {
           lat_any[i & 1] = 1;
