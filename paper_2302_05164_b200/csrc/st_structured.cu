@@ -716,7 +716,9 @@ struct Structured : Backend {
   int launch_xmarch_t(const SArgs& A) {
     constexpr int PL = (P * CY + 1) * (P * CZ + 1);
     constexpr int EW = P * (P + 1) * (P + 1);
-    const size_t smem = (size_t)((2 * P + 1) * PL + (LAT ? 2 : 1) * EW * CY * CZ) * sizeof(double);
+    const size_t smem =
+        (size_t)((2 * P + 1) * PL + (LAT ? 2 : 1) * EW * CY * CZ + (P + 1) * (P + 1) * CY * CZ) *
+        sizeof(double);
     auto kern = k_xmarch<P, CY, CZ, LAT, RCF>;
     static bool attr = false;
     if (!attr) {

@@ -37,6 +37,9 @@ __global__ void __launch_bounds__(CY* CZ, MinBlocks<P>::v) k_xmarch(SArgs A) {
   double* Tr = sm;            // NR planes of T
   double* E = sm + NR * PL;   // E[q * NT + cell]
   double* Ec = E + EW * NT;   // latent increments (LATENT)
+  // x face carried to the next layer (thread-private slots; smem keeps it
+  // out of the register budget of the cell evaluation)
+  double* Cx = Ec + (LATENT ? EW * NT : 0);
   __shared__ int lat_any[2];  // latent increments in the current / previous layer
   const int tid = threadIdx.x;
   const int lane = tid & 31, warp = tid >> 5;
@@ -85,9 +88,9 @@ __global__ void __launch_bounds__(CY* CZ, MinBlocks<P>::v) k_xmarch(SArgs A) {
   const double my_0 = inv_mass1<P>(A, P * j, A.NY), my_P = inv_mass1<P>(A, P * j + P, A.NY);
   const double mz_0 = inv_mass1<P>(A, P * k, A.NZ), mz_P = inv_mass1<P>(A, P * k + P, A.NZ);
 
-  double carry[Q * Q], carryC[LATENT ? Q * Q : 1];
+  double carryC[LATENT ? Q * Q : 1];
 #pragma unroll
-  for (int q = 0; q < Q * Q; q++) carry[q] = 0.0;
+  for (int q = 0; q < Q * Q; q++) Cx[q * NT + tid] = 0.0;
   if (LATENT)
 #pragma unroll
     for (int q = 0; q < Q * Q; q++) carryC[q] = 0.0;
@@ -202,8 +205,8 @@ __global__ void __launch_bounds__(CY* CZ, MinBlocks<P>::v) k_xmarch(SArgs A) {
       // x face shared with the previous layer: add the carry, keep the new one
 #pragma unroll
       for (int q = 0; q < Q * Q; q++) {
-        G[q] += carry[q];
-        carry[q] = G[P * Q * Q + q];
+        G[q] += Cx[q * NT + tid];
+        Cx[q * NT + tid] = G[P * Q * Q + q];
       }
 #pragma unroll
       for (int q = 0; q < EW; q++) E[q * NT + tid] = G[q];
@@ -220,7 +223,7 @@ __global__ void __launch_bounds__(CY* CZ, MinBlocks<P>::v) k_xmarch(SArgs A) {
   // last node plane of the chunk: the carried x face (as element plane 0)
   if (live) {
 #pragma unroll
-    for (int q = 0; q < Q * Q; q++) E[q * NT + tid] = carry[q];
+    for (int q = 0; q < Q * Q; q++) E[q * NT + tid] = Cx[q * NT + tid];
     if (LATENT)
 #pragma unroll
       for (int q = 0; q < Q * Q; q++) Ec[q * NT + tid] = carryC[q];
