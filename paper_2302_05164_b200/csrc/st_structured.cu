@@ -23,6 +23,8 @@
 // Nodes on tile seams (shared with another CTA) are sent with fp64
 // atomics to a seam buffer and finalised by k_seams.
 #include <cmath>
+#include <cstdlib>
+#include <cstring>
 #include <vector>
 
 #include "st_common.cuh"
@@ -620,6 +622,7 @@ struct Structured : Backend {
   int p = 1;
   int NX = 0, NY = 0, NZ = 0;
   int Lx = 1, cy = 8, cz = 8;
+  bool slab = false;  // k_xslab (p+1 threads per cell) instead of k_xmarch
   int use_lat = 0;
   long long lx = 0, ly = 0, lz = 0;
   DevBuf<double> cinv, fseam, cseam, packf[2], packc[2];
@@ -730,6 +733,30 @@ struct Structured : Backend {
     return launched();
   }
 
+  template <int P, int CY, int CZ, bool LAT, bool RCF>
+  int launch_xslab_t(const SArgs& A) {
+    const size_t smem = (size_t)slab_smem_doubles<P, CY, CZ, LAT>() * sizeof(double);
+    auto kern = k_xslab<P, CY, CZ, LAT, RCF>;
+    static bool attr = false;
+    if (!attr) {
+      ST_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+      attr = true;
+    }
+    dim3 grid((m.ny + CY - 1) / CY, (m.nz + CZ - 1) / CZ, (m.nx + Lx - 1) / Lx);
+    kern<<<grid, (P + 1) * CY * CZ, smem, c->stream>>>(A);
+    return launched();
+  }
+
+  template <int P>
+  int launch_xslab_p(const SArgs& A, bool lat, bool rcf) {
+    constexpr int CY = SlabTile<P>::CY, CZ = SlabTile<P>::CZ;
+    if (lat)
+      return rcf ? launch_xslab_t<P, CY, CZ, true, true>(A)
+                 : launch_xslab_t<P, CY, CZ, true, false>(A);
+    return rcf ? launch_xslab_t<P, CY, CZ, false, true>(A)
+               : launch_xslab_t<P, CY, CZ, false, false>(A);
+  }
+
   template <int P, int CY, int CZ>
   int launch_tile(const SArgs& A, bool lat, bool rcf) {
     if (lat)
@@ -767,11 +794,20 @@ struct Structured : Backend {
     const bool lat = c->dp.latent != 0 && A.mode == 0;
     c->prof_begin();
     int rc;
-    switch (p) {
-      case 1: rc = launch_xmarch_p<1>(A, lat, rcf); break;
-      case 2: rc = launch_xmarch_p<2>(A, lat, rcf); break;
-      case 3: rc = launch_xmarch_p<3>(A, lat, rcf); break;
-      default: rc = launch_xmarch_p<4>(A, lat, rcf); break;
+    if (slab) {
+      switch (p) {
+        case 1: rc = launch_xslab_p<1>(A, lat, rcf); break;
+        case 2: rc = launch_xslab_p<2>(A, lat, rcf); break;
+        case 3: rc = launch_xslab_p<3>(A, lat, rcf); break;
+        default: rc = launch_xslab_p<4>(A, lat, rcf); break;
+      }
+    } else {
+      switch (p) {
+        case 1: rc = launch_xmarch_p<1>(A, lat, rcf); break;
+        case 2: rc = launch_xmarch_p<2>(A, lat, rcf); break;
+        case 3: rc = launch_xmarch_p<3>(A, lat, rcf); break;
+        default: rc = launch_xmarch_p<4>(A, lat, rcf); break;
+      }
     }
     c->prof_end();
     ST_TRY(rc);
@@ -991,11 +1027,26 @@ Backend* make_structured(Ctx* c, const st_structured_mesh* m, int* err) {
   s->NY = m->degree * m->ny + 1;
   s->NZ = m->degree * m->nz + 1;
   s->nv = (int64_t)s->NX * s->NY * s->NZ;
-  switch (s->p) {
-    case 1: s->cy = Tile<1>::CY; s->cz = Tile<1>::CZ; break;
-    case 2: s->cy = Tile<2>::CY; s->cz = Tile<2>::CZ; break;
-    case 3: s->cy = Tile<3>::CY; s->cz = Tile<3>::CZ; break;
-    default: s->cy = Tile<4>::CY; s->cz = Tile<4>::CZ; break;
+  // kernel per degree (measured); ST_KERNEL=march|slab overrides
+  s->slab = s->p >= 3;
+  if (const char* e = getenv("ST_KERNEL")) {
+    if (!strcmp(e, "slab")) s->slab = true;
+    if (!strcmp(e, "march")) s->slab = false;
+  }
+  if (s->slab) {
+    switch (s->p) {
+      case 1: s->cy = SlabTile<1>::CY; s->cz = SlabTile<1>::CZ; break;
+      case 2: s->cy = SlabTile<2>::CY; s->cz = SlabTile<2>::CZ; break;
+      case 3: s->cy = SlabTile<3>::CY; s->cz = SlabTile<3>::CZ; break;
+      default: s->cy = SlabTile<4>::CY; s->cz = SlabTile<4>::CZ; break;
+    }
+  } else {
+    switch (s->p) {
+      case 1: s->cy = Tile<1>::CY; s->cz = Tile<1>::CZ; break;
+      case 2: s->cy = Tile<2>::CY; s->cz = Tile<2>::CZ; break;
+      case 3: s->cy = Tile<3>::CY; s->cz = Tile<3>::CZ; break;
+      default: s->cy = Tile<4>::CY; s->cz = Tile<4>::CZ; break;
+    }
   }
   // x chunk: enough CTAs for ~4 per SM on 148 SMs
   const int64_t nyz = (int64_t)((m->ny + s->cy - 1) / s->cy) * ((m->nz + s->cz - 1) / s->cz);

@@ -248,3 +248,4 @@ __device__ __forceinline__ void static_for(F&& f) {
   static_for_(f, std::make_integer_sequence<int, N>{});
 }
 #include "st_xmarch_kernel.cuh"
+#include "st_xslab_kernel.cuh"

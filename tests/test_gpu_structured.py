@@ -81,7 +81,7 @@ def test_structured_implicit_pieces_match_oracle(p):
         assert rel(op.jacobian_diagonal(T, rc, dt), orc.jacobian_diagonal(T, rc, dt)) < 1e-12
 
 
-@pytest.mark.parametrize("p", [1, 2])
+@pytest.mark.parametrize("p", [1, 2, 3, 4])
 def test_structured_latent_heat_and_convection(p):
     box, op, orc, T, rc, beams, tb = _setup(p, latent=True, hconv=10.0, seed=3)
     # put a band of nodes inside the latent interval
@@ -93,7 +93,7 @@ def test_structured_latent_heat_and_convection(p):
     assert rel(op.lumped_capacity(T), orc.lumped_capacity(T)) < 1e-12
 
 
-@pytest.mark.parametrize("p", [1, 2])
+@pytest.mark.parametrize("p", [1, 2, 3, 4])
 def test_structured_resident_loop_matches_oracle(p):
     """Multi-step device loop with a per-qp history field and the fused
     (deferred) history update."""
@@ -113,6 +113,19 @@ def test_structured_resident_loop_matches_oracle(p):
     assert rel(Tg, To) < 1e-12
     assert rel(rcg, rco.reshape(-1)) < 1e-13
     assert tmax == pytest.approx(max(float(To.max()), 0.0), rel=1e-3) or tmax >= To.max() - 1
+
+
+@pytest.mark.parametrize("kernel", ["march", "slab"])
+@pytest.mark.parametrize("p", [1, 2, 3, 4])
+def test_structured_both_hot_kernels_match_oracle(p, kernel, monkeypatch):
+    """k_xmarch (one thread per cell) and k_xslab (p+1 threads per cell)
+    are both kept; ST_KERNEL picks one at context creation."""
+    monkeypatch.setenv("ST_KERNEL", kernel)
+    box, op, orc, T, rc, beams, tb = _setup(p, latent=True, hconv=10.0, seed=21)
+    T[::5] = 1900.0
+    dt = 2e-7
+    assert rel(op.explicit_fused_step(T, dt, rc, beams), orc.explicit_step(T, dt, rc, tb)) < 1e-12
+    assert rel(op.evaluate_rhs(T, rc, beams), orc.evaluate_rhs(T, rc, tb)) < 1e-12
 
 
 def test_structured_q1_config0_matches_reference():
