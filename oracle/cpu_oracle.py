@@ -302,6 +302,11 @@ class OracleOperator:
         V = self.tb.V
         elem = sweep3_t(V, V, V, rc * self.det_w)
         out = self.scatter(elem.reshape(self.n, -1))
+        if T is not None:
+            # extension rule: the latent increment counts only when positive
+            # (degree >= 2 Lagrange bases are negative at some Gauss points,
+            # so a cell partly in the latent interval can lump a negative one)
+            out = np.maximum(out, self.lumped_capacity())
         out[self.M["is_slave"]] = 1.0
         return out
 

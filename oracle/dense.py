@@ -53,6 +53,7 @@ def dense_system(M, params, T, r_c, beams=()):
     nv = int(M["nv"])
     D = np.zeros((nv, nv))
     Cl = np.zeros(nv)
+    Cl0 = np.zeros(nv)
     f = np.zeros(nv)
     L = float(getattr(mat, "latent_heat", 0.0) or 0.0)
     hconv = float(getattr(bp, "h_conv", 0.0) or 0.0)
@@ -91,6 +92,7 @@ def dense_system(M, params, T, r_c, beams=()):
                         cap += mat.rho * L / (mat.T_lat_l - mat.T_lat_s)
                     D[np.ix_(nodes, nodes)] += w * k * grad @ grad.T
                     Cl[nodes] += w * cap * phi
+                    Cl0[nodes] += w * (mat.rho * mat.c) * phi
                     X = x0 + (np.array([qa, qb, qc]) + 1.0) / 2.0 * h
                     for (bx, by, zt, P) in beams:
                         if P <= 0.0:
@@ -124,4 +126,6 @@ def dense_system(M, params, T, r_c, beams=()):
                         qf += mdot * (bp.h_v + mat.c * (Tc - bp.T_h0))
                     qf += hconv * (Tq - bp.T_inf)
                     f[ids] -= w * qf * phi
-    return -D @ T + f, Cl
+    # extension rule: the latent increment of a lumped row counts only when
+    # positive (degree >= 2 bases are negative at some Gauss points)
+    return -D @ T + f, np.maximum(Cl, Cl0)

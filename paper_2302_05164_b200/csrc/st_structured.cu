@@ -448,6 +448,15 @@ __global__ void k_sgeneric(GArgs A, int mode) {
 
 // C^-1 of the constant lumped capacity as a tensor product of 1D lumped
 // masses (row sums of the consistent capacity, operators.py:325-334)
+// lumped apparent capacity floored at the constant one (finalize_node)
+__global__ void k_cap_floor(int64_t n, const double* cinv, double* out) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i < n) {
+    const double c0 = 1.0 / cinv[i];
+    out[i] = out[i] > c0 ? out[i] : c0;
+  }
+}
+
 template <int P>
 __global__ void k_cinv(int NX, int NY, int NZ, double rc_detw, double* out) {
   const int64_t n = (int64_t)NX * NY * NZ;
@@ -931,7 +940,9 @@ struct Structured : Backend {
       return ST_OK;
     }
     ST_CUDA(cudaMemsetAsync(out, 0, nv * sizeof(double), c->stream));
-    return generic(1, T, nullptr, nullptr, 0.0, out);
+    ST_TRY(generic(1, T, nullptr, nullptr, 0.0, out));
+    k_cap_floor<<<(unsigned)((nv + 255) / 256), 256, 0, c->stream>>>(nv, cinv.p, out);
+    return launched();
   }
 
   int mass(const double* v, double* out) override {

@@ -230,7 +230,10 @@ __device__ __forceinline__ void cell_element(const SArgs& A, const CellFlags& F,
 __device__ __forceinline__ double finalize_node(const SArgs& A, double ci, bool bottom, double T,
                                                 double f, double dc, bool latent) {
   if (A.mode == 1) return f;
-  if (latent && dc != 0.0) ci = 1.0 / (1.0 / ci + dc);
+  // the latent increment of the lumped capacity only counts when positive:
+  // Lagrange bases of degree >= 2 are negative at some Gauss points, so a
+  // cell partly in the latent interval can lump a negative increment
+  if (latent && dc > 0.0) ci = 1.0 / (1.0 / ci + dc);
   double o = T + A.dt * (ci * f);
   if (A.dir_bottom && bottom) o = A.P.T_inf;
   return o;
