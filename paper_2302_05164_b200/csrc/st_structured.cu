@@ -34,6 +34,7 @@ namespace st {
 
 constexpr int kMQ = 5;
 __constant__ double sV[4][kMQ][kMQ];   // V[a][q]   nodal basis a at Gauss point q
+__constant__ double sD[4][kMQ][kMQ];  // D[a][q] = l_a'(x_q) (reference-coordinate slope)
 __constant__ double sDq[4][kMQ][kMQ];  // Dq[m][q]: dT/dxi(q) = sum_m Dq[m][q] T(m)
 __constant__ double sW[4][kMQ];        // Gauss weights
 __constant__ double sU[4][kMQ];        // (x_q + 1) / 2
@@ -283,7 +284,6 @@ __global__ void k_iface_pack(SArgs A, int P, int CY, int CZ, int side, int laten
 // generic one-thread-per-cell kernels with fp64 atomics (per-call API and
 // the implicit path on structured meshes; not the explicit hot loop)
 // ---------------------------------------------------------------------------
-__constant__ double sD[4][kMQ][kMQ];  // D[a][q] = l_a'(x_q) (reference-coordinate slope)
 
 struct GArgs {
   int nx, ny, nz, NX, NY, NZ;

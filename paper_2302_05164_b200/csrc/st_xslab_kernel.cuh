@@ -8,13 +8,12 @@
 // through conflict-free shared-memory exchanges among the p+1 slab threads
 // of the cell (entry-major X[(b, c, s)][cell], a warp = 32 cells of one s).
 // Per cell layer:
-//   B1  the layer's node planes are in the ring (cp.async, prefetched one
-//       layer ahead)
-//   1.  x-interpolation from the ring at Gauss point s, y/z sweeps -> T_q
-//       of slab s; write T_q to X                                     B2
-//   2.  grad_x from X (Dq column s), grad_y / grad_z in registers,
-//       k(T, r_c), fluxes; y/z flux terms accumulated in registers, x
-//       fluxes written to Y                                           B3
+//   B1  the layer's node planes are in the ring (cp.async, prefetched
+//       from B3 of the previous layer)
+//   1.  T and dT/dx at Gauss point s of x in one pass over the ring (V and
+//       D columns s), y/z interpolation sweeps of both; top facet term
+//   2.  grad_y / grad_z by Gauss-point collocation, k(T, r_c), fluxes; y/z
+//       flux terms accumulated in registers, x fluxes written to Y      B3
 //   3.  x flux term from Y (Dq row s); y/z transposed sweeps; Gaussian
 //       source (x factor at Gauss point s) and top facet (x-interpolated
 //       at s) added before the x projection; write to X              B4
@@ -23,28 +22,36 @@
 //       carry, planes a < p go to Y as element planes                 B5
 //   5.  node finalisation of planes a < p (same fixed-order gather and
 //       seam slots as k_xmarch)
-// The latent capacity increments follow the same projections (XL / EL /
-// CL) in layers where some cell of the CTA has a Gauss point in the
-// latent interval (__syncthreads_or at B4).
+// The latent capacity increments follow the same projections through X
+// (three extra barriers) in layers where some cell of the CTA has a Gauss
+// point in the latent interval (__syncthreads_or at B4); their element
+// planes stay in X for the finalisation and their x face is carried in CL.
 #pragma once
 
+// tile (CY x CZ cells), min CTAs per SM, and the ring: SHORT keeps only the
+// layer's P+1 planes (prefetch after step 1, finalisation reads T from
+// global), otherwise 2P+1 planes (prefetch a whole layer ahead)
 template <int P>
 struct SlabTile;
 template <>
 struct SlabTile<1> {
-  static constexpr int CY = 4, CZ = 32;
+  static constexpr int CY = 4, CZ = 32, MINB = 2;
+  static constexpr bool SHORT = false;
 };
 template <>
 struct SlabTile<2> {
-  static constexpr int CY = 2, CZ = 16;
+  static constexpr int CY = 2, CZ = 16, MINB = 5;
+  static constexpr bool SHORT = false;
 };
 template <>
 struct SlabTile<3> {
-  static constexpr int CY = 4, CZ = 8;
+  static constexpr int CY = 4, CZ = 8, MINB = 3;
+  static constexpr bool SHORT = true;
 };
 template <>
 struct SlabTile<4> {
-  static constexpr int CY = 4, CZ = 8;
+  static constexpr int CY = 4, CZ = 8, MINB = 1;
+  static constexpr bool SHORT = false;
 };
 
 // shared memory of k_xslab in doubles
@@ -52,8 +59,8 @@ template <int P, int CY, int CZ, bool LATENT>
 constexpr int slab_smem_doubles() {
   constexpr int Q = P + 1, Q2 = Q * Q, Q3 = Q2 * Q, NC = CY * CZ;
   constexpr int PL = (P * CY + 1) * (P * CZ + 1);
-  return (2 * P + 1) * PL + 2 * Q3 * NC + 2 * Q2 * NC +
-         (LATENT ? Q3 * NC + P * Q2 * NC + 2 * Q2 * NC : 0);
+  return (SlabTile<P>::SHORT ? P + 1 : 2 * P + 1) * PL + 2 * Q3 * NC + 2 * Q2 * NC +
+         (LATENT ? 2 * Q2 * NC : 0);
 }
 
 // in-place 1D sweep of a Q x Q register slab t[b * Q + c] along b (AX 0)
@@ -79,20 +86,21 @@ __device__ __forceinline__ void sweep2(double* t) {
 }
 
 template <int P, int CY, int CZ, bool LATENT, bool RCF>
-__global__ void __launch_bounds__((P + 1) * CY * CZ) k_xslab(SArgs A) {
+__global__ void __launch_bounds__((P + 1) * CY * CZ, SlabTile<P>::MINB) k_xslab(SArgs A) {
   constexpr int Q = P + 1, Q2 = Q * Q, Q3 = Q2 * Q;
   constexpr int NC = CY * CZ, NT = Q * NC;
   constexpr int NYT = P * CY + 1, NZT = P * CZ + 1, PL = NYT * NZT;
-  constexpr int NR = 2 * P + 1;  // ring: current layer (P+1 planes) + next layer (P)
+  // ring: the layer's P+1 node planes; the next layer's P new planes are
+  // prefetched into the first P slots once step 1 is done with them (B3)
+  constexpr bool SHORT = SlabTile<P>::SHORT;
+  constexpr int NR = SHORT ? P + 1 : 2 * P + 1;
   using B = Basis<P>;
   extern __shared__ double sm[];
   double* Tr = sm;                 // NR planes of T
   double* X = Tr + NR * PL;        // exchange: Gauss-point T, then y/z-projected G
   double* Y = X + Q3 * NC;         // exchange: x fluxes, then element planes a < P
   double* Cx = Y + Q3 * NC;        // carried x face [layer parity][Q2][NC]
-  double* XL = Cx + 2 * Q2 * NC;   // LATENT: y/z-projected capacity increments
-  double* EL = XL + Q3 * NC;       // LATENT: element planes a < P of the increments
-  double* CL = EL + P * Q2 * NC;   // LATENT: carried face [parity][Q2][NC]
+  double* CL = Cx + 2 * Q2 * NC;   // LATENT: carried face of the increments
   const int tid = threadIdx.x;
   const int s = tid / NC, cl = tid - (tid / NC) * NC;
   const int jl = cl / CZ, kl = cl - (cl / CZ) * CZ;
@@ -162,7 +170,8 @@ __global__ void __launch_bounds__((P + 1) * CY * CZ) k_xslab(SArgs A) {
       const double mzc = c == 0 ? mz_0 : (c == P ? mz_P : A.imr[c]);
       const double myb = b == 0 ? my_0 : (b == P ? my_P : A.imr[b]);
       const double ci = mzc * (myb * imIs);
-      const double o = finalize_node(A, ci, c == 0 && k == 0, tpl[b * NZT + c], f, dc, LATENT);
+      const double Tn = SHORT ? A.T[idx] : tpl[b * NZT + c];
+      const double o = finalize_node(A, ci, c == 0 && k == 0, Tn, f, dc, LATENT);
       A.out[idx] = o;
       amax = dmax(amax, fabs(o));
       smax = dmax(smax, o);
@@ -173,8 +182,8 @@ __global__ void __launch_bounds__((P + 1) * CY * CZ) k_xslab(SArgs A) {
   // nodes of plane I owned by this cell, element plane at pe (stride NC)
   auto finalize_owned = [&](int I, const double* pe, const double* pc, int xc, bool latn) {
     const double imIs = inv_mass1<P>(A, I + A.gI0, A.gNX) * A.inv_rcdw;
-    const double* tpl = Tr + (I % NR) * PL + ms0;
     const int64_t g0 = (int64_t)I * plane_stride + my0;
+    const double* tpl = Tr + (I % NR) * PL + ms0;
     static_for<P>([&](auto bb) {
       static_for<P>([&](auto cc) { finalize_node3(bb, cc, pe, pc, tpl, g0, xc, latn, imIs); });
     });
@@ -198,50 +207,73 @@ __global__ void __launch_bounds__((P + 1) * CY * CZ) k_xslab(SArgs A) {
 #pragma unroll 1
   for (int i = i0; i < i1; i++) {
     cp_wait<0>();
-    __syncthreads();  // B1: ring holds layer i; last layer's X / Y / ring reads are done
-    if (i + 1 < i1) {
+    __syncthreads();  // B1: ring holds layer i; last layer's X / Y reads are done
+    if (!SHORT && i + 1 < i1) {
       load_planes(P * (i + 1) + 1, P);
       cp_commit();
     }
     const int ib = P * i;
     const int64_t cell = ((int64_t)i * A.ny + j) * A.nz + k;
-    double T[Q2], G[Q2];
+    double T[Q2], G[Q2], ftop[Q];
     unsigned lmask = 0;
     if (live) {
-      // 1. x interpolation at Gauss point s, then the y and z sweeps
+      // 1. T and dT/dx at Gauss point s of x from the ring (one pass over
+      //    the layer's nodes), then the y and z interpolation sweeps
+      double Tx[Q2];
 #pragma unroll
-      for (int q = 0; q < Q2; q++) T[q] = 0.0;
+      for (int q = 0; q < Q2; q++) {
+        T[q] = 0.0;
+        Tx[q] = 0.0;
+      }
 #pragma unroll
       for (int a = 0; a < Q; a++) {
-        const double va = sV[P - 1][a][s];
+        const double va = sV[P - 1][a][s], da = sD[P - 1][a][s];
         const double* tp = Tr + ((ib + a) % NR) * PL + ms0;
 #pragma unroll
         for (int b = 0; b < Q; b++)
 #pragma unroll
-          for (int c = 0; c < Q; c++) T[b * Q + c] = fma(va, tp[b * NZT + c], T[b * Q + c]);
+          for (int c = 0; c < Q; c++) {
+            const double v = tp[b * NZT + c];
+            T[b * Q + c] = fma(va, v, T[b * Q + c]);
+            Tx[b * Q + c] = fma(da, v, Tx[b * Q + c]);
+          }
+      }
+      if (top) {
+        // +z facet (operators.py:275-290): the c = P face values are
+        // x-interpolated at Gauss point s already; y-interpolate, flux,
+        // y-project onto the nodes (b, P)
+        const double area0 = A.hh * A.hh;
+        const double ws = sW[P - 1][s];
+        double fq[Q];
+#pragma unroll
+        for (int qb = 0; qb < Q; qb++) {
+          double acc = B::V(0, qb) * T[0 * Q + P];
+#pragma unroll
+          for (int b = 1; b < Q; b++) acc = fma(B::V(b, qb), T[b * Q + P], acc);
+          fq[qb] = surface_flux(PP, acc) * (-(area0 * (ws * B::W(qb))));
+        }
+#pragma unroll
+        for (int b = 0; b < Q; b++) {
+          double acc = B::V(b, 0) * fq[0];
+#pragma unroll
+          for (int qb = 1; qb < Q; qb++) acc = fma(B::V(b, qb), fq[qb], acc);
+          ftop[b] = acc;
+        }
       }
       sweep2<P, 1, false, false>(T);
       sweep2<P, 0, false, false>(T);
 #pragma unroll
-      for (int q = 0; q < Q2; q++) X[(q * Q + s) * NC + cl] = T[q];
-    }
-    __syncthreads();  // B2
-    if (live) {
-#pragma unroll
       for (int q = 0; q < Q2; q++) G[q] = 0.0;
       if (F.diffusion) {
-        double dqs[Q];
-#pragma unroll
-        for (int m = 0; m < Q; m++) dqs[m] = sDq[P - 1][m][s];
+        sweep2<P, 1, false, false>(Tx);
+        sweep2<P, 0, false, false>(Tx);
+        // 2. fluxes at the Gauss points of slab s
 #pragma unroll
         for (int qb = 0; qb < Q; qb++)
 #pragma unroll
           for (int qc = 0; qc < Q; qc++) {
             const int q = qb * Q + qc;
-            const double* xp = X + q * Q * NC + cl;
-            double gx = dqs[0] * xp[0];
-#pragma unroll
-            for (int m = 1; m < Q; m++) gx = fma(dqs[m], xp[m * NC], gx);
+            const double gx = Tx[q];
             double gy = B::Dq(0, qb) * T[0 * Q + qc];
             double gz = B::Dq(0, qc) * T[qb * Q + 0];
 #pragma unroll
@@ -282,7 +314,11 @@ __global__ void __launch_bounds__((P + 1) * CY * CZ) k_xslab(SArgs A) {
           if (fabs(T[q] - A.lat_mid) < A.lat_half) lmask |= 1u << q;
       }
     }
-    __syncthreads();  // B3
+    __syncthreads();  // B3: (SHORT) the ring's first P slots are free
+    if (SHORT && i + 1 < i1) {
+      load_planes(P * (i + 1) + 1, P);
+      cp_commit();
+    }
     if (live) {
       if (F.diffusion) {
         double dqt[Q];
@@ -337,58 +373,30 @@ __global__ void __launch_bounds__((P + 1) * CY * CZ) k_xslab(SArgs A) {
         }
       }
       if (top) {
-        // +z facet (operators.py:275-290): face values x-interpolated at
-        // Gauss point s, y-interpolated, flux, y-projected onto c = P
-        double tf[Q];
 #pragma unroll
-        for (int b = 0; b < Q; b++) tf[b] = 0.0;
-#pragma unroll
-        for (int a = 0; a < Q; a++) {
-          const double va = sV[P - 1][a][s];
-          const double* tp = Tr + ((ib + a) % NR) * PL + ms0;
-#pragma unroll
-          for (int b = 0; b < Q; b++) tf[b] = fma(va, tp[b * NZT + P], tf[b]);
-        }
-        const double area0 = A.hh * A.hh;
-        const double ws = sW[P - 1][s];
-        double fq[Q];
-#pragma unroll
-        for (int qb = 0; qb < Q; qb++) {
-          double acc = B::V(0, qb) * tf[0];
-#pragma unroll
-          for (int b = 1; b < Q; b++) acc = fma(B::V(b, qb), tf[b], acc);
-          fq[qb] = surface_flux(PP, acc) * (-(area0 * (ws * B::W(qb))));
-        }
-#pragma unroll
-        for (int b = 0; b < Q; b++) {
-          double acc = B::V(b, 0) * fq[0];
-#pragma unroll
-          for (int qb = 1; qb < Q; qb++) acc = fma(B::V(b, qb), fq[qb], acc);
-          G[b * Q + P] += acc;
-        }
+        for (int b = 0; b < Q; b++) G[b * Q + P] += ftop[b];
       }
 #pragma unroll
       for (int q = 0; q < Q2; q++) X[(q * Q + s) * NC + cl] = G[q];
-      if (LATENT && lmask) {
+      if (LATENT) {
+        // y/z-projected capacity increments of slab s, kept in T
 #pragma unroll
         for (int q = 0; q < Q2; q++) T[q] = (lmask >> q) & 1u ? A.lw3[s * Q2 + q] : 0.0;
-        sweep2<P, 0, true, false>(T);
-        sweep2<P, 1, true, false>(T);
-#pragma unroll
-        for (int q = 0; q < Q2; q++) XL[(q * Q + s) * NC + cl] = T[q];
-      } else if (LATENT) {
-#pragma unroll
-        for (int q = 0; q < Q2; q++) XL[(q * Q + s) * NC + cl] = 0.0;
+        if (lmask) {
+          sweep2<P, 0, true, false>(T);
+          sweep2<P, 1, true, false>(T);
+        }
       }
     }
     // B4 (+ does any cell of the tile have latent increments in this layer)
     const bool lat_now = LATENT ? __syncthreads_or(lmask != 0u) != 0 : (__syncthreads(), false);
+    const bool latn = LATENT && (lat_now || lat_prev);
     const int par = i & 1;
+    double vt[Q];
+#pragma unroll
+    for (int m = 0; m < Q; m++) vt[m] = sV[P - 1][s][m];
     if (live) {
       // 4. x projection onto node plane a = s
-      double vt[Q];
-#pragma unroll
-      for (int m = 0; m < Q; m++) vt[m] = sV[P - 1][s][m];
 #pragma unroll
       for (int q = 0; q < Q2; q++) {
         const double* xp = X + q * Q * NC + cl;
@@ -404,33 +412,45 @@ __global__ void __launch_bounds__((P + 1) * CY * CZ) k_xslab(SArgs A) {
       double* dst = s == P ? Cx + par * Q2 * NC : Y + s * Q2 * NC;
 #pragma unroll
       for (int q = 0; q < Q2; q++) dst[q * NC + cl] = G[q];
-      if (LATENT && (lat_now || lat_prev)) {
-        if (lat_now) {
+    }
+    if (LATENT && latn) {
+      // latent layers only: the same x projection through X (three extra
+      // barriers), element planes of the increments back into X
+      if (lat_now) {
+        __syncthreads();
+        if (live) {
+#pragma unroll
+          for (int q = 0; q < Q2; q++) X[(q * Q + s) * NC + cl] = T[q];
+        }
+        __syncthreads();
+        if (live) {
 #pragma unroll
           for (int q = 0; q < Q2; q++) {
-            const double* xp = XL + q * Q * NC + cl;
+            const double* xp = X + q * Q * NC + cl;
             double acc = vt[0] * xp[0];
 #pragma unroll
             for (int m = 1; m < Q; m++) acc = fma(vt[m], xp[m * NC], acc);
             T[q] = acc;
           }
-        } else {
-#pragma unroll
-          for (int q = 0; q < Q2; q++) T[q] = 0.0;
         }
-        if (s == 0 && lat_prev) {
+      } else {
 #pragma unroll
-          for (int q = 0; q < Q2; q++) T[q] += CL[((par ^ 1) * Q2 + q) * NC + cl];
-        }
-        double* dl = s == P ? CL + par * Q2 * NC : EL + s * Q2 * NC;
+        for (int q = 0; q < Q2; q++) T[q] = 0.0;
+      }
+      if (live && s == 0 && lat_prev) {
+#pragma unroll
+        for (int q = 0; q < Q2; q++) T[q] += CL[((par ^ 1) * Q2 + q) * NC + cl];
+      }
+      __syncthreads();
+      if (live) {
+        double* dl = s == P ? CL + par * Q2 * NC : X + s * Q2 * NC;
 #pragma unroll
         for (int q = 0; q < Q2; q++) dl[q * NC + cl] = T[q];
       }
     }
     __syncthreads();  // B5
-    const bool latn = LATENT && (lat_now || lat_prev);
     if (live && s < P)
-      finalize_owned(ib + s, Y + s * Q2 * NC + cl, EL + s * Q2 * NC + cl,
+      finalize_owned(ib + s, Y + s * Q2 * NC + cl, X + s * Q2 * NC + cl,
                      (s == 0 && i == i0 && (i0 > 0 || A.iface_lo)) ? 2 : 0, latn);
     lat_prev = lat_now;
   }
