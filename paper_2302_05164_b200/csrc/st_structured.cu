@@ -178,8 +178,9 @@ __global__ void k_seams(SArgs A, int P, int CY, int CZ, int nxs, int nys, int nz
   const int nvb = bx * nxs + by * nys + bz * nzs;
   const int sx = P * A.Lx, sy = P * CY;
   const int nchunk = nxs - A.iface_lo - A.iface_hi;  // chunk-boundary x planes
-#pragma unroll 1
-  for (int vb = blockIdx.x; vb < nvb; vb += gridDim.x) {
+  // one node per thread (all loads of the pass in flight at once)
+  {
+    const int vb = blockIdx.x;
     int b = vb, pl;
     if (b < bx * nxs) {
       pl = b / bx;
@@ -218,7 +219,8 @@ __global__ void k_seams(SArgs A, int P, int CY, int CZ, int nxs, int nys, int nz
       J = t - I * A.NY;
       mine = I < A.NX && !x_seam(A, P, I) && !(J > 0 && J < A.NY - 1 && (J % sy) == 0);
     }
-    if (!mine) continue;
+    if (!mine || vb >= nvb) goto done;
+    {
     const int64_t idx = ((int64_t)I * A.NY + J) * A.NZ + K;
     const double T = A.T[idx];
     const bool xs = x_seam(A, P, I);
@@ -250,10 +252,12 @@ __global__ void k_seams(SArgs A, int P, int CY, int CZ, int nxs, int nys, int nz
                        (inv_mass1_rt(A, P, I + A.gI0, A.gNX) * A.inv_rcdw));
     const double o = finalize_node(A, ci, K == 0, T, f, dc, latent != 0);
     A.out[idx] = o;
-    amax = fmax(amax, fabs(o));
-    smax = fmax(smax, o);
-    bad |= (o != o);
+    amax = fabs(o);
+    smax = o;
+    bad = (o != o);
+    }
   }
+done:
   block_max2(bad ? (double)NAN : amax, smax, A.red);
 }
 
@@ -724,13 +728,51 @@ struct Structured : Backend {
     return A;
   }
 
-  template <int P, int CY, int CZ, bool LAT, bool RCF>
-  int launch_xmarch_t(const SArgs& A) {
+  template <int P, int CY, int CZ, bool LAT>
+  static constexpr size_t march_smem() {
     constexpr int PL = (P * CY + 1) * (P * CZ + 1);
     constexpr int EW = P * (P + 1) * (P + 1);
-    const size_t smem =
-        (size_t)((2 * P + 1) * PL + (LAT ? 2 : 1) * EW * CY * CZ + (P + 1) * (P + 1) * CY * CZ) *
-        sizeof(double);
+    return (size_t)((2 * P + 1) * PL + (LAT ? 2 : 1) * EW * CY * CZ +
+                    (P + 1) * (P + 1) * CY * CZ) *
+           sizeof(double);
+  }
+
+  // resident CTAs per SM of the hot kernel this context launches
+  template <int P>
+  int resident_p(bool lat) const {
+    int nb = 0;
+    if (slab) {
+      constexpr int CY = SlabTile<P>::CY, CZ = SlabTile<P>::CZ;
+      const size_t smem = (size_t)(lat ? slab_smem_doubles<P, CY, CZ, true>()
+                                       : slab_smem_doubles<P, CY, CZ, false>()) *
+                          sizeof(double);
+      auto k = lat ? k_xslab<P, CY, CZ, true, false> : k_xslab<P, CY, CZ, false, false>;
+      if (cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) ==
+          cudaSuccess)
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k, (P + 1) * CY * CZ, smem);
+    } else {
+      constexpr int CY = Tile<P>::CY, CZ = Tile<P>::CZ;
+      const size_t smem = lat ? march_smem<P, CY, CZ, true>() : march_smem<P, CY, CZ, false>();
+      auto k = lat ? k_xmarch<P, CY, CZ, true, false> : k_xmarch<P, CY, CZ, false, false>;
+      if (cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) ==
+          cudaSuccess)
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k, CY * CZ, smem);
+    }
+    cudaGetLastError();
+    return nb > 0 ? nb : 1;
+  }
+  int resident(bool lat) const {
+    switch (p) {
+      case 1: return resident_p<1>(lat);
+      case 2: return resident_p<2>(lat);
+      case 3: return resident_p<3>(lat);
+      default: return resident_p<4>(lat);
+    }
+  }
+
+  template <int P, int CY, int CZ, bool LAT, bool RCF>
+  int launch_xmarch_t(const SArgs& A) {
+    const size_t smem = march_smem<P, CY, CZ, LAT>();
     auto kern = k_xmarch<P, CY, CZ, LAT, RCF>;
     static bool attr = false;
     if (!attr) {
@@ -791,7 +833,7 @@ struct Structured : Backend {
     const int bz = (int)(((int64_t)NX * NY + kThreads - 1) / kThreads);
     const int64_t blocks = (int64_t)bx * nxs + (int64_t)by * nys + (int64_t)bz * nzs;
     if (blocks > 0) {
-      const unsigned grid = (unsigned)std::min<int64_t>(blocks, 4 * 148);
+      const unsigned grid = (unsigned)blocks;
       k_seams<<<grid, kThreads, 0, c->stream>>>(A, p, cy, cz, nxs, nys, nzs, bx, by, bz,
                                                 lat ? 1 : 0);
       ST_TRY(launched());
@@ -1059,12 +1101,26 @@ Backend* make_structured(Ctx* c, const st_structured_mesh* m, int* err) {
       default: s->cy = Tile<4>::CY; s->cz = Tile<4>::CZ; break;
     }
   }
-  // x chunk: enough CTAs for ~4 per SM on 148 SMs
+  // x chunk length: the CTAs (yz tiles x chunks) run in waves of
+  // (resident per SM) x (SMs); pick the chunking with the smallest
+  // waves x (layers per CTA + overhead) (ties: fewer chunks, fewer x seams)
   const int64_t nyz = (int64_t)((m->ny + s->cy - 1) / s->cy) * ((m->nz + s->cz - 1) / s->cz);
-  const int64_t want = 4 * 148;
-  int64_t chunks = std::max<int64_t>(1, (want + nyz - 1) / nyz);
-  s->Lx = (int)std::max<int64_t>(4, (m->nx + chunks - 1) / chunks);
-  s->Lx = std::min(s->Lx, m->nx);
+  int sms = 148;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c->device);
+  const int64_t slots = (int64_t)s->resident(c->dp.latent != 0) * std::max(sms, 1);
+  int64_t best = -1;
+  s->Lx = m->nx;
+  for (int L = m->nx; L >= std::min(2, m->nx); L--) {
+    const int64_t ch = (m->nx + L - 1) / L;
+    if ((m->nx + ch - 1) / ch != L) continue;  // same chunking as a longer L
+    // + 2 layers per CTA for its prologue planes, tail plane and x seam
+    const int64_t cost = ((nyz * ch + slots - 1) / slots) * (int64_t)(L + 2);
+    if (best < 0 || cost < best) {
+      best = cost;
+      s->Lx = L;
+    }
+  }
+  if (const char* e = getenv("ST_LX")) s->Lx = std::max(1, std::min(atoi(e), m->nx));
   s->use_lat = lattice_origin(m->x0, m->h, &s->lx) && lattice_origin(m->y0, m->h, &s->ly) &&
                lattice_origin(m->z0, m->h, &s->lz);
   c->nv = s->nv;

@@ -40,7 +40,7 @@ struct SlabTile<1> {
 };
 template <>
 struct SlabTile<2> {
-  static constexpr int CY = 2, CZ = 16, MINB = 5;
+  static constexpr int CY = 4, CZ = 8, MINB = 5;
   static constexpr bool SHORT = false;
 };
 template <>

@@ -7,7 +7,7 @@ cmd="python bench.py --steps 3 --warmup 3 --sweep 0 --no-cpu-baseline $*"
 $cmd > gpurun_out/plain_$tag.log 2>&1
 ncu --metrics gpu__time_duration.sum --clock-control none --csv \
     --log-file gpurun_out/launches_$tag.csv $cmd > gpurun_out/ncu_launch_$tag.log 2>&1
-ncu --set full --clock-control none --import-source on -k regex:"k_x(march|slab)" -s 4 -c 1 \
+ncu --set full --clock-control none --import-source on -k regex:"${KREGEX:-k_x(march|slab)}" -s 4 -c 1 \
     -o gpurun_out/prof_$tag -f $cmd > gpurun_out/ncu_full_$tag.log 2>&1
 # export the pages read here (raw metrics, source/SASS with per-line counts);
 # the report itself is dropped unless KEEP_REP=1 (gpurun_out is capped at 64 MiB)
