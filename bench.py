@@ -256,6 +256,20 @@ def cpu_baseline(w, seconds=15.0):
 # GPU runs
 # ---------------------------------------------------------------------------
 
+def ncu_traffic(key, kernel):
+    """DRAM bytes per launch of the hot kernel from the committed ncu
+    capture of the same workload (profiles/traffic.json), if it is the
+    kernel that ran."""
+    try:
+        idx = json.load(open(os.path.join(ROOT, "profiles", "traffic.json")))
+    except (OSError, ValueError):
+        return None
+    e = idx.get(key or "")
+    if not e or not kernel or kernel.split("<")[0] not in e["kernel"]:
+        return None
+    return e
+
+
 def dist_env():
     return (int(os.environ.get("WORLD_SIZE", "1")), int(os.environ.get("RANK", "0")),
             int(os.environ.get("LOCAL_RANK", "0")))
@@ -282,11 +296,16 @@ def gpu_measure(w, steps, warmup, device, clocks=True):
     peak, peak_kind = measured_hbm_peak()
     achieved = bpd * box.n_dofs / main_avg_s / 1e9
     _, _, main_name = op.profile_read()
+    ncu = ncu_traffic(w.get("key"), main_name)
     roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                "frac": achieved / peak, "traffic": None, "kernel": main_name,
+                "frac": achieved / peak, "traffic": ncu.get("dram_bytes") if ncu else None,
+                "kernel": main_name,
                 "bytes_per_dof": bpd, "peak_source": peak_kind,
                 "kernel_ms": float(np.mean(main_ms)),
                 "kernel_share_of_step": float(np.sum(main_ms) / np.sum(step_ms))}
+    if ncu:
+        roofline["ncu"] = {k: ncu[k] for k in ("fp64_pipe_pct", "issue_active_pct", "duration_us",
+                                               "source") if k in ncu}
     return dict(op=op, box=box, dts=dts, beams=beams, T0=T0, step_ms=step_ms,
                 launches=launches, roofline=roofline, clocks=clk.summary() if clk else None)
 
@@ -303,7 +322,7 @@ def run_slabs(args):
     ws, rank, local = dist_env()
     torch.cuda.set_device(local)
     dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    w = WORKLOADS[args.workload]()
+    w = dict(WORKLOADS[args.workload](), key=args.workload)
     nx, ny, nz = w["dims"]
     glob = st.StructuredBox(nx * ws, ny, nz, w["h"], degree=w["degree"])
     c0, c1 = partition(glob.nx, ws)[rank]
@@ -381,7 +400,7 @@ def run_ours(args):
     ws, rank, local = dist_env()
     if ws > 1:
         return run_slabs(args)
-    w = WORKLOADS[args.workload]()
+    w = dict(WORKLOADS[args.workload](), key=args.workload)
     if ws > 1:
         torch.distributed.barrier()
     torch.cuda.synchronize()
@@ -425,13 +444,15 @@ def run_ours(args):
     if rank == 0 and ws == 1 and args.sweep:
         sweep = {}
         for p in (1, 2, 3, 4):
-            wp = workload_config2(p)
+            wp = dict(workload_config2(p), key=f"config2_p{p}")
             rp = gpu_measure(wp, args.sweep_steps, 3, local, clocks=False)
             sweep[f"q{p}"] = {"dofs": rp["box"].n_dofs,
                               "value": rp["box"].n_dofs * args.sweep_steps
                               / (float(np.sum(rp["step_ms"])) * 1e-3),
                               "ms_per_step": float(np.mean(rp["step_ms"])),
                               "roofline_frac": rp["roofline"]["frac"],
+                              "kernel": rp["roofline"]["kernel"],
+                              "traffic": rp["roofline"]["traffic"],
                               "achieved_GBps": rp["roofline"]["achieved"]}
             rp["op"].close()
         out["sweep_config2"] = sweep
@@ -451,7 +472,7 @@ def run_reference(args):
     if rank != 0:
         return
     from threadpoolctl import threadpool_limits
-    w = WORKLOADS[args.workload]()
+    w = dict(WORKLOADS[args.workload](), key=args.workload)
     cores = os.cpu_count() or 1
     s = CpuSample(w)
     with threadpool_limits(limits=cores):
