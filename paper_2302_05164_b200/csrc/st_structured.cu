@@ -27,12 +27,10 @@
 #include <cstring>
 #include <vector>
 
-#include "st_common.cuh"
-#include "st_basis_tables.h"
+#include "st_structured.cuh"
 
 namespace st {
 
-constexpr int kMQ = 5;
 __constant__ double sV[4][kMQ][kMQ];   // V[a][q]   nodal basis a at Gauss point q
 __constant__ double sD[4][kMQ][kMQ];  // D[a][q] = l_a'(x_q) (reference-coordinate slope)
 __constant__ double sDq[4][kMQ][kMQ];  // Dq[m][q]: dT/dxi(q) = sum_m Dq[m][q] T(m)
@@ -40,69 +38,6 @@ __constant__ double sW[4][kMQ];        // Gauss weights
 __constant__ double sU[4][kMQ];        // (x_q + 1) / 2
 __constant__ double sM[4][kMQ];        // 1D lumped mass of node a: sum_q W_q V[a][q]
 
-struct SArgs {
-  int nx, ny, nz, NX, NY, NZ;
-  int Lx;
-  double h, hh, detw0;  // h, h/2, (h/2)^3
-  double ox, oy, oz;    // origin (m)
-  long long lx, ly, lz; // lattice origin (cells) when exact
-  int use_lat;
-  int dir_bottom, top_faces;
-  int mode;  // 0: explicit step (out = T'), 1: rhs (out = f)
-  int flags;
-  double frozen_k;
-  const double* T;
-  double* out;
-  const double* cinv;
-  double* rc;
-  double rc_value;
-  int pending;
-  // seam partial sums: 8 slot arrays of nv doubles (slot = x side + 2 y
-  // side + 4 z side of the writing CTA), plain stores, no clearing
-  double* fseam;
-  double* cseam;
-  int64_t snv;
-  // rank interfaces: own pre-summed plane (packed after the sweep) and the
-  // neighbour's, per side (0: local plane 0, 1: local plane NX-1)
-  double* ipf[2];
-  double* ipc[2];
-  const double* irf[2];
-  const double* irc[2];
-  int nb;
-  const DevBeam* beams;
-  double dt;
-  DevParams P;
-  unsigned long long* red;
-  // uniform consolidated history (r_c = rc_value >= 1 >= g): the law
-  // k = (r_p k_p + g k_m) + r_s k_s collapses to k = kA + g kB
-  double kA, kB;
-  double glo;     // -T_s / (T_l - T_s): g = clamp(T * inv_dT_l + glo)
-  double lat_mid, lat_half;  // latent interval as |T - mid| < half
-  double hw3[125];  // (h/2) W_qa W_qb W_qc      (diffusion weight)
-  double lw3[125];  // rho L/dT (h/2)^3 W3        (latent capacity bump)
-  // C^-1 of the constant lumped capacity as a tensor product of inverse
-  // 1D lumped masses (row sums, operators.py:325-334):
-  // C^-1(I,J,K) = inv_rcdw im(I) im(J) im(K)
-  double inv_rcdw;
-  double imr[5];          // interior node residue a = 1..P-1
-  double imv_int, imv_end;  // cell vertex inside / at the end of the line
-  // x-slab of a larger box: global plane offset / count, rank interfaces
-  int gI0, gNX, iface_lo, iface_hi;
-};
-
-// x seam: chunk boundary inside the slab, or a rank interface
-__device__ __forceinline__ bool x_seam(const SArgs& A, int P, int I) {
-  return (I > 0 && I < A.NX - 1 && (I % (P * A.Lx)) == 0) || (I == 0 && A.iface_lo) ||
-         (I == A.NX - 1 && A.iface_hi);
-}
-
-// inverse 1D lumped mass of node L on a line of N nodes
-template <int P>
-__device__ __forceinline__ double inv_mass1(const SArgs& A, int L, int N) {
-  const int a = L % P;
-  if (a != 0) return A.imr[a];
-  return (L == 0 || L == N - 1) ? A.imv_end : A.imv_int;
-}
 
 template <int P>
 __device__ __forceinline__ double coord(const SArgs& A, int axis, int cell, int q) {
@@ -119,47 +54,6 @@ __device__ __forceinline__ double coord(const SArgs& A, int axis, int cell, int 
   return q < 0 ? anc : anc + sU[P - 1][q] * A.h;
 }
 
-// in-place 1D sweep along one axis of a Q^3 register tensor:
-// out[.., q, ..] = sum_m M[m][q] in[.., m, ..]   (TR: M[q][m])
-template <int P, int AX, bool TR>
-__device__ __forceinline__ void sweep_v(double* t) {
-  constexpr int Q = P + 1;
-  constexpr int S = AX == 0 ? Q * Q : (AX == 1 ? Q : 1);
-#pragma unroll
-  for (int o1 = 0; o1 < Q; o1++)
-#pragma unroll
-    for (int o2 = 0; o2 < Q; o2++) {
-      int base = AX == 0 ? (o1 * Q + o2) : (AX == 1 ? (o1 * Q * Q + o2) : (o1 * Q * Q + o2 * Q));
-      double in[Q];
-#pragma unroll
-      for (int m = 0; m < Q; m++) in[m] = t[base + m * S];
-#pragma unroll
-      for (int q = 0; q < Q; q++) {
-        // compile-time coefficients (st_basis_tables.h): exact zeros of the
-        // GLL/Gauss tables vanish from the instruction stream
-        double acc = (TR ? Basis<P>::V(q, 0) : Basis<P>::V(0, q)) * in[0];
-#pragma unroll
-        for (int m = 1; m < Q; m++)
-          acc = fma(TR ? Basis<P>::V(q, m) : Basis<P>::V(m, q), in[m], acc);
-        t[base + q * S] = acc;
-      }
-    }
-}
-
-template <int P>
-__device__ __forceinline__ void interp3(double* t) {
-  sweep_v<P, 2, false>(t);
-  sweep_v<P, 1, false>(t);
-  sweep_v<P, 0, false>(t);
-}
-template <int P>
-__device__ __forceinline__ void project3(double* t) {
-  sweep_v<P, 0, true>(t);
-  sweep_v<P, 1, true>(t);
-  sweep_v<P, 2, true>(t);
-}
-
-#include "st_xmarch.cuh"
 
 // inverse 1D lumped mass, runtime degree (seam kernel)
 __device__ __forceinline__ double inv_mass1_rt(const SArgs& A, int P, int L, int N) {
@@ -611,25 +505,6 @@ static int init_struct_constants() {
   return ST_OK;
 }
 
-template <int P>
-struct Tile;
-template <>
-struct Tile<1> {
-  static constexpr int CY = 8, CZ = 32;
-};
-template <>
-struct Tile<2> {
-  static constexpr int CY = 8, CZ = 16;
-};
-template <>
-struct Tile<3> {
-  static constexpr int CY = 8, CZ = 8;
-};
-template <>
-struct Tile<4> {
-  static constexpr int CY = 4, CZ = 8;
-};
-
 struct Structured : Backend {
   st_structured_mesh m{};
   int p = 1;
@@ -638,7 +513,7 @@ struct Structured : Backend {
   bool slab = false;  // k_xslab (p+1 threads per cell) instead of k_xmarch
   int use_lat = 0;
   long long lx = 0, ly = 0, lz = 0;
-  DevBuf<double> cinv, fseam, cseam, packf[2], packc[2];
+  DevBuf<double> cinv, fseam, cseam, lcarry, packf[2], packc[2];
   int64_t nv = 0;
 
   int launched() {
@@ -672,6 +547,7 @@ struct Structured : Backend {
     A.rc_value = c->rc_value;
     A.fseam = fseam.p;
     A.cseam = cseam.p;
+    A.lcarry = lcarry.p;
     A.snv = nv;
     for (int sd = 0; sd < 2; sd++) {
       A.ipf[sd] = packf[sd].p;
@@ -728,98 +604,14 @@ struct Structured : Backend {
     return A;
   }
 
-  template <int P, int CY, int CZ, bool LAT>
-  static constexpr size_t march_smem() {
-    constexpr int PL = (P * CY + 1) * (P * CZ + 1);
-    constexpr int EW = P * (P + 1) * (P + 1);
-    return (size_t)((2 * P + 1) * PL + (LAT ? 2 : 1) * EW * CY * CZ +
-                    (P + 1) * (P + 1) * CY * CZ) *
-           sizeof(double);
-  }
-
   // resident CTAs per SM of the hot kernel this context launches
-  template <int P>
-  int resident_p(bool lat) const {
-    int nb = 0;
-    if (slab) {
-      constexpr int CY = SlabTile<P>::CY, CZ = SlabTile<P>::CZ;
-      const size_t smem = (size_t)(lat ? slab_smem_doubles<P, CY, CZ, true>()
-                                       : slab_smem_doubles<P, CY, CZ, false>()) *
-                          sizeof(double);
-      auto k = lat ? k_xslab<P, CY, CZ, true, false> : k_xslab<P, CY, CZ, false, false>;
-      if (cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) ==
-          cudaSuccess)
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k, (P + 1) * CY * CZ, smem);
-    } else {
-      constexpr int CY = Tile<P>::CY, CZ = Tile<P>::CZ;
-      const size_t smem = lat ? march_smem<P, CY, CZ, true>() : march_smem<P, CY, CZ, false>();
-      auto k = lat ? k_xmarch<P, CY, CZ, true, false> : k_xmarch<P, CY, CZ, false, false>;
-      if (cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) ==
-          cudaSuccess)
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k, CY * CZ, smem);
-    }
-    cudaGetLastError();
-    return nb > 0 ? nb : 1;
-  }
   int resident(bool lat) const {
     switch (p) {
-      case 1: return resident_p<1>(lat);
-      case 2: return resident_p<2>(lat);
-      case 3: return resident_p<3>(lat);
-      default: return resident_p<4>(lat);
+      case 1: return hot_resident<1>(slab, lat);
+      case 2: return hot_resident<2>(slab, lat);
+      case 3: return hot_resident<3>(slab, lat);
+      default: return hot_resident<4>(slab, lat);
     }
-  }
-
-  template <int P, int CY, int CZ, bool LAT, bool RCF>
-  int launch_xmarch_t(const SArgs& A) {
-    const size_t smem = march_smem<P, CY, CZ, LAT>();
-    auto kern = k_xmarch<P, CY, CZ, LAT, RCF>;
-    static bool attr = false;
-    if (!attr) {
-      ST_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-      attr = true;
-    }
-    dim3 grid((m.ny + CY - 1) / CY, (m.nz + CZ - 1) / CZ, (m.nx + Lx - 1) / Lx);
-    kern<<<grid, CY * CZ, smem, c->stream>>>(A);
-    return launched();
-  }
-
-  template <int P, int CY, int CZ, bool LAT, bool RCF>
-  int launch_xslab_t(const SArgs& A) {
-    const size_t smem = (size_t)slab_smem_doubles<P, CY, CZ, LAT>() * sizeof(double);
-    auto kern = k_xslab<P, CY, CZ, LAT, RCF>;
-    static bool attr = false;
-    if (!attr) {
-      ST_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-      attr = true;
-    }
-    dim3 grid((m.ny + CY - 1) / CY, (m.nz + CZ - 1) / CZ, (m.nx + Lx - 1) / Lx);
-    kern<<<grid, (P + 1) * CY * CZ, smem, c->stream>>>(A);
-    return launched();
-  }
-
-  template <int P>
-  int launch_xslab_p(const SArgs& A, bool lat, bool rcf) {
-    constexpr int CY = SlabTile<P>::CY, CZ = SlabTile<P>::CZ;
-    if (lat)
-      return rcf ? launch_xslab_t<P, CY, CZ, true, true>(A)
-                 : launch_xslab_t<P, CY, CZ, true, false>(A);
-    return rcf ? launch_xslab_t<P, CY, CZ, false, true>(A)
-               : launch_xslab_t<P, CY, CZ, false, false>(A);
-  }
-
-  template <int P, int CY, int CZ>
-  int launch_tile(const SArgs& A, bool lat, bool rcf) {
-    if (lat)
-      return rcf ? launch_xmarch_t<P, CY, CZ, true, true>(A)
-                 : launch_xmarch_t<P, CY, CZ, true, false>(A);
-    return rcf ? launch_xmarch_t<P, CY, CZ, false, true>(A)
-               : launch_xmarch_t<P, CY, CZ, false, false>(A);
-  }
-
-  template <int P>
-  int launch_xmarch_p(const SArgs& A, bool lat, bool rcf) {
-    return launch_tile<P, Tile<P>::CY, Tile<P>::CZ>(A, lat, rcf);
   }
 
   int seams(SArgs& A) {
@@ -844,21 +636,20 @@ struct Structured : Backend {
   int xmarch(SArgs& A, bool rcf, bool with_seams = true) {
     const bool lat = c->dp.latent != 0 && A.mode == 0;
     c->prof_begin();
-    int rc;
-    if (slab) {
-      switch (p) {
-        case 1: rc = launch_xslab_p<1>(A, lat, rcf); break;
-        case 2: rc = launch_xslab_p<2>(A, lat, rcf); break;
-        case 3: rc = launch_xslab_p<3>(A, lat, rcf); break;
-        default: rc = launch_xslab_p<4>(A, lat, rcf); break;
-      }
+    const dim3 grid((m.ny + cy - 1) / cy, (m.nz + cz - 1) / cz, (m.nx + Lx - 1) / Lx);
+    cudaError_t e;
+    switch (p) {
+      case 1: e = hot_launch<1>(A, slab, lat, rcf, grid, c->stream); break;
+      case 2: e = hot_launch<2>(A, slab, lat, rcf, grid, c->stream); break;
+      case 3: e = hot_launch<3>(A, slab, lat, rcf, grid, c->stream); break;
+      default: e = hot_launch<4>(A, slab, lat, rcf, grid, c->stream); break;
+    }
+    int rc = ST_OK;
+    if (e != cudaSuccess) {
+      set_error(std::string("hot kernel launch: ") + cudaGetErrorString(e));
+      rc = ST_ECUDA;
     } else {
-      switch (p) {
-        case 1: rc = launch_xmarch_p<1>(A, lat, rcf); break;
-        case 2: rc = launch_xmarch_p<2>(A, lat, rcf); break;
-        case 3: rc = launch_xmarch_p<3>(A, lat, rcf); break;
-        default: rc = launch_xmarch_p<4>(A, lat, rcf); break;
-      }
+      rc = launched();
     }
     c->prof_end();
     ST_TRY(rc);
@@ -1129,6 +920,11 @@ Backend* make_structured(Ctx* c, const st_structured_mesh* m, int* err) {
   rc = s->cinv.alloc(s->nv);
   if (rc == ST_OK) rc = s->fseam.alloc(8 * s->nv);
   if (rc == ST_OK && c->dp.latent) rc = s->cseam.alloc(8 * s->nv);
+  if (rc == ST_OK && c->dp.latent && !s->slab) {
+    const size_t ctas = (size_t)((m->ny + s->cy - 1) / s->cy) * ((m->nz + s->cz - 1) / s->cz) *
+                        ((m->nx + s->Lx - 1) / s->Lx);
+    rc = s->lcarry.alloc(ctas * s->cy * s->cz * (s->p + 1) * (s->p + 1));
+  }
   if (rc == ST_OK &&
       cudaMemsetAsync(s->fseam.p, 0, 8 * s->nv * sizeof(double), c->stream) != cudaSuccess)
     rc = ST_ECUDA;

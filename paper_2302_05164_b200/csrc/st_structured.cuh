@@ -1,0 +1,189 @@
+// Structured backend: kernel argument block and the device helpers shared
+// by the host-side backend (st_structured.cu) and the per-degree hot-kernel
+// translation units (st_hot_p{1..4}.cu, compiled in parallel).
+#pragma once
+#include "st_common.cuh"
+#include "st_basis_tables.h"
+
+namespace st {
+
+constexpr int kMQ = 5;
+
+struct SArgs {
+  int nx, ny, nz, NX, NY, NZ;
+  int Lx;
+  double h, hh, detw0;  // h, h/2, (h/2)^3
+  double ox, oy, oz;    // origin (m)
+  long long lx, ly, lz; // lattice origin (cells) when exact
+  int use_lat;
+  int dir_bottom, top_faces;
+  int mode;  // 0: explicit step (out = T'), 1: rhs (out = f)
+  int flags;
+  double frozen_k;
+  const double* T;
+  double* out;
+  const double* cinv;
+  double* rc;
+  double rc_value;
+  int pending;
+  // seam partial sums: 8 slot arrays of nv doubles (slot = x side + 2 y
+  // side + 4 z side of the writing CTA), plain stores, no clearing
+  double* fseam;
+  double* cseam;
+  // k_xmarch latent x-face carry, per (CTA, thread) slot (Q^2 doubles
+  // entry-major); only touched by cells with latent Gauss points
+  double* lcarry;
+  int64_t snv;
+  // rank interfaces: own pre-summed plane (packed after the sweep) and the
+  // neighbour's, per side (0: local plane 0, 1: local plane NX-1)
+  double* ipf[2];
+  double* ipc[2];
+  const double* irf[2];
+  const double* irc[2];
+  int nb;
+  const DevBeam* beams;
+  double dt;
+  DevParams P;
+  unsigned long long* red;
+  // uniform consolidated history (r_c = rc_value >= 1 >= g): the law
+  // k = (r_p k_p + g k_m) + r_s k_s collapses to k = kA + g kB
+  double kA, kB;
+  double glo;     // -T_s / (T_l - T_s): g = clamp(T * inv_dT_l + glo)
+  double lat_mid, lat_half;  // latent interval as |T - mid| < half
+  double hw3[125];  // (h/2) W_qa W_qb W_qc      (diffusion weight)
+  double lw3[125];  // rho L/dT (h/2)^3 W3        (latent capacity bump)
+  // C^-1 of the constant lumped capacity as a tensor product of inverse
+  // 1D lumped masses (row sums, operators.py:325-334):
+  // C^-1(I,J,K) = inv_rcdw im(I) im(J) im(K)
+  double inv_rcdw;
+  double imr[5];          // interior node residue a = 1..P-1
+  double imv_int, imv_end;  // cell vertex inside / at the end of the line
+  // x-slab of a larger box: global plane offset / count, rank interfaces
+  int gI0, gNX, iface_lo, iface_hi;
+};
+
+// x seam: chunk boundary inside the slab, or a rank interface
+__device__ __forceinline__ bool x_seam(const SArgs& A, int P, int I) {
+  return (I > 0 && I < A.NX - 1 && (I % (P * A.Lx)) == 0) || (I == 0 && A.iface_lo) ||
+         (I == A.NX - 1 && A.iface_hi);
+}
+
+// inverse 1D lumped mass of node L on a line of N nodes
+template <int P>
+__device__ __forceinline__ double inv_mass1(const SArgs& A, int L, int N) {
+  const int a = L % P;
+  if (a != 0) return A.imr[a];
+  return (L == 0 || L == N - 1) ? A.imv_end : A.imv_int;
+}
+
+// in-place 1D sweep along one axis of a Q^3 register tensor:
+// out[.., q, ..] = sum_m M[m][q] in[.., m, ..]   (TR: M[q][m])
+template <int P, int AX, bool TR>
+__device__ __forceinline__ void sweep_v(double* t) {
+  constexpr int Q = P + 1;
+  constexpr int S = AX == 0 ? Q * Q : (AX == 1 ? Q : 1);
+#pragma unroll
+  for (int o1 = 0; o1 < Q; o1++)
+#pragma unroll
+    for (int o2 = 0; o2 < Q; o2++) {
+      int base = AX == 0 ? (o1 * Q + o2) : (AX == 1 ? (o1 * Q * Q + o2) : (o1 * Q * Q + o2 * Q));
+      double in[Q];
+#pragma unroll
+      for (int m = 0; m < Q; m++) in[m] = t[base + m * S];
+#pragma unroll
+      for (int q = 0; q < Q; q++) {
+        // compile-time coefficients (st_basis_tables.h): exact zeros of the
+        // GLL/Gauss tables vanish from the instruction stream
+        double acc = (TR ? Basis<P>::V(q, 0) : Basis<P>::V(0, q)) * in[0];
+#pragma unroll
+        for (int m = 1; m < Q; m++)
+          acc = fma(TR ? Basis<P>::V(q, m) : Basis<P>::V(m, q), in[m], acc);
+        t[base + q * S] = acc;
+      }
+    }
+}
+
+template <int P>
+__device__ __forceinline__ void interp3(double* t) {
+  sweep_v<P, 2, false>(t);
+  sweep_v<P, 1, false>(t);
+  sweep_v<P, 0, false>(t);
+}
+template <int P>
+__device__ __forceinline__ void project3(double* t) {
+  sweep_v<P, 0, true>(t);
+  sweep_v<P, 1, true>(t);
+  sweep_v<P, 2, true>(t);
+}
+
+
+// node update with its complete f (operators.py:359-368); with the latent
+// extension the lumped capacity is C_const + dC(T)
+__device__ __forceinline__ double finalize_node(const SArgs& A, double ci, bool bottom, double T,
+                                                double f, double dc, bool latent) {
+  if (A.mode == 1) return f;
+  // the latent increment of the lumped capacity only counts when positive:
+  // Lagrange bases of degree >= 2 are negative at some Gauss points, so a
+  // cell partly in the latent interval can lump a negative increment
+  if (latent && dc > 0.0) ci = 1.0 / (1.0 / ci + dc);
+  double o = T + A.dt * (ci * f);
+  if (A.dir_bottom && bottom) o = A.P.T_inf;
+  return o;
+}
+
+// tile of k_xmarch (CY x CZ cells, one thread per cell)
+template <int P>
+struct Tile;
+template <>
+struct Tile<1> {
+  static constexpr int CY = 8, CZ = 32;
+};
+template <>
+struct Tile<2> {
+  static constexpr int CY = 8, CZ = 16;
+};
+template <>
+struct Tile<3> {
+  static constexpr int CY = 8, CZ = 8;
+};
+template <>
+struct Tile<4> {
+  static constexpr int CY = 4, CZ = 8;
+};
+
+// tile of k_xslab (CY x CZ cells, p+1 threads per cell), min CTAs per SM,
+// and the ring: SHORT keeps only the layer's P+1 planes (prefetch after
+// step 1, finalisation reads T from global), otherwise 2P+1 planes
+template <int P>
+struct SlabTile;
+template <>
+struct SlabTile<1> {
+  static constexpr int CY = 4, CZ = 32, MINB = 2;
+  static constexpr bool SHORT = false;
+};
+template <>
+struct SlabTile<2> {
+  static constexpr int CY = 4, CZ = 8, MINB = 5;
+  static constexpr bool SHORT = false;
+};
+template <>
+struct SlabTile<3> {
+  static constexpr int CY = 4, CZ = 8, MINB = 3;
+  static constexpr bool SHORT = true;
+};
+template <>
+struct SlabTile<4> {
+  static constexpr int CY = 4, CZ = 8, MINB = 1;
+  static constexpr bool SHORT = false;
+};
+
+// Hot kernels of degree P (defined in st_hot_p<P>.cu):
+//   hot_resident: resident CTAs per SM of the kernel a context launches
+//   hot_launch:   one launch of k_xmarch / k_xslab over `grid`
+template <int P>
+int hot_resident(bool slab, bool lat);
+template <int P>
+cudaError_t hot_launch(const SArgs& A, bool slab, bool lat, bool rcf, dim3 grid,
+                       cudaStream_t stream);
+
+}  // namespace st

@@ -5,6 +5,8 @@
 #include <type_traits>
 #include <utility>
 
+namespace st {
+
 struct CellFlags {
   bool diffusion, faces, source, frozen;
 };
@@ -65,23 +67,41 @@ __device__ __forceinline__ void source_factors(const SArgs& A, const DevBeam& b,
   }
 }
 
+// Beams whose cell-level hit test (beam_hits_cell) can pass for some cell
+// of the (y, z) column (j, k): the y box distance and the slab overlap are
+// fixed over the x march, and dy^2 <= cut^2 is necessary for
+// dx^2 + dy^2 <= cut^2.  The exact test still runs per cell.
+template <int P>
+__device__ __forceinline__ unsigned beam_column_mask(const SArgs& A, int j, int k) {
+  unsigned mask = 0;
+  const double ay = anchor<P>(A, 1, j), az = anchor<P>(A, 2, k);
+  const int nb = A.nb < 32 ? A.nb : 32;
+#pragma unroll 1
+  for (int b = 0; b < nb; b++) {
+    const DevBeam bm = A.beams[b];
+    if (bm.peak == 0.0) continue;
+    const double dy = fmax(fmax(ay - bm.y, bm.y - ay - A.h), 0.0);
+    if (dy * dy <= A.P.cut2 && az <= bm.z_top && az + A.h >= bm.z_top - A.P.h_powder)
+      mask |= 1u << b;
+  }
+  return mask;
+}
+
 // Element vector of one cell, degree P (operators.py:247-316 generalised):
-//   t in : node values (a x b x c, z fastest)
+//   t in : T at the Gauss points (a x b x c, z fastest; kept for the
+//          latent capacity pass of the caller)
 //   G out: element vector
-//   t out: with LATENT and has_lat, the projected apparent-capacity
-//          increment rho L/dT_lat over the Gauss points in the interval
 //   node(a, b, c): re-reads a node value (top facet; keeps t's copy out of
 //          the register budget)
-template <int P, bool RCF, bool LATENT, class NodeF>
+template <int P, bool RCF, class NodeF>
 __device__ __forceinline__ void cell_element(const SArgs& A, const CellFlags& F, int i, int j,
-                                             int k, int64_t cell, double* t, double* G,
-                                             bool& has_lat, const NodeF& node) {
+                                             int k, int64_t cell, const double* t, double* G,
+                                             unsigned ymask, const NodeF& node) {
   constexpr int Q = P + 1;
   constexpr int Q3 = Q * Q * Q;
   using B = Basis<P>;
   const DevParams& PP = A.P;
   const bool top = F.faces && A.top_faces && (k == A.nz - 1);
-  interp3<P>(t);  // T at the Gauss points
 #pragma unroll
   for (int q = 0; q < Q3; q++) G[q] = 0.0;
   if (F.diffusion) {
@@ -131,20 +151,11 @@ __device__ __forceinline__ void cell_element(const SArgs& A, const CellFlags& F,
         }
   }
   project3<P>(G);
-  if (LATENT) {
-    has_lat = false;
-#pragma unroll
-    for (int q = 0; q < Q3; q++) {
-      const bool in = fabs(t[q] - A.lat_mid) < A.lat_half;
-      has_lat |= in;
-      t[q] = in ? A.lw3[q] : 0.0;
-    }
-    if (has_lat) project3<P>(t);
-  }
-  if (F.source) {
+  if (F.source && (ymask || A.nb > 32)) {
     const double ax = anchor<P>(A, 0, i), ay = anchor<P>(A, 1, j), az = anchor<P>(A, 2, k);
 #pragma unroll 1
     for (int b = 0; b < A.nb; b++) {
+      if (b < 32 && !((ymask >> b) & 1u)) continue;  // column prefilter
       const DevBeam bm = A.beams[b];
       if (!beam_hits_cell(PP, bm, ax, ay, az, A.h)) continue;
       double sx[Q], sy[Q], sz[Q];
@@ -195,11 +206,11 @@ __device__ __forceinline__ void cell_element(const SArgs& A, const CellFlags& F,
       }
     }
     const double area0 = A.hh * A.hh;
-#pragma unroll 1
-    for (int q = 0; q < Q * Q; q++) {
-      const int qa = q / Q, qb = q - (q / Q) * Q;
-      fq[q] = surface_flux(PP, fq[q]) * (-(area0 * (sW[P - 1][qa] * sW[P - 1][qb])));
-    }
+#pragma unroll
+    for (int qa = 0; qa < Q; qa++)
+#pragma unroll
+      for (int qb = 0; qb < Q; qb++)
+        fq[qa * Q + qb] = surface_flux(PP, fq[qa * Q + qb]) * (-(area0 * (B::W(qa) * B::W(qb))));
 #pragma unroll
     for (int qb = 0; qb < Q; qb++) {
       double in[Q];
@@ -225,20 +236,6 @@ __device__ __forceinline__ void cell_element(const SArgs& A, const CellFlags& F,
   }
 }
 
-// node update with its complete f (operators.py:359-368); with the latent
-// extension the lumped capacity is C_const + dC(T)
-__device__ __forceinline__ double finalize_node(const SArgs& A, double ci, bool bottom, double T,
-                                                double f, double dc, bool latent) {
-  if (A.mode == 1) return f;
-  // the latent increment of the lumped capacity only counts when positive:
-  // Lagrange bases of degree >= 2 are negative at some Gauss points, so a
-  // cell partly in the latent interval can lump a negative increment
-  if (latent && dc > 0.0) ci = 1.0 / (1.0 / ci + dc);
-  double o = T + A.dt * (ci * f);
-  if (A.dir_bottom && bottom) o = A.P.T_inf;
-  return o;
-}
-
 // compile-time loops (node offsets inside a cell become immediates)
 template <int N>
 using IC = std::integral_constant<int, N>;
@@ -252,3 +249,5 @@ __device__ __forceinline__ void static_for(F&& f) {
 }
 #include "st_xmarch_kernel.cuh"
 #include "st_xslab_kernel.cuh"
+
+}  // namespace st

@@ -43,7 +43,13 @@ __global__ void __launch_bounds__(CY* CZ, MinBlocks<P>::v) k_xmarch(SArgs A) {
   __shared__ int lat_any[2];  // latent increments in the current / previous layer
   const int tid = threadIdx.x;
   const int lane = tid & 31, warp = tid >> 5;
-  const int jl = tid / CZ, kl = tid - (tid / CZ) * CZ;
+  // P >= 2: z-major cell order inside the CTA (tid = kl * CY + jl), so the
+  // top cell row of a tile (facet term) falls in one warp instead of every
+  // warp.  P = 1 keeps z-fastest lanes (unit-stride ring reads and T'
+  // stores; its facet term is cheap)
+  constexpr bool ZMAJ = P >= 2;
+  const int kl = ZMAJ ? tid / CY : tid % CZ, jl = ZMAJ ? tid % CY : tid / CZ;
+  constexpr int SY = ZMAJ ? 1 : CZ, SZ = ZMAJ ? CY : 1;  // tid stride of the y / z neighbour
   const int j0 = blockIdx.x * CY, k0 = blockIdx.y * CZ, i0 = blockIdx.z * A.Lx;
   if (i0 >= A.nx) return;
   const int i1 = min(i0 + A.Lx, A.nx);
@@ -66,19 +72,19 @@ __global__ void __launch_bounds__(CY* CZ, MinBlocks<P>::v) k_xmarch(SArgs A) {
   const int ms0 = P * jl * NZT + P * kl;
   if (tid < 2) lat_any[tid] = 0;
 
-  // stage planes Ib .. Ib+n-1: thread tid copies tile entries e = tid,
-  // tid + NT, ... (row r = e / NZT of the tile, column e % NZT)
+  // stage planes Ib .. Ib+n-1: warp w copies tile rows w, w + NW, ...;
+  // lane l the row entries l and l + 32 (rows run along z, contiguous)
+  static_assert(NZT <= 64, "tile row wider than two warp passes");
+  const bool c_lo = lane < Kn, c_hi = NZT > 32 && lane + 32 < Kn;
   auto load_planes = [&](int Ib, int n) {
 #pragma unroll 1
     for (int pa = 0; pa < n; pa++) {
-      const double* srcT = A.T + (int64_t)(Ib + pa) * plane_stride + tile0;
-      double* dT = Tr + ((Ib + pa) % NR) * PL;
-#pragma unroll
-      for (int e0 = 0; e0 < PL; e0 += NT) {
-        const int e = e0 + tid;
-        const int r = e / NZT, cc = e - (e / NZT) * NZT;
-        if ((e0 + NT <= PL || e < PL) && r < Jn && cc < Kn)
-          cp_async8(dT + e, srcT + r * A.NZ + cc);
+      const double* srcT = A.T + (int64_t)(Ib + pa) * plane_stride + tile0 + lane;
+      double* dT = Tr + ((Ib + pa) % NR) * PL + lane;
+#pragma unroll 1
+      for (int r = warp; r < Jn; r += NW) {
+        if (c_lo) cp_async8(dT + r * NZT, srcT + (int64_t)r * A.NZ);
+        if (c_hi) cp_async8(dT + r * NZT + 32, srcT + (int64_t)r * A.NZ + 32);
       }
     }
   };
@@ -88,12 +94,14 @@ __global__ void __launch_bounds__(CY* CZ, MinBlocks<P>::v) k_xmarch(SArgs A) {
   const double my_0 = inv_mass1<P>(A, P * j, A.NY), my_P = inv_mass1<P>(A, P * j + P, A.NY);
   const double mz_0 = inv_mass1<P>(A, P * k, A.NZ), mz_P = inv_mass1<P>(A, P * k + P, A.NZ);
 
-  double carryC[LATENT ? Q * Q : 1];
 #pragma unroll
   for (int q = 0; q < Q * Q; q++) Cx[q * NT + tid] = 0.0;
-  if (LATENT)
-#pragma unroll
-    for (int q = 0; q < Q * Q; q++) carryC[q] = 0.0;
+  // latent x-face carry of this thread (global scratch, valid when lat_had)
+  double* lcar = LATENT ? A.lcarry + (((int64_t)blockIdx.z * gridDim.y + blockIdx.y) * gridDim.x +
+                                      blockIdx.x) * (Q * Q * NT) + tid
+                        : nullptr;
+  bool lat_had = false;
+  const unsigned ymask = F.source && live ? beam_column_mask<P>(A, j, k) : 0u;
   double amax = 0.0, smax = -INFINITY;
   bool bad = false;
 
@@ -106,18 +114,18 @@ __global__ void __launch_bounds__(CY* CZ, MinBlocks<P>::v) k_xmarch(SArgs A) {
     constexpr int b = decltype(bb)::value, c = decltype(cc)::value;
     // own cell, then the y-, z- and yz-neighbour below (fixed order)
     double f = pe[(b * Q + c) * NT];
-    if (b == 0 && jl > 0) f += pe[(P * Q + c) * NT - CZ];
-    if (c == 0 && kl > 0) f += pe[(b * Q + P) * NT - 1];
-    if (b == 0 && c == 0 && jl > 0 && kl > 0) f += pe[(P * Q + P) * NT - CZ - 1];
+    if (b == 0 && jl > 0) f += pe[(P * Q + c) * NT - SY];
+    if (c == 0 && kl > 0) f += pe[(b * Q + P) * NT - SZ];
+    if (b == 0 && c == 0 && jl > 0 && kl > 0) f += pe[(P * Q + P) * NT - SY - SZ];
     const int64_t idx = g0 + b * A.NZ + c;
     const bool ys_lo = b == 0 && sy_lo, zs_lo = c == 0 && sz_lo;
     const bool seam = xc || ys_lo || (b == P && sy_hi) || zs_lo || (c == P && sz_hi);
     double dc = 0.0;
     if (LATENT && latn) {
       dc = pc[(b * Q + c) * NT];
-      if (b == 0 && jl > 0) dc += pc[(P * Q + c) * NT - CZ];
-      if (c == 0 && kl > 0) dc += pc[(b * Q + P) * NT - 1];
-      if (b == 0 && c == 0 && jl > 0 && kl > 0) dc += pc[(P * Q + P) * NT - CZ - 1];
+      if (b == 0 && jl > 0) dc += pc[(P * Q + c) * NT - SY];
+      if (c == 0 && kl > 0) dc += pc[(b * Q + P) * NT - SZ];
+      if (b == 0 && c == 0 && jl > 0 && kl > 0) dc += pc[(P * Q + P) * NT - SY - SZ];
     }
     if (seam) {
       // this CTA's partial goes to its own slot (side code per seam axis)
@@ -168,7 +176,6 @@ __global__ void __launch_bounds__(CY* CZ, MinBlocks<P>::v) k_xmarch(SArgs A) {
     __syncthreads();
     if (live) {
       double t[Q3], G[Q3];
-      bool lat = false;
 #pragma unroll
       for (int a = 0; a < Q; a++) {
         const double* tp = Tr + ((P * i + a) % NR) * PL + ms0;
@@ -177,31 +184,12 @@ __global__ void __launch_bounds__(CY* CZ, MinBlocks<P>::v) k_xmarch(SArgs A) {
 #pragma unroll
           for (int c = 0; c < Q; c++) t[(a * Q + b) * Q + c] = tp[b * NZT + c];
       }
+      interp3<P>(t);  // T at the Gauss points
       const int64_t cell = ((int64_t)i * A.ny + j) * A.nz + k;
       const int ib = P * i;
-      cell_element<P, RCF, LATENT>(A, F, i, j, k, cell, t, G, lat, [&](int a, int b, int c) {
+      cell_element<P, RCF>(A, F, i, j, k, cell, t, G, ymask, [&](int a, int b, int c) {
         return Tr[((ib + a) % NR) * PL + ms0 + b * NZT + c];
       });
-      if (LATENT) {
-        if (lat) {
-          lat_any[i & 1] = 1;
-#pragma unroll
-          for (int q = 0; q < Q * Q; q++) {
-            t[q] += carryC[q];
-            carryC[q] = t[P * Q * Q + q];
-          }
-        } else {
-#pragma unroll
-          for (int q = 0; q < Q * Q; q++) {
-            t[q] = carryC[q];
-            carryC[q] = 0.0;
-          }
-#pragma unroll
-          for (int q = Q * Q; q < Q3; q++) t[q] = 0.0;
-        }
-#pragma unroll
-        for (int q = 0; q < EW; q++) Ec[q * NT + tid] = t[q];
-      }
       // x face shared with the previous layer: add the carry, keep the new one
 #pragma unroll
       for (int q = 0; q < Q * Q; q++) {
@@ -210,6 +198,33 @@ __global__ void __launch_bounds__(CY* CZ, MinBlocks<P>::v) k_xmarch(SArgs A) {
       }
 #pragma unroll
       for (int q = 0; q < EW; q++) E[q * NT + tid] = G[q];
+      if (LATENT) {
+        // apparent-capacity increments rho L/dT_lat projected from the Gauss
+        // points inside the latent interval (G is dead here, so t can be
+        // reused); a predicate pass first, most cells have none
+        bool lat = false;
+#pragma unroll
+        for (int q = 0; q < Q3; q++) lat |= fabs(t[q] - A.lat_mid) < A.lat_half;
+        if (lat) {
+          lat_any[i & 1] = 1;
+#pragma unroll
+          for (int q = 0; q < Q3; q++) t[q] = fabs(t[q] - A.lat_mid) < A.lat_half ? A.lw3[q] : 0.0;
+          project3<P>(t);
+#pragma unroll
+          for (int q = 0; q < Q * Q; q++) {
+            if (lat_had) t[q] += lcar[q * NT];
+            lcar[q * NT] = t[P * Q * Q + q];
+          }
+        } else {
+#pragma unroll
+          for (int q = 0; q < Q * Q; q++) t[q] = lat_had ? lcar[q * NT] : 0.0;
+#pragma unroll
+          for (int q = Q * Q; q < EW; q++) t[q] = 0.0;
+        }
+        lat_had = lat;
+#pragma unroll
+        for (int q = 0; q < EW; q++) Ec[q * NT + tid] = t[q];
+      }
     }
     __syncthreads();
     const bool latn = LATENT && (lat_any[0] | lat_any[1]);
@@ -226,7 +241,7 @@ __global__ void __launch_bounds__(CY* CZ, MinBlocks<P>::v) k_xmarch(SArgs A) {
     for (int q = 0; q < Q * Q; q++) E[q * NT + tid] = Cx[q * NT + tid];
     if (LATENT)
 #pragma unroll
-      for (int q = 0; q < Q * Q; q++) Ec[q * NT + tid] = carryC[q];
+      for (int q = 0; q < Q * Q; q++) Ec[q * NT + tid] = lat_had ? lcar[q * NT] : 0.0;
   }
   __syncthreads();
   finalize_owned(P * i1, 0, (i1 < A.nx || A.iface_hi) ? 1 : 0,

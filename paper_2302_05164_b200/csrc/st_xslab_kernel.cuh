@@ -28,32 +28,6 @@
 // planes stay in X for the finalisation and their x face is carried in CL.
 #pragma once
 
-// tile (CY x CZ cells), min CTAs per SM, and the ring: SHORT keeps only the
-// layer's P+1 planes (prefetch after step 1, finalisation reads T from
-// global), otherwise 2P+1 planes (prefetch a whole layer ahead)
-template <int P>
-struct SlabTile;
-template <>
-struct SlabTile<1> {
-  static constexpr int CY = 4, CZ = 32, MINB = 2;
-  static constexpr bool SHORT = false;
-};
-template <>
-struct SlabTile<2> {
-  static constexpr int CY = 4, CZ = 8, MINB = 5;
-  static constexpr bool SHORT = false;
-};
-template <>
-struct SlabTile<3> {
-  static constexpr int CY = 4, CZ = 8, MINB = 3;
-  static constexpr bool SHORT = true;
-};
-template <>
-struct SlabTile<4> {
-  static constexpr int CY = 4, CZ = 8, MINB = 1;
-  static constexpr bool SHORT = false;
-};
-
 // shared memory of k_xslab in doubles
 template <int P, int CY, int CZ, bool LATENT>
 constexpr int slab_smem_doubles() {
@@ -227,7 +201,7 @@ __global__ void __launch_bounds__((P + 1) * CY * CZ, SlabTile<P>::MINB) k_xslab(
       }
 #pragma unroll
       for (int a = 0; a < Q; a++) {
-        const double va = sV[P - 1][a][s], da = sD[P - 1][a][s];
+        const double va = kTab.V[a][s], da = kTab.D[a][s];
         const double* tp = Tr + ((ib + a) % NR) * PL + ms0;
 #pragma unroll
         for (int b = 0; b < Q; b++)
@@ -243,7 +217,7 @@ __global__ void __launch_bounds__((P + 1) * CY * CZ, SlabTile<P>::MINB) k_xslab(
         // x-interpolated at Gauss point s already; y-interpolate, flux,
         // y-project onto the nodes (b, P)
         const double area0 = A.hh * A.hh;
-        const double ws = sW[P - 1][s];
+        const double ws = kTab.W[s];
         double fq[Q];
 #pragma unroll
         for (int qb = 0; qb < Q; qb++) {
@@ -323,7 +297,7 @@ __global__ void __launch_bounds__((P + 1) * CY * CZ, SlabTile<P>::MINB) k_xslab(
       if (F.diffusion) {
         double dqt[Q];
 #pragma unroll
-        for (int m = 0; m < Q; m++) dqt[m] = sDq[P - 1][s][m];
+        for (int m = 0; m < Q; m++) dqt[m] = kTab.Dq[s][m];
 #pragma unroll
         for (int q = 0; q < Q2; q++) {
           const double* yp = Y + q * Q * NC + cl;
@@ -361,8 +335,8 @@ __global__ void __launch_bounds__((P + 1) * CY * CZ, SlabTile<P>::MINB) k_xslab(
             sy[a] = y;
             sz[a] = zz;
           }
-          const double dx = (ax + sU[P - 1][s] * A.h) - bm.x;
-          const double fxs = exp((-2.0 * (dx * dx)) / PP.R2) * sW[P - 1][s];
+          const double dx = (ax + kTab.U[s] * A.h) - bm.x;
+          const double fxs = exp((-2.0 * (dx * dx)) / PP.R2) * kTab.W[s];
           const double coef = (bm.peak * A.detw0) * fxs;
 #pragma unroll
           for (int b = 0; b < Q; b++) {
@@ -394,7 +368,7 @@ __global__ void __launch_bounds__((P + 1) * CY * CZ, SlabTile<P>::MINB) k_xslab(
     const int par = i & 1;
     double vt[Q];
 #pragma unroll
-    for (int m = 0; m < Q; m++) vt[m] = sV[P - 1][s][m];
+    for (int m = 0; m < Q; m++) vt[m] = kTab.V[s][m];
     if (live) {
       // 4. x projection onto node plane a = s
 #pragma unroll
