@@ -17,6 +17,15 @@ OUT = os.path.join(HERE, "libscantherm_b200.so")
 OBJ = os.path.join(HERE, "build")
 ARCH = "-gencode=arch=compute_100a,code=sm_100a"
 FLAGS = [ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC"]
+# experiments only (A/B of kernel variants): ST_VARIANT=name with
+# ST_NVCC_EXTRA="-D..." builds libscantherm_b200_<name>.so from its own
+# object directory; _lib loads it when ST_VARIANT is set at run time
+EXTRA = os.environ.get("ST_NVCC_EXTRA", "").split()
+VARIANT = os.environ.get("ST_VARIANT", "")
+if VARIANT:
+    OBJ = OBJ + "_" + VARIANT
+    OUT = os.path.join(HERE, "libscantherm_b200_" + VARIANT + ".so")
+    FLAGS = FLAGS + EXTRA
 
 
 def sources():

@@ -13,6 +13,8 @@ import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "libscantherm_b200.so")
+if os.environ.get("ST_VARIANT"):  # kernel A/B experiments (see _build.py)
+    LIB_PATH = os.path.join(_HERE, "libscantherm_b200_" + os.environ["ST_VARIANT"] + ".so")
 
 ST_RHS_DIFFUSION = 1
 ST_RHS_FACES = 2

@@ -14,6 +14,35 @@ __device__ __forceinline__ double dmax(double a, double b) { return a > b ? a : 
 __device__ __forceinline__ double clamp01(double x) { return x < 0.0 ? 0.0 : (x > 1.0 ? 1.0 : x); }
 
 
+// any(|x_i - mid| < half) over N values as one chain of predicated
+// compares (setp ... .or, DSETP.OR in SASS), 8 per inline-asm block: the
+// predicate stays in a predicate register instead of the min-reduction
+// nvcc forms from an |=-loop
+__device__ __forceinline__ unsigned any_abs_lt8(unsigned p, const double* x, double mid,
+                                                double half) {
+  unsigned r;
+  asm("{\n\t.reg .pred q;\n\tsetp.ne.u32 q, %1, 0;\n\t"
+      "setp.lt.or.f64 q, %2, %10, q;\n\tsetp.lt.or.f64 q, %3, %10, q;\n\t"
+      "setp.lt.or.f64 q, %4, %10, q;\n\tsetp.lt.or.f64 q, %5, %10, q;\n\t"
+      "setp.lt.or.f64 q, %6, %10, q;\n\tsetp.lt.or.f64 q, %7, %10, q;\n\t"
+      "setp.lt.or.f64 q, %8, %10, q;\n\tsetp.lt.or.f64 q, %9, %10, q;\n\t"
+      "selp.u32 %0, 1, 0, q;\n\t}"
+      : "=r"(r)
+      : "r"(p), "d"(fabs(x[0] - mid)), "d"(fabs(x[1] - mid)), "d"(fabs(x[2] - mid)),
+        "d"(fabs(x[3] - mid)), "d"(fabs(x[4] - mid)), "d"(fabs(x[5] - mid)),
+        "d"(fabs(x[6] - mid)), "d"(fabs(x[7] - mid)), "d"(half));
+  return r;
+}
+template <int N>
+__device__ __forceinline__ bool any_abs_lt(const double* x, double mid, double half) {
+  unsigned p = 0;
+#pragma unroll
+  for (int i = 0; i + 8 <= N; i += 8) p = any_abs_lt8(p, x + i, mid, half);
+#pragma unroll
+  for (int i = N - N % 8; i < N; i++) p |= fabs(x[i] - mid) < half ? 1u : 0u;
+  return p != 0;
+}
+
 // g(T) (material.py:46-57): 0 below T_s, 1 above T_l, ramp between.
 __device__ __forceinline__ double liquid_fraction(const DevParams& P, double T) {
   double ramp = (T - P.T_s) / P.dT_l;
@@ -47,6 +76,17 @@ __device__ __forceinline__ double heat_capacity(const DevParams& P, double T) {
   return v;
 }
 
+// Evaporation term (physics.py:186-202) at a clamped temperature above
+// T_v.  Out of line: it only runs on vapourising facets, and inlining its
+// exp / sqrt / divisions into every facet quadrature point of the hot
+// kernels costs instruction cache on every step.
+static __device__ __noinline__ double evaporation_term(double Tc, double cp082, double C_T, double inv_Tv,
+                                                double C_M, double h_v, double c_mat,
+                                                double T_h0) {
+  double mdot = cp082 * exp(-C_T * (1.0 / Tc - inv_Tv)) * sqrt(C_M / Tc);
+  return mdot * (h_v + c_mat * (Tc - T_h0));
+}
+
 // Outward surface flux: radiation (physics.py:174-183) + evaporation
 // (physics.py:186-202) + convection (extension).
 __device__ __forceinline__ double surface_flux(const DevParams& P, double T) {
@@ -55,10 +95,8 @@ __device__ __forceinline__ double surface_flux(const DevParams& P, double T) {
   if (P.evap_on) {
     double Tc = T < P.T_max ? T : P.T_max;
     Tc = Tc < 1.0 ? 1.0 : Tc;
-    if (Tc > P.T_v) {
-      double mdot = P.cp082 * exp(-P.C_T * (1.0 / Tc - P.inv_Tv)) * sqrt(P.C_M / Tc);
-      q = q + mdot * (P.h_v + P.c_mat * (Tc - P.T_h0));
-    }
+    if (Tc > P.T_v)
+      q = q + evaporation_term(Tc, P.cp082, P.C_T, P.inv_Tv, P.C_M, P.h_v, P.c_mat, P.T_h0);
   }
   if (P.h_conv != 0.0) q = q + P.h_conv * (T - P.T_inf);
   return q;

@@ -62,96 +62,60 @@ __device__ __forceinline__ double inv_mass1_rt(const SArgs& A, int P, int L, int
   return (L == 0 || L == N - 1) ? A.imv_end : A.imv_int;
 }
 
-// Finalise the seam nodes: x planes, then y planes not on an x seam, then
-// z planes on neither.  A flat "virtual block" index (one block row per
-// plane, 32-bit in-plane indexing) is walked grid-stride by a small grid.
-__global__ void k_seams(SArgs A, int P, int CY, int CZ, int nxs, int nys, int nzs, int bx, int by,
-                        int bz, int latent) {
+// Seam nodes as a static list (built once per context, st_structured.cu
+// build_seam_list): entry e is node sidx[e] with code bits
+//   0 x seam, 1 y seam, 2 z seam, 3-4 rank-interface side + 1, 5 bottom plane
+// and its inverse lumped capacity sci[e] (k_seam_ci, the hot kernel's
+// expression).  The partials are summed in the fixed order of k_seams: x
+// side outermost, then z side, then y side; a remote x side reads the
+// neighbour rank's pre-summed plane.
+__global__ void k_seam_ci(SArgs A, int P, int64_t n, const int64_t* sidx, double* sci) {
+  const int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (e >= n) return;
+  const int64_t idx = sidx[e], plane = (int64_t)A.NY * A.NZ;
+  const int I = (int)(idx / plane);
+  const int64_t r = idx - (int64_t)I * plane;
+  const int J = (int)(r / A.NZ), K = (int)(r - (int64_t)J * A.NZ);
+  sci[e] = inv_mass1_rt(A, P, K, A.NZ) *
+           (inv_mass1_rt(A, P, J, A.NY) * (inv_mass1_rt(A, P, I + A.gI0, A.gNX) * A.inv_rcdw));
+}
+
+__global__ void __launch_bounds__(256) k_seam_list(SArgs A, int64_t n,
+                                                   const int64_t* __restrict__ sidx,
+                                                   const unsigned char* __restrict__ scode,
+                                                   const double* __restrict__ sci, int latent) {
   double amax = 0.0, smax = -INFINITY;
   bool bad = false;
-  const int nvb = bx * nxs + by * nys + bz * nzs;
-  const int sx = P * A.Lx, sy = P * CY;
-  const int nchunk = nxs - A.iface_lo - A.iface_hi;  // chunk-boundary x planes
-  // one node per thread (all loads of the pass in flight at once)
-  {
-    const int vb = blockIdx.x;
-    int b = vb, pl;
-    if (b < bx * nxs) {
-      pl = b / bx;
-      b -= pl * bx;
-    } else if ((b -= bx * nxs) < by * nys) {
-      pl = b / by;
-      b -= pl * by;
-      pl += nxs;
-    } else {
-      b -= by * nys;
-      pl = b / bz;
-      b -= pl * bz;
-      pl += nxs + nys;
-    }
-    const int t = b * blockDim.x + threadIdx.x;
-    int I, J, K;
-    bool mine;
-    if (pl < nxs) {  // x plane: (J, K) contiguous; interfaces first / last
-      if (A.iface_lo && pl == 0)
-        I = 0;
-      else if (pl - A.iface_lo < nchunk)
-        I = sx * (pl - A.iface_lo + 1);
-      else
-        I = A.NX - 1;
-      J = t / A.NZ;
-      K = t - J * A.NZ;
-      mine = J < A.NY;
-    } else if (pl < nxs + nys) {  // y plane: rows of K for each I
-      J = sy * (pl - nxs + 1);
-      I = t / A.NZ;
-      K = t - I * A.NZ;
-      mine = I < A.NX && !x_seam(A, P, I);
-    } else {  // z plane: strided
-      K = P * CZ * (pl - nxs - nys + 1);
-      I = t / A.NY;
-      J = t - I * A.NY;
-      mine = I < A.NX && !x_seam(A, P, I) && !(J > 0 && J < A.NY - 1 && (J % sy) == 0);
-    }
-    if (!mine || vb >= nvb) goto done;
-    {
-    const int64_t idx = ((int64_t)I * A.NY + J) * A.NZ + K;
+  const int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (e < n) {
+    const int64_t idx = sidx[e];
+    const unsigned code = scode[e];
+    const double ci = sci[e];
     const double T = A.T[idx];
-    const bool xs = x_seam(A, P, I);
-    const bool ys = J > 0 && J < A.NY - 1 && (J % sy) == 0;
-    const bool zs = K > 0 && K < A.NZ - 1 && (K % (P * CZ)) == 0;
-    // fixed order: x side outermost, then z side, then y side
+    const int nxb = (code & 1u) ? 2 : 1, nyb = (code & 2u) ? 2 : 1, nzb = (code & 4u) ? 2 : 1;
+    const int side = (int)((code >> 3) & 3u) - 1;
     double f = 0.0, dc = 0.0;
-    for (int xb = 0; xb <= (xs ? 1 : 0); xb++) {
+    for (int xb = 0; xb < nxb; xb++) {
       double sf_ = 0.0, sc_ = 0.0;
-      const int side = (I == 0 && A.iface_lo) ? 0 : ((I == A.NX - 1 && A.iface_hi) ? 1 : -1);
-      const bool remote = side >= 0 && xb == (side == 0 ? 0 : 1);
-      if (remote) {
-        sf_ = A.irf[side][(int64_t)J * A.NZ + K];
-        if (latent) sc_ = A.irc[side][(int64_t)J * A.NZ + K];
+      if (side >= 0 && xb == side) {
+        const int64_t o = side == 0 ? idx : idx - (int64_t)(A.NX - 1) * A.NY * A.NZ;
+        sf_ = A.irf[side][o];
+        if (latent) sc_ = A.irc[side][o];
       } else {
-        for (int zb = 0; zb <= (zs ? 1 : 0); zb++)
-          for (int yb = 0; yb <= (ys ? 1 : 0); yb++) {
-            const int64_t so = (int64_t)(xb + 2 * yb + 4 * zb) * A.snv + idx;
-            sf_ += A.fseam[so];
-            if (latent) sc_ += A.cseam[so];
+        for (int zb = 0; zb < nzb; zb++)
+          for (int yb = 0; yb < nyb; yb++) {
+            seam_add(A, idx, xb + 2 * yb + 4 * zb, sf_, sc_, latent != 0);
           }
       }
       f += sf_;
       dc += sc_;
     }
-    // the same C^-1 as the hot kernel (tensor-product lumped mass)
-    const double ci = inv_mass1_rt(A, P, K, A.NZ) *
-                      (inv_mass1_rt(A, P, J, A.NY) *
-                       (inv_mass1_rt(A, P, I + A.gI0, A.gNX) * A.inv_rcdw));
-    const double o = finalize_node(A, ci, K == 0, T, f, dc, latent != 0);
+    const double o = finalize_node(A, ci, (code & 32u) != 0, T, f, dc, latent != 0);
     A.out[idx] = o;
     amax = fabs(o);
     smax = o;
     bad = (o != o);
-    }
   }
-done:
   block_max2(bad ? (double)NAN : amax, smax, A.red);
 }
 
@@ -170,9 +134,7 @@ __global__ void k_iface_pack(SArgs A, int P, int CY, int CZ, int side, int laten
   double sf_ = 0.0, sc_ = 0.0;
   for (int zb = 0; zb <= (zs ? 1 : 0); zb++)
     for (int yb = 0; yb <= (ys ? 1 : 0); yb++) {
-      const int64_t so = (int64_t)(xb + 2 * yb + 4 * zb) * A.snv + idx;
-      sf_ += A.fseam[so];
-      if (latent) sc_ += A.cseam[so];
+      seam_add(A, idx, xb + 2 * yb + 4 * zb, sf_, sc_, latent != 0);
     }
   A.ipf[side][t] = sf_;
   if (latent) A.ipc[side][t] = sc_;
@@ -514,6 +476,10 @@ struct Structured : Backend {
   int use_lat = 0;
   long long lx = 0, ly = 0, lz = 0;
   DevBuf<double> cinv, fseam, cseam, lcarry, packf[2], packc[2];
+  DevBuf<int64_t> sidx;
+  DevBuf<unsigned char> scode;
+  DevBuf<double> sci;
+  int64_t n_seam = 0;
   int64_t nv = 0;
 
   int launched() {
@@ -547,6 +513,7 @@ struct Structured : Backend {
     A.rc_value = c->rc_value;
     A.fseam = fseam.p;
     A.cseam = cseam.p;
+    A.seam_pair = slab && c->dp.latent ? 1 : 0;
     A.lcarry = lcarry.p;
     A.snv = nv;
     for (int sd = 0; sd < 2; sd++) {
@@ -616,20 +583,61 @@ struct Structured : Backend {
 
   int seams(SArgs& A) {
     const bool lat = c->dp.latent != 0 && A.mode == 0;
-    // x planes: chunk boundaries + rank interfaces (x_seam order)
-    const int nxs = (m.nx + Lx - 1) / Lx - 1 + A.iface_lo + A.iface_hi;
-    const int nys = (m.ny + cy - 1) / cy - 1, nzs = (m.nz + cz - 1) / cz - 1;
-    // one launch over all seam planes (x, then y, then z families)
-    const int bx = (int)(((int64_t)NY * NZ + kThreads - 1) / kThreads);
-    const int by = (int)(((int64_t)NX * NZ + kThreads - 1) / kThreads);
-    const int bz = (int)(((int64_t)NX * NY + kThreads - 1) / kThreads);
-    const int64_t blocks = (int64_t)bx * nxs + (int64_t)by * nys + (int64_t)bz * nzs;
-    if (blocks > 0) {
-      const unsigned grid = (unsigned)blocks;
-      k_seams<<<grid, kThreads, 0, c->stream>>>(A, p, cy, cz, nxs, nys, nzs, bx, by, bz,
-                                                lat ? 1 : 0);
+    if (n_seam > 0) {
+      const unsigned grid = (unsigned)((n_seam + kThreads - 1) / kThreads);
+      k_seam_list<<<grid, kThreads, 0, c->stream>>>(A, n_seam, sidx.p, scode.p, sci.p,
+                                                    lat ? 1 : 0);
       ST_TRY(launched());
     }
+    return ST_OK;
+  }
+
+  // static seam-node list (see k_seam_list): x-seam planes (chunk
+  // boundaries, rank interfaces), then y-seam planes off x seams, then
+  // z-seam planes off both
+  int build_seam_list() {
+    const int sx = p * Lx, sy = p * cy, sz = p * cz;
+    auto xseam = [&](int I) {
+      return (I > 0 && I < NX - 1 && I % sx == 0) || (I == 0 && m.iface_lo) ||
+             (I == NX - 1 && m.iface_hi);
+    };
+    auto yseam = [&](int J) { return J > 0 && J < NY - 1 && J % sy == 0; };
+    auto zseam = [&](int K) { return K > 0 && K < NZ - 1 && K % sz == 0; };
+    std::vector<int64_t> idx;
+    std::vector<unsigned char> code;
+    auto add = [&](int I, int J, int K) {
+      const bool xs = xseam(I), ys = yseam(J), zs = zseam(K);
+      const int side = (I == 0 && m.iface_lo) ? 0 : ((I == NX - 1 && m.iface_hi) ? 1 : -1);
+      idx.push_back(((int64_t)I * NY + J) * NZ + K);
+      code.push_back((unsigned char)((xs ? 1 : 0) | (ys ? 2 : 0) | (zs ? 4 : 0) |
+                                     ((side + 1) << 3) | (K == 0 ? 32 : 0)));
+    };
+    for (int I = 0; I < NX; I++)
+      if (xseam(I))
+        for (int J = 0; J < NY; J++)
+          for (int K = 0; K < NZ; K++) add(I, J, K);
+    for (int J = 0; J < NY; J++)
+      if (yseam(J))
+        for (int I = 0; I < NX; I++)
+          if (!xseam(I))
+            for (int K = 0; K < NZ; K++) add(I, J, K);
+    for (int K = 0; K < NZ; K++)
+      if (zseam(K))
+        for (int I = 0; I < NX; I++)
+          if (!xseam(I))
+            for (int J = 0; J < NY; J++)
+              if (!yseam(J)) add(I, J, K);
+    n_seam = (int64_t)idx.size();
+    if (n_seam == 0) return ST_OK;
+    ST_TRY(sidx.upload(idx.data(), idx.size(), c->stream));
+    ST_TRY(scode.upload(code.data(), code.size(), c->stream));
+    ST_TRY(sci.alloc(idx.size()));
+    SArgs A = sargs();
+    k_seam_ci<<<(unsigned)((n_seam + kThreads - 1) / kThreads), kThreads, 0, c->stream>>>(
+        A, p, n_seam, sidx.p, sci.p);
+    ST_LAUNCHED();
+    // the host vectors die here: finish the uploads first
+    ST_CUDA(cudaStreamSynchronize(c->stream));
     return ST_OK;
   }
 
@@ -918,18 +926,21 @@ Backend* make_structured(Ctx* c, const st_structured_mesh* m, int* err) {
   c->n_cells = (int64_t)m->nx * m->ny * m->nz;
   c->qpc = (s->p + 1) * (s->p + 1) * (s->p + 1);
   rc = s->cinv.alloc(s->nv);
-  if (rc == ST_OK) rc = s->fseam.alloc(8 * s->nv);
-  if (rc == ST_OK && c->dp.latent) rc = s->cseam.alloc(8 * s->nv);
+  // seam slots (see SArgs::fseam / seam_pair)
+  const bool pair = s->slab && c->dp.latent;
+  const size_t nseam = (size_t)(pair ? 16 : 8) * s->nv;
+  if (rc == ST_OK) rc = s->fseam.alloc(nseam);
+  if (rc == ST_OK && c->dp.latent && !pair) rc = s->cseam.alloc(nseam);
   if (rc == ST_OK && c->dp.latent && !s->slab) {
     const size_t ctas = (size_t)((m->ny + s->cy - 1) / s->cy) * ((m->nz + s->cz - 1) / s->cz) *
                         ((m->nx + s->Lx - 1) / s->Lx);
     rc = s->lcarry.alloc(ctas * s->cy * s->cz * (s->p + 1) * (s->p + 1));
   }
   if (rc == ST_OK &&
-      cudaMemsetAsync(s->fseam.p, 0, 8 * s->nv * sizeof(double), c->stream) != cudaSuccess)
+      cudaMemsetAsync(s->fseam.p, 0, nseam * sizeof(double), c->stream) != cudaSuccess)
     rc = ST_ECUDA;
-  if (rc == ST_OK && c->dp.latent &&
-      cudaMemsetAsync(s->cseam.p, 0, 8 * s->nv * sizeof(double), c->stream) != cudaSuccess)
+  if (rc == ST_OK && s->cseam.p &&
+      cudaMemsetAsync(s->cseam.p, 0, nseam * sizeof(double), c->stream) != cudaSuccess)
     rc = ST_ECUDA;
   for (int sd = 0; sd < 2 && rc == ST_OK; sd++) {
     if (!(sd == 0 ? m->iface_lo : m->iface_hi)) continue;
@@ -950,6 +961,7 @@ Backend* make_structured(Ctx* c, const st_structured_mesh* m, int* err) {
       rc = ST_ECUDA;
     }
   }
+  if (rc == ST_OK) rc = s->build_seam_list();
   if (rc != ST_OK) {
     delete s;
     *err = rc;

@@ -28,8 +28,15 @@ struct SArgs {
   int pending;
   // seam partial sums: 8 slot arrays of nv doubles (slot = x side + 2 y
   // side + 4 z side of the writing CTA), plain stores, no clearing
+  // seam partials, slot-major: slot s of node idx at s * snv + idx (the
+  // partials of consecutive seam nodes are stored coalesced); cseam holds
+  // the latent capacity increments in the same layout
   double* fseam;
   double* cseam;
+  // k_xslab contexts with latent heat: (f, dc) as one double2 per entry
+  // in fseam instead (one 16-byte store per seam node, measured faster
+  // there; k_xmarch is faster with the split arrays)
+  int seam_pair;
   // k_xmarch latent x-face carry, per (CTA, thread) slot (Q^2 doubles
   // entry-major); only touched by cells with latent Gauss points
   double* lcarry;
@@ -61,6 +68,30 @@ struct SArgs {
   // x-slab of a larger box: global plane offset / count, rank interfaces
   int gI0, gNX, iface_lo, iface_hi;
 };
+
+// seam slot access (see SArgs::fseam)
+__device__ __forceinline__ void seam_store(const SArgs& A, int64_t idx, int slot, double f,
+                                           double dc, bool latent) {
+  const int64_t so = (int64_t)slot * A.snv + idx;
+  if (latent && A.seam_pair) {
+    reinterpret_cast<double2*>(A.fseam)[so] = make_double2(f, dc);
+  } else {
+    A.fseam[so] = f;
+    if (latent) A.cseam[so] = dc;
+  }
+}
+__device__ __forceinline__ void seam_add(const SArgs& A, int64_t idx, int slot, double& f,
+                                         double& dc, bool latent) {
+  const int64_t so = (int64_t)slot * A.snv + idx;
+  if (latent && A.seam_pair) {
+    const double2 v = reinterpret_cast<const double2*>(A.fseam)[so];
+    f += v.x;
+    dc += v.y;
+  } else {
+    f += A.fseam[so];
+    if (latent) dc += A.cseam[so];
+  }
+}
 
 // x seam: chunk boundary inside the slab, or a rank interface
 __device__ __forceinline__ bool x_seam(const SArgs& A, int P, int I) {
@@ -125,7 +156,8 @@ __device__ __forceinline__ double finalize_node(const SArgs& A, double ci, bool 
   // the latent increment of the lumped capacity only counts when positive:
   // Lagrange bases of degree >= 2 are negative at some Gauss points, so a
   // cell partly in the latent interval can lump a negative increment
-  if (latent && dc > 0.0) ci = 1.0 / (1.0 / ci + dc);
+  // 1 / (1/ci + dc) with one division
+  if (latent && dc > 0.0) ci = ci / fma(ci, dc, 1.0);
   double o = T + A.dt * (ci * f);
   if (A.dir_bottom && bottom) o = A.P.T_inf;
   return o;

@@ -45,12 +45,12 @@ __device__ __forceinline__ void source_factors(const SArgs& A, const DevBeam& b,
   double fx[Q], fy[Q], fz[Q];
 #pragma unroll
   for (int q = 0; q < Q; q++) {
-    const double dx = (ax + Basis<P>::U(q) * A.h) - b.x;
-    const double dy = (ay + Basis<P>::U(q) * A.h) - b.y;
-    const double z = az + Basis<P>::U(q) * A.h;
-    fx[q] = exp((-2.0 * (dx * dx)) / PP.R2) * Basis<P>::W(q);
-    fy[q] = exp((-2.0 * (dy * dy)) / PP.R2) * Basis<P>::W(q);
-    fz[q] = (z >= b.z_top - PP.h_powder && z <= b.z_top) ? Basis<P>::W(q) : 0.0;
+    const double dx = (ax + kTab.U[q] * A.h) - b.x;
+    const double dy = (ay + kTab.U[q] * A.h) - b.y;
+    const double z = az + kTab.U[q] * A.h;
+    fx[q] = exp((-2.0 * (dx * dx)) / PP.R2) * kTab.W[q];
+    fy[q] = exp((-2.0 * (dy * dy)) / PP.R2) * kTab.W[q];
+    fz[q] = (z >= b.z_top - PP.h_powder && z <= b.z_top) ? kTab.W[q] : 0.0;
   }
 #pragma unroll
   for (int a = 0; a < Q; a++) {

@@ -40,7 +40,7 @@ __global__ void __launch_bounds__(CY* CZ, MinBlocks<P>::v) k_xmarch(SArgs A) {
   // x face carried to the next layer (thread-private slots; smem keeps it
   // out of the register budget of the cell evaluation)
   double* Cx = Ec + (LATENT ? EW * NT : 0);
-  __shared__ int lat_any[2];  // latent increments in the current / previous layer
+  __shared__ int lat_any[3];  // latent increments per layer (slot i % 3)
   const int tid = threadIdx.x;
   const int lane = tid & 31, warp = tid >> 5;
   // P >= 2: z-major cell order inside the CTA (tid = kl * CY + jl), so the
@@ -70,7 +70,7 @@ __global__ void __launch_bounds__(CY* CZ, MinBlocks<P>::v) k_xmarch(SArgs A) {
   // this thread's node origin within a plane (global offset and smem slot)
   const int64_t my0 = (int64_t)P * j * A.NZ + (int64_t)P * k;
   const int ms0 = P * jl * NZT + P * kl;
-  if (tid < 2) lat_any[tid] = 0;
+  if (tid < 3) lat_any[tid] = 0;
 
   // stage planes Ib .. Ib+n-1: warp w copies tile rows w, w + NW, ...;
   // lane l the row entries l and l + 32 (rows run along z, contiguous)
@@ -127,18 +127,17 @@ __global__ void __launch_bounds__(CY* CZ, MinBlocks<P>::v) k_xmarch(SArgs A) {
       if (c == 0 && kl > 0) dc += pc[(b * Q + P) * NT - SZ];
       if (b == 0 && c == 0 && jl > 0 && kl > 0) dc += pc[(P * Q + P) * NT - SY - SZ];
     }
-    if (seam) {
-      // this CTA's partial goes to its own slot (side code per seam axis)
-      const int slot = (xc == 2 ? 1 : 0) + (ys_lo ? 2 : 0) + (zs_lo ? 4 : 0);
-      const int64_t so = (int64_t)slot * A.snv + idx;
-      A.fseam[so] = f;
-      if (LATENT) A.cseam[so] = dc;
-    } else {
-      const double mzc = c == 0 ? mz_0 : (c == P ? mz_P : A.imr[c]);
-      const double myb = b == 0 ? my_0 : (b == P ? my_P : A.imr[b]);
-      const double ci = mzc * (myb * imIs);
-      const double o = finalize_node(A, ci, c == 0 && k == 0, tpl[b * NZT + c], f, dc, LATENT);
-      A.out[idx] = o;
+    // branch-free: a seam node stores its partial to this CTA's slot (side
+    // code per seam axis), any other node its update
+    const double mzc = c == 0 ? mz_0 : (c == P ? mz_P : A.imr[c]);
+    const double myb = b == 0 ? my_0 : (b == P ? my_P : A.imr[b]);
+    const double ci = mzc * (myb * imIs);
+    const double o = finalize_node(A, ci, c == 0 && k == 0, tpl[b * NZT + c], f, dc, LATENT);
+    const int slot = (xc == 2 ? 1 : 0) + (ys_lo ? 2 : 0) + (zs_lo ? 4 : 0);
+    const int64_t so = (int64_t)slot * A.snv + idx;
+    *(seam ? A.fseam + so : A.out + idx) = seam ? f : o;
+    if (LATENT && seam) A.cseam[so] = dc;
+    if (!seam) {
       amax = dmax(amax, fabs(o));
       smax = dmax(smax, o);
       bad |= (o != o);
@@ -168,12 +167,17 @@ __global__ void __launch_bounds__(CY* CZ, MinBlocks<P>::v) k_xmarch(SArgs A) {
   load_planes(P * i0, P + 1);
   cp_commit();
 
+  // two barriers per layer: the top one publishes the layer's staged planes
+  // and retires the previous layer's finalisation (E, its ring slots and its
+  // latent flag slot are free), so the next layer's prefetch goes out right
+  // after it and has a whole layer to land
 #pragma unroll 1
   for (int i = i0; i < i1; i++) {
+    cp_wait<0>();
+    __syncthreads();
     if (i + 1 < i1) load_planes(P * (i + 1) + 1, P);
     cp_commit();
-    cp_wait<1>();
-    __syncthreads();
+    if (LATENT && tid == 0) lat_any[(i + 1) % 3] = 0;  // last read by layer i-1
     if (live) {
       double t[Q3], G[Q3];
 #pragma unroll
@@ -202,11 +206,9 @@ __global__ void __launch_bounds__(CY* CZ, MinBlocks<P>::v) k_xmarch(SArgs A) {
         // apparent-capacity increments rho L/dT_lat projected from the Gauss
         // points inside the latent interval (G is dead here, so t can be
         // reused); a predicate pass first, most cells have none
-        bool lat = false;
-#pragma unroll
-        for (int q = 0; q < Q3; q++) lat |= fabs(t[q] - A.lat_mid) < A.lat_half;
+        const bool lat = any_abs_lt<Q3>(t, A.lat_mid, A.lat_half);
         if (lat) {
-          lat_any[i & 1] = 1;
+          lat_any[i % 3] = 1;
 #pragma unroll
           for (int q = 0; q < Q3; q++) t[q] = fabs(t[q] - A.lat_mid) < A.lat_half ? A.lw3[q] : 0.0;
           project3<P>(t);
@@ -227,14 +229,14 @@ __global__ void __launch_bounds__(CY* CZ, MinBlocks<P>::v) k_xmarch(SArgs A) {
       }
     }
     __syncthreads();
-    const bool latn = LATENT && (lat_any[0] | lat_any[1]);
+    // latent increments of this layer or carried from the previous one
+    const bool latn = LATENT && (lat_any[i % 3] | lat_any[(i + 2) % 3]);
 #pragma unroll 1
     for (int a = 0; a < P; a++)
       finalize_owned(P * i + a, a, (a == 0 && i == i0 && (i0 > 0 || A.iface_lo)) ? 2 : 0, latn);
-    __syncthreads();
-    if (tid == 0) lat_any[(i + 1) & 1] = 0;  // slot reused by the next layer
   }
   cp_wait<0>();
+  __syncthreads();  // the last layer's finalisation is done with E
   // last node plane of the chunk: the carried x face (as element plane 0)
   if (live) {
 #pragma unroll
@@ -245,6 +247,6 @@ __global__ void __launch_bounds__(CY* CZ, MinBlocks<P>::v) k_xmarch(SArgs A) {
   }
   __syncthreads();
   finalize_owned(P * i1, 0, (i1 < A.nx || A.iface_hi) ? 1 : 0,
-                 LATENT && (lat_any[0] | lat_any[1]));
+                 LATENT && lat_any[(i1 - 1) % 3] != 0);
   block_max2(bad ? (double)NAN : amax, smax, A.red);
 }

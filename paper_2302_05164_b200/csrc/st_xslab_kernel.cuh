@@ -137,9 +137,7 @@ __global__ void __launch_bounds__((P + 1) * CY * CZ, SlabTile<P>::MINB) k_xslab(
     }
     if (seam) {
       const int slot = (xc == 2 ? 1 : 0) + (ys_lo ? 2 : 0) + (zs_lo ? 4 : 0);
-      const int64_t so = (int64_t)slot * A.snv + idx;
-      A.fseam[so] = f;
-      if (LATENT) A.cseam[so] = dc;
+      seam_store(A, idx, slot, f, dc, LATENT);
     } else {
       const double mzc = c == 0 ? mz_0 : (c == P ? mz_P : A.imr[c]);
       const double myb = b == 0 ? my_0 : (b == P ? my_P : A.imr[b]);
