@@ -150,6 +150,10 @@ int st_get_field(st_ctx* ctx, int field, double* host, int64_t n);
 /* r_c == value everywhere (e.g. a fully consolidated plate); the
  * structured backend then stores no history at all. */
 int st_set_uniform_rc(st_ctx* ctx, double value);
+/* 1 (and *value) when the resident r_c is uniform (st_set_uniform_rc with
+ * value >= 1: the history is a fixed point and is never stored), else 0;
+ * < 0 on error.  Lets a caller read the state without expanding r_c. */
+int st_get_uniform_rc(st_ctx* ctx, double* value);
 /* raw device pointer of a resident field (for zero-copy interop) */
 double* st_field_device_ptr(st_ctx* ctx, int field);
 

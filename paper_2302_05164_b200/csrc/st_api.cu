@@ -392,6 +392,14 @@ int st_set_field(st_ctx* ctx, int field, const double* host, int64_t n) {
   return ST_EINVAL;
 }
 
+int st_get_uniform_rc(st_ctx* ctx, double* value) {
+  ST_TRY(check_ctx(ctx));
+  Ctx& c = ctx->impl;
+  if (!c.rc_uniform) return 0;
+  if (value) *value = c.rc_value;
+  return 1;
+}
+
 int st_set_uniform_rc(st_ctx* ctx, double value) {
   ST_TRY(check_ctx(ctx));
   Ctx& c = ctx->impl;

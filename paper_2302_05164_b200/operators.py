@@ -302,15 +302,29 @@ class ThermalOperator:
             _lib.check(self._lib.st_set_field(self._ctx, _lib.ST_FIELD_RC, _lib.dptr(rc),
                                               rc.size), "set r_c")
 
-    def get_state(self, r_c_shape=None):
-        T = np.empty(self.nv)
+    def get_state(self, r_c_shape=None, out=None):
+        """Download (T, r_c).  `out` may be a caller-owned float64 array of
+        n_vertices (e.g. pinned host memory) that receives T.  A uniform
+        resident r_c (st_set_uniform_rc, r_c >= 1) is never stored on the
+        device, so it comes back as a read-only broadcast of that value
+        instead of an expanded copy."""
+        T = np.empty(self.nv) if out is None else out
         _lib.check(self._lib.st_get_field(self._ctx, _lib.ST_FIELD_T, _lib.dptr(T), T.size),
                    "get T")
-        rc = np.empty(self.n_cells * self.qpc)
-        _lib.check(self._lib.st_get_field(self._ctx, _lib.ST_FIELD_RC, _lib.dptr(rc),
-                                          rc.size), "get r_c")
+        n = self.n_cells * self.qpc
+        v = ctypes.c_double()
+        uni = self._lib.st_get_uniform_rc(self._ctx, ctypes.byref(v))
+        if uni < 0:
+            _lib.check(uni, "get r_c")
+        if uni == 1:
+            rc = np.broadcast_to(np.float64(v.value), (n,))
+        else:
+            rc = np.empty(n)
+            _lib.check(self._lib.st_get_field(self._ctx, _lib.ST_FIELD_RC, _lib.dptr(rc), n),
+                       "get r_c")
         if r_c_shape is not None:
-            rc = rc.reshape(r_c_shape)
+            rc = rc.reshape(r_c_shape) if uni != 1 else np.broadcast_to(np.float64(v.value),
+                                                                          r_c_shape)
         return T, rc
 
     def run_explicit(self, dts, beams):
