@@ -80,41 +80,72 @@ __global__ void k_seam_ci(SArgs A, int P, int64_t n, const int64_t* sidx, double
            (inv_mass1_rt(A, P, J, A.NY) * (inv_mass1_rt(A, P, I + A.gI0, A.gNX) * A.inv_rcdw));
 }
 
+// Seam pass over the static list: for each entry the (up to 8) slot
+// partials are all loaded up front (predicated, 0 for slots the node does
+// not have), then summed in the fixed order of the old per-plane pass: x
+// side outermost, then z side, then y side (adding the exact zeros of
+// absent slots does not change the sum).  A remote x side (rank interface)
+// reads the neighbour rank's pre-summed plane instead of its slots.
+template <bool LAT>
 __global__ void __launch_bounds__(256) k_seam_list(SArgs A, int64_t n,
                                                    const int64_t* __restrict__ sidx,
                                                    const unsigned char* __restrict__ scode,
-                                                   const double* __restrict__ sci, int latent) {
+                                                   const double* __restrict__ sci) {
   double amax = 0.0, smax = -INFINITY;
   bool bad = false;
-  const int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (e < n) {
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  const bool pair = LAT && A.seam_pair;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n; e += stride) {
     const int64_t idx = sidx[e];
     const unsigned code = scode[e];
     const double ci = sci[e];
     const double T = A.T[idx];
-    const int nxb = (code & 1u) ? 2 : 1, nyb = (code & 2u) ? 2 : 1, nzb = (code & 4u) ? 2 : 1;
+    const bool xs = code & 1u, ys = code & 2u, zs = code & 4u;
     const int side = (int)((code >> 3) & 3u) - 1;
+    double fv[8], cv[8];
+#pragma unroll
+    for (int s = 0; s < 8; s++) {
+      const int xb = s & 1, yb = (s >> 1) & 1, zb = s >> 2;
+      const bool use = (xb == 0 || xs) && (yb == 0 || ys) && (zb == 0 || zs) && xb != side;
+      const int64_t so = (int64_t)s * A.snv + idx;
+      fv[s] = 0.0;
+      cv[s] = 0.0;
+      if (use) {
+        if (pair) {
+          const double2 v = reinterpret_cast<const double2*>(A.fseam)[so];
+          fv[s] = v.x;
+          cv[s] = v.y;
+        } else {
+          fv[s] = A.fseam[so];
+          if (LAT) cv[s] = A.cseam[so];
+        }
+      }
+    }
+    double rf[2] = {0.0, 0.0}, rc[2] = {0.0, 0.0};
+    if (side >= 0) {
+      const int64_t o = side == 0 ? idx : idx - (int64_t)(A.NX - 1) * A.NY * A.NZ;
+      rf[side] = A.irf[side][o];
+      if (LAT) rc[side] = A.irc[side][o];
+    }
     double f = 0.0, dc = 0.0;
-    for (int xb = 0; xb < nxb; xb++) {
-      double sf_ = 0.0, sc_ = 0.0;
-      if (side >= 0 && xb == side) {
-        const int64_t o = side == 0 ? idx : idx - (int64_t)(A.NX - 1) * A.NY * A.NZ;
-        sf_ = A.irf[side][o];
-        if (latent) sc_ = A.irc[side][o];
+#pragma unroll
+    for (int xb = 0; xb < 2; xb++) {
+      double sf_, sc_;
+      if (xb == side) {
+        sf_ = rf[xb];
+        sc_ = rc[xb];
       } else {
-        for (int zb = 0; zb < nzb; zb++)
-          for (int yb = 0; yb < nyb; yb++) {
-            seam_add(A, idx, xb + 2 * yb + 4 * zb, sf_, sc_, latent != 0);
-          }
+        sf_ = ((fv[xb] + fv[xb + 2]) + fv[xb + 4]) + fv[xb + 6];
+        sc_ = ((cv[xb] + cv[xb + 2]) + cv[xb + 4]) + cv[xb + 6];
       }
       f += sf_;
       dc += sc_;
     }
-    const double o = finalize_node(A, ci, (code & 32u) != 0, T, f, dc, latent != 0);
+    const double o = finalize_node(A, ci, (code & 32u) != 0, T, f, dc, LAT);
     A.out[idx] = o;
-    amax = fabs(o);
-    smax = o;
-    bad = (o != o);
+    amax = dmax(amax, fabs(o));
+    smax = dmax(smax, o);
+    bad |= (o != o);
   }
   block_max2(bad ? (double)NAN : amax, smax, A.red);
 }
@@ -584,9 +615,13 @@ struct Structured : Backend {
   int seams(SArgs& A) {
     const bool lat = c->dp.latent != 0 && A.mode == 0;
     if (n_seam > 0) {
-      const unsigned grid = (unsigned)((n_seam + kThreads - 1) / kThreads);
-      k_seam_list<<<grid, kThreads, 0, c->stream>>>(A, n_seam, sidx.p, scode.p, sci.p,
-                                                    lat ? 1 : 0);
+      // enough resident threads for the memory latency, a few entries each
+      const int64_t need = (n_seam + kThreads - 1) / kThreads;
+      const unsigned grid = (unsigned)std::max<int64_t>(1, std::min<int64_t>(need, 148 * 8));
+      if (lat)
+        k_seam_list<true><<<grid, kThreads, 0, c->stream>>>(A, n_seam, sidx.p, scode.p, sci.p);
+      else
+        k_seam_list<false><<<grid, kThreads, 0, c->stream>>>(A, n_seam, sidx.p, scode.p, sci.p);
       ST_TRY(launched());
     }
     return ST_OK;
