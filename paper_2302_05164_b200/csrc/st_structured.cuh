@@ -203,10 +203,10 @@ struct SlabTile<3> {
   static constexpr int CY = 4, CZ = 8, MINB = 3;
   static constexpr bool SHORT = true;
 };
-template <>
 struct SlabTile<4> {
-  static constexpr int CY = 4, CZ = 8, MINB = 1;
-  static constexpr bool SHORT = false;
+  // two CTAs per SM (168 registers, short ring: 112 KB of shared memory)
+  static constexpr int CY = 4, CZ = 8, MINB = 2;
+  static constexpr bool SHORT = true;
 };
 
 // Hot kernels of degree P (defined in st_hot_p<P>.cu):
