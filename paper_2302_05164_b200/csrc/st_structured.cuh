@@ -203,6 +203,7 @@ struct SlabTile<3> {
   static constexpr int CY = 4, CZ = 8, MINB = 3;
   static constexpr bool SHORT = true;
 };
+template <>
 struct SlabTile<4> {
   // two CTAs per SM (168 registers, short ring: 112 KB of shared memory)
   static constexpr int CY = 4, CZ = 8, MINB = 2;
