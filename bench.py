@@ -192,6 +192,17 @@ class Clocks:
                 "samples": len(self.samples)}
 
 
+def fp64_peak_tflops(flop_per_cycle=None):
+    """Whole-GPU fp64 FMA peak: ncu's DFMA lanes x 2 flop at the measured
+    maximum SM clock (MEASURED_PEAKS.json), else 148 SMs x 64 lanes."""
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            mhz = float(json.load(f)["sm_max_mhz"])
+    except Exception:
+        mhz = 1965.0
+    return (flop_per_cycle or 148 * 64 * 2) * mhz * 1e6 / 1e12
+
+
 def measured_hbm_peak():
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
@@ -308,6 +319,16 @@ def gpu_measure(w, steps, warmup, device, clocks=True):
     if ncu:
         roofline["ncu"] = {k: ncu[k] for k in ("fp64_pipe_pct", "issue_active_pct", "duration_us",
                                                "source") if k in ncu}
+        if ncu.get("fp64_flop"):
+            # the kernel is fp64-issue bound, not HBM bound: its
+            # fp64 flop per launch (ncu instruction counts of the same
+            # workload) over the live-measured launch time, against the fp64
+            # peak (64 DFMA lanes per SM x 2 flop x SMs x max SM clock)
+            peak = fp64_peak_tflops(ncu.get("fp64_peak_flop_per_cycle"))
+            ach = ncu["fp64_flop"] / main_avg_s / 1e12
+            roofline["fp64"] = {"achieved": ach, "peak": peak, "unit": "TFLOP/s",
+                                "frac": ach / peak,
+                                "flop_per_dof": ncu["fp64_flop"] / box.n_dofs}
     return dict(op=op, box=box, dts=dts, beams=beams, T0=T0, step_ms=step_ms,
                 launches=launches, roofline=roofline, clocks=clk.summary() if clk else None)
 
@@ -464,7 +485,8 @@ def run_ours(args):
                               "roofline_frac": rp["roofline"]["frac"],
                               "kernel": rp["roofline"]["kernel"],
                               "traffic": rp["roofline"]["traffic"],
-                              "achieved_GBps": rp["roofline"]["achieved"]}
+                              "achieved_GBps": rp["roofline"]["achieved"],
+                              "fp64": rp["roofline"].get("fp64")}
             rp["op"].close()
         out["sweep_config2"] = sweep
     if rank == 0 and ws == 1 and not args.no_cpu_baseline:

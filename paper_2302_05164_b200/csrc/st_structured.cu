@@ -91,61 +91,80 @@ __global__ void __launch_bounds__(256) k_seam_list(SArgs A, int64_t n,
                                                    const int64_t* __restrict__ sidx,
                                                    const unsigned char* __restrict__ scode,
                                                    const double* __restrict__ sci) {
+  // one entry per thread (measured: maximal parallelism beats batching
+  // entries per thread); the loop form keeps U > 1 available
+  constexpr int U = 1;
   double amax = 0.0, smax = -INFINITY;
   bool bad = false;
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
   const bool pair = LAT && A.seam_pair;
-  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n; e += stride) {
-    const int64_t idx = sidx[e];
-    const unsigned code = scode[e];
-    const double ci = sci[e];
-    const double T = A.T[idx];
-    const bool xs = code & 1u, ys = code & 2u, zs = code & 4u;
-    const int side = (int)((code >> 3) & 3u) - 1;
-    double fv[8], cv[8];
+  for (int64_t eb = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; eb < n; eb += U * stride) {
+    int64_t idx[U];
+    unsigned code[U];
+    double ci[U], T[U], fv[U][8], cv[U][8];
 #pragma unroll
-    for (int s = 0; s < 8; s++) {
-      const int xb = s & 1, yb = (s >> 1) & 1, zb = s >> 2;
-      const bool use = (xb == 0 || xs) && (yb == 0 || ys) && (zb == 0 || zs) && xb != side;
-      const int64_t so = (int64_t)s * A.snv + idx;
-      fv[s] = 0.0;
-      cv[s] = 0.0;
-      if (use) {
-        if (pair) {
-          const double2 v = reinterpret_cast<const double2*>(A.fseam)[so];
-          fv[s] = v.x;
-          cv[s] = v.y;
-        } else {
-          fv[s] = A.fseam[so];
-          if (LAT) cv[s] = A.cseam[so];
+    for (int u = 0; u < U; u++) {
+      const int64_t e = eb + u * stride;
+      idx[u] = e < n ? sidx[e] : -1;
+      code[u] = e < n ? scode[e] : 0u;
+      ci[u] = e < n ? sci[e] : 0.0;
+    }
+#pragma unroll
+    for (int u = 0; u < U; u++) {
+      const bool in = idx[u] >= 0;
+      T[u] = in ? A.T[idx[u]] : 0.0;
+      const bool xs = code[u] & 1u, ys = code[u] & 2u, zs = code[u] & 4u;
+      const int side = (int)((code[u] >> 3) & 3u) - 1;
+#pragma unroll
+      for (int s = 0; s < 8; s++) {
+        const int xb = s & 1, yb = (s >> 1) & 1, zb = s >> 2;
+        const bool use =
+            in && (xb == 0 || xs) && (yb == 0 || ys) && (zb == 0 || zs) && xb != side;
+        const int64_t so = (int64_t)s * A.snv + idx[u];
+        fv[u][s] = 0.0;
+        cv[u][s] = 0.0;
+        if (use) {
+          if (pair) {
+            const double2 v = reinterpret_cast<const double2*>(A.fseam)[so];
+            fv[u][s] = v.x;
+            cv[u][s] = v.y;
+          } else {
+            fv[u][s] = A.fseam[so];
+            if (LAT) cv[u][s] = A.cseam[so];
+          }
         }
       }
     }
-    double rf[2] = {0.0, 0.0}, rc[2] = {0.0, 0.0};
-    if (side >= 0) {
-      const int64_t o = side == 0 ? idx : idx - (int64_t)(A.NX - 1) * A.NY * A.NZ;
-      rf[side] = A.irf[side][o];
-      if (LAT) rc[side] = A.irc[side][o];
-    }
-    double f = 0.0, dc = 0.0;
 #pragma unroll
-    for (int xb = 0; xb < 2; xb++) {
-      double sf_, sc_;
-      if (xb == side) {
-        sf_ = rf[xb];
-        sc_ = rc[xb];
-      } else {
-        sf_ = ((fv[xb] + fv[xb + 2]) + fv[xb + 4]) + fv[xb + 6];
-        sc_ = ((cv[xb] + cv[xb + 2]) + cv[xb + 4]) + cv[xb + 6];
+    for (int u = 0; u < U; u++) {
+      if (idx[u] < 0) continue;
+      const int side = (int)((code[u] >> 3) & 3u) - 1;
+      double rf[2] = {0.0, 0.0}, rc[2] = {0.0, 0.0};
+      if (side >= 0) {
+        const int64_t o = side == 0 ? idx[u] : idx[u] - (int64_t)(A.NX - 1) * A.NY * A.NZ;
+        rf[side] = A.irf[side][o];
+        if (LAT) rc[side] = A.irc[side][o];
       }
-      f += sf_;
-      dc += sc_;
+      double f = 0.0, dc = 0.0;
+#pragma unroll
+      for (int xb = 0; xb < 2; xb++) {
+        double sf_, sc_;
+        if (xb == side) {
+          sf_ = rf[xb];
+          sc_ = rc[xb];
+        } else {
+          sf_ = ((fv[u][xb] + fv[u][xb + 2]) + fv[u][xb + 4]) + fv[u][xb + 6];
+          sc_ = ((cv[u][xb] + cv[u][xb + 2]) + cv[u][xb + 4]) + cv[u][xb + 6];
+        }
+        f += sf_;
+        dc += sc_;
+      }
+      const double o = finalize_node(A, ci[u], (code[u] & 32u) != 0, T[u], f, dc, LAT);
+      A.out[idx[u]] = o;
+      amax = dmax(amax, fabs(o));
+      smax = dmax(smax, o);
+      bad |= (o != o);
     }
-    const double o = finalize_node(A, ci, (code & 32u) != 0, T, f, dc, LAT);
-    A.out[idx] = o;
-    amax = dmax(amax, fabs(o));
-    smax = dmax(smax, o);
-    bad |= (o != o);
   }
   block_max2(bad ? (double)NAN : amax, smax, A.red);
 }
@@ -615,9 +634,8 @@ struct Structured : Backend {
   int seams(SArgs& A) {
     const bool lat = c->dp.latent != 0 && A.mode == 0;
     if (n_seam > 0) {
-      // enough resident threads for the memory latency, a few entries each
-      const int64_t need = (n_seam + kThreads - 1) / kThreads;
-      const unsigned grid = (unsigned)std::max<int64_t>(1, std::min<int64_t>(need, 148 * 8));
+      // one thread per seam node: the pass is latency bound
+      const unsigned grid = (unsigned)((n_seam + kThreads - 1) / kThreads);
       if (lat)
         k_seam_list<true><<<grid, kThreads, 0, c->stream>>>(A, n_seam, sidx.p, scode.p, sci.p);
       else
@@ -877,7 +895,7 @@ struct Structured : Backend {
     }
     return b;
   }
-  const char* main_kernel() const override { return "k_xmarch"; }
+  const char* main_kernel() const override { return slab ? "k_xslab" : "k_xmarch"; }
 };
 
 static bool lattice_origin(double o, double h, long long* l) {

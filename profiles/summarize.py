@@ -56,6 +56,17 @@ def summarize(path):
     out["stall_top"] = {k: round(v / tot, 3) for v, k in sorted(stalls, reverse=True)[:8]}
     if "dram_read_bytes" in out and "dram_write_bytes" in out:
         out["dram_bytes"] = out["dram_read_bytes"] + out["dram_write_bytes"]
+    # fp64 work of the launch: thread-level DFMA (2 flop), DMUL, DADD per
+    # elapsed SMSP cycle summed over SMSPs, times the elapsed SM cycles
+    fma = units(d.get("smsp__sass_thread_inst_executed_op_dfma_pred_on.sum.per_cycle_elapsed", ""))
+    mul = units(d.get("smsp__sass_thread_inst_executed_op_dmul_pred_on.sum.per_cycle_elapsed", ""))
+    add = units(d.get("smsp__sass_thread_inst_executed_op_dadd_pred_on.sum.per_cycle_elapsed", ""))
+    cyc = units(d.get("sm__cycles_elapsed.avg", ""))
+    peak = units(d.get("sm__sass_thread_inst_executed_op_dfma_pred_on.sum.peak_sustained", ""))
+    if None not in (fma, mul, add, cyc):
+        out["fp64_flop"] = (2.0 * fma + mul + add) * cyc
+    if peak is not None:
+        out["fp64_peak_flop_per_cycle"] = 2.0 * peak  # DFMA lanes x 2, whole GPU
     return out
 
 
