@@ -42,7 +42,10 @@ template <int P, int CY, int CZ, bool LAT>
 static constexpr size_t march_smem() {
   constexpr int PL = (P * CY + 1) * (P * CZ + 1);
   constexpr int EW = P * (P + 1) * (P + 1);
-  return (size_t)((2 * P + 1) * PL + (LAT ? 2 : 1) * EW * CY * CZ + (P + 1) * (P + 1) * CY * CZ) *
+  constexpr int Q = P + 1;
+  // COOP tables of k_xmarch (p >= 2): Sy, Sz, Sx, facet fluxes and terms
+  constexpr int TAB = P >= 2 ? (CY + CZ + 1) * kMaxTabBeams * Q + 2 * CY * Q * Q : 0;
+  return (size_t)((2 * P + 1) * PL + (LAT ? 2 : 1) * EW * CY * CZ + Q * Q * CY * CZ + TAB) *
          sizeof(double);
 }
 

@@ -696,6 +696,11 @@ struct Structured : Backend {
 
   int xmarch(SArgs& A, bool rcf, bool with_seams = true) {
     const bool lat = c->dp.latent != 0 && A.mode == 0;
+    if (!slab && p >= 2 && (A.flags & ST_RHS_SOURCE) && A.nb > kMaxTabBeams) {
+      set_error("the structured p >= 2 kernel tables at most " + std::to_string(kMaxTabBeams) +
+                " beams per step");
+      return ST_EUNSUPPORTED;
+    }
     c->prof_begin();
     const dim3 grid((m.ny + cy - 1) / cy, (m.nz + cz - 1) / cz, (m.nx + Lx - 1) / Lx);
     cudaError_t e;

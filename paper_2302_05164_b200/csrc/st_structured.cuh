@@ -210,6 +210,9 @@ struct SlabTile<4> {
   static constexpr bool SHORT = true;
 };
 
+// beams the p >= 2 k_xmarch tables per step (separable source factors)
+constexpr int kMaxTabBeams = 8;
+
 // Hot kernels of degree P (defined in st_hot_p<P>.cu):
 //   hot_resident: resident CTAs per SM of the kernel a context launches
 //   hot_launch:   one launch of k_xmarch / k_xslab over `grid`

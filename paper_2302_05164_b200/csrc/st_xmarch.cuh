@@ -87,16 +87,106 @@ __device__ __forceinline__ unsigned beam_column_mask(const SArgs& A, int j, int 
   return mask;
 }
 
+// Separable source tables of a k_xmarch CTA (COOP): per beam, the y factor
+// of each tile row jl and the z factor of each tile column kl are fixed over
+// the x march (Sy[(jl * kMaxTabBeams + b) * Q + a], Sz likewise); the x
+// factor Sx[b * Q + a] changes per cell layer (kMaxTabBeams beams).
+
+// 1D projected factor s[a] = sum_q V(a, q) f(q) of one axis of the
+// separable slab source (the expressions of source_factors)
+template <int P>
+__device__ __forceinline__ void src_factor_xy(const SArgs& A, double anc, double bc, double* s) {
+  constexpr int Q = P + 1;
+  double f[Q];
+#pragma unroll
+  for (int q = 0; q < Q; q++) {
+    const double d = (anc + kTab.U[q] * A.h) - bc;
+    f[q] = exp((-2.0 * (d * d)) / A.P.R2) * kTab.W[q];
+  }
+#pragma unroll
+  for (int a = 0; a < Q; a++) {
+    double x = 0.0;
+#pragma unroll
+    for (int q = 0; q < Q; q++) x = fma(Basis<P>::V(a, q), f[q], x);
+    s[a] = x;
+  }
+}
+template <int P>
+__device__ __forceinline__ void src_factor_z(const SArgs& A, double az, const DevBeam& b,
+                                             double* s) {
+  constexpr int Q = P + 1;
+  double f[Q];
+#pragma unroll
+  for (int q = 0; q < Q; q++) {
+    const double z = az + kTab.U[q] * A.h;
+    f[q] = (z >= b.z_top - A.P.h_powder && z <= b.z_top) ? kTab.W[q] : 0.0;
+  }
+#pragma unroll
+  for (int a = 0; a < Q; a++) {
+    double x = 0.0;
+#pragma unroll
+    for (int q = 0; q < Q; q++) x = fma(Basis<P>::V(a, q), f[q], x);
+    s[a] = x;
+  }
+}
+
+// +z facet term of top cells r0 .. r1-1 of a tile row, by the 32 lanes of
+// one warp (COOP): Gauss-point temperatures and fluxes, then the
+// projection to the facet nodes, each item in the summation order of the
+// per-cell code (operators.py:275-290); fo[r][a * Q + b]
+template <int P, class NodeF>
+__device__ __forceinline__ void face_phase(const SArgs& A, int lane, int r0, int r1, double* fq,
+                                           double* fo, const NodeF& node) {
+  constexpr int Q = P + 1, Q2 = Q * Q;
+  const double area0 = A.hh * A.hh;
+  const int n = (r1 - r0) * Q2;
+#pragma unroll 1
+  for (int it = lane; it < n; it += 32) {
+    const int r = r0 + it / Q2, s = it - (it / Q2) * Q2, qa = s / Q, qb = s - (s / Q) * Q;
+    double acc = 0.0;
+#pragma unroll
+    for (int a = 0; a < Q; a++) {
+      double v = kTab.V[0][qb] * node(r, a, 0);
+#pragma unroll
+      for (int b = 1; b < Q; b++) v = fma(kTab.V[b][qb], node(r, a, b), v);
+      acc = a == 0 ? kTab.V[0][qa] * v : fma(kTab.V[a][qa], v, acc);
+    }
+    fq[r * Q2 + s] = surface_flux(A.P, acc) * (-(area0 * (kTab.W[qa] * kTab.W[qb])));
+  }
+  __syncwarp();
+#pragma unroll 1
+  for (int it = lane; it < n; it += 32) {
+    const int r = r0 + it / Q2, s = it - (it / Q2) * Q2, a = s / Q, b = s - (s / Q) * Q;
+    const double* f = fq + r * Q2;
+    double acc = 0.0;
+#pragma unroll
+    for (int qb = 0; qb < Q; qb++) {
+      double v = kTab.V[a][0] * f[qb];
+#pragma unroll
+      for (int qa = 1; qa < Q; qa++) v = fma(kTab.V[a][qa], f[qa * Q + qb], v);
+      acc = qb == 0 ? kTab.V[b][0] * v : fma(kTab.V[b][qb], v, acc);
+    }
+    fo[r * Q2 + s] = acc;
+  }
+}
+
 // Element vector of one cell, degree P (operators.py:247-316 generalised):
 //   t in : T at the Gauss points (a x b x c, z fastest; kept for the
 //          latent capacity pass of the caller)
 //   G out: element vector
 //   node(a, b, c): re-reads a node value (top facet; keeps t's copy out of
 //          the register budget)
-template <int P, bool RCF, class NodeF>
+// COOP (p >= 2, z-major cells): the source uses the CTA's separable factor
+// tables (sxl: Sx of this layer, syj / szk: this cell's [beam][Q] rows of
+// Sy / Sz, see kMaxTabBeams) and the +z facet term of a
+// top cell comes precomputed from the top warp (fo: [a * Q + b], face_phase);
+// both give the same values in the same summation order as the per-cell code.
+template <int P, bool RCF, bool COOP, class NodeF>
 __device__ __forceinline__ void cell_element(const SArgs& A, const CellFlags& F, int i, int j,
                                              int k, int64_t cell, const double* t, double* G,
-                                             unsigned ymask, const NodeF& node) {
+                                             unsigned ymask, const NodeF& node, const double* sxl,
+                                             const double* syj, const double* szk,
+                                             const double* fo) {
   constexpr int Q = P + 1;
   constexpr int Q3 = Q * Q * Q;
   using B = Basis<P>;
@@ -159,7 +249,16 @@ __device__ __forceinline__ void cell_element(const SArgs& A, const CellFlags& F,
       const DevBeam bm = A.beams[b];
       if (!beam_hits_cell(PP, bm, ax, ay, az, A.h)) continue;
       double sx[Q], sy[Q], sz[Q];
-      source_factors<P>(A, bm, ax, ay, az, sx, sy, sz);
+      if (COOP) {
+#pragma unroll
+        for (int a = 0; a < Q; a++) {
+          sx[a] = sxl[b * Q + a];
+          sy[a] = syj[b * Q + a];
+          sz[a] = szk[b * Q + a];
+        }
+      } else {
+        source_factors<P>(A, bm, ax, ay, az, sx, sy, sz);
+      }
       const double coef = bm.peak * A.detw0;
 #pragma unroll
       for (int a = 0; a < Q; a++)
@@ -171,7 +270,13 @@ __device__ __forceinline__ void cell_element(const SArgs& A, const CellFlags& F,
         }
     }
   }
-  if (top) {
+  if (COOP && top) {
+#pragma unroll
+    for (int a = 0; a < Q; a++)
+#pragma unroll
+      for (int b = 0; b < Q; b++) G[(a * Q + b) * Q + P] += fo[a * Q + b];
+  }
+  if (!COOP && top) {
     // +z facet quadrature (operators.py:275-290), full facets
     double tf[Q * Q];
 #pragma unroll

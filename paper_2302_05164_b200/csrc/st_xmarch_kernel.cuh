@@ -40,6 +40,14 @@ __global__ void __launch_bounds__(CY* CZ, MinBlocks<P>::v) k_xmarch(SArgs A) {
   // x face carried to the next layer (thread-private slots; smem keeps it
   // out of the register budget of the cell evaluation)
   double* Cx = Ec + (LATENT ? EW * NT : 0);
+  // COOP (p >= 2): separable source tables and the top row's facet term
+  constexpr bool COOP = P >= 2;
+  constexpr int MB = kMaxTabBeams;
+  double* Sy = Cx + Q * Q * NT;          // [CY][MB][Q]
+  double* Sz = Sy + (COOP ? CY * MB * Q : 0);  // [CZ][MB][Q]
+  double* Sx = Sz + (COOP ? CZ * MB * Q : 0);  // [MB][Q], current layer
+  double* Fq = Sx + (COOP ? MB * Q : 0);       // [CY][Q * Q] facet fluxes
+  double* Fo = Fq + (COOP ? CY * Q * Q : 0);   // [CY][Q * Q] facet node terms
   __shared__ int lat_any[3];  // latent increments per layer (slot i % 3)
   const int tid = threadIdx.x;
   const int lane = tid & 31, warp = tid >> 5;
@@ -63,8 +71,17 @@ __global__ void __launch_bounds__(CY* CZ, MinBlocks<P>::v) k_xmarch(SArgs A) {
   // tile-edge node planes are seams unless they are the domain boundary
   const bool sy_lo = jl == 0 && j0 > 0, sy_hi = jl == CY - 1 && j0 + CY < A.ny;
   const bool sz_lo = kl == 0 && k0 > 0, sz_hi = kl == CZ - 1 && k0 + CZ < A.nz;
+#ifdef ST_EXP_NORARE
+  const CellFlags F{(A.flags & ST_RHS_DIFFUSION) != 0, false, false, false};
+#elif defined(ST_EXP_NOFACE)
+  const CellFlags F{(A.flags & ST_RHS_DIFFUSION) != 0, false,
+                    (A.flags & ST_RHS_SOURCE) != 0 && A.nb > 0, false};
+#elif defined(ST_EXP_NOSRC)
+  const CellFlags F{(A.flags & ST_RHS_DIFFUSION) != 0, (A.flags & ST_RHS_FACES) != 0, false, false};
+#else
   const CellFlags F{(A.flags & ST_RHS_DIFFUSION) != 0, (A.flags & ST_RHS_FACES) != 0,
                     (A.flags & ST_RHS_SOURCE) != 0 && A.nb > 0, (A.flags & ST_RHS_FROZEN_K) != 0};
+#endif
   const int64_t plane_stride = (int64_t)A.NY * A.NZ;
   const int64_t tile0 = (int64_t)P * j0 * A.NZ + (int64_t)P * k0;
   // this thread's node origin within a plane (global offset and smem slot)
@@ -102,6 +119,33 @@ __global__ void __launch_bounds__(CY* CZ, MinBlocks<P>::v) k_xmarch(SArgs A) {
                         : nullptr;
   bool lat_had = false;
   const unsigned ymask = F.source && live ? beam_column_mask<P>(A, j, k) : 0u;
+  const int nbt = F.source ? min(A.nb, MB) : 0;  // tabled beams (host: nb <= MB)
+  if (COOP) {
+    for (int e = tid; e < nbt * CY; e += NT) {
+      const int b = e / CY, r = e - (e / CY) * CY;
+      src_factor_xy<P>(A, anchor<P>(A, 1, j0 + r), A.beams[b].y, Sy + (r * MB + b) * Q);
+    }
+    for (int e = tid; e < nbt * CZ; e += NT) {
+      const int b = e / CZ, r = e - (e / CZ) * CZ;
+      src_factor_z<P>(A, anchor<P>(A, 2, k0 + r), A.beams[b], Sz + (r * MB + b) * Q);
+    }
+  }
+  // the tile row of top cells (facet term) and its warp
+  const int kl_top = A.nz - 1 - k0;
+  const bool has_top = COOP && F.faces && A.top_faces && kl_top < CZ;
+  // per-layer side work of COOP, spread over all warps: the facet terms of
+  // the top row (cells split between the warps) and the source x factors
+  constexpr int CPW = (CY + NW - 1) / NW;  // top-row cells per warp
+  auto side_work = [&](int il) {
+    if (has_top) {
+      const int ib = P * il;
+      face_phase<P>(A, lane, min(warp * CPW, CY), min(warp * CPW + CPW, CY), Fq, Fo,
+                    [&](int r, int a, int b) {
+                      return Tr[((ib + a) % NR) * PL + P * r * NZT + P * kl_top + b * NZT + P];
+                    });
+    }
+    if (COOP && tid < nbt) src_factor_xy<P>(A, anchor<P>(A, 0, il), A.beams[tid].x, Sx + tid * Q);
+  };
   double amax = 0.0, smax = -INFINITY;
   bool bad = false;
 
@@ -163,9 +207,14 @@ __global__ void __launch_bounds__(CY* CZ, MinBlocks<P>::v) k_xmarch(SArgs A) {
     }
   };
 
-  // prologue: the first layer's P+1 planes
+  // prologue: the first layer's P+1 planes (and its COOP side work)
   load_planes(P * i0, P + 1);
   cp_commit();
+  if (COOP) {
+    cp_wait<0>();
+    __syncthreads();
+    side_work(i0);
+  }
 
   // two barriers per layer: the top one publishes the layer's staged planes
   // and retires the previous layer's finalisation (E, its ring slots and its
@@ -173,6 +222,9 @@ __global__ void __launch_bounds__(CY* CZ, MinBlocks<P>::v) k_xmarch(SArgs A) {
   // after it and has a whole layer to land
 #pragma unroll 1
   for (int i = i0; i < i1; i++) {
+    // the layer's planes landed before the previous mid barrier (or in the
+    // prologue); this barrier retires the previous finalisation and
+    // publishes the facet terms / x factors made during it
     cp_wait<0>();
     __syncthreads();
     if (i + 1 < i1) load_planes(P * (i + 1) + 1, P);
@@ -191,9 +243,10 @@ __global__ void __launch_bounds__(CY* CZ, MinBlocks<P>::v) k_xmarch(SArgs A) {
       interp3<P>(t);  // T at the Gauss points
       const int64_t cell = ((int64_t)i * A.ny + j) * A.nz + k;
       const int ib = P * i;
-      cell_element<P, RCF>(A, F, i, j, k, cell, t, G, ymask, [&](int a, int b, int c) {
-        return Tr[((ib + a) % NR) * PL + ms0 + b * NZT + c];
-      });
+      cell_element<P, RCF, COOP>(
+          A, F, i, j, k, cell, t, G, ymask,
+          [&](int a, int b, int c) { return Tr[((ib + a) % NR) * PL + ms0 + b * NZT + c]; }, Sx,
+          Sy + jl * MB * Q, Sz + kl * MB * Q, Fo + jl * Q * Q);
       // x face shared with the previous layer: add the carry, keep the new one
 #pragma unroll
       for (int q = 0; q < Q * Q; q++) {
@@ -228,7 +281,9 @@ __global__ void __launch_bounds__(CY* CZ, MinBlocks<P>::v) k_xmarch(SArgs A) {
         for (int q = 0; q < EW; q++) Ec[q * NT + tid] = t[q];
       }
     }
+    cp_wait<0>();  // the next layer's planes (prefetched at the top) have landed
     __syncthreads();
+    if (COOP && i + 1 < i1) side_work(i + 1);
     // latent increments of this layer or carried from the previous one
     const bool latn = LATENT && (lat_any[i % 3] | lat_any[(i + 2) % 3]);
 #pragma unroll 1
