@@ -71,17 +71,8 @@ __global__ void __launch_bounds__(CY* CZ, MinBlocks<P>::v) k_xmarch(SArgs A) {
   // tile-edge node planes are seams unless they are the domain boundary
   const bool sy_lo = jl == 0 && j0 > 0, sy_hi = jl == CY - 1 && j0 + CY < A.ny;
   const bool sz_lo = kl == 0 && k0 > 0, sz_hi = kl == CZ - 1 && k0 + CZ < A.nz;
-#ifdef ST_EXP_NORARE
-  const CellFlags F{(A.flags & ST_RHS_DIFFUSION) != 0, false, false, false};
-#elif defined(ST_EXP_NOFACE)
-  const CellFlags F{(A.flags & ST_RHS_DIFFUSION) != 0, false,
-                    (A.flags & ST_RHS_SOURCE) != 0 && A.nb > 0, false};
-#elif defined(ST_EXP_NOSRC)
-  const CellFlags F{(A.flags & ST_RHS_DIFFUSION) != 0, (A.flags & ST_RHS_FACES) != 0, false, false};
-#else
   const CellFlags F{(A.flags & ST_RHS_DIFFUSION) != 0, (A.flags & ST_RHS_FACES) != 0,
                     (A.flags & ST_RHS_SOURCE) != 0 && A.nb > 0, (A.flags & ST_RHS_FROZEN_K) != 0};
-#endif
   const int64_t plane_stride = (int64_t)A.NY * A.NZ;
   const int64_t tile0 = (int64_t)P * j0 * A.NZ + (int64_t)P * k0;
   // this thread's node origin within a plane (global offset and smem slot)
@@ -146,8 +137,10 @@ __global__ void __launch_bounds__(CY* CZ, MinBlocks<P>::v) k_xmarch(SArgs A) {
     }
     if (COOP && tid < nbt) src_factor_xy<P>(A, anchor<P>(A, 0, il), A.beams[tid].x, Sx + tid * Q);
   };
-  double amax = 0.0, smax = -INFINITY;
-  bool bad = false;
+  // max |T'| as the bit pattern of |T'| (monotone for non-negative doubles;
+  // a NaN is above +inf, so it sticks without a separate flag)
+  unsigned long long amaxb = 0ull;
+  double smax = -INFINITY;
 
   // node (b, c) of plane I owned by this thread (element plane a at pe);
   // b, c are compile-time.  xc: 0 = not an x seam, 1 = x seam with this CTA
@@ -182,9 +175,9 @@ __global__ void __launch_bounds__(CY* CZ, MinBlocks<P>::v) k_xmarch(SArgs A) {
     *(seam ? A.fseam + so : A.out + idx) = seam ? f : o;
     if (LATENT && seam) A.cseam[so] = dc;
     if (!seam) {
-      amax = dmax(amax, fabs(o));
+      const unsigned long long ab = (unsigned long long)__double_as_longlong(o) & 0x7fffffffffffffffull;
+      amaxb = ab > amaxb ? ab : amaxb;
       smax = dmax(smax, o);
-      bad |= (o != o);
     }
   };
 
@@ -303,5 +296,5 @@ __global__ void __launch_bounds__(CY* CZ, MinBlocks<P>::v) k_xmarch(SArgs A) {
   __syncthreads();
   finalize_owned(P * i1, 0, (i1 < A.nx || A.iface_hi) ? 1 : 0,
                  LATENT && lat_any[(i1 - 1) % 3] != 0);
-  block_max2(bad ? (double)NAN : amax, smax, A.red);
+  block_max2(__longlong_as_double((long long)amaxb), smax, A.red);
 }

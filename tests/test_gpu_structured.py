@@ -152,3 +152,64 @@ def test_structured_determinism_run_to_run():
     b = op.evaluate_rhs(T, rc, beams)
     # seams are combined with atomics: order noise only
     assert rel(a, b) < 1e-15
+
+
+@pytest.mark.parametrize("kernel", ["march", "slab"])
+@pytest.mark.parametrize("p", [1, 2, 3, 4])
+def test_structured_uniform_history_loop_matches_oracle(p, kernel, monkeypatch):
+    """The config-1 path: consolidated material (r_c = 1 everywhere, never
+    stored), latent heat, convection, two beams, resident multi-step loop."""
+    from cpu_oracle import beam_tuple, run_explicit
+    monkeypatch.setenv("ST_KERNEL", kernel)
+    box, op, orc, T, rc, beams, tb = _setup(p, latent=True, hconv=10.0, seed=31)
+    T = 300.0 + np.random.default_rng(4).uniform(0.0, 1700.0, op.nv)
+    T[box.is_dirichlet] = 300.0
+    # two concurrent beams (one LayerPath each)
+    lp1 = st.LayerPath(0, 0.0, [st.Segment(0.0, box.ny * H / 2, box.nx * H, box.ny * H / 2,
+                                           1.0, 150.0)], 0.0)
+    lp2 = st.LayerPath(0, 0.0, [st.Segment(box.nx * H, box.ny * H * 0.3, 0.0, box.ny * H * 0.3,
+                                           1.0, 80.0)], 0.0)
+    dts, bm = st.flatten_schedule([lp1, lp2], 1e-7, 20)
+    assert bm.shape[1] == 2
+    op.set_state(T, 1.0)
+    fail, ext, tmax = op.run_explicit(dts, bm)
+    assert fail == 0
+    Tg, rcg = op.get_state()
+    ones = np.ones((op.n_cells, p + 1, p + 1, p + 1))
+    To, _ = run_explicit(orc, T, ones, dts, [[beam_tuple(b) for b in row] for row in bm])
+    assert rel(Tg, To) < 1e-12
+    assert np.all(rcg == 1.0)
+
+
+@pytest.mark.parametrize("kernel", ["march", "slab"])
+@pytest.mark.parametrize("p", [1, 2, 3])
+def test_structured_instability_is_reported(p, kernel, monkeypatch):
+    """run_scan_phase's divergence check on the resident loop: the failing
+    step and a non-finite or > 1e7 K extreme (timestepping.py:186-192)."""
+    monkeypatch.setenv("ST_KERNEL", kernel)
+    box, op, orc, T, rc, beams, tb = _setup(p, seed=41)
+    T = 300.0 + np.random.default_rng(5).uniform(0.0, 10.0, op.nv)
+    lp = st.LayerPath(0, 0.0, [st.Segment(0.0, box.ny * H / 2, box.nx * H, box.ny * H / 2,
+                                          1.0, 150.0)], 0.0)
+    _, bm = st.flatten_schedule(lp, 1e-7, 40)
+    dts = np.full(40, 1e-3)  # far above the stability bound
+    op.set_state(T, 1.0)
+    fail, ext, tmax = op.run_explicit(dts, bm)
+    assert fail >= 1
+    assert not (np.isfinite(ext) and ext <= 1e7)
+
+
+def test_structured_too_many_tabled_beams_fail_loudly():
+    box, op, orc, T, rc, beams, tb = _setup(2, seed=1)
+    many = [BeamState(np.array([H * (1 + i), H * 3]), 0.0, 10.0, True) for i in range(9)]
+    with pytest.raises(Exception):
+        op.evaluate_rhs(T, rc, many)
+
+
+def test_structured_seams_are_deterministic():
+    """Seam partials go to per-CTA slots and are summed in a fixed order:
+    repeated evaluations are bitwise identical."""
+    box, op, orc, T, rc, beams, tb = _setup(2, seed=21)
+    a = op.evaluate_rhs(T, rc, beams)
+    b = op.evaluate_rhs(T, rc, beams)
+    assert np.array_equal(a, b)
