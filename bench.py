@@ -410,20 +410,25 @@ def run_slabs(args):
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     total_ms = float(t.item())
     # end to end: host slab in -> K split steps with the exchange -> host out
-    T_host = box.local_of(T0)
+    # (pinned host buffers, as in the single-GPU line)
+    T_loc = box.local_of(T0)
+    T_host = torch.empty(len(T_loc), dtype=torch.float64, pin_memory=True).numpy()
+    T_host[:] = T_loc
+    T_buf = torch.empty(len(T_loc), dtype=torch.float64, pin_memory=True).numpy()
     dist.barrier()
     t0 = time.perf_counter()
     op.set_state(T_host, 1.0)
     with torch.cuda.stream(stepper.stream):
         for i in range(args.warmup, args.warmup + args.steps):
             drv.step(float(dts[i]), beams[i])
-    T_out, rc_out = op.get_state()
+    T_out, rc_out = op.get_state(out=T_buf)
     e2e_s = torch.tensor([time.perf_counter() - t0], device="cuda")
     dist.all_reduce(e2e_s, op=dist.ReduceOp.MAX)
     nb = beams.shape[1]
     e2e = {"value": glob.n_dofs * args.steps / float(e2e_s.item()), "unit": "DoF-updates/s",
            "h2d_bytes_per_step": (T_host.nbytes + args.steps * nb * 40) / args.steps,
-           "d2h_bytes_per_step": (T_out.nbytes + rc_out.nbytes) / args.steps,
+           "d2h_bytes_per_step": (T_out.nbytes + (0 if rc_out.strides == (0,) else rc_out.nbytes))
+           / args.steps,
            "api": "per rank: set_state + split steps (NCCL exchange) + get_state; max over ranks"}
     am, _ = stepper.maxima()
     amt = torch.tensor([am], device="cuda")
