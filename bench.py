@@ -479,13 +479,19 @@ def run_ours(args):
     T_host = torch.empty(len(r["T0"]), dtype=torch.float64, pin_memory=True).numpy()
     T_host[:] = r["T0"]
     T_buf = torch.empty(len(r["T0"]), dtype=torch.float64, pin_memory=True).numpy()
-    t0 = time.perf_counter()
-    op.set_state(T_host, 1.0)
-    fail, _, _ = op.run_explicit(dts, beams)
-    T_out, rc_out = op.get_state(out=T_buf)
-    e2e_s = time.perf_counter() - t0
-    if fail or not np.all(np.isfinite(T_out)):
-        raise RuntimeError("end-to-end run diverged")
+    # one untimed pass (first-touch of the pinned pages and the beam
+    # schedule buffer), then the median of three timed passes (wall clock)
+    e2e_runs = []
+    for rep in range(4):
+        t0 = time.perf_counter()
+        op.set_state(T_host, 1.0)
+        fail, _, _ = op.run_explicit(dts, beams)
+        T_out, rc_out = op.get_state(out=T_buf)
+        if rep:
+            e2e_runs.append(time.perf_counter() - t0)
+        if fail or not np.all(np.isfinite(T_out)):
+            raise RuntimeError("end-to-end run diverged")
+    e2e_s = float(np.median(e2e_runs))
     nb = beams.shape[1]
     h2d = T_host.nbytes + args.steps * (nb * 40 + 8)
     # r_c = 1 stays uniform on the device (never stored, never copied):
@@ -496,7 +502,8 @@ def run_ours(args):
            "h2d_bytes_per_step": h2d / args.steps, "d2h_bytes_per_step": d2h / args.steps,
            "api": "ThermalOperator.set_state(T pinned host) + run_explicit(K steps, "
                   "st_explicit_steps; per step dt + beams in, stability maxima out) + "
-                  "get_state(T into pinned host; uniform r_c as a scalar); wall clock"}
+                  "get_state(T into pinned host; uniform r_c as a scalar); wall clock, "
+                  "median of 3 passes after one untimed pass"}
     cfg = dict(workload=w["name"], dofs=dofs, backend="structured",
                l2=L2_NOTE,
                parallelism=f"replicas x{ws}", **w["cfg"])
