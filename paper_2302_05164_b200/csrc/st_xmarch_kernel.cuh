@@ -67,7 +67,6 @@ __global__ void __launch_bounds__(CY* CZ, MinBlocks<P>::v) k_xmarch(SArgs A) {
   const bool hiZ = live && (kl == CZ - 1 || k == A.nz - 1);
   const int Jn = min(P * CY, P * (A.ny - j0)) + 1;
   const int Kn = min(P * CZ, P * (A.nz - k0)) + 1;
-  const bool step = A.mode == 0;
   // tile-edge node planes are seams unless they are the domain boundary
   const bool sy_lo = jl == 0 && j0 > 0, sy_hi = jl == CY - 1 && j0 + CY < A.ny;
   const bool sz_lo = kl == 0 && k0 > 0, sz_hi = kl == CZ - 1 && k0 + CZ < A.nz;
