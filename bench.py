@@ -452,6 +452,59 @@ def run_slabs(args):
     dist.destroy_process_group()
 
 
+def implicit_measure(device, n_steps=10, cpu=True):
+    """Backward-Euler cool-down steps (Newton + Jacobi-PCG on the device,
+    SURVEY §8 rows a14-a18) on a BASELINE configs[3]-sized Q1 mesh: a
+    40x40x14 box through the unstructured (Forest/DofMap) backend, 24,600
+    DoFs, reference default material, krylov_tol 1e-10, dt 1 ms, from a
+    synthetic post-scan field (300 K + a 1700 K Gaussian bump at the top).
+    Returns ms per BE step, iterations, and the oracle's time for one step."""
+    st = _st()
+    h = 80e-6
+    box = st.StructuredBox(40, 40, 14, h, degree=1)
+    forest, dm = box.to_forest_dofmap()
+    params = st.ProcessParams(st.MaterialParams(), st.BoundaryParams(), st.HeatSourceParams(),
+                              st.MeshParams(h_coarse=h, n_refine=0, h_powder=h))
+    s = st.SolverSettings(explicit_cooldown_steps=0, dt_implicit=1e-3, krylov_tol=1e-10,
+                          preconditioner="diagonal")
+    op = st.ThermalOperator(forest, dm, params, s, device=device)
+    n = op.nv
+    NY, NZ = box.ny + 1, box.nz + 1  # vertex lattice, x-major / z-fastest (mesh.py:712-715)
+    idx = np.arange(n)
+    x, y, z = (idx // (NY * NZ)) * h, ((idx // NZ) % NY) * h, (idx % NZ - box.nz) * h
+    r2 = (x - 20 * h) ** 2 + (y - 20 * h) ** 2 + z ** 2
+    T0 = 300.0 + 1700.0 * np.exp(-r2 / (4e-4) ** 2)
+    rc0 = np.ones(op.n_cells * op.qpc)
+    op.set_state(T0, rc0)
+    op.implicit_step(1e-3, s)
+    op.finish_implicit_step()
+    op.set_state(T0, rc0)
+    nn = nk = 0
+    t0 = time.perf_counter()
+    for _ in range(n_steps):
+        out = op.implicit_step(1e-3, s)
+        if out is None:
+            raise RuntimeError("implicit step did not converge")
+        op.finish_implicit_step()
+        nn += out[0]
+        nk += out[1]
+    el = time.perf_counter() - t0
+    res = {"workload": "config3-sized cool-down: 40x40x14 Q1 box, unstructured backend",
+           "dofs": int(n), "be_steps": n_steps, "ms_per_be_step": el / n_steps * 1e3,
+           "newton_per_step": nn / n_steps, "cg_per_step": nk / n_steps,
+           "us_per_cg_iteration": el / max(nk, 1) * 1e6}
+    if cpu:
+        sys.path.insert(0, os.path.join(ROOT, "oracle"))
+        from cpu_oracle import OracleOperator, implicit_step, structured_tables
+        orc = OracleOperator(structured_tables(box.nx, box.ny, box.nz, h, 1), params)
+        t1 = time.perf_counter()
+        implicit_step(orc, T0, rc0.reshape(-1, 2, 2, 2), 1e-3, s)
+        res["cpu_oracle_ms_per_be_step"] = (time.perf_counter() - t1) * 1e3
+        res["cpu_oracle"] = "oracle/cpu_oracle.py implicit_step on the same box, one BE step"
+    op.close()
+    return res
+
+
 def run_ours(args):
     import torch
     ws, rank, local = dist_env()
@@ -528,6 +581,8 @@ def run_ours(args):
                               "fp64": rp["roofline"].get("fp64")}
             rp["op"].close()
         out["sweep_config2"] = sweep
+    if rank == 0 and ws == 1 and args.sweep:
+        out["implicit_config3"] = implicit_measure(local, cpu=not args.no_cpu_baseline)
     if rank == 0 and ws == 1 and not args.no_cpu_baseline:
         out["cpu_baseline"] = cpu_baseline(w, seconds=args.cpu_seconds)
     if rank == 0:

@@ -175,6 +175,9 @@ static void ctx_free(st_ctx* c) {
   if (x.pinned) cudaFreeHost(x.pinned);
   if (x.ev0) cudaEventDestroy(x.ev0);
   if (x.ev1) cudaEventDestroy(x.ev1);
+  for (auto& e : x.cg_ev)
+    if (e) cudaEventDestroy(e);
+  x.cgs.free();
   x.T.free();
   x.T_alt.free();
   x.rc.free();
@@ -324,35 +327,44 @@ static int pcg_dev(Ctx& c, const double* Tl, const double* rc, double dt, const 
   if (bnorm == 0.0) return ST_OK;
   ST_CUDA(cudaMemcpyAsync(r, b, nv * sizeof(double), cudaMemcpyDeviceToDevice, c.stream));
   if (bnorm <= tol * bnorm) return ST_OK;
+  // scalars stay on the device; the host reads r.r of iteration it while
+  // iteration it + 1 is already queued (its kernels turn into no-ops once
+  // the device-side copy of the stopping rule has fired)
+  if ((int64_t)c.cgs.n < 2 * kRedBlocks + 8) ST_TRY(c.cgs.alloc(2 * kRedBlocks + 8));
+  double* part = c.cgs.p;
+  double* s = c.cgs.p + 2 * kRedBlocks;
+  const double thr = tol * bnorm;
+  ST_CUDA(cudaMemsetAsync(s + 6, 0, sizeof(double), c.stream));
   if (diag_inv)
     ST_TRY(vec_mul(&c, r, diag_inv, z, nv));
   else
     ST_CUDA(cudaMemcpyAsync(z, r, nv * sizeof(double), cudaMemcpyDeviceToDevice, c.stream));
   ST_CUDA(cudaMemcpyAsync(p, z, nv * sizeof(double), cudaMemcpyDeviceToDevice, c.stream));
-  double rz;
-  ST_TRY(c.dot(r, z, nv, &rz));
-  for (int it = 1; it <= max_iter; it++) {
+  ST_TRY(dot_to_device(&c, r, z, nv, part, s));  // s[0] = rz
+  if (!c.cg_ev[0]) {
+    for (auto& e : c.cg_ev) ST_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  }
+  auto enqueue = [&](int it) -> int {
     ST_TRY(c.be->jacobian(p, Tl, rc, dt, Ap));
-    double pAp;
-    ST_TRY(c.dot(p, Ap, nv, &pAp));
-    double alpha = rz / pAp;
-    ST_TRY(vec_axpy(&c, alpha, p, x, nv));
-    ST_TRY(vec_axpy(&c, -alpha, Ap, r, nv));
-    double rr;
-    ST_TRY(c.dot(r, r, nv, &rr));
-    if (std::sqrt(rr) <= tol * bnorm) {
+    ST_TRY(cg_alpha(&c, p, Ap, nv, part, s));
+    ST_TRY(cg_update(&c, p, Ap, diag_inv, x, r, z, nv, part, s, thr));
+    ST_CUDA(cudaMemcpyAsync(c.pinned + (it & 1), s + 3, sizeof(double), cudaMemcpyDeviceToHost,
+                            c.stream));
+    ST_CUDA(cudaEventRecord(c.cg_ev[it & 1], c.stream));
+    ST_TRY(cg_p(&c, s, z, p, nv));
+    return ST_OK;
+  };
+  ST_TRY(enqueue(1));
+  for (int it = 1; it <= max_iter; it++) {
+    if (it < max_iter) ST_TRY(enqueue(it + 1));
+    ST_CUDA(cudaEventSynchronize(c.cg_ev[it & 1]));
+    if (std::sqrt(c.pinned[it & 1]) <= thr) {
       *iters = it;
+      ST_CUDA(cudaStreamSynchronize(c.stream));  // the queued no-op iteration
       return ST_OK;
     }
-    if (diag_inv)
-      ST_TRY(vec_mul(&c, r, diag_inv, z, nv));
-    else
-      ST_CUDA(cudaMemcpyAsync(z, r, nv * sizeof(double), cudaMemcpyDeviceToDevice, c.stream));
-    double rz_new;
-    ST_TRY(c.dot(r, z, nv, &rz_new));
-    ST_TRY(vec_xpby(&c, z, rz_new / rz, p, nv));
-    rz = rz_new;
   }
+  ST_CUDA(cudaStreamSynchronize(c.stream));
   *iters = max_iter;
   *converged = 0;
   return ST_OK;

@@ -172,6 +172,8 @@ struct Ctx {
   int history_pending = 0;
   DevBuf<DevBeam> beams;
   DevBuf<double> red;       // reduction partials / small results
+  DevBuf<double> cgs;       // PCG partials (2 kRedBlocks) + scalars
+  cudaEvent_t cg_ev[2] = {nullptr, nullptr};  // PCG residual reads in flight
   DevBuf<double> scratch[8];
   double* pinned = nullptr;  // small pinned host staging
   // profiling of the dominant kernel
@@ -206,6 +208,13 @@ int vec_sub_scale(Ctx* c, const double* a, const double* b, double s,
                   const double* m, double* y, int64_t n);  // y = a/s - (b + m)
 int vec_sub(Ctx* c, const double* a, const double* b, double* y, int64_t n);
 int vec_scal_copy(Ctx* c, double s, const double* x, double* y, int64_t n);
+// PCG with device-resident scalars (st_reduce.cu); part: 2 kRedBlocks
+// doubles, s: 7 scalars (rz, pAp, alpha, rr, rz_new, beta, converged)
+int cg_alpha(Ctx* c, const double* p, const double* Ap, int64_t n, double* part, double* s);
+int cg_update(Ctx* c, const double* p, const double* Ap, const double* dinv, double* x, double* r,
+              double* z, int64_t n, double* part, double* s, double thr);
+int cg_p(Ctx* c, const double* s, const double* z, double* p, int64_t n);
+int dot_to_device(Ctx* c, const double* a, const double* b, int64_t n, double* part, double* out);
 
 constexpr int kRedBlocks = 296;  // 2 x 148 SMs
 constexpr int kThreads = 256;

@@ -90,6 +90,127 @@ __global__ void k_scal_copy(double s, const double* x, double* y, int64_t n) {
   if (i < n) y[i] = s * x[i];
 }
 
+// --- Jacobi-PCG with device-resident scalars (pcg_dev): one host read per
+// iteration (the residual norm for the stopping rule).  Scalars s[]:
+// 0 rz, 1 pAp, 2 alpha, 3 rr, 4 rz_new, 5 beta, 6 converged flag.  Once the
+// flag is set the kernels are no-ops, so the host can keep one iteration
+// in flight while it reads the previous residual norm.  The vector updates and
+// the dot products use the same expressions, grid and summation order as
+// k_axpy / k_mul / k_xpby / k_dot_partial + k_sum_partials.
+__device__ __forceinline__ double block_sum(double v, double* sm) {
+  sm[threadIdx.x] = v;
+  __syncthreads();
+  for (int s = blockDim.x / 2; s > 0; s >>= 1) {
+    if ((int)threadIdx.x < s) sm[threadIdx.x] += sm[threadIdx.x + s];
+    __syncthreads();
+  }
+  const double r = sm[0];
+  __syncthreads();
+  return r;
+}
+
+__global__ void k_cg_alpha(const double* part, int np, double* s) {
+  if (s[6] != 0.0) return;
+  __shared__ double sm[512];
+  double acc = 0.0;
+  for (int i = threadIdx.x; i < np; i += blockDim.x) acc += part[i];
+  const double pAp = block_sum(acc, sm);
+  if (threadIdx.x == 0) {
+    s[1] = pAp;
+    s[2] = s[0] / pAp;
+  }
+}
+
+// x += alpha p; r -= alpha Ap; z = D^-1 r; partials of r.r and r.z
+__global__ void k_cg_update(const double* s, const double* p, const double* Ap,
+                            const double* dinv, double* x, double* r, double* z, int64_t n,
+                            double* part) {
+  if (s[6] != 0.0) return;
+  __shared__ double sm[kThreads];
+  const double alpha = s[2];
+  double arr = 0.0, arz = 0.0;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    x[i] = fma(alpha, p[i], x[i]);
+    const double ri = fma(-alpha, Ap[i], r[i]);
+    r[i] = ri;
+    const double zi = dinv ? ri * dinv[i] : ri;
+    z[i] = zi;
+    arr = fma(ri, ri, arr);
+    arz = fma(ri, zi, arz);
+  }
+  const double brr = block_sum(arr, sm);
+  const double brz = block_sum(arz, sm);
+  if (threadIdx.x == 0) {
+    part[blockIdx.x] = brr;
+    part[gridDim.x + blockIdx.x] = brz;
+  }
+}
+
+__global__ void k_cg_sum2(const double* part, int np, double* s, double thr) {
+  if (s[6] != 0.0) return;
+  __shared__ double sm[512];
+  double a = 0.0, b = 0.0;
+  for (int i = threadIdx.x; i < np; i += blockDim.x) {
+    a += part[i];
+    b += part[np + i];
+  }
+  const double rr = block_sum(a, sm);
+  const double rz_new = block_sum(b, sm);
+  if (threadIdx.x == 0) {
+    s[3] = rr;
+    s[4] = rz_new;
+    s[5] = rz_new / s[0];
+    s[0] = rz_new;
+    s[6] = sqrt(rr) <= thr ? 1.0 : 0.0;  // the host's stopping rule, same doubles
+  }
+}
+
+// p = z + beta p
+__global__ void k_cg_p(const double* s, const double* z, double* p, int64_t n) {
+  if (s[6] != 0.0) return;
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i < n) p[i] = fma(s[5], p[i], z[i]);
+}
+
+int cg_alpha(Ctx* c, const double* p, const double* Ap, int64_t n, double* part, double* s) {
+  k_dot_partial<<<kRedBlocks, kThreads, 0, c->stream>>>(p, Ap, n, part);
+  c->launches++;
+  ST_LAUNCHED();
+  k_cg_alpha<<<1, 512, 0, c->stream>>>(part, kRedBlocks, s);
+  c->launches++;
+  ST_LAUNCHED();
+  return ST_OK;
+}
+
+int cg_update(Ctx* c, const double* p, const double* Ap, const double* dinv, double* x, double* r,
+              double* z, int64_t n, double* part, double* s, double thr) {
+  k_cg_update<<<kRedBlocks, kThreads, 0, c->stream>>>(s, p, Ap, dinv, x, r, z, n, part);
+  c->launches++;
+  ST_LAUNCHED();
+  k_cg_sum2<<<1, 512, 0, c->stream>>>(part, kRedBlocks, s, thr);
+  c->launches++;
+  ST_LAUNCHED();
+  return ST_OK;
+}
+
+int cg_p(Ctx* c, const double* s, const double* z, double* p, int64_t n) {
+  k_cg_p<<<nb(n), kThreads, 0, c->stream>>>(s, z, p, n);
+  c->launches++;
+  ST_LAUNCHED();
+  return ST_OK;
+}
+
+int dot_to_device(Ctx* c, const double* a, const double* b, int64_t n, double* part, double* out) {
+  k_dot_partial<<<kRedBlocks, kThreads, 0, c->stream>>>(a, b, n, part);
+  c->launches++;
+  ST_LAUNCHED();
+  k_sum_partials<<<1, 512, 0, c->stream>>>(part, kRedBlocks, out);
+  c->launches++;
+  ST_LAUNCHED();
+  return ST_OK;
+}
+
 #define ST_VEC_LAUNCH(kern, ...)                                   \
   do {                                                             \
     kern<<<nb(n), kThreads, 0, c->stream>>>(__VA_ARGS__);          \
