@@ -177,6 +177,8 @@ static void ctx_free(st_ctx* c) {
   if (x.ev1) cudaEventDestroy(x.ev1);
   for (auto& e : x.cg_ev)
     if (e) cudaEventDestroy(e);
+  for (auto& g : x.cg_exec)
+    if (g) cudaGraphExecDestroy(g);
   x.cgs.free();
   x.T.free();
   x.T_alt.free();
@@ -344,17 +346,63 @@ static int pcg_dev(Ctx& c, const double* Tl, const double* rc, double dt, const 
   if (!c.cg_ev[0]) {
     for (auto& e : c.cg_ev) ST_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
   }
-  auto enqueue = [&](int it) -> int {
+  auto body = [&](int par) -> int {
     ST_TRY(c.be->jacobian(p, Tl, rc, dt, Ap));
     ST_TRY(cg_alpha(&c, p, Ap, nv, part, s));
     ST_TRY(cg_update(&c, p, Ap, diag_inv, x, r, z, nv, part, s, thr));
-    ST_CUDA(cudaMemcpyAsync(c.pinned + (it & 1), s + 3, sizeof(double), cudaMemcpyDeviceToHost,
+    ST_CUDA(cudaMemcpyAsync(c.pinned + par, s + 3, sizeof(double), cudaMemcpyDeviceToHost,
                             c.stream));
-    ST_CUDA(cudaEventRecord(c.cg_ev[it & 1], c.stream));
     ST_TRY(cg_p(&c, s, z, p, nv));
     return ST_OK;
   };
+  // iterations 2.. replay a captured graph of the iteration (one per
+  // parity of the pinned slot): the ~10 small launches of an iteration
+  // dominate at cool-down mesh sizes.  ST_CG_GRAPH=0 launches directly.
+  static const bool use_graph = !(getenv("ST_CG_GRAPH") && getenv("ST_CG_GRAPH")[0] == '0');
+  int64_t graph_kernels = 0;
+  auto capture = [&](int par) -> int {
+    cudaGraph_t g = nullptr;
+    const int64_t l0 = c.launches;
+    ST_CUDA(cudaStreamBeginCapture(c.stream, cudaStreamCaptureModeThreadLocal));
+    const int brc = body(par);
+    const cudaError_t e = cudaStreamEndCapture(c.stream, &g);
+    graph_kernels = c.launches - l0;
+    c.launches = l0;
+    if (brc != ST_OK || e != cudaSuccess) {
+      if (g) cudaGraphDestroy(g);
+      cudaGetLastError();
+      if (brc != ST_OK) return brc;
+      ST_CUDA(e);
+    }
+    cudaGraphExec_t& ex = c.cg_exec[par];
+    if (ex) {
+      cudaGraphExecUpdateResultInfo info;
+      if (cudaGraphExecUpdate(ex, g, &info) != cudaSuccess) {
+        cudaGetLastError();
+        cudaGraphExecDestroy(ex);
+        ex = nullptr;
+      }
+    }
+    cudaError_t ie = ex ? cudaSuccess : cudaGraphInstantiate(&ex, g, 0);
+    cudaGraphDestroy(g);
+    ST_CUDA(ie);
+    return ST_OK;
+  };
+  auto enqueue = [&](int it) -> int {
+    if (use_graph && it > 1) {
+      ST_CUDA(cudaGraphLaunch(c.cg_exec[it & 1], c.stream));
+      c.launches += graph_kernels;
+    } else {
+      ST_TRY(body(it & 1));
+    }
+    ST_CUDA(cudaEventRecord(c.cg_ev[it & 1], c.stream));
+    return ST_OK;
+  };
   ST_TRY(enqueue(1));
+  if (use_graph && max_iter > 1) {
+    ST_TRY(capture(0));
+    ST_TRY(capture(1));
+  }
   for (int it = 1; it <= max_iter; it++) {
     if (it < max_iter) ST_TRY(enqueue(it + 1));
     ST_CUDA(cudaEventSynchronize(c.cg_ev[it & 1]));

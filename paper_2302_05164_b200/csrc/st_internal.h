@@ -174,6 +174,7 @@ struct Ctx {
   DevBuf<double> red;       // reduction partials / small results
   DevBuf<double> cgs;       // PCG partials (2 kRedBlocks) + scalars
   cudaEvent_t cg_ev[2] = {nullptr, nullptr};  // PCG residual reads in flight
+  cudaGraphExec_t cg_exec[2] = {nullptr, nullptr};  // captured PCG iteration per parity
   DevBuf<double> scratch[8];
   double* pinned = nullptr;  // small pinned host staging
   // profiling of the dominant kernel
