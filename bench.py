@@ -489,10 +489,20 @@ def implicit_measure(device, n_steps=10, cpu=True):
         nn += out[0]
         nk += out[1]
     el = time.perf_counter() - t0
+    # the explicit scan steps of the same backend (config 3 integrates 40k
+    # of them per layer): 2 x 512 device-resident steps of a 1 m/s track
+    lp = st.LayerPath(0, 0.0, [st.Segment(5 * h, 20 * h, 35 * h, 20 * h, 1.0, 70.0)], 0.0)
+    dts_e, bm_e = st.flatten_schedule(lp, 1e-6, 1024)
+    op.set_state(T0, rc0)
+    op.run_explicit(dts_e[:512], bm_e[:512])  # returns after the batch's stability read
+    te = time.perf_counter()
+    fail, _, _ = op.run_explicit(dts_e[512:], bm_e[512:])
+    el_e = time.perf_counter() - te
+    res_e = {"explicit_us_per_step": el_e / 512 * 1e6, "explicit_fail": int(fail)}
     res = {"workload": "config3-sized cool-down: 40x40x14 Q1 box, unstructured backend",
            "dofs": int(n), "be_steps": n_steps, "ms_per_be_step": el / n_steps * 1e3,
            "newton_per_step": nn / n_steps, "cg_per_step": nk / n_steps,
-           "us_per_cg_iteration": el / max(nk, 1) * 1e6}
+           "us_per_cg_iteration": el / max(nk, 1) * 1e6, **res_e}
     if cpu:
         sys.path.insert(0, os.path.join(ROOT, "oracle"))
         from cpu_oracle import OracleOperator, implicit_step, structured_tables
