@@ -510,6 +510,25 @@ __global__ void k_prep_v(int64_t nv, const uint8_t* is_dir, const double* v, dou
   vd[i] = is_dir[i] ? 0.0 : v[i];
 }
 
+// Jacobian input in one launch: threads < nv copy v with Dirichlet rows
+// zeroed (non-slave nodes), threads nv .. nv+ns-1 interpolate the slaves
+// from v (the same values the copy -> distribute -> zero sequence gives:
+// slaves and Dirichlet nodes are disjoint, masters are read before zeroing)
+__global__ void k_prep_jac(int64_t nv, int64_t ns, const uint8_t* is_dir, const uint8_t* is_slave,
+                           const double* v, const int64_t* slaves, const int64_t* ptr,
+                           const int64_t* masters, const double* w, double* vd) {
+  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i < nv) {
+    if (!is_slave[i]) vd[i] = is_dir[i] ? 0.0 : v[i];
+    return;
+  }
+  i -= nv;
+  if (i >= ns) return;
+  double acc = 0.0;
+  for (int64_t p = ptr[i]; p < ptr[i + 1]; p++) acc += w[p] * v[masters[p]];
+  vd[slaves[i]] = acc;
+}
+
 __global__ void k_mask_rows(int64_t nv, const uint8_t* is_dir, const uint8_t* is_slave, double* v) {
   int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (i >= nv) return;
@@ -656,9 +675,8 @@ struct Unstructured : Backend {
                double* out) override {
     double* vd;
     ST_TRY(c->vec(5, &vd));
-    ST_CUDA(cudaMemcpyAsync(vd, v, nv * sizeof(double), cudaMemcpyDeviceToDevice, c->stream));
-    ST_TRY(distribute(vd));
-    k_prep_v<<<nblk(nv), kThreads, 0, c->stream>>>(nv, is_dir.p, vd, vd);
+    k_prep_jac<<<nblk(nv + ns), kThreads, 0, c->stream>>>(nv, ns, is_dir.p, is_slave.p, v,
+                                                          slaves.p, sptr.p, smast.p, sw.p, vd);
     ST_TRY(launched());
     c->prof_begin();
     k_jac_cells<<<nblk(n), kThreads, 0, c->stream>>>(n, geo(), c->dp, vd, Tl, rc,
