@@ -109,7 +109,9 @@ __global__ void __launch_bounds__(CY* CZ, MinBlocks<P>::v) k_xmarch(SArgs A) {
                         : nullptr;
   bool lat_had = false;
   const unsigned ymask = F.source && live ? beam_column_mask<P>(A, j, k) : 0u;
-  const int nbt = F.source ? min(A.nb, MB) : 0;  // tabled beams (host: nb <= MB)
+  // tabled beams (host: nb <= MB); none when no cell of the tile is within
+  // a beam's y / z reach (the x factors are then never read)
+  const int nbt = (F.source && __syncthreads_or(ymask != 0u)) ? min(A.nb, MB) : 0;
   if (COOP) {
     for (int e = tid; e < nbt * CY; e += NT) {
       const int b = e / CY, r = e - (e / CY) * CY;
