@@ -119,13 +119,69 @@ def pack_beams(beams):
     return out
 
 
+def _beam_track(lp, taus):
+    """Vectorised layer_beam_state over an array of tau: the same closed
+    segment windows (first match), the same float expressions in the same
+    order; returns (x, y, z_top, power, active)."""
+    n = len(taus)
+    x = np.zeros(n)
+    y = np.zeros(n)
+    power = np.zeros(n)
+    active = np.zeros(n, dtype=np.int32)
+    if np.any(taus < 0.0):
+        raise ScheduleError(f"tau = {float(taus.min())} before the layer starts")
+    segs = lp.segments
+    found = np.zeros(n, dtype=bool)
+    t_seg = 0.0
+    for seg in segs:
+        d = seg.duration
+        hit = (~found) & (t_seg <= taus) & (taus <= t_seg + d)
+        if np.any(hit):
+            s = (taus[hit] - t_seg) * seg.v
+            frac = s / seg.length if seg.length > 0.0 else np.zeros_like(s)
+            x[hit] = seg.x0 + frac * (seg.x1 - seg.x0)
+            y[hit] = seg.y0 + frac * (seg.y1 - seg.y0)
+            power[hit] = seg.power
+            active[hit] = 1 if seg.power > 0.0 else 0
+            found |= hit
+        t_seg += d
+    rest = ~found
+    if np.any(rest & (taus > lp.duration())):
+        raise ScheduleError(f"tau = {float(taus[rest].max())} beyond the layer duration "
+                            f"{lp.duration()}")
+    return x, y, np.full(n, float(lp.z)), power, active
+
+
 def flatten_schedule(layer_paths, dt, n_steps, step0=1):
     """Beam records for steps step0 .. step0+n_steps-1 of a scan phase.
 
     ``layer_paths`` is one LayerPath or a list of concurrently scanned
     LayerPaths (multi-spot, BASELINE config 4: the source is linear in
     the beams).  Returns (dt_steps (n,), beams (n, n_beams) BEAM_DTYPE).
+    Vectorised over the steps (a layer is tens of thousands of steps);
+    identical to evaluating ``layer_beam_state`` at tau = (step - 1) dt
+    for every step (tests/test_schedule.py).
     """
+    if not isinstance(layer_paths, (list, tuple)):
+        layer_paths = [layer_paths]
+    duration = layer_paths[0].scan_duration()
+    nb = len(layer_paths)
+    steps = np.arange(step0, step0 + n_steps, dtype=np.int64)
+    taus = (steps - 1).astype(np.float64) * dt
+    dts = np.minimum(dt, duration - taus)
+    beams = np.zeros((n_steps, nb), dtype=BEAM_DTYPE)
+    for k, lp in enumerate(layer_paths):
+        x, y, z, pw, act = _beam_track(lp, taus)
+        beams["x"][:, k] = x
+        beams["y"][:, k] = y
+        beams["z_top"][:, k] = z
+        beams["power"][:, k] = pw
+        beams["active"][:, k] = act & (pw > 0.0)
+    return dts, beams
+
+
+def flatten_schedule_loop(layer_paths, dt, n_steps, step0=1):
+    """Per-step reference form of flatten_schedule (tests)."""
     if not isinstance(layer_paths, (list, tuple)):
         layer_paths = [layer_paths]
     duration = layer_paths[0].scan_duration()
