@@ -39,20 +39,6 @@ __constant__ double sU[4][kMQ];        // (x_q + 1) / 2
 __constant__ double sM[4][kMQ];        // 1D lumped mass of node a: sum_q W_q V[a][q]
 
 
-template <int P>
-__device__ __forceinline__ double coord(const SArgs& A, int axis, int cell, int q) {
-  // qp coordinate = anchor + u_q h with anchor = lattice * h when the box
-  // origin is on the lattice (one rounding, like the reference's
-  // anchor * h_fine, operators.py:105-112)
-  double anc;
-  if (A.use_lat) {
-    long long l = axis == 0 ? A.lx : (axis == 1 ? A.ly : A.lz);
-    anc = (double)(cell + l) * A.h;
-  } else {
-    anc = (axis == 0 ? A.ox : (axis == 1 ? A.oy : A.oz)) + (double)cell * A.h;
-  }
-  return q < 0 ? anc : anc + sU[P - 1][q] * A.h;
-}
 
 
 // inverse 1D lumped mass, runtime degree (seam kernel)

@@ -93,11 +93,6 @@ __device__ __forceinline__ void seam_add(const SArgs& A, int64_t idx, int slot, 
   }
 }
 
-// x seam: chunk boundary inside the slab, or a rank interface
-__device__ __forceinline__ bool x_seam(const SArgs& A, int P, int I) {
-  return (I > 0 && I < A.NX - 1 && (I % (P * A.Lx)) == 0) || (I == 0 && A.iface_lo) ||
-         (I == A.NX - 1 && A.iface_hi);
-}
 
 // inverse 1D lumped mass of node L on a line of N nodes
 template <int P>

@@ -504,11 +504,6 @@ __global__ void k_fold(int64_t nv, const int* fptr, const int* fent, const doubl
   diag[v] = d;
 }
 
-__global__ void k_prep_v(int64_t nv, const uint8_t* is_dir, const double* v, double* vd) {
-  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (i >= nv) return;
-  vd[i] = is_dir[i] ? 0.0 : v[i];
-}
 
 // Jacobian input in one launch: threads < nv copy v with Dirichlet rows
 // zeroed (non-slave nodes), threads nv .. nv+ns-1 interpolate the slaves
