@@ -1,0 +1,93 @@
+"""Size-independent properties at BASELINE.json's full sizes (the oracle is
+too slow there): config 1 (128x128x32 Q2, 4.29 M DoFs) and config 2
+(~50 M DoFs, p = 1 and 4).
+
+* heat conservation of the discrete diffusion operator: with adiabatic
+  boundaries (no Dirichlet plane, no facets, no source) the condensed
+  element sums cancel, sum_i f_i = 0 up to round-off
+  (reference test_acceptance.py::test_c05 checks the same law per step);
+* linearity of the source in the beam power;
+* positivity of the lumped apparent capacity with latent heat;
+* bitwise run-to-run determinism of the full explicit step (fixed-order
+  gathers and seam sums, no atomics).
+"""
+
+import numpy as np
+import pytest
+
+import paper_2302_05164_b200 as st
+from paper_2302_05164_b200.physics import BeamState
+
+pytestmark = pytest.mark.gpu
+
+
+def _params(h, latent=True):
+    mat = st.MaterialParams(k_p=6.7, k_m=32.0, k_s=6.7, T_s=300.0, T_l=1928.0, rho=4430.0,
+                            c=526.0, latent_heat=2.86e5 if latent else 0.0, T_lat_s=1878.0,
+                            T_lat_l=1928.0)
+    bnd = st.BoundaryParams(emissivity=0.3, T_inf=300.0, T_v=1e9, h_conv=10.0)
+    las = st.HeatSourceParams(radius=50e-6, h_powder=40e-6, power=70.0)
+    return st.ProcessParams(mat, bnd, las, st.MeshParams(h_coarse=h, n_refine=0, h_powder=h))
+
+
+def _box(dims, h, p, adiabatic):
+    nx, ny, nz = dims
+    return st.StructuredBox(nx, ny, nz, h, degree=p, dirichlet_bottom=not adiabatic,
+                            top_faces=not adiabatic)
+
+
+CASES = [("config1", (128, 128, 32), 31.25e-6, 2), ("config2_p1", (367, 367, 367), 1.0 / 367, 1),
+         ("config2_p4", (92, 92, 92), 1.0 / 92, 4)]
+
+
+@pytest.mark.parametrize("name,dims,h,p", CASES)
+def test_full_size_diffusion_conserves_heat(name, dims, h, p):
+    box = _box(dims, h, p, adiabatic=True)
+    op = st.ThermalOperator(box, box, _params(h), st.SolverSettings())
+    T = np.random.default_rng(7).uniform(300.0, 2500.0, op.nv)
+    if name == "config1":
+        # the nonlinear conductivity k(T) of config 1 (r_c = 1 everywhere)
+        rc = np.ones(op.n_cells * op.qpc)
+        f = op.evaluate_rhs(T, rc, None, faces=False, source=False)
+    else:
+        # ~50 M DoFs: frozen conductivity (the per-qp history array would be GBs)
+        f = op.evaluate_rhs(T, None, None, faces=False, source=False, frozen_k=20.0)
+    assert abs(float(f.sum())) <= 1e-11 * float(np.abs(f).sum())
+    op.close()
+
+
+def test_config1_source_is_linear_in_power_and_capacity_positive():
+    h = 31.25e-6
+    box = _box((128, 128, 32), h, 2, adiabatic=False)
+    op = st.ThermalOperator(box, box, _params(h), st.SolverSettings())
+    T = 300.0 + np.random.default_rng(1).uniform(0.0, 1700.0, op.nv)
+    b1 = BeamState(np.array([2.1e-3, 1.9e-3]), 0.0, 70.0, True)
+    b2 = BeamState(np.array([2.1e-3, 1.9e-3]), 0.0, 140.0, True)
+    s1 = op.evaluate_rhs(T, 1.0, b1, diffusion=False, faces=False)
+    s2 = op.evaluate_rhs(T, 1.0, b2, diffusion=False, faces=False)
+    assert np.max(np.abs(s2 - 2.0 * s1)) <= 1e-13 * np.max(np.abs(s2))
+    assert s1.sum() > 0.0
+    cap = op.lumped_capacity(T)
+    assert np.all(cap > 0.0)
+    op.close()
+
+
+def test_config1_full_step_is_bitwise_deterministic():
+    """Two resident runs of 3 full config-1 steps (k(T), latent heat, facets,
+    moving beam) from the same state agree bit for bit."""
+    h = 31.25e-6
+    box = _box((128, 128, 32), h, 2, adiabatic=False)
+    op = st.ThermalOperator(box, box, _params(h), st.SolverSettings())
+    T = 300.0 + np.random.default_rng(2).uniform(0.0, 1700.0, op.nv)
+    T[box.is_dirichlet] = 300.0
+    lp = st.LayerPath(0, 0.0, [st.Segment(1e-3, 2e-3, 3e-3, 2e-3, 1.0, 70.0)], 0.0)
+    dts, bm = st.flatten_schedule(lp, 5e-7, 3)
+    out = []
+    for _ in range(2):
+        op.set_state(T, 1.0)
+        fail, _, _ = op.run_explicit(dts, bm)
+        assert fail == 0
+        out.append(op.get_state()[0])
+    assert np.array_equal(out[0], out[1])
+    assert np.all(np.isfinite(out[0]))
+    op.close()
