@@ -213,3 +213,16 @@ def test_structured_seams_are_deterministic():
     a = op.evaluate_rhs(T, rc, beams)
     b = op.evaluate_rhs(T, rc, beams)
     assert np.array_equal(a, b)
+
+
+@pytest.mark.parametrize("lx", ["1", "2", "3"])
+@pytest.mark.parametrize("p", [1, 2, 3])
+def test_structured_extreme_x_chunking_matches_oracle(p, lx, monkeypatch):
+    """Short x chunks make most node planes x seams (every p-th plane for
+    Lx = 1): the seam list, its slot sums and the chunk-boundary facets."""
+    monkeypatch.setenv("ST_LX", lx)
+    box, op, orc, T, rc, beams, tb = _setup(p, latent=True, hconv=10.0, seed=51)
+    T[::6] = 1900.0
+    dt = 2e-7
+    assert rel(op.explicit_fused_step(T, dt, rc, beams), orc.explicit_step(T, dt, rc, tb)) < 1e-12
+    assert rel(op.evaluate_rhs(T, rc, beams), orc.evaluate_rhs(T, rc, tb)) < 1e-12
