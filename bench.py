@@ -458,7 +458,8 @@ def implicit_measure(device, n_steps=10, cpu=True):
     40x40x14 box through the unstructured (Forest/DofMap) backend, 24,600
     DoFs, reference default material, krylov_tol 1e-10, dt 1 ms, from a
     synthetic post-scan field (300 K + a 1700 K Gaussian bump at the top).
-    Returns ms per BE step, iterations, and the oracle's time for one step."""
+    Returns ms per BE step, iterations, and (CPU-baseline leg) the oracle
+    port's time for one step on the host."""
     st = _st()
     h = 80e-6
     box = st.StructuredBox(40, 40, 14, h, degree=1)
@@ -509,8 +510,10 @@ def implicit_measure(device, n_steps=10, cpu=True):
         orc = OracleOperator(structured_tables(box.nx, box.ny, box.nz, h, 1), params)
         t1 = time.perf_counter()
         implicit_step(orc, T0, rc0.reshape(-1, 2, 2, 2), 1e-3, s)
-        res["cpu_oracle_ms_per_be_step"] = (time.perf_counter() - t1) * 1e3
-        res["cpu_oracle"] = "oracle/cpu_oracle.py implicit_step on the same box, one BE step"
+        res["cpu_baseline"] = {"value": (time.perf_counter() - t1) * 1e3, "unit": "ms per BE step",
+                               "cores": os.cpu_count() or 1, "kind": "port",
+                               "sample": "one BE step of oracle/cpu_oracle.py implicit_step on "
+                                         "the same box (the CPU-baseline leg of this entry)"}
     op.close()
     return res
 
