@@ -546,6 +546,13 @@ __global__ void k_diag_fix(int64_t nv, const uint8_t* is_dir, const uint8_t* is_
 // backend
 // ---------------------------------------------------------------------------
 static inline unsigned nblk(int64_t n) { return (unsigned)((n + kThreads - 1) / kThreads); }
+// per-cell kernels at cool-down mesh sizes (~2e4 cells) are latency bound:
+// 64-thread blocks spread them over every SM (measured 8 % faster explicit
+// steps than 256 at 25k DoFs)
+constexpr int kCellThreads = 64;
+static inline unsigned nblk_cells(int64_t n) {
+  return (unsigned)((n + kCellThreads - 1) / kCellThreads);
+}
 
 struct Unstructured : Backend {
   int64_t n = 0, nv = 0, ns = 0, nf = 0;
@@ -589,7 +596,7 @@ struct Unstructured : Backend {
                 double* c_atomic) {
     double* rcp = rc;
     bool det = c->deterministic || f_atomic == nullptr;
-    k_rhs_cells<<<nblk(n), kThreads, 0, c->stream>>>(
+    k_rhs_cells<<<nblk_cells(n), kCellThreads, 0, c->stream>>>(
         n, geo(), faces(), c->dp, T, rcp, c->rc_value, flags, frozen_k, pending, nb, beams,
         det ? E.p : nullptr, (det && want_cap) ? Ec.p : nullptr, det ? nullptr : f_atomic,
         (!det && want_cap) ? c_atomic : nullptr);
@@ -674,7 +681,7 @@ struct Unstructured : Backend {
                                                           slaves.p, sptr.p, smast.p, sw.p, vd);
     ST_TRY(launched());
     c->prof_begin();
-    k_jac_cells<<<nblk(n), kThreads, 0, c->stream>>>(n, geo(), c->dp, vd, Tl, rc,
+    k_jac_cells<<<nblk_cells(n), kCellThreads, 0, c->stream>>>(n, geo(), c->dp, vd, Tl, rc,
                                                       c->rc_value, dt, E.p);
     ST_TRY(launched());
     c->prof_end();
