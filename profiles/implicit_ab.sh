@@ -1,4 +1,4 @@
-for v in base cb64 cb128 base cb64 cb128; do
+for v in ${VARIANTS:-base}; do
   if [ $v = base ]; then unset ST_VARIANT; else export ST_VARIANT=$v; fi
   python -c "
 import sys; sys.argv=['bench.py']; sys.path.insert(0,'.')
