@@ -67,6 +67,18 @@ __device__ __forceinline__ void source_factors(const SArgs& A, const DevBeam& b,
   }
 }
 
+// Which update of the diffusion loop touches G[(A, B, C)] first (0: the
+// x-term at q = (0, B, C), m = A; 1: the y-term at (A, 0, C), m = B; 2: the
+// z-term at (A, B, 0), m = C), in the loop's order: q lexicographic, then m,
+// then x, y, z
+template <int Q>
+__host__ __device__ constexpr int first_touch(int A, int B, int C) {
+  const int kx = ((0 * Q + B) * Q + C) * 3 * Q + A * 3 + 0;
+  const int ky = ((A * Q + 0) * Q + C) * 3 * Q + B * 3 + 1;
+  const int kz = ((A * Q + B) * Q + 0) * 3 * Q + C * 3 + 2;
+  return kx <= ky ? (kx <= kz ? 0 : 2) : (ky <= kz ? 1 : 2);
+}
+
 // Beams whose cell-level hit test (beam_hits_cell) can pass for some cell
 // of the (y, z) column (j, k): the y box distance and the slab overlap are
 // fixed over the x march, and dy^2 <= cut^2 is necessary for
@@ -192,8 +204,12 @@ __device__ __forceinline__ void cell_element(const SArgs& A, const CellFlags& F,
   using B = Basis<P>;
   const DevParams& PP = A.P;
   const bool top = F.faces && A.top_faces && (k == A.nz - 1);
+  // p >= 2: the first update of each flux-accumulator entry is a product,
+  // so no zero initialisation (measured: config 1 -1.5 %, p = 1 +3 %)
+  constexpr bool FT = P >= 2;
+  if (!FT || !F.diffusion)
 #pragma unroll
-  for (int q = 0; q < Q3; q++) G[q] = 0.0;
+    for (int q = 0; q < Q3; q++) G[q] = 0.0;
   if (F.diffusion) {
 #pragma unroll
     for (int qa = 0; qa < Q; qa++)
@@ -234,9 +250,19 @@ __device__ __forceinline__ void cell_element(const SArgs& A, const CellFlags& F,
           const double fx = c * gx, fy = c * gy, fz = c * gz;
 #pragma unroll
           for (int m = 0; m < Q; m++) {
-            G[(m * Q + qb) * Q + qc] = fma(B::Dq(m, qa), fx, G[(m * Q + qb) * Q + qc]);
-            G[(qa * Q + m) * Q + qc] = fma(B::Dq(m, qb), fy, G[(qa * Q + m) * Q + qc]);
-            G[(qa * Q + qb) * Q + m] = fma(B::Dq(m, qc), fz, G[(qa * Q + qb) * Q + m]);
+            // first touches are folded at compile time after unrolling
+            if (FT && qa == 0 && first_touch<Q>(m, qb, qc) == 0)
+              G[(m * Q + qb) * Q + qc] = B::Dq(m, qa) * fx;
+            else
+              G[(m * Q + qb) * Q + qc] = fma(B::Dq(m, qa), fx, G[(m * Q + qb) * Q + qc]);
+            if (FT && qb == 0 && first_touch<Q>(qa, m, qc) == 1)
+              G[(qa * Q + m) * Q + qc] = B::Dq(m, qb) * fy;
+            else
+              G[(qa * Q + m) * Q + qc] = fma(B::Dq(m, qb), fy, G[(qa * Q + m) * Q + qc]);
+            if (FT && qc == 0 && first_touch<Q>(qa, qb, m) == 2)
+              G[(qa * Q + qb) * Q + m] = B::Dq(m, qc) * fz;
+            else
+              G[(qa * Q + qb) * Q + m] = fma(B::Dq(m, qc), fz, G[(qa * Q + qb) * Q + m]);
           }
         }
   }
