@@ -193,11 +193,6 @@ __global__ void __launch_bounds__((P + 1) * CY * CZ, SlabTile<P>::MINB) k_xslab(
       //    the layer's nodes), then the y and z interpolation sweeps
       double Tx[Q2];
 #pragma unroll
-      for (int q = 0; q < Q2; q++) {
-        T[q] = 0.0;
-        Tx[q] = 0.0;
-      }
-#pragma unroll
       for (int a = 0; a < Q; a++) {
         const double va = kTab.V[a][s], da = kTab.D[a][s];
         const double* tp = Tr + ((ib + a) % NR) * PL + ms0;
@@ -206,8 +201,9 @@ __global__ void __launch_bounds__((P + 1) * CY * CZ, SlabTile<P>::MINB) k_xslab(
 #pragma unroll
           for (int c = 0; c < Q; c++) {
             const double v = tp[b * NZT + c];
-            T[b * Q + c] = fma(va, v, T[b * Q + c]);
-            Tx[b * Q + c] = fma(da, v, Tx[b * Q + c]);
+            // first plane: a product (no zero initialisation)
+            T[b * Q + c] = a == 0 ? va * v : fma(va, v, T[b * Q + c]);
+            Tx[b * Q + c] = a == 0 ? da * v : fma(da, v, Tx[b * Q + c]);
           }
       }
       if (top) {
