@@ -118,12 +118,20 @@ __device__ __forceinline__ void sweep_v(double* t) {
       for (int m = 0; m < Q; m++) in[m] = t[base + m * S];
 #pragma unroll
       for (int q = 0; q < Q; q++) {
-        // compile-time coefficients (st_basis_tables.h): exact zeros of the
-        // GLL/Gauss tables vanish from the instruction stream
-        double acc = (TR ? Basis<P>::V(q, 0) : Basis<P>::V(0, q)) * in[0];
+        // compile-time coefficients (st_basis_tables.h): nvcc keeps IEEE
+        // products by 0.0 (0 x inf = NaN), so the exact zeros of the
+        // GLL/Gauss tables are skipped here explicitly (the tests resolve
+        // after unrolling); a leading 1.0 is a copy.  Bitwise the same for
+        // finite inputs.
+        double acc = 0.0;
+        bool init = false;
 #pragma unroll
-        for (int m = 1; m < Q; m++)
-          acc = fma(TR ? Basis<P>::V(q, m) : Basis<P>::V(m, q), in[m], acc);
+        for (int m = 0; m < Q; m++) {
+          const double cf = TR ? Basis<P>::V(q, m) : Basis<P>::V(m, q);
+          if (cf == 0.0) continue;
+          acc = init ? fma(cf, in[m], acc) : (cf == 1.0 ? in[m] : cf * in[m]);
+          init = true;
+        }
         t[base + q * S] = acc;
       }
     }

@@ -218,15 +218,27 @@ __device__ __forceinline__ void cell_element(const SArgs& A, const CellFlags& F,
 #pragma unroll
         for (int qc = 0; qc < Q; qc++) {
           const int q = (qa * Q + qb) * Q + qc;
-          // reference-coordinate gradient by Gauss-point collocation
-          double gx = B::Dq(0, qa) * t[(0 * Q + qb) * Q + qc];
-          double gy = B::Dq(0, qb) * t[(qa * Q + 0) * Q + qc];
-          double gz = B::Dq(0, qc) * t[(qa * Q + qb) * Q + 0];
+          // reference-coordinate gradient by Gauss-point collocation (exact
+          // zeros of Dq skipped at compile time, see sweep_v)
+          double gx = 0.0, gy = 0.0, gz = 0.0;
+          bool ix = false, iy = false, iz = false;
 #pragma unroll
-          for (int m = 1; m < Q; m++) {
-            gx = fma(B::Dq(m, qa), t[(m * Q + qb) * Q + qc], gx);
-            gy = fma(B::Dq(m, qb), t[(qa * Q + m) * Q + qc], gy);
-            gz = fma(B::Dq(m, qc), t[(qa * Q + qb) * Q + m], gz);
+          for (int mm = 0; mm < Q; mm++) {
+            if (B::Dq(mm, qa) != 0.0) {
+              gx = ix ? fma(B::Dq(mm, qa), t[(mm * Q + qb) * Q + qc], gx)
+                      : B::Dq(mm, qa) * t[(mm * Q + qb) * Q + qc];
+              ix = true;
+            }
+            if (B::Dq(mm, qb) != 0.0) {
+              gy = iy ? fma(B::Dq(mm, qb), t[(qa * Q + mm) * Q + qc], gy)
+                      : B::Dq(mm, qb) * t[(qa * Q + mm) * Q + qc];
+              iy = true;
+            }
+            if (B::Dq(mm, qc) != 0.0) {
+              gz = iz ? fma(B::Dq(mm, qc), t[(qa * Q + qb) * Q + mm], gz)
+                      : B::Dq(mm, qc) * t[(qa * Q + qb) * Q + mm];
+              iz = true;
+            }
           }
           double kq;
           if (F.frozen) {
@@ -250,18 +262,20 @@ __device__ __forceinline__ void cell_element(const SArgs& A, const CellFlags& F,
           const double fx = c * gx, fy = c * gy, fz = c * gz;
 #pragma unroll
           for (int m = 0; m < Q; m++) {
-            // first touches are folded at compile time after unrolling
+            // first touches (a product, or 0 for a zero coefficient) and
+            // exact-zero coefficients are folded at compile time after
+            // unrolling
             if (FT && qa == 0 && first_touch<Q>(m, qb, qc) == 0)
-              G[(m * Q + qb) * Q + qc] = B::Dq(m, qa) * fx;
-            else
+              G[(m * Q + qb) * Q + qc] = B::Dq(m, qa) == 0.0 ? 0.0 : B::Dq(m, qa) * fx;
+            else if (B::Dq(m, qa) != 0.0)
               G[(m * Q + qb) * Q + qc] = fma(B::Dq(m, qa), fx, G[(m * Q + qb) * Q + qc]);
             if (FT && qb == 0 && first_touch<Q>(qa, m, qc) == 1)
-              G[(qa * Q + m) * Q + qc] = B::Dq(m, qb) * fy;
-            else
+              G[(qa * Q + m) * Q + qc] = B::Dq(m, qb) == 0.0 ? 0.0 : B::Dq(m, qb) * fy;
+            else if (B::Dq(m, qb) != 0.0)
               G[(qa * Q + m) * Q + qc] = fma(B::Dq(m, qb), fy, G[(qa * Q + m) * Q + qc]);
             if (FT && qc == 0 && first_touch<Q>(qa, qb, m) == 2)
-              G[(qa * Q + qb) * Q + m] = B::Dq(m, qc) * fz;
-            else
+              G[(qa * Q + qb) * Q + m] = B::Dq(m, qc) == 0.0 ? 0.0 : B::Dq(m, qc) * fz;
+            else if (B::Dq(m, qc) != 0.0)
               G[(qa * Q + qb) * Q + m] = fma(B::Dq(m, qc), fz, G[(qa * Q + qb) * Q + m]);
           }
         }
