@@ -51,9 +51,16 @@ __device__ __forceinline__ void sweep2(double* t) {
 #pragma unroll
     for (int q = 0; q < Q; q++) {
       auto M = [](int r, int cidx) { return DER ? B::Dq(r, cidx) : B::V(r, cidx); };
-      double acc = (TR ? M(q, 0) : M(0, q)) * in[0];
+      // exact zeros skipped, a leading 1.0 copied (see sweep_v)
+      double acc = 0.0;
+      bool init = false;
 #pragma unroll
-      for (int m = 1; m < Q; m++) acc = fma(TR ? M(q, m) : M(m, q), in[m], acc);
+      for (int m = 0; m < Q; m++) {
+        const double cf = TR ? M(q, m) : M(m, q);
+        if (cf == 0.0) continue;
+        acc = init ? fma(cf, in[m], acc) : (cf == 1.0 ? in[m] : cf * in[m]);
+        init = true;
+      }
       t[AX == 0 ? q * Q + o : o * Q + q] = acc;
     }
   }
