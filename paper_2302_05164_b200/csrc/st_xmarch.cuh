@@ -241,7 +241,22 @@ __device__ __forceinline__ void cell_element(const SArgs& A, const CellFlags& F,
             }
           }
           double kq;
-          if (F.frozen) {
+          if (P >= 2) {
+            // branch-free: the law always, the frozen value selected
+            // (measured: p = 2 faster, p = 1 slightly slower)
+            const double g = clamp01(fma(t[q], PP.inv_dT_l, A.glo));
+            if (RCF) {
+              double r = A.rc[cell * Q3 + q];
+              if (A.pending && !F.frozen) {
+                r = dmax(r, g);
+                A.rc[cell * Q3 + q] = r;
+              }
+              kq = conductivity(PP, g, r);
+            } else {
+              kq = fma(g, A.kB, A.kA);
+            }
+            kq = F.frozen ? A.frozen_k : kq;
+          } else if (F.frozen) {
             kq = A.frozen_k;
           } else {
             // g(T) (material.py:46-57) as a clamped ramp
