@@ -155,15 +155,16 @@ __device__ __forceinline__ void project3(double* t) {
 // extension the lumped capacity is C_const + dC(T)
 __device__ __forceinline__ double finalize_node(const SArgs& A, double ci, bool bottom, double T,
                                                 double f, double dc, bool latent) {
-  if (A.mode == 1) return f;
   // the latent increment of the lumped capacity only counts when positive:
   // Lagrange bases of degree >= 2 are negative at some Gauss points, so a
   // cell partly in the latent interval can lump a negative increment
   // 1 / (1/ci + dc) with one division
   if (latent && dc > 0.0) ci = ci / fma(ci, dc, 1.0);
   double o = T + A.dt * (ci * f);
-  if (A.dir_bottom && bottom) o = A.P.T_inf;
-  return o;
+  o = (A.dir_bottom && bottom) ? A.P.T_inf : o;
+  // selects, not branches (measured faster in every hot kernel): rhs mode
+  // (mode 1) returns f
+  return A.mode == 1 ? f : o;
 }
 
 // tile of k_xmarch (CY x CZ cells, one thread per cell)
