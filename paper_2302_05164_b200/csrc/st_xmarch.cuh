@@ -244,7 +244,7 @@ __device__ __forceinline__ void cell_element(const SArgs& A, const CellFlags& F,
           if (P >= 2) {
             // branch-free: the law always, the frozen value selected
             // (measured: p = 2 faster, p = 1 slightly slower)
-            const double g = clamp01(fma(t[q], PP.inv_dT_l, A.glo));
+            const double g = clamp01_int(fma(t[q], PP.inv_dT_l, A.glo));
             if (RCF) {
               double r = A.rc[cell * Q3 + q];
               if (A.pending && !F.frozen) {
