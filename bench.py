@@ -500,10 +500,18 @@ def implicit_measure(device, n_steps=10, cpu=True):
     fail, _, _ = op.run_explicit(dts_e[512:], bm_e[512:])
     el_e = time.perf_counter() - te
     res_e = {"explicit_us_per_step": el_e / 512 * 1e6, "explicit_fail": int(fail)}
+    # step criteria (row a19 / §8f row 4): the whole power iteration on the
+    # device, once per layer in the reference driver (driver.py:225)
+    st.compute_step_criteria(op)
+    tc = time.perf_counter()
+    crit = st.compute_step_criteria(op)
+    el_c = time.perf_counter() - tc
+    res_c = {"step_criteria_ms": el_c * 1e3, "power_iterations": op.last_power_iterations,
+             "dt_stability": crit.dt_stability}
     res = {"workload": "config3-sized cool-down: 40x40x14 Q1 box, unstructured backend",
            "dofs": int(n), "be_steps": n_steps, "ms_per_be_step": el / n_steps * 1e3,
            "newton_per_step": nn / n_steps, "cg_per_step": nk / n_steps,
-           "us_per_cg_iteration": el / max(nk, 1) * 1e6, **res_e}
+           "us_per_cg_iteration": el / max(nk, 1) * 1e6, **res_e, **res_c}
     if cpu:
         sys.path.insert(0, os.path.join(ROOT, "oracle"))
         from cpu_oracle import OracleOperator, implicit_step, structured_tables
@@ -514,6 +522,25 @@ def implicit_measure(device, n_steps=10, cpu=True):
                                "cores": os.cpu_count() or 1, "kind": "port",
                                "sample": "one BE step of oracle/cpu_oracle.py implicit_step on "
                                          "the same box (the CPU-baseline leg of this entry)"}
+        # oracle power iteration: 20 applies timed, scaled to the device's count
+        from cpu_oracle import spectral_radius
+        mat = params.material
+        kf = max(mat.k_m, mat.k_s)
+        cinv = orc.capacity_inverse()
+        isd = orc.M["is_dirichlet"]
+
+        def apply(v):
+            vd = v.copy()
+            vd[isd] = 0.0
+            w = -orc.evaluate_rhs(vd, None, faces=False, source=False, frozen_k=kf) * cinv
+            w[isd] = 0.0
+            return w
+        t2 = time.perf_counter()
+        spectral_radius(apply, orc.nv, max_iter=20)
+        per = (time.perf_counter() - t2) / 20
+        res["cpu_step_criteria_ms"] = per * op.last_power_iterations * 1e3
+        res["cpu_step_criteria_sample"] = ("20 oracle power-iteration applies, scaled to the "
+                                           f"{op.last_power_iterations} the device ran")
     op.close()
     return res
 

@@ -207,6 +207,16 @@ int st_finish_implicit_step(st_ctx* ctx);
 int st_pcg(st_ctx* ctx, const double* T_lin, const double* rc, double dt,
            const double* b, double tol, int max_iter, int precond, double* x,
            int* iters, int* converged);
+/* compute_step_criteria / estimate_spectral_radius (timestepping.py:49-99):
+ * rho(C~^-1 K) at conductivity k_frozen by power iteration, entirely on the
+ * device.  v0 is the caller's normalised start vector (the reference draws
+ * default_rng(0).standard_normal(n) / norm); each apply closes constraints,
+ * zeroes Dirichlet entries, evaluates the diffusion-only rhs, scales by
+ * C~^-1 and zeroes Dirichlet/slave rows; stop when two Rayleigh quotients
+ * agree to tol or after max_iter applies.  *rho = max(|lam|, |lam_prev|)
+ * (0 when an apply returns the zero vector), *iters = applies. */
+int st_spectral_radius(st_ctx* ctx, double k_frozen, const double* v0, double tol,
+                       int max_iter, double* rho, int* iters);
 
 /* --- multi-GPU slabs (structured backend) ------------------------------ */
 /* One explicit step split around the rank-interface exchange: _begin runs

@@ -456,6 +456,50 @@ def pcg(apply_fn, b, diag_inv=None, tol=1e-10, max_iter=2000):
     return x, max_iter, False
 
 
+def spectral_radius(apply_fn, n, seed=0, tol=1e-9, max_iter=500, lams=None):
+    """Power iteration (timestepping.py:49-67): v0 ~ N(0,1) from
+    default_rng(seed), normalised; returns (max(|lam|, |lam_prev|), applies).
+    `lams`, when a list, receives every Rayleigh quotient."""
+    v = np.random.default_rng(seed).standard_normal(n)
+    v /= np.linalg.norm(v)
+    lam_prev = lam = 0.0
+    it = 0
+    for it in range(1, max_iter + 1):
+        w = apply_fn(v)
+        nw = np.linalg.norm(w)
+        if nw == 0.0:
+            return 0.0, it
+        lam_prev, lam = lam, float(np.dot(v, w))
+        if lams is not None:
+            lams.append(lam)
+        v = w / nw
+        if abs(lam - lam_prev) <= tol * abs(lam):
+            break
+    return max(abs(lam), abs(lam_prev)), it
+
+
+def step_criteria_rho(op):
+    """rho(C~^-1 K) at k frozen to max(k_m, k_s) (timestepping.py:70-99):
+    the apply closes constraints, zeroes Dirichlet entries, evaluates the
+    diffusion-only rhs, scales by C~^-1 and zeroes Dirichlet/slave rows.
+    Returns (rho, applies); dt_stability = 2 / rho."""
+    mat = op.params.material
+    k_frozen = max(mat.k_m, mat.k_s)
+    cinv = op.capacity_inverse()
+    M = op.M
+
+    def apply(v):
+        vd = op.distribute(v.copy())
+        vd[M["is_dirichlet"]] = 0.0
+        w = -op.evaluate_rhs(vd, None, faces=False, source=False, frozen_k=k_frozen)
+        w *= cinv
+        w[M["is_dirichlet"]] = 0.0
+        w[M["is_slave"]] = 0.0
+        return w
+
+    return spectral_radius(apply, op.nv)
+
+
 def implicit_step(op, T_n, r_c, dt, settings):
     """Backward Euler with Newton + Jacobi-PCG (timestepping.py:229-283)."""
     M = op.M

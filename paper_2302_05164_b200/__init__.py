@@ -14,4 +14,5 @@ from .mesh import (DofMap, Forest, StructuredBox, build_dofmap, initial_history,
                    interface_faces)
 from .operators import ThermalOperator, close_constraints
 from .timestepping import (InstabilityError, JacobianApply, PhaseStats, SimulationState,
+                           StepCriteria, compute_step_criteria, estimate_spectral_radius,
                            krylov_solve, run_cooldown_phase, run_scan_phase)

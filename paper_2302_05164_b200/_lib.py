@@ -121,6 +121,9 @@ SIGNATURES = [
     ("st_pcg", ctypes.c_int,
      [_VP, _dp, _dp, ctypes.c_double, _dp, ctypes.c_double, ctypes.c_int,
       ctypes.c_int, _dp, ctypes.POINTER(ctypes.c_int), ctypes.POINTER(ctypes.c_int)]),
+    ("st_spectral_radius", ctypes.c_int,
+     [_VP, ctypes.c_double, _dp, ctypes.c_double, ctypes.c_int, _dp,
+      ctypes.POINTER(ctypes.c_int)]),
     ("st_profile_enable", ctypes.c_int, [_VP, ctypes.c_int]),
     ("st_profile_read", ctypes.c_int,
      [_VP, _dp, _i64p, ctypes.c_char_p, ctypes.c_int]),

@@ -634,6 +634,54 @@ int st_pcg(st_ctx* ctx, const double* T_lin, const double* rc, double dt, const 
   return c.d2h(x, xd, c.nv);
 }
 
+// estimate_spectral_radius over the step-criteria apply (timestepping.py:49-99),
+// all vectors on the device; the host reads the two dot products per
+// iteration for the stopping rule.
+int st_spectral_radius(st_ctx* ctx, double k_frozen, const double* v0, double tol, int max_iter,
+                       double* rho, int* iters) {
+  ST_TRY(check_ctx(ctx));
+  Ctx& c = ctx->impl;
+  if (!v0 || !rho || !iters || max_iter < 0) {
+    set_error("spectral_radius: null argument or negative max_iter");
+    return ST_EINVAL;
+  }
+  const int64_t nv = c.nv;
+  double *v, *vd, *f, *w, *cinv;
+  ST_TRY(c.vec(0, &v));
+  ST_TRY(c.vec(1, &vd));
+  ST_TRY(c.vec(2, &f));
+  ST_TRY(c.vec(3, &w));
+  ST_TRY(c.vec(4, &cinv));
+  ST_TRY(c.h2d(v, v0, nv));
+  ST_TRY(c.be->capacity(nullptr, cinv));
+  ST_TRY(vec_recip(&c, cinv, cinv, nv));
+  double lam_prev = 0.0, lam = 0.0;
+  *rho = 0.0;
+  *iters = 0;
+  for (int it = 1; it <= max_iter; it++) {
+    *iters = it;
+    ST_CUDA(cudaMemcpyAsync(vd, v, nv * sizeof(double), cudaMemcpyDeviceToDevice, c.stream));
+    ST_TRY(c.be->distribute(vd));
+    ST_TRY(c.be->pin_dirichlet(vd, 0.0));
+    ST_TRY(c.be->rhs(vd, nullptr, ST_RHS_DIFFUSION | ST_RHS_FROZEN_K, k_frozen, 0, nullptr, f,
+                     0));
+    ST_TRY(vec_neg_mul(&c, f, cinv, w, nv));
+    ST_TRY(c.be->mask_rows(w));
+    double ww, vw;
+    ST_TRY(c.dot(w, w, nv, &ww));
+    ST_TRY(c.dot(v, w, nv, &vw));
+    const double nw = std::sqrt(ww);
+    if (nw == 0.0) return ST_OK;
+    lam_prev = lam;
+    lam = vw;
+    ST_TRY(vec_div(&c, w, nw, v, nv));
+    if (std::fabs(lam - lam_prev) <= tol * std::fabs(lam)) break;
+  }
+  ST_TRY(c.sync());
+  *rho = std::max(std::fabs(lam), std::fabs(lam_prev));
+  return ST_OK;
+}
+
 // ---------------------------------------------------------------------------
 // device-resident explicit loop (run_scan_phase, timestepping.py:195-226)
 // ---------------------------------------------------------------------------

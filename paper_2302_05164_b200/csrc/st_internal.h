@@ -209,6 +209,8 @@ int vec_sub_scale(Ctx* c, const double* a, const double* b, double s,
                   const double* m, double* y, int64_t n);  // y = a/s - (b + m)
 int vec_sub(Ctx* c, const double* a, const double* b, double* y, int64_t n);
 int vec_scal_copy(Ctx* c, double s, const double* x, double* y, int64_t n);
+int vec_neg_mul(Ctx* c, const double* f, const double* cinv, double* w, int64_t n);  // w = -f cinv
+int vec_div(Ctx* c, const double* x, double d, double* y, int64_t n);               // y = x / d
 // PCG with device-resident scalars (st_reduce.cu); part: 2 kRedBlocks
 // doubles, s: 7 scalars (rz, pAp, alpha, rr, rz_new, beta, converged)
 int cg_alpha(Ctx* c, const double* p, const double* Ap, int64_t n, double* part, double* s);

@@ -89,6 +89,15 @@ __global__ void k_scal_copy(double s, const double* x, double* y, int64_t n) {
   int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (i < n) y[i] = s * x[i];
 }
+// power iteration (timestepping.py:88-90, :62): w = (-f) * cinv; v = w / nw
+__global__ void k_neg_mul(const double* f, const double* cinv, double* w, int64_t n) {
+  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i < n) w[i] = (-f[i]) * cinv[i];
+}
+__global__ void k_div(const double* x, double d, double* y, int64_t n) {
+  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i < n) y[i] = x[i] / d;
+}
 
 // --- Jacobi-PCG with device-resident scalars (pcg_dev): one host read per
 // iteration (the residual norm for the stopping rule).  Scalars s[]:
@@ -240,6 +249,12 @@ int vec_sub(Ctx* c, const double* a, const double* b, double* y, int64_t n) {
 }
 int vec_scal_copy(Ctx* c, double s, const double* x, double* y, int64_t n) {
   ST_VEC_LAUNCH(k_scal_copy, s, x, y, n);
+}
+int vec_neg_mul(Ctx* c, const double* f, const double* cinv, double* w, int64_t n) {
+  ST_VEC_LAUNCH(k_neg_mul, f, cinv, w, n);
+}
+int vec_div(Ctx* c, const double* x, double d, double* y, int64_t n) {
+  ST_VEC_LAUNCH(k_div, x, d, y, n);
 }
 
 }  // namespace st

@@ -286,6 +286,23 @@ class ThermalOperator:
                                     ctypes.byref(ok)), "pcg")
         return x, it.value, bool(ok.value)
 
+    def spectral_radius(self, k_frozen, seed=0, tol=1e-9, max_iter=500):
+        """rho(C~^-1 K) at conductivity k_frozen by power iteration on the
+        device (timestepping.py:49-99): the start vector is the reference's
+        (default_rng(seed), normalised on the host), the apply is the
+        reference's (close constraints, zero Dirichlet entries, diffusion-only
+        rhs, scale by C~^-1, zero Dirichlet/slave rows).  The number of
+        operator applies is kept in ``last_power_iterations``."""
+        v0 = np.random.default_rng(seed).standard_normal(self.nv)
+        v0 /= np.linalg.norm(v0)
+        rho = ctypes.c_double()
+        it = ctypes.c_int()
+        _lib.check(self._lib.st_spectral_radius(self._ctx, float(k_frozen), _lib.dptr(v0),
+                                                float(tol), int(max_iter), ctypes.byref(rho),
+                                                ctypes.byref(it)), "spectral_radius")
+        self.last_power_iterations = it.value
+        return rho.value
+
     # -- resident state ----------------------------------------------------------------
     def set_state(self, T, r_c):
         """Upload (T, r_c) to HBM; r_c may be a scalar >= 1 (consolidated)."""

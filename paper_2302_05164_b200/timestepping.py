@@ -187,6 +187,52 @@ def run_cooldown_phase(state, layer_path, dt_explicit, settings=None,
     return stats
 
 
+@dataclass
+class StepCriteria:
+    """Stability and accuracy step bounds (timestepping.py:35-46)."""
+    dt_stability: float
+    dt_accuracy: float
+    safety: float
+
+    @property
+    def dt_used(self):
+        return self.safety * min(self.dt_stability, self.dt_accuracy)
+
+
+def estimate_spectral_radius(apply_fn, n, seed=0, tol=1e-9, max_iter=500):
+    """Power iteration on a host callback (timestepping.py:49-67): start
+    N(0,1) from default_rng(seed), normalised; stop when two Rayleigh
+    quotients agree to tol; return the larger magnitude of the last two.
+    ``compute_step_criteria`` runs the same iteration on the device."""
+    rng = np.random.default_rng(seed)
+    v = rng.standard_normal(n)
+    v /= np.linalg.norm(v)
+    lam_prev = lam = 0.0
+    for _ in range(max_iter):
+        w = apply_fn(v)
+        nw = np.linalg.norm(w)
+        if nw == 0.0:
+            return 0.0
+        lam_prev, lam = lam, float(np.dot(v, w))
+        v = w / nw
+        if abs(lam - lam_prev) <= tol * abs(lam):
+            break
+    return max(abs(lam), abs(lam_prev))
+
+
+def compute_step_criteria(op, settings=None, seed=0, tol=1e-9, max_iter=500) -> StepCriteria:
+    """timestepping.py:70-99: rho(C~^-1 K) at the stiffest admissible state
+    (k frozen to max(k_m, k_s)), dt_stability = 2 / rho, dt_accuracy = R / v.
+    The whole power iteration runs on the device (st_spectral_radius); the
+    host only draws the same start vector."""
+    settings = settings or op.settings
+    mat = op.params.material
+    rho = op.spectral_radius(max(mat.k_m, mat.k_s), seed=seed, tol=tol, max_iter=max_iter)
+    hs = op.params.laser
+    return StepCriteria(dt_stability=2.0 / rho, dt_accuracy=hs.radius / hs.scan_velocity,
+                        safety=settings.safety_factor)
+
+
 class JacobianApply:
     """``apply_fn`` for krylov_solve that the device PCG recognises."""
 
