@@ -179,6 +179,8 @@ static void ctx_free(st_ctx* c) {
     if (e) cudaEventDestroy(e);
   for (auto& g : x.cg_exec)
     if (g) cudaGraphExecDestroy(g);
+  if (x.pw_exec) cudaGraphExecDestroy(x.pw_exec);
+  x.pws.free();
   x.cgs.free();
   x.T.free();
   x.T_alt.free();
@@ -635,8 +637,14 @@ int st_pcg(st_ctx* ctx, const double* T_lin, const double* rc, double dt, const 
 }
 
 // estimate_spectral_radius over the step-criteria apply (timestepping.py:49-99),
-// all vectors on the device; the host reads the two dot products per
-// iteration for the stopping rule.
+// all vectors and scalars on the device.  The iterations run in batches
+// without a host round-trip: each records its (w.w, v.w) pair in a device
+// history and normalises v by the device ||w||; the host then applies the
+// reference's stopping rule to the history in order.  Iterations queued
+// past the stopping one only touch scratch vectors, so the result is the
+// one-iteration-at-a-time result (same kernels, same sqrt and division).
+// Iterations 2.. replay a captured graph of one iteration (ST_PW_GRAPH=0
+// launches directly).
 int st_spectral_radius(st_ctx* ctx, double k_frozen, const double* v0, double tol, int max_iter,
                        double* rho, int* iters) {
   ST_TRY(check_ctx(ctx));
@@ -655,11 +663,15 @@ int st_spectral_radius(st_ctx* ctx, double k_frozen, const double* v0, double to
   ST_TRY(c.h2d(v, v0, nv));
   ST_TRY(c.be->capacity(nullptr, cinv));
   ST_TRY(vec_recip(&c, cinv, cinv, nv));
-  double lam_prev = 0.0, lam = 0.0;
   *rho = 0.0;
   *iters = 0;
-  for (int it = 1; it <= max_iter; it++) {
-    *iters = it;
+  if (max_iter == 0) return c.sync();
+  constexpr int kMaxBatch = 64;
+  if ((int64_t)c.cgs.n < 2 * kRedBlocks + 8) ST_TRY(c.cgs.alloc(2 * kRedBlocks + 8));
+  if ((int64_t)c.pws.n < 4 + 2 * kMaxBatch) ST_TRY(c.pws.alloc(4 + 2 * kMaxBatch));
+  double* part = c.cgs.p;
+  double* pws = c.pws.p;
+  auto body = [&]() -> int {
     ST_CUDA(cudaMemcpyAsync(vd, v, nv * sizeof(double), cudaMemcpyDeviceToDevice, c.stream));
     ST_TRY(c.be->distribute(vd));
     ST_TRY(c.be->pin_dirichlet(vd, 0.0));
@@ -667,17 +679,74 @@ int st_spectral_radius(st_ctx* ctx, double k_frozen, const double* v0, double to
                      0));
     ST_TRY(vec_neg_mul(&c, f, cinv, w, nv));
     ST_TRY(c.be->mask_rows(w));
-    double ww, vw;
-    ST_TRY(c.dot(w, w, nv, &ww));
-    ST_TRY(c.dot(v, w, nv, &vw));
-    const double nw = std::sqrt(ww);
-    if (nw == 0.0) return ST_OK;
-    lam_prev = lam;
-    lam = vw;
-    ST_TRY(vec_div(&c, w, nw, v, nv));
-    if (std::fabs(lam - lam_prev) <= tol * std::fabs(lam)) break;
+    ST_TRY(dot_to_device(&c, w, w, nv, part, pws + 1));
+    ST_TRY(dot_to_device(&c, v, w, nv, part, pws + 2));
+    ST_TRY(pw_record(&c, pws));
+    ST_TRY(pw_div(&c, w, pws, v, nv));
+    return ST_OK;
+  };
+  static const bool use_graph = !(getenv("ST_PW_GRAPH") && getenv("ST_PW_GRAPH")[0] == '0');
+  bool graph = false;
+  int64_t graph_kernels = 0;
+  std::vector<double> hist(2 * kMaxBatch);
+  double lam_prev = 0.0, lam = 0.0;
+  int done = 0, batch = 4;
+  while (done < max_iter) {
+    const int nb_ = std::min(batch, max_iter - done);
+    ST_CUDA(cudaMemsetAsync(pws, 0, sizeof(double), c.stream));
+    for (int i = 0; i < nb_; i++) {
+      if (graph) {
+        ST_CUDA(cudaGraphLaunch(c.pw_exec, c.stream));
+        c.launches += graph_kernels;
+      } else {
+        ST_TRY(body());
+      }
+    }
+    if (use_graph && !graph && nb_ < max_iter - done) {
+      // the first batch ran directly (lazy allocations are done); capture
+      cudaGraph_t g = nullptr;
+      const int64_t l0 = c.launches;
+      ST_CUDA(cudaStreamBeginCapture(c.stream, cudaStreamCaptureModeThreadLocal));
+      const int brc = body();
+      const cudaError_t e = cudaStreamEndCapture(c.stream, &g);
+      graph_kernels = c.launches - l0;
+      c.launches = l0;
+      if (brc != ST_OK || e != cudaSuccess) {
+        if (g) cudaGraphDestroy(g);
+        cudaGetLastError();
+        if (brc != ST_OK) return brc;
+        ST_CUDA(e);
+      }
+      if (c.pw_exec) {
+        cudaGraphExecUpdateResultInfo info;
+        if (cudaGraphExecUpdate(c.pw_exec, g, &info) != cudaSuccess) {
+          cudaGetLastError();
+          cudaGraphExecDestroy(c.pw_exec);
+          c.pw_exec = nullptr;
+        }
+      }
+      const cudaError_t ie = c.pw_exec ? cudaSuccess : cudaGraphInstantiate(&c.pw_exec, g, 0);
+      cudaGraphDestroy(g);
+      ST_CUDA(ie);
+      graph = true;
+    }
+    ST_CUDA(cudaMemcpyAsync(hist.data(), pws + 4, 2 * nb_ * sizeof(double),
+                            cudaMemcpyDeviceToHost, c.stream));
+    ST_CUDA(cudaStreamSynchronize(c.stream));
+    for (int i = 0; i < nb_; i++) {
+      *iters = done + i + 1;
+      const double nw = std::sqrt(hist[2 * i]);
+      if (nw == 0.0) return ST_OK;
+      lam_prev = lam;
+      lam = hist[2 * i + 1];
+      if (std::fabs(lam - lam_prev) <= tol * std::fabs(lam)) {
+        *rho = std::max(std::fabs(lam), std::fabs(lam_prev));
+        return ST_OK;
+      }
+    }
+    done += nb_;
+    batch = std::min(2 * batch, kMaxBatch);
   }
-  ST_TRY(c.sync());
   *rho = std::max(std::fabs(lam), std::fabs(lam_prev));
   return ST_OK;
 }

@@ -175,6 +175,8 @@ struct Ctx {
   DevBuf<double> cgs;       // PCG partials (2 kRedBlocks) + scalars
   cudaEvent_t cg_ev[2] = {nullptr, nullptr};  // PCG residual reads in flight
   cudaGraphExec_t cg_exec[2] = {nullptr, nullptr};  // captured PCG iteration per parity
+  DevBuf<double> pws;       // power iteration: counter, scalars, (ww, vw) history
+  cudaGraphExec_t pw_exec = nullptr;  // captured power iteration
   DevBuf<double> scratch[8];
   double* pinned = nullptr;  // small pinned host staging
   // profiling of the dominant kernel
@@ -217,6 +219,10 @@ int cg_alpha(Ctx* c, const double* p, const double* Ap, int64_t n, double* part,
 int cg_update(Ctx* c, const double* p, const double* Ap, const double* dinv, double* x, double* r,
               double* z, int64_t n, double* part, double* s, double thr);
 int cg_p(Ctx* c, const double* s, const double* z, double* p, int64_t n);
+// power iteration on device scalars (st_spectral_radius): pw_record keeps
+// (ww, vw) of the iteration in the history and sqrt(ww); pw_div: y = x / nw
+int pw_record(Ctx* c, double* pws);
+int pw_div(Ctx* c, const double* x, const double* pws, double* y, int64_t n);
 int dot_to_device(Ctx* c, const double* a, const double* b, int64_t n, double* part, double* out);
 
 constexpr int kRedBlocks = 296;  // 2 x 148 SMs

@@ -220,6 +220,26 @@ int dot_to_device(Ctx* c, const double* a, const double* b, int64_t n, double* p
   return ST_OK;
 }
 
+// power iteration scalars pws: [0] iteration counter, [1] w.w, [2] v.w,
+// [3] ||w||, [4 + 2i], [5 + 2i] the (w.w, v.w) pair of iteration i
+__global__ void k_pw_record(double* pws) {
+  const int i = (int)pws[0];
+  pws[4 + 2 * i] = pws[1];
+  pws[5 + 2 * i] = pws[2];
+  pws[3] = sqrt(pws[1]);  // correctly rounded, as std::sqrt on the host
+  pws[0] = (double)(i + 1);
+}
+__global__ void k_pw_div(const double* x, const double* pws, double* y, int64_t n) {
+  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i < n) y[i] = x[i] / pws[3];
+}
+int pw_record(Ctx* c, double* pws) {
+  k_pw_record<<<1, 1, 0, c->stream>>>(pws);
+  c->launches++;
+  ST_LAUNCHED();
+  return ST_OK;
+}
+
 #define ST_VEC_LAUNCH(kern, ...)                                   \
   do {                                                             \
     kern<<<nb(n), kThreads, 0, c->stream>>>(__VA_ARGS__);          \
@@ -255,6 +275,9 @@ int vec_neg_mul(Ctx* c, const double* f, const double* cinv, double* w, int64_t 
 }
 int vec_div(Ctx* c, const double* x, double d, double* y, int64_t n) {
   ST_VEC_LAUNCH(k_div, x, d, y, n);
+}
+int pw_div(Ctx* c, const double* x, const double* pws, double* y, int64_t n) {
+  ST_VEC_LAUNCH(k_pw_div, x, pws, y, n);
 }
 
 }  // namespace st

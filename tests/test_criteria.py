@@ -97,3 +97,26 @@ def test_gpu_step_criteria_structured_match_oracle(p):
     assert abs(rho - ref) <= 2e-9 * ref
     assert abs(op.last_power_iterations - applies) <= 1
     op.close()
+
+
+@pytest.mark.gpu
+def test_gpu_power_iteration_batches_are_exact():
+    """Batched device power iteration (history of (w.w, v.w) read per batch,
+    graph replay after the first batch): two calls on one context give the
+    same rho and iteration count bitwise."""
+    from cpu_oracle import structured_tables  # noqa: F401  (oracle on path)
+    h = 1.0 / 8
+    params = st.ProcessParams(
+        st.MaterialParams(k_p=6.7, k_m=32.0, k_s=6.7, T_s=300.0, T_l=1928.0, rho=4430.0,
+                          c=526.0),
+        st.BoundaryParams(emissivity=0.3, T_inf=300.0, T_v=1e9),
+        st.HeatSourceParams(radius=50e-6, h_powder=40e-6, power=70.0),
+        st.MeshParams(h_coarse=h, n_refine=0, h_powder=h))
+    box = st.StructuredBox(8, 6, 5, h, degree=2)
+    op = st.ThermalOperator(box, box, params, st.SolverSettings())
+    r1 = 2.0 / st.compute_step_criteria(op).dt_stability
+    n1 = op.last_power_iterations
+    r2 = 2.0 / st.compute_step_criteria(op).dt_stability
+    assert r1 == r2 and op.last_power_iterations == n1
+    assert n1 > 4  # crosses at least one batch boundary
+    op.close()
