@@ -348,12 +348,17 @@ static int pcg_dev(Ctx& c, const double* Tl, const double* rc, double dt, const 
   if (!c.cg_ev[0]) {
     for (auto& e : c.cg_ev) ST_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
   }
+  static const bool zero_copy = !(getenv("ST_CG_ZC") && getenv("ST_CG_ZC")[0] == '0');
   auto body = [&](int par) -> int {
     ST_TRY(c.be->jacobian(p, Tl, rc, dt, Ap));
     ST_TRY(cg_alpha(&c, p, Ap, nv, part, s));
-    ST_TRY(cg_update(&c, p, Ap, diag_inv, x, r, z, nv, part, s, thr));
-    ST_CUDA(cudaMemcpyAsync(c.pinned + par, s + 3, sizeof(double), cudaMemcpyDeviceToHost,
-                            c.stream));
+    // r.r reaches the host's pinned slot from k_cg_sum2 itself (the pinned
+    // buffer is device-mapped under UVA); ST_CG_ZC=0 copies it instead
+    ST_TRY(cg_update(&c, p, Ap, diag_inv, x, r, z, nv, part, s, thr,
+                     zero_copy ? c.pinned + par : nullptr));
+    if (!zero_copy)
+      ST_CUDA(cudaMemcpyAsync(c.pinned + par, s + 3, sizeof(double), cudaMemcpyDeviceToHost,
+                              c.stream));
     ST_TRY(cg_p(&c, s, z, p, nv));
     return ST_OK;
   };

@@ -217,7 +217,8 @@ int vec_div(Ctx* c, const double* x, double d, double* y, int64_t n);           
 // doubles, s: 7 scalars (rz, pAp, alpha, rr, rz_new, beta, converged)
 int cg_alpha(Ctx* c, const double* p, const double* Ap, int64_t n, double* part, double* s);
 int cg_update(Ctx* c, const double* p, const double* Ap, const double* dinv, double* x, double* r,
-              double* z, int64_t n, double* part, double* s, double thr);
+              double* z, int64_t n, double* part, double* s, double thr,
+              double* hrr = nullptr);
 int cg_p(Ctx* c, const double* s, const double* z, double* p, int64_t n);
 // power iteration on device scalars (st_spectral_radius): pw_record keeps
 // (ww, vw) of the iteration in the history and sqrt(ww); pw_div: y = x / nw

@@ -156,7 +156,7 @@ __global__ void k_cg_update(const double* s, const double* p, const double* Ap,
   }
 }
 
-__global__ void k_cg_sum2(const double* part, int np, double* s, double thr) {
+__global__ void k_cg_sum2(const double* part, int np, double* s, double thr, double* hrr) {
   if (s[6] != 0.0) return;
   __shared__ double sm[512];
   double a = 0.0, b = 0.0;
@@ -172,6 +172,9 @@ __global__ void k_cg_sum2(const double* part, int np, double* s, double thr) {
     s[5] = rz_new / s[0];
     s[0] = rz_new;
     s[6] = sqrt(rr) <= thr ? 1.0 : 0.0;  // the host's stopping rule, same doubles
+    // r.r straight into the host's pinned slot (zero-copy; no copy-engine
+    // node between this kernel and the next in the captured iteration)
+    if (hrr) *reinterpret_cast<volatile double*>(hrr) = rr;
   }
 }
 
@@ -193,11 +196,11 @@ int cg_alpha(Ctx* c, const double* p, const double* Ap, int64_t n, double* part,
 }
 
 int cg_update(Ctx* c, const double* p, const double* Ap, const double* dinv, double* x, double* r,
-              double* z, int64_t n, double* part, double* s, double thr) {
+              double* z, int64_t n, double* part, double* s, double thr, double* hrr) {
   k_cg_update<<<kRedBlocks, kThreads, 0, c->stream>>>(s, p, Ap, dinv, x, r, z, n, part);
   c->launches++;
   ST_LAUNCHED();
-  k_cg_sum2<<<1, 512, 0, c->stream>>>(part, kRedBlocks, s, thr);
+  k_cg_sum2<<<1, 512, 0, c->stream>>>(part, kRedBlocks, s, thr, hrr);
   c->launches++;
   ST_LAUNCHED();
   return ST_OK;
