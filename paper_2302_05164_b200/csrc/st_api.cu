@@ -334,9 +334,10 @@ static int pcg_dev(Ctx& c, const double* Tl, const double* rc, double dt, const 
   // scalars stay on the device; the host reads r.r of iteration it while
   // iteration it + 1 is already queued (its kernels turn into no-ops once
   // the device-side copy of the stopping rule has fired)
-  if ((int64_t)c.cgs.n < 2 * kRedBlocks + 8) ST_TRY(c.cgs.alloc(2 * kRedBlocks + 8));
-  double* part = c.cgs.p;
-  double* s = c.cgs.p + 2 * kRedBlocks;
+  if ((int64_t)c.cgs.n < kCgsSize) ST_TRY(c.cgs.alloc(kCgsSize));
+  double* part = c.cgs.p;                     // r.r / r.z partials
+  double* ppart = c.cgs.p + 2 * kRedBlocks;   // p.Ap partials
+  double* s = c.cgs.p + 3 * kRedBlocks;
   const double thr = tol * bnorm;
   ST_CUDA(cudaMemsetAsync(s + 6, 0, sizeof(double), c.stream));
   if (diag_inv)
@@ -344,22 +345,21 @@ static int pcg_dev(Ctx& c, const double* Tl, const double* rc, double dt, const 
   else
     ST_CUDA(cudaMemcpyAsync(z, r, nv * sizeof(double), cudaMemcpyDeviceToDevice, c.stream));
   ST_CUDA(cudaMemcpyAsync(p, z, nv * sizeof(double), cudaMemcpyDeviceToDevice, c.stream));
-  ST_TRY(dot_to_device(&c, r, z, nv, part, s));  // s[0] = rz
+  ST_TRY(dot_to_device(&c, r, z, nv, part, s + 9));  // rz of iteration 1 (parity 1)
   if (!c.cg_ev[0]) {
     for (auto& e : c.cg_ev) ST_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
   }
   static const bool zero_copy = !(getenv("ST_CG_ZC") && getenv("ST_CG_ZC")[0] == '0');
   auto body = [&](int par) -> int {
     ST_TRY(c.be->jacobian(p, Tl, rc, dt, Ap));
-    ST_TRY(cg_alpha(&c, p, Ap, nv, part, s));
-    // r.r reaches the host's pinned slot from k_cg_sum2 itself (the pinned
-    // buffer is device-mapped under UVA); ST_CG_ZC=0 copies it instead
-    ST_TRY(cg_update(&c, p, Ap, diag_inv, x, r, z, nv, part, s, thr,
-                     zero_copy ? c.pinned + par : nullptr));
+    ST_TRY(cg_alpha(&c, p, Ap, nv, ppart));
+    ST_TRY(cg_update(&c, par, ppart, p, Ap, diag_inv, x, r, z, nv, part, s));
+    // r.r reaches the host's pinned slot from k_cg_beta_p itself (the
+    // pinned buffer is device-mapped under UVA); ST_CG_ZC=0 copies it instead
+    ST_TRY(cg_beta_p(&c, par, part, thr, zero_copy ? c.pinned + par : nullptr, z, p, nv, s));
     if (!zero_copy)
       ST_CUDA(cudaMemcpyAsync(c.pinned + par, s + 3, sizeof(double), cudaMemcpyDeviceToHost,
                               c.stream));
-    ST_TRY(cg_p(&c, s, z, p, nv));
     return ST_OK;
   };
   // iterations 2.. replay a captured graph of the iteration (one per
@@ -672,7 +672,7 @@ int st_spectral_radius(st_ctx* ctx, double k_frozen, const double* v0, double to
   *iters = 0;
   if (max_iter == 0) return c.sync();
   constexpr int kMaxBatch = 64;
-  if ((int64_t)c.cgs.n < 2 * kRedBlocks + 8) ST_TRY(c.cgs.alloc(2 * kRedBlocks + 8));
+  if ((int64_t)c.cgs.n < kCgsSize) ST_TRY(c.cgs.alloc(kCgsSize));
   if ((int64_t)c.pws.n < 4 + 2 * kMaxBatch) ST_TRY(c.pws.alloc(4 + 2 * kMaxBatch));
   double* part = c.cgs.p;
   double* pws = c.pws.p;

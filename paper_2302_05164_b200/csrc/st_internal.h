@@ -172,7 +172,7 @@ struct Ctx {
   int history_pending = 0;
   DevBuf<DevBeam> beams;
   DevBuf<double> red;       // reduction partials / small results
-  DevBuf<double> cgs;       // PCG partials (2 kRedBlocks) + scalars
+  DevBuf<double> cgs;       // PCG partials (3 kRedBlocks) + scalars (kCgsSize)
   cudaEvent_t cg_ev[2] = {nullptr, nullptr};  // PCG residual reads in flight
   cudaGraphExec_t cg_exec[2] = {nullptr, nullptr};  // captured PCG iteration per parity
   DevBuf<double> pws;       // power iteration: counter, scalars, (ww, vw) history
@@ -215,11 +215,13 @@ int vec_neg_mul(Ctx* c, const double* f, const double* cinv, double* w, int64_t 
 int vec_div(Ctx* c, const double* x, double d, double* y, int64_t n);               // y = x / d
 // PCG with device-resident scalars (st_reduce.cu); part: 2 kRedBlocks
 // doubles, s: 7 scalars (rz, pAp, alpha, rr, rz_new, beta, converged)
-int cg_alpha(Ctx* c, const double* p, const double* Ap, int64_t n, double* part, double* s);
-int cg_update(Ctx* c, const double* p, const double* Ap, const double* dinv, double* x, double* r,
-              double* z, int64_t n, double* part, double* s, double thr,
-              double* hrr = nullptr);
-int cg_p(Ctx* c, const double* s, const double* z, double* p, int64_t n);
+// Jacobi-PCG pieces with device-resident scalars (st_reduce.cu, pcg_dev)
+int cg_alpha(Ctx* c, const double* p, const double* Ap, int64_t n, double* ppart);
+int cg_update(Ctx* c, int par, const double* ppart, const double* p, const double* Ap,
+              const double* dinv, double* x, double* r, double* z, int64_t n, double* part,
+              double* s);
+int cg_beta_p(Ctx* c, int par, const double* part, double thr, double* hrr, const double* z,
+              double* p, int64_t n, double* s);
 // power iteration on device scalars (st_spectral_radius): pw_record keeps
 // (ww, vw) of the iteration in the history and sqrt(ww); pw_div: y = x / nw
 int pw_record(Ctx* c, double* pws);
@@ -228,6 +230,7 @@ int dot_to_device(Ctx* c, const double* a, const double* b, int64_t n, double* p
 
 constexpr int kRedBlocks = 296;  // 2 x 148 SMs
 constexpr int kThreads = 256;
+constexpr int kCgsSize = 3 * kRedBlocks + 16;
 
 }  // namespace st
 

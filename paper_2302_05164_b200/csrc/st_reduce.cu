@@ -2,6 +2,8 @@
 // loops (timestepping.py:102-131, 229-283).  Reductions run on a fixed
 // grid of kRedBlocks blocks in a fixed order, so results are identical
 // run to run.
+#include <algorithm>
+
 #include "st_common.cuh"
 
 namespace st {
@@ -101,7 +103,8 @@ __global__ void k_div(const double* x, double d, double* y, int64_t n) {
 
 // --- Jacobi-PCG with device-resident scalars (pcg_dev): one host read per
 // iteration (the residual norm for the stopping rule).  Scalars s[]:
-// 0 rz, 1 pAp, 2 alpha, 3 rr, 4 rz_new, 5 beta, 6 converged flag.  Once the
+// 1 pAp, 2 alpha, 3 rr, 4 rz_new, 5 beta, 6 converged flag, 8/9 rz by
+// iteration parity.  Three kernels per iteration after the Jacobian apply.  Once the
 // flag is set the kernels are no-ops, so the host can keep one iteration
 // in flight while it reads the previous residual norm.  The vector updates and
 // the dot products use the same expressions, grid and summation order as
@@ -118,25 +121,36 @@ __device__ __forceinline__ double block_sum(double v, double* sm) {
   return r;
 }
 
-__global__ void k_cg_alpha(const double* part, int np, double* s) {
-  if (s[6] != 0.0) return;
-  __shared__ double sm[512];
-  double acc = 0.0;
-  for (int i = threadIdx.x; i < np; i += blockDim.x) acc += part[i];
-  const double pAp = block_sum(acc, sm);
-  if (threadIdx.x == 0) {
-    s[1] = pAp;
-    s[2] = s[0] / pAp;
-  }
+// the 512-thread k_sum_partials sum of np <= 512 partials, by a 256-thread
+// block: thread t folds its two 512-thread slots (t, t + 256) first, which
+// is the first step of the 512-wide tree, then the same tree follows, so
+// every block gets the bitwise-same total as the single-block kernel
+__device__ __forceinline__ double sum512(const double* part, int np, double* sm) {
+  const int t = threadIdx.x;
+  double a = 0.0, b = 0.0;
+  if (t < np) a += part[t];
+  if (t + 256 < np) b += part[t + 256];
+  return block_sum(a + b, sm);
 }
 
+// Iteration scalars (parity par = iteration & 1): rz of the iteration is in
+// s[8 + par], the next one goes to s[8 + (par ^ 1)], so blocks of one
+// kernel never read a slot another block of it writes.
+
+// alpha = rz / pAp (pAp from the k_dot_partial partials, summed per block);
 // x += alpha p; r -= alpha Ap; z = D^-1 r; partials of r.r and r.z
-__global__ void k_cg_update(const double* s, const double* p, const double* Ap,
-                            const double* dinv, double* x, double* r, double* z, int64_t n,
-                            double* part) {
+__global__ void __launch_bounds__(kThreads) k_cg_update(double* s, int par, const double* ppart,
+                                                        const double* p, const double* Ap,
+                                                        const double* dinv, double* x, double* r,
+                                                        double* z, int64_t n, double* part) {
   if (s[6] != 0.0) return;
   __shared__ double sm[kThreads];
-  const double alpha = s[2];
+  const double pAp = sum512(ppart, kRedBlocks, sm);
+  const double alpha = s[8 + par] / pAp;
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    s[1] = pAp;
+    s[2] = alpha;
+  }
   double arr = 0.0, arz = 0.0;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
        i += (int64_t)gridDim.x * blockDim.x) {
@@ -156,58 +170,55 @@ __global__ void k_cg_update(const double* s, const double* p, const double* Ap,
   }
 }
 
-__global__ void k_cg_sum2(const double* part, int np, double* s, double thr, double* hrr) {
+// r.r, rz_new (per block, from the k_cg_update partials), the stopping
+// rule, beta = rz_new / rz and p = z + beta p.  Block 0 publishes the
+// scalars, the flag and r.r into the host's pinned slot (zero-copy: no
+// copy-engine node in the captured iteration).  A block that already sees
+// the flag block 0 raises in this kernel skips p, which is never read again.
+__global__ void __launch_bounds__(kThreads) k_cg_beta_p(double* s, int par, const double* part,
+                                                        double thr, double* hrr, const double* z,
+                                                        double* p, int64_t n) {
   if (s[6] != 0.0) return;
-  __shared__ double sm[512];
-  double a = 0.0, b = 0.0;
-  for (int i = threadIdx.x; i < np; i += blockDim.x) {
-    a += part[i];
-    b += part[np + i];
-  }
-  const double rr = block_sum(a, sm);
-  const double rz_new = block_sum(b, sm);
-  if (threadIdx.x == 0) {
+  __shared__ double sm[kThreads];
+  const double rr = sum512(part, kRedBlocks, sm);
+  const double rz_new = sum512(part + kRedBlocks, kRedBlocks, sm);
+  const double beta = rz_new / s[8 + par];
+  const bool conv = sqrt(rr) <= thr;  // the host's stopping rule, same doubles
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
     s[3] = rr;
     s[4] = rz_new;
-    s[5] = rz_new / s[0];
-    s[0] = rz_new;
-    s[6] = sqrt(rr) <= thr ? 1.0 : 0.0;  // the host's stopping rule, same doubles
-    // r.r straight into the host's pinned slot (zero-copy; no copy-engine
-    // node between this kernel and the next in the captured iteration)
+    s[5] = beta;
+    s[8 + (par ^ 1)] = rz_new;
+    s[6] = conv ? 1.0 : 0.0;
     if (hrr) *reinterpret_cast<volatile double*>(hrr) = rr;
   }
+  if (conv) return;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    p[i] = fma(beta, p[i], z[i]);
 }
 
-// p = z + beta p
-__global__ void k_cg_p(const double* s, const double* z, double* p, int64_t n) {
-  if (s[6] != 0.0) return;
-  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (i < n) p[i] = fma(s[5], p[i], z[i]);
-}
-
-int cg_alpha(Ctx* c, const double* p, const double* Ap, int64_t n, double* part, double* s) {
-  k_dot_partial<<<kRedBlocks, kThreads, 0, c->stream>>>(p, Ap, n, part);
-  c->launches++;
-  ST_LAUNCHED();
-  k_cg_alpha<<<1, 512, 0, c->stream>>>(part, kRedBlocks, s);
+int cg_alpha(Ctx* c, const double* p, const double* Ap, int64_t n, double* ppart) {
+  k_dot_partial<<<kRedBlocks, kThreads, 0, c->stream>>>(p, Ap, n, ppart);
   c->launches++;
   ST_LAUNCHED();
   return ST_OK;
 }
 
-int cg_update(Ctx* c, const double* p, const double* Ap, const double* dinv, double* x, double* r,
-              double* z, int64_t n, double* part, double* s, double thr, double* hrr) {
-  k_cg_update<<<kRedBlocks, kThreads, 0, c->stream>>>(s, p, Ap, dinv, x, r, z, n, part);
-  c->launches++;
-  ST_LAUNCHED();
-  k_cg_sum2<<<1, 512, 0, c->stream>>>(part, kRedBlocks, s, thr, hrr);
+int cg_update(Ctx* c, int par, const double* ppart, const double* p, const double* Ap,
+              const double* dinv, double* x, double* r, double* z, int64_t n, double* part,
+              double* s) {
+  k_cg_update<<<kRedBlocks, kThreads, 0, c->stream>>>(s, par, ppart, p, Ap, dinv, x, r, z, n,
+                                                      part);
   c->launches++;
   ST_LAUNCHED();
   return ST_OK;
 }
 
-int cg_p(Ctx* c, const double* s, const double* z, double* p, int64_t n) {
-  k_cg_p<<<nb(n), kThreads, 0, c->stream>>>(s, z, p, n);
+int cg_beta_p(Ctx* c, int par, const double* part, double thr, double* hrr, const double* z,
+              double* p, int64_t n, double* s) {
+  const unsigned g = std::min<unsigned>(nb(n), 4 * kRedBlocks);
+  k_cg_beta_p<<<g, kThreads, 0, c->stream>>>(s, par, part, thr, hrr, z, p, n);
   c->launches++;
   ST_LAUNCHED();
   return ST_OK;
