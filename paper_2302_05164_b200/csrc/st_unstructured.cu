@@ -14,6 +14,7 @@
 // An atomic-scatter variant (SolverSettings.deterministic = False, the
 // analogue of the reference's colored scatter) skips the element buffer.
 #include <algorithm>
+#include <cstdlib>
 #include <cmath>
 #include <map>
 #include <vector>
@@ -21,6 +22,38 @@
 #include "st_common.cuh"
 
 namespace st {
+
+// programmatic dependent launch (PDL) of the explicit scan loop's chain
+// k_rhs_cells -> k_step_nodes (-> k_distribute) -> next step: a kernel
+// launched with the attribute may start while its predecessor drains; each
+// CTA waits for the predecessor's completion (and memory flush) before it
+// reads or writes anything, then lets its own successor be staged.  With a
+// plain launch both instructions are no-ops.
+__device__ __forceinline__ void pdl_wait_release() {
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+
+template <typename... KArgs, typename... Args>
+static cudaError_t launch_pdl(bool pdl, void (*k)(KArgs...), dim3 grid, dim3 block,
+                              cudaStream_t stream, Args... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = 0;
+  cfg.stream = stream;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = pdl ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, k, static_cast<KArgs>(args)...);
+}
+
+static bool use_pdl() {
+  static const bool on = !(getenv("ST_NO_PDL") && getenv("ST_NO_PDL")[0] == '1');
+  return on;
+}
 
 __constant__ double cV[2][2];   // V1[i][q] (operators.py:33-34)
 __constant__ double cD[2][2];   // D1
@@ -109,6 +142,9 @@ __global__ void k_rhs_cells(int64_t n, CellGeo g, FaceTab ft, DevParams P,
                             int pending, int nb, const DevBeam* beams,
                             double* E, double* Ec, double* f_atomic,
                             double* c_atomic) {
+  // programmatic dependent launch (explicit scan loop): wait for the
+  // previous kernel of the stream in every CTA, then release the next one
+  pdl_wait_release();
   int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (c >= n) return;
   double t[8], e[8];
@@ -454,6 +490,9 @@ __global__ void k_step_nodes(int64_t nv, NodeTab nt, const double* E, const doub
                              const double* f_atomic, const double* c_atomic,
                              const double* cinv, const double* T, double dt, double T_inf,
                              double* Tout, unsigned long long* red) {
+  // programmatic dependent launch (explicit scan loop): wait for the
+  // previous kernel of the stream in every CTA, then release the next one
+  pdl_wait_release();
   int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   double out = 0.0;
   bool live = v < nv && !nt.is_slave[v];
@@ -476,6 +515,9 @@ __global__ void k_step_nodes(int64_t nv, NodeTab nt, const double* E, const doub
 // hanging-vertex closure (mesh.py:652-661)
 __global__ void k_distribute(int64_t ns, const int64_t* slaves, const int64_t* ptr,
                              const int64_t* masters, const double* w, double* v) {
+  // programmatic dependent launch (explicit scan loop): wait for the
+  // previous kernel of the stream in every CTA, then release the next one
+  pdl_wait_release();
   int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (i >= ns) return;
   double acc = 0.0;
@@ -575,9 +617,13 @@ struct Unstructured : Backend {
     return ST_OK;
   }
 
-  int distribute(double* v) override {
+  int distribute(double* v) override { return distribute_pdl(v, false); }
+
+  int distribute_pdl(double* v, bool pdl) {
     if (!ns) return ST_OK;
-    k_distribute<<<nblk(ns), kThreads, 0, c->stream>>>(ns, slaves.p, sptr.p, smast.p, sw.p, v);
+    ST_CUDA(launch_pdl(pdl, k_distribute, dim3(nblk(ns)), dim3(kThreads), c->stream, ns,
+                       (const int64_t*)slaves.p, (const int64_t*)sptr.p, (const int64_t*)smast.p,
+                       (const double*)sw.p, v));
     return launched();
   }
 
@@ -593,13 +639,13 @@ struct Unstructured : Backend {
 
   int cells_rhs(const double* T, double* rc, int flags, double frozen_k, int nb,
                 const DevBeam* beams, int pending, bool want_cap, double* f_atomic,
-                double* c_atomic) {
+                double* c_atomic, bool pdl = false) {
     double* rcp = rc;
     bool det = c->deterministic || f_atomic == nullptr;
-    k_rhs_cells<<<nblk_cells(n), kCellThreads, 0, c->stream>>>(
-        n, geo(), faces(), c->dp, T, rcp, c->rc_value, flags, frozen_k, pending, nb, beams,
-        det ? E.p : nullptr, (det && want_cap) ? Ec.p : nullptr, det ? nullptr : f_atomic,
-        (!det && want_cap) ? c_atomic : nullptr);
+    ST_CUDA(launch_pdl(pdl, k_rhs_cells, dim3(nblk_cells(n)), dim3(kCellThreads), c->stream, n,
+                       geo(), faces(), c->dp, T, rcp, c->rc_value, flags, frozen_k, pending, nb,
+                       beams, det ? E.p : nullptr, (det && want_cap) ? Ec.p : nullptr,
+                       det ? nullptr : f_atomic, (!det && want_cap) ? c_atomic : nullptr));
     return launched();
   }
 
@@ -633,8 +679,12 @@ struct Unstructured : Backend {
         ST_CUDA(cudaMemsetAsync(ca, 0, nv * sizeof(double), c->stream));
       }
     }
+    // the scan loop chains its kernels with programmatic dependent launch
+    // (ST_NO_PDL=1 turns it off); every kernel waits for its predecessor
+    // before touching memory, so the order is the plain stream order
+    const bool pdl = use_pdl() && c->deterministic && !c->prof;
     c->prof_begin();
-    ST_TRY(cells_rhs(T, rc, flags, 0.0, nb, beams, pending, latent, fa, ca));
+    ST_TRY(cells_rhs(T, rc, flags, 0.0, nb, beams, pending, latent, fa, ca, pdl));
     c->prof_end();
     if (!c->deterministic && ns) {
       k_condense_atomic<<<nblk(ns), kThreads, 0, c->stream>>>(ns, slaves.p, sptr.p, smast.p, sw.p, fa);
@@ -645,12 +695,14 @@ struct Unstructured : Backend {
       }
     }
     const bool det = c->deterministic != 0;
-    k_step_nodes<<<nblk(nv), kThreads, 0, c->stream>>>(
-        nv, nodes(), det ? E.p : nullptr, (det && latent) ? Ec.p : nullptr, det ? nullptr : fa,
-        (!det && latent) ? ca : nullptr, cinv.p, T, dt, c->dp.T_inf, Tout,
-        reinterpret_cast<unsigned long long*>(red));
+    ST_CUDA(launch_pdl(pdl, k_step_nodes, dim3(nblk(nv)), dim3(kThreads), c->stream, nv,
+                       nodes(), (const double*)(det ? E.p : nullptr),
+                       (const double*)((det && latent) ? Ec.p : nullptr),
+                       (const double*)(det ? nullptr : fa),
+                       (const double*)((!det && latent) ? ca : nullptr), (const double*)cinv.p, T,
+                       dt, c->dp.T_inf, Tout, reinterpret_cast<unsigned long long*>(red)));
     ST_TRY(launched());
-    return distribute(Tout);
+    return distribute_pdl(Tout, pdl);
   }
 
   int history(const double* T, double* rc) override {
