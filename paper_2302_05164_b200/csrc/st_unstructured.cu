@@ -23,37 +23,6 @@
 
 namespace st {
 
-// programmatic dependent launch (PDL) of the explicit scan loop's chain
-// k_rhs_cells -> k_step_nodes (-> k_distribute) -> next step: a kernel
-// launched with the attribute may start while its predecessor drains; each
-// CTA waits for the predecessor's completion (and memory flush) before it
-// reads or writes anything, then lets its own successor be staged.  With a
-// plain launch both instructions are no-ops.
-__device__ __forceinline__ void pdl_wait_release() {
-  asm volatile("griddepcontrol.wait;" ::: "memory");
-  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
-}
-
-template <typename... KArgs, typename... Args>
-static cudaError_t launch_pdl(bool pdl, void (*k)(KArgs...), dim3 grid, dim3 block,
-                              cudaStream_t stream, Args... args) {
-  cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = grid;
-  cfg.blockDim = block;
-  cfg.dynamicSmemBytes = 0;
-  cfg.stream = stream;
-  cudaLaunchAttribute at[1];
-  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-  at[0].val.programmaticStreamSerializationAllowed = 1;
-  cfg.attrs = at;
-  cfg.numAttrs = pdl ? 1 : 0;
-  return cudaLaunchKernelEx(&cfg, k, static_cast<KArgs>(args)...);
-}
-
-static bool use_pdl() {
-  static const bool on = !(getenv("ST_NO_PDL") && getenv("ST_NO_PDL")[0] == '1');
-  return on;
-}
 
 __constant__ double cV[2][2];   // V1[i][q] (operators.py:33-34)
 __constant__ double cD[2][2];   // D1
