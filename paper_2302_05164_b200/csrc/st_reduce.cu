@@ -14,6 +14,7 @@ static inline unsigned nb(int64_t n) {
 }
 
 __global__ void k_dot_partial(const double* a, const double* b, int64_t n, double* part) {
+  pdl_wait_release();  // see st_common.cuh
   __shared__ double sm[kThreads];
   double acc = 0.0;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
@@ -143,6 +144,7 @@ __global__ void __launch_bounds__(kThreads) k_cg_update(double* s, int par, cons
                                                         const double* p, const double* Ap,
                                                         const double* dinv, double* x, double* r,
                                                         double* z, int64_t n, double* part) {
+  pdl_wait_release();  // see st_common.cuh
   if (s[6] != 0.0) return;
   __shared__ double sm[kThreads];
   const double pAp = sum512(ppart, kRedBlocks, sm);
@@ -178,6 +180,7 @@ __global__ void __launch_bounds__(kThreads) k_cg_update(double* s, int par, cons
 __global__ void __launch_bounds__(kThreads) k_cg_beta_p(double* s, int par, const double* part,
                                                         double thr, double* hrr, const double* z,
                                                         double* p, int64_t n) {
+  pdl_wait_release();  // see st_common.cuh
   if (s[6] != 0.0) return;
   __shared__ double sm[kThreads];
   const double rr = sum512(part, kRedBlocks, sm);
@@ -198,8 +201,10 @@ __global__ void __launch_bounds__(kThreads) k_cg_beta_p(double* s, int par, cons
     p[i] = fma(beta, p[i], z[i]);
 }
 
+// the PCG iteration's kernels are chained with programmatic dependent launch
 int cg_alpha(Ctx* c, const double* p, const double* Ap, int64_t n, double* ppart) {
-  k_dot_partial<<<kRedBlocks, kThreads, 0, c->stream>>>(p, Ap, n, ppart);
+  ST_CUDA(launch_pdl(use_pdl(), k_dot_partial, dim3(kRedBlocks), dim3(kThreads), c->stream, p,
+                     Ap, n, ppart));
   c->launches++;
   ST_LAUNCHED();
   return ST_OK;
@@ -208,8 +213,8 @@ int cg_alpha(Ctx* c, const double* p, const double* Ap, int64_t n, double* ppart
 int cg_update(Ctx* c, int par, const double* ppart, const double* p, const double* Ap,
               const double* dinv, double* x, double* r, double* z, int64_t n, double* part,
               double* s) {
-  k_cg_update<<<kRedBlocks, kThreads, 0, c->stream>>>(s, par, ppart, p, Ap, dinv, x, r, z, n,
-                                                      part);
+  ST_CUDA(launch_pdl(use_pdl(), k_cg_update, dim3(kRedBlocks), dim3(kThreads), c->stream, s,
+                     par, ppart, p, Ap, dinv, x, r, z, n, part));
   c->launches++;
   ST_LAUNCHED();
   return ST_OK;
@@ -218,7 +223,8 @@ int cg_update(Ctx* c, int par, const double* ppart, const double* p, const doubl
 int cg_beta_p(Ctx* c, int par, const double* part, double thr, double* hrr, const double* z,
               double* p, int64_t n, double* s) {
   const unsigned g = std::min<unsigned>(nb(n), 4 * kRedBlocks);
-  k_cg_beta_p<<<g, kThreads, 0, c->stream>>>(s, par, part, thr, hrr, z, p, n);
+  ST_CUDA(launch_pdl(use_pdl(), k_cg_beta_p, dim3(g), dim3(kThreads), c->stream, s, par, part,
+                     thr, hrr, z, p, n));
   c->launches++;
   ST_LAUNCHED();
   return ST_OK;

@@ -304,6 +304,7 @@ __device__ __forceinline__ void tangent(const DevParams& P, const double* tl, co
 __global__ void k_jac_cells(int64_t n, CellGeo g, DevParams P, const double* vd,
                             const double* Tl, const double* rc, double rc_value,
                             double dt, double* E) {
+  pdl_wait_release();  // see st_common.cuh
   int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (c >= n) return;
   double v[8], tl[8], k[8], dk[8], gx[8], gy[8], gz[8], e[8], tmp[8], pr[8];
@@ -442,6 +443,7 @@ __device__ __forceinline__ double gather_condensed(const NodeTab& nt, const doub
 // out = condensed(E); slave rows 0; optional: dirichlet rows <- dir_src, slave rows <- slave_val
 __global__ void k_gather(int64_t nv, NodeTab nt, const double* E, double* out,
                          const double* dir_src, int set_slave, double slave_val) {
+  pdl_wait_release();  // see st_common.cuh
   int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (v >= nv) return;
   double r;
@@ -523,6 +525,7 @@ __global__ void k_fold(int64_t nv, const int* fptr, const int* fent, const doubl
 __global__ void k_prep_jac(int64_t nv, int64_t ns, const uint8_t* is_dir, const uint8_t* is_slave,
                            const double* v, const int64_t* slaves, const int64_t* ptr,
                            const int64_t* masters, const double* w, double* vd) {
+  pdl_wait_release();  // see st_common.cuh
   int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (i < nv) {
     if (!is_slave[i]) vd[i] = is_dir[i] ? 0.0 : v[i];
@@ -698,15 +701,20 @@ struct Unstructured : Backend {
                double* out) override {
     double* vd;
     ST_TRY(c->vec(5, &vd));
-    k_prep_jac<<<nblk(nv + ns), kThreads, 0, c->stream>>>(nv, ns, is_dir.p, is_slave.p, v,
-                                                          slaves.p, sptr.p, smast.p, sw.p, vd);
+    // chained with programmatic dependent launch (the PCG iteration)
+    const bool pdl = use_pdl() && !c->prof;
+    ST_CUDA(launch_pdl(pdl, k_prep_jac, dim3(nblk(nv + ns)), dim3(kThreads), c->stream, nv, ns,
+                       (const uint8_t*)is_dir.p, (const uint8_t*)is_slave.p, v,
+                       (const int64_t*)slaves.p, (const int64_t*)sptr.p, (const int64_t*)smast.p,
+                       (const double*)sw.p, vd));
     ST_TRY(launched());
     c->prof_begin();
-    k_jac_cells<<<nblk_cells(n), kCellThreads, 0, c->stream>>>(n, geo(), c->dp, vd, Tl, rc,
-                                                      c->rc_value, dt, E.p);
+    ST_CUDA(launch_pdl(pdl, k_jac_cells, dim3(nblk_cells(n)), dim3(kCellThreads), c->stream, n,
+                       geo(), c->dp, (const double*)vd, Tl, rc, c->rc_value, dt, E.p));
     ST_TRY(launched());
     c->prof_end();
-    k_gather<<<nblk(nv), kThreads, 0, c->stream>>>(nv, nodes(), E.p, out, v, 0, 0.0);
+    ST_CUDA(launch_pdl(pdl, k_gather, dim3(nblk(nv)), dim3(kThreads), c->stream, nv, nodes(),
+                       (const double*)E.p, out, v, 0, 0.0));
     return launched();
   }
 
