@@ -677,7 +677,9 @@ int st_spectral_radius(st_ctx* ctx, double k_frozen, const double* v0, double to
   double* part = c.cgs.p;
   double* pws = c.pws.p;
   auto body = [&]() -> int {
-    ST_CUDA(cudaMemcpyAsync(vd, v, nv * sizeof(double), cudaMemcpyDeviceToDevice, c.stream));
+    // vd = v by a kernel (1.0 * x is exact), not a copy node: the
+    // iteration's kernels are chained with programmatic dependent launch
+    ST_TRY(vec_scal_copy(&c, 1.0, v, vd, nv));
     ST_TRY(c.be->distribute(vd));
     ST_TRY(c.be->pin_dirichlet(vd, 0.0));
     ST_TRY(c.be->rhs(vd, nullptr, ST_RHS_DIFFUSION | ST_RHS_FROZEN_K, k_frozen, 0, nullptr, f,

@@ -30,6 +30,7 @@ __global__ void k_dot_partial(const double* a, const double* b, int64_t n, doubl
 }
 
 __global__ void k_sum_partials(const double* part, int np, double* out) {
+  pdl_wait_release();  // see st_common.cuh
   __shared__ double sm[512];
   double acc = 0.0;
   for (int i = threadIdx.x; i < np; i += blockDim.x) acc += part[i];
@@ -89,11 +90,13 @@ __global__ void k_sub(const double* a, const double* b, double* y, int64_t n) {
   if (i < n) y[i] = a[i] - b[i];
 }
 __global__ void k_scal_copy(double s, const double* x, double* y, int64_t n) {
+  pdl_wait_release();  // see st_common.cuh
   int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (i < n) y[i] = s * x[i];
 }
 // power iteration (timestepping.py:88-90, :62): w = (-f) * cinv; v = w / nw
 __global__ void k_neg_mul(const double* f, const double* cinv, double* w, int64_t n) {
+  pdl_wait_release();  // see st_common.cuh
   int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (i < n) w[i] = (-f[i]) * cinv[i];
 }
@@ -231,10 +234,12 @@ int cg_beta_p(Ctx* c, int par, const double* part, double thr, double* hrr, cons
 }
 
 int dot_to_device(Ctx* c, const double* a, const double* b, int64_t n, double* part, double* out) {
-  k_dot_partial<<<kRedBlocks, kThreads, 0, c->stream>>>(a, b, n, part);
+  ST_CUDA(launch_pdl(use_pdl(), k_dot_partial, dim3(kRedBlocks), dim3(kThreads), c->stream, a,
+                     b, n, part));
   c->launches++;
   ST_LAUNCHED();
-  k_sum_partials<<<1, 512, 0, c->stream>>>(part, kRedBlocks, out);
+  ST_CUDA(launch_pdl(use_pdl(), k_sum_partials, dim3(1), dim3(512), c->stream,
+                     (const double*)part, kRedBlocks, out));
   c->launches++;
   ST_LAUNCHED();
   return ST_OK;
@@ -243,6 +248,7 @@ int dot_to_device(Ctx* c, const double* a, const double* b, int64_t n, double* p
 // power iteration scalars pws: [0] iteration counter, [1] w.w, [2] v.w,
 // [3] ||w||, [4 + 2i], [5 + 2i] the (w.w, v.w) pair of iteration i
 __global__ void k_pw_record(double* pws) {
+  pdl_wait_release();  // see st_common.cuh
   const int i = (int)pws[0];
   pws[4 + 2 * i] = pws[1];
   pws[5 + 2 * i] = pws[2];
@@ -250,15 +256,24 @@ __global__ void k_pw_record(double* pws) {
   pws[0] = (double)(i + 1);
 }
 __global__ void k_pw_div(const double* x, const double* pws, double* y, int64_t n) {
+  pdl_wait_release();  // see st_common.cuh
   int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (i < n) y[i] = x[i] / pws[3];
 }
 int pw_record(Ctx* c, double* pws) {
-  k_pw_record<<<1, 1, 0, c->stream>>>(pws);
+  ST_CUDA(launch_pdl(use_pdl(), k_pw_record, dim3(1), dim3(1), c->stream, pws));
   c->launches++;
   ST_LAUNCHED();
   return ST_OK;
 }
+
+#define ST_VEC_LAUNCH_PDL(kern, ...)                                                  \
+  do {                                                                                \
+    ST_CUDA(launch_pdl(use_pdl(), kern, dim3(nb(n)), dim3(kThreads), c->stream, __VA_ARGS__)); \
+    c->launches++;                                                                    \
+    ST_LAUNCHED();                                                                    \
+    return ST_OK;                                                                     \
+  } while (0)
 
 #define ST_VEC_LAUNCH(kern, ...)                                   \
   do {                                                             \
@@ -288,16 +303,16 @@ int vec_sub(Ctx* c, const double* a, const double* b, double* y, int64_t n) {
   ST_VEC_LAUNCH(k_sub, a, b, y, n);
 }
 int vec_scal_copy(Ctx* c, double s, const double* x, double* y, int64_t n) {
-  ST_VEC_LAUNCH(k_scal_copy, s, x, y, n);
+  ST_VEC_LAUNCH_PDL(k_scal_copy, s, x, y, n);
 }
 int vec_neg_mul(Ctx* c, const double* f, const double* cinv, double* w, int64_t n) {
-  ST_VEC_LAUNCH(k_neg_mul, f, cinv, w, n);
+  ST_VEC_LAUNCH_PDL(k_neg_mul, f, cinv, w, n);
 }
 int vec_div(Ctx* c, const double* x, double d, double* y, int64_t n) {
   ST_VEC_LAUNCH(k_div, x, d, y, n);
 }
 int pw_div(Ctx* c, const double* x, const double* pws, double* y, int64_t n) {
-  ST_VEC_LAUNCH(k_pw_div, x, pws, y, n);
+  ST_VEC_LAUNCH_PDL(k_pw_div, x, pws, y, n);
 }
 
 }  // namespace st

@@ -539,12 +539,14 @@ __global__ void k_prep_jac(int64_t nv, int64_t ns, const uint8_t* is_dir, const 
 }
 
 __global__ void k_mask_rows(int64_t nv, const uint8_t* is_dir, const uint8_t* is_slave, double* v) {
+  pdl_wait_release();  // see st_common.cuh
   int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (i >= nv) return;
   if (is_dir[i] || is_slave[i]) v[i] = 0.0;
 }
 
 __global__ void k_pin(int64_t nv, const uint8_t* is_dir, double* v, double val) {
+  pdl_wait_release();  // see st_common.cuh
   int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (i >= nv) return;
   if (is_dir[i]) v[i] = val;
@@ -589,7 +591,7 @@ struct Unstructured : Backend {
     return ST_OK;
   }
 
-  int distribute(double* v) override { return distribute_pdl(v, false); }
+  int distribute(double* v) override { return distribute_pdl(v, use_pdl() && !c->prof); }
 
   int distribute_pdl(double* v, bool pdl) {
     if (!ns) return ST_OK;
@@ -600,12 +602,14 @@ struct Unstructured : Backend {
   }
 
   int mask_rows(double* v) override {
-    k_mask_rows<<<nblk(nv), kThreads, 0, c->stream>>>(nv, is_dir.p, is_slave.p, v);
+    ST_CUDA(launch_pdl(use_pdl(), k_mask_rows, dim3(nblk(nv)), dim3(kThreads), c->stream, nv,
+                       (const uint8_t*)is_dir.p, (const uint8_t*)is_slave.p, v));
     return launched();
   }
 
   int pin_dirichlet(double* v, double value) override {
-    k_pin<<<nblk(nv), kThreads, 0, c->stream>>>(nv, is_dir.p, v, value);
+    ST_CUDA(launch_pdl(use_pdl(), k_pin, dim3(nblk(nv)), dim3(kThreads), c->stream, nv,
+                       (const uint8_t*)is_dir.p, v, value));
     return launched();
   }
 
@@ -624,8 +628,10 @@ struct Unstructured : Backend {
   int rhs(const double* T, double* rc, int flags, double frozen_k, int nb,
           const DevBeam* beams, double* f, int pending) override {
     if (c->deterministic) {
-      ST_TRY(cells_rhs(T, rc, flags, frozen_k, nb, beams, pending, false, nullptr, nullptr));
-      k_gather<<<nblk(nv), kThreads, 0, c->stream>>>(nv, nodes(), E.p, f, nullptr, 0, 0.0);
+      const bool pdl = use_pdl() && !c->prof;
+      ST_TRY(cells_rhs(T, rc, flags, frozen_k, nb, beams, pending, false, nullptr, nullptr, pdl));
+      ST_CUDA(launch_pdl(pdl, k_gather, dim3(nblk(nv)), dim3(kThreads), c->stream, nv, nodes(),
+                         (const double*)E.p, f, (const double*)nullptr, 0, 0.0));
       return launched();
     }
     ST_CUDA(cudaMemsetAsync(f, 0, nv * sizeof(double), c->stream));
