@@ -563,9 +563,13 @@ __global__ void k_diag_fix(int64_t nv, const uint8_t* is_dir, const uint8_t* is_
 // ---------------------------------------------------------------------------
 static inline unsigned nblk(int64_t n) { return (unsigned)((n + kThreads - 1) / kThreads); }
 // per-cell kernels at cool-down mesh sizes (~2e4 cells) are latency bound:
-// 64-thread blocks spread them over every SM (measured 8 % faster explicit
-// steps than 256 at 25k DoFs)
-constexpr int kCellThreads = 64;
+// small blocks spread them over every SM.  Config-3-sized explicit step with
+// the PDL chain: 32 -> 10.6, 64 -> 10.7, 128 -> 10.3, 256 -> 10.95 us (before
+// PDL, 64 was 8 % faster than 256)
+#ifndef ST_CELL_THREADS
+#define ST_CELL_THREADS 128  // A/B hook (ST_VARIANT builds)
+#endif
+constexpr int kCellThreads = ST_CELL_THREADS;
 static inline unsigned nblk_cells(int64_t n) {
   return (unsigned)((n + kCellThreads - 1) / kCellThreads);
 }
