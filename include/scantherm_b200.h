@@ -252,6 +252,81 @@ double st_algorithmic_bytes_per_dof(const st_ctx* ctx);
 int st_bench_explicit(st_ctx* ctx, int n_steps, const double* dts, const st_beam* beams,
                       int n_beams, int64_t flush_bytes, float* step_ms, float* main_ms);
 
+/* --- leaf tables of the growing adaptive mesh (host C++, st_forest.cpp) --
+ * The reference keeps these in numpy (pkg/src/scantherm/mesh.py); these
+ * entry points build bit-identical tables from a leaf set.  No device
+ * work, no context: they run on any host. */
+
+/* Leaf table (reference Forest, mesh.py:143-157): lattice anchors in
+ * finest units, level in [.., depth], canonical order (key, level). */
+typedef struct st_leaves {
+  int64_t n;
+  int32_t depth;  /* finest level (MeshParams.total_depth)        */
+  int32_t cpl;    /* finest cells per powder layer                */
+  const int8_t* level;
+  const int64_t* anchor;      /* (n, 3) */
+  const uint8_t* active;
+  const uint8_t* init_consol; /* nullable */
+} st_leaves;
+
+/* Variable-size results: a bag of named arrays owned by the library. */
+typedef struct st_tables st_tables;
+#define ST_DT_I8 1
+#define ST_DT_U8 2
+#define ST_DT_I32 3
+#define ST_DT_I64 4
+#define ST_DT_F64 5
+/* dims has room for 4 entries; *data stays valid until st_tables_free. */
+int st_tables_get(const st_tables* t, const char* name, int* dtype, int* ndim, int64_t* dims,
+                  const void** data);
+void st_tables_free(st_tables* t);
+
+/* Level-0 tiling of integer boxes (m, 6) [x0 y0 z0 x1 y1 z1], each box
+ * active (plate) or void (build volume): replaces build_coarse_grid
+ * (mesh.py:289-333).  Arrays: level, anchor, active, init_consol. */
+int st_coarse_grid(int32_t depth, int32_t cpl, int64_t n_boxes, const int64_t* boxes,
+                   const uint8_t* box_active, st_tables** out);
+/* Vertex numbering by packed lattice key, hanging-node constraints with
+ * chains expanded, Dirichlet on the z_min plane: replaces build_dofmap
+ * (mesh.py:706-779).  Arrays: vertices, cell_verts, active_rows,
+ * is_slave, is_dirichlet, slaves, slave_ptr, slave_masters,
+ * slave_weights. */
+int st_build_dofmap(const st_leaves* leaves, int64_t z_min, int dirichlet_bottom,
+                    st_tables** out);
+/* Radiating +z facets (full or quarter): replaces interface_faces
+ * (mesh.py:998-1072).  Arrays: cell_rows, offset, fsize. */
+int st_interface_faces(const st_leaves* leaves, st_tables** out);
+/* Plan of the update activating layer new_layer: replaces advance_layer
+ * (mesh.py:439-549) and _lineage (:552-602).  rc: the history
+ * (n_active, nq) of the old leaves, or NULL (no coarsening gate).
+ * Arrays: level, anchor, active, init_consol, same_src, ancestor_src,
+ * group_rows, group_ptr, group_kids (coarse_groups as CSR),
+ * coarsened_min_rc. */
+int st_plan_layer(const st_leaves* leaves, int32_t new_layer, const double* rc, int32_t nq,
+                  st_tables** out);
+/* Nodal transfer of n_fields fields (field-major) onto the new vertices:
+ * copy / trilinear from the old containing cell / T_0, then the new
+ * slaves re-interpolated; source[v] = 0 / 1 / 2 (TransferReport).
+ * Replaces the nodal half of apply_update (mesh.py:823-866). */
+int st_transfer_nodal(const st_leaves* old_leaves, const int64_t* old_verts, int64_t nv_old,
+                      const int32_t* old_cell_verts, const int64_t* new_verts, int64_t nv_new,
+                      const int64_t* slave_ptr, const int64_t* slaves, int64_t n_slaves,
+                      const int64_t* slave_masters, const double* slave_weights, int32_t n_fields,
+                      const double* fields_old, double T_0, double* fields_new, int8_t* source);
+/* History transfer (n_active, 8): octant copy down, octant mean up;
+ * replaces mesh.py:868-896. */
+int st_transfer_history(const st_leaves* old_leaves, const st_leaves* new_leaves,
+                        const int64_t* same_src, const int64_t* ancestor_src, int64_t n_groups,
+                        const int64_t* group_rows, const int64_t* group_ptr,
+                        const int64_t* group_kids, const double* rc_old, double* rc_new);
+
+/* Host constraint plumbing on a vertex vector, in place (replaces
+ * DofMap.distribute / DofMap.condense, mesh.py:652-670). */
+int st_host_distribute(int64_t n_slaves, const int64_t* slaves, const int64_t* slave_ptr,
+                       const int64_t* slave_masters, const double* slave_weights, double* values);
+int st_host_condense(int64_t n_slaves, const int64_t* slaves, const int64_t* slave_ptr,
+                     const int64_t* slave_masters, const double* slave_weights, double* values);
+
 #ifdef __cplusplus
 }
 #endif

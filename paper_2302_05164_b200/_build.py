@@ -29,7 +29,8 @@ if VARIANT:
 
 
 def sources():
-    return sorted(glob.glob(os.path.join(HERE, "csrc", "*.cu")))
+    return sorted(glob.glob(os.path.join(HERE, "csrc", "*.cu")) +
+                  glob.glob(os.path.join(HERE, "csrc", "*.cpp")))
 
 
 def headers():
@@ -39,7 +40,7 @@ def headers():
 
 
 def _obj(src):
-    return os.path.join(OBJ, os.path.basename(src)[:-3] + ".o")
+    return os.path.join(OBJ, os.path.splitext(os.path.basename(src))[0] + ".o")
 
 
 def _stale(target, deps):
@@ -57,6 +58,8 @@ def needs_build():
 
 def _compile(src, nvcc, verbose):
     cmd = [nvcc] + FLAGS + ["-c", src, "-o", _obj(src) + ".tmp"]
+    if src.endswith(".cpp"):  # host table builder: numpy-order arithmetic, no FMA contraction
+        cmd += ["-Xcompiler", "-ffp-contract=off"]
     if verbose:
         cmd.insert(1, "-Xptxas=-v")
     r = subprocess.run(cmd, capture_output=True, text=True)

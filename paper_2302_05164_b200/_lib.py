@@ -76,6 +76,16 @@ class StStructuredMesh(ctypes.Structure):
                 ("iface_lo", ctypes.c_int32), ("iface_hi", ctypes.c_int32)]
 
 
+class StLeaves(ctypes.Structure):
+    _fields_ = [("n", ctypes.c_int64), ("depth", ctypes.c_int32), ("cpl", ctypes.c_int32),
+                ("level", ctypes.POINTER(ctypes.c_int8)), ("anchor", _i64p),
+                ("active", _u8p), ("init_consol", _u8p)]
+
+
+_i8p = ctypes.POINTER(ctypes.c_int8)
+_DT = {1: np.int8, 2: np.uint8, 3: np.int32, 4: np.int64, 5: np.float64}
+
+
 # (name, restype, argtypes) for every symbol of include/scantherm_b200.h
 _VP = ctypes.c_void_p
 SIGNATURES = [
@@ -137,6 +147,26 @@ SIGNATURES = [
     ("st_bench_explicit", ctypes.c_int,
      [_VP, ctypes.c_int, _dp, ctypes.POINTER(StBeam), ctypes.c_int, ctypes.c_int64,
       ctypes.POINTER(ctypes.c_float), ctypes.POINTER(ctypes.c_float)]),
+    # leaf tables (host C++, st_forest.cpp)
+    ("st_tables_get", ctypes.c_int,
+     [_VP, ctypes.c_char_p, ctypes.POINTER(ctypes.c_int), ctypes.POINTER(ctypes.c_int), _i64p,
+      ctypes.POINTER(_VP)]),
+    ("st_tables_free", None, [_VP]),
+    ("st_coarse_grid", ctypes.c_int,
+     [ctypes.c_int32, ctypes.c_int32, ctypes.c_int64, _i64p, _u8p, ctypes.POINTER(_VP)]),
+    ("st_build_dofmap", ctypes.c_int,
+     [ctypes.POINTER(StLeaves), ctypes.c_int64, ctypes.c_int, ctypes.POINTER(_VP)]),
+    ("st_interface_faces", ctypes.c_int, [ctypes.POINTER(StLeaves), ctypes.POINTER(_VP)]),
+    ("st_plan_layer", ctypes.c_int,
+     [ctypes.POINTER(StLeaves), ctypes.c_int32, _dp, ctypes.c_int32, ctypes.POINTER(_VP)]),
+    ("st_transfer_nodal", ctypes.c_int,
+     [ctypes.POINTER(StLeaves), _i64p, ctypes.c_int64, _i32p, _i64p, ctypes.c_int64, _i64p,
+      _i64p, ctypes.c_int64, _i64p, _dp, ctypes.c_int32, _dp, ctypes.c_double, _dp, _i8p]),
+    ("st_transfer_history", ctypes.c_int,
+     [ctypes.POINTER(StLeaves), ctypes.POINTER(StLeaves), _i64p, _i64p, ctypes.c_int64, _i64p,
+      _i64p, _i64p, _dp, _dp]),
+    ("st_host_distribute", ctypes.c_int, [ctypes.c_int64, _i64p, _i64p, _i64p, _dp, _dp]),
+    ("st_host_condense", ctypes.c_int, [ctypes.c_int64, _i64p, _i64p, _i64p, _dp, _dp]),
 ]
 
 _lib = None
@@ -171,6 +201,33 @@ def check(rc, what=""):
         if rc == -1:
             raise ValueError(f"{what}: {msg}")
         raise StError(f"{what} failed ({rc}): {msg}")
+
+
+def tables_dict(t):
+    """Copy every array of an st_tables bag into numpy (names probed from
+    the known result sets)."""
+    lib = load()
+    names = ("level", "anchor", "active", "init_consol", "same_src", "ancestor_src",
+             "group_rows", "group_ptr", "group_kids", "coarsened_min_rc", "vertices",
+             "cell_verts", "active_rows", "is_slave", "is_dirichlet", "slaves", "slave_ptr",
+             "slave_masters", "slave_weights", "cell_rows", "offset", "fsize")
+    out = {}
+    dt, nd = ctypes.c_int(), ctypes.c_int()
+    dims = (ctypes.c_int64 * 4)()
+    data = ctypes.c_void_p()
+    for n in names:
+        if lib.st_tables_get(t, n.encode(), ctypes.byref(dt), ctypes.byref(nd), dims,
+                             ctypes.byref(data)) != 0:
+            continue
+        shape = tuple(dims[i] for i in range(nd.value))
+        typ = _DT[dt.value]
+        count = int(np.prod(shape)) if shape else 0
+        if count == 0:
+            out[n] = np.zeros(shape, dtype=typ)
+            continue
+        buf = (ctypes.c_char * (count * np.dtype(typ).itemsize)).from_address(data.value)
+        out[n] = np.frombuffer(buf, dtype=typ).reshape(shape).copy()
+    return out
 
 
 def dptr(a):

@@ -1,65 +1,53 @@
-"""Host-side mesh tables for the B200 operator.
+"""Mesh tables of the B200 operator: leaf sets, DoF maps, facets, layer
+activation and transfer.
 
 The reference keeps its adaptive voxel forest and DoF map in numpy
-(``scantherm/mesh.py``).  The device only needs flat tables: per-cell
-corner ids, sizes and anchors, the hanging-node CSR, the Dirichlet mask
-and the radiating facets.  This module holds
+(``pkg/src/scantherm/mesh.py``).  Here the table construction runs in
+host C++ (``csrc/st_forest.cpp``, exported through the C ABI in
+``include/scantherm_b200.h``); this module holds the Python containers
+the operator and the time integrators read and thin wrappers around the
+native builders:
 
-* :class:`Forest` / :class:`DofMap` — minimal containers with the
-  attributes the operator reads (duck-compatible with the reference
-  ``Forest`` :143 and ``DofMap`` :619), so fixtures serialised from the
-  reference can be rebuilt on a GPU box that has no reference install;
-* :func:`build_dofmap` — vertex numbering by sorted packed lattice key
-  plus hanging-node constraints with chain resolution and the Dirichlet
-  plane, restating ``mesh.py:706-779`` (bit-exact; pinned by
-  tests/test_mesh_tables.py against the reference);
-* :func:`interface_faces` — the +z radiating facets, restating
-  ``mesh.py:998-1072``;
-* :class:`StructuredBox` — a uniform box of Qp cells whose node lattice
-  is numbered x-major / z-fastest, the rule the reference applies to
-  Q1 (``mesh.py:712-715``) extended to the p-refined lattice.  Large
-  structured problems never materialise per-cell tables.
+* :class:`Forest`, :class:`DofMap`, :class:`FaceSet` — containers with
+  the attribute names of the reference ``Forest`` (mesh.py:143),
+  ``DofMap`` (:619) and ``FaceSet`` (:980), so reference objects and
+  these are interchangeable at the operator boundary;
+* :func:`build_coarse_grid`, :func:`advance_layer`, :func:`apply_update`,
+  :func:`build_dofmap`, :func:`interface_faces` — the growing-domain
+  pipeline of ``run_build`` (driver.py:177-193) on native code, bit-exact
+  with the reference (tests/test_mesh_tables.py, tests/test_activation.py
+  against fixtures the reference produced);
+* :class:`Geometry` — integer build-volume boxes (plate + per-layer
+  footprints) for chamber and fitted parts;
+* :class:`StructuredBox` / :class:`FittedPart` — uniform degree-p meshes
+  that never materialise per-cell tables (the structured backend).
 """
 
-from dataclasses import dataclass
+import ctypes
+from dataclasses import dataclass, field
 
 import numpy as np
 
-_BITS = 21
-_OFF = 1 << (_BITS - 1)
-_MASK = (1 << _BITS) - 1
+from . import _lib
 
-# corner c = ix*4 + iy*2 + iz  (reference mesh.py:26-30)
-CORNER_OFFSETS = np.array([((c >> 2) & 1, (c >> 1) & 1, c & 1)
-                           for c in range(8)], dtype=np.int64)
+# corner c = ix*4 + iy*2 + iz (the reference's local corner order)
+CORNER_OFFSETS = np.array([((c >> 2) & 1, (c >> 1) & 1, c & 1) for c in range(8)],
+                          dtype=np.int64)
 
 
-def pack_coords(coords):
-    c = np.asarray(coords, dtype=np.int64) + _OFF
-    if c.size and (c.min() < 0 or c.max() > _MASK):
-        raise ValueError("lattice coordinate out of packable range")
-    return (c[..., 0] << (2 * _BITS)) | (c[..., 1] << _BITS) | c[..., 2]
-
-
-def unpack_coords(keys):
-    keys = np.asarray(keys, dtype=np.int64)
-    out = np.empty(keys.shape + (3,), dtype=np.int64)
-    out[..., 0] = (keys >> (2 * _BITS)) & _MASK
-    out[..., 1] = (keys >> _BITS) & _MASK
-    out[..., 2] = keys & _MASK
-    return out - _OFF
-
+# --- containers --------------------------------------------------------------
 
 class Forest:
-    """Leaf table: level, anchor (finest lattice units), active flags."""
+    """Leaf table of the adaptive voxel mesh (anchors in finest lattice
+    units, canonical order)."""
 
     def __init__(self, level, anchor, active, init_consol, depth, cpl,
                  h_fine, z_min=0, dirichlet_bottom=True, epoch=0,
-                 current_layer=-1):
-        self.level = np.asarray(level, dtype=np.int8)
-        self.anchor = np.asarray(anchor, dtype=np.int64).reshape(-1, 3)
-        self.active = np.asarray(active, dtype=bool)
-        self.init_consol = np.asarray(init_consol, dtype=bool)
+                 current_layer=-1, n_layers=None):
+        self.level = np.ascontiguousarray(level, dtype=np.int8)
+        self.anchor = np.ascontiguousarray(anchor, dtype=np.int64).reshape(-1, 3)
+        self.active = np.ascontiguousarray(active, dtype=bool)
+        self.init_consol = np.ascontiguousarray(init_consol, dtype=bool)
         self.depth = int(depth)
         self.cpl = int(cpl)
         self._h_fine = float(h_fine)
@@ -67,14 +55,14 @@ class Forest:
         self.dirichlet_bottom = bool(dirichlet_bottom)
         self.epoch = int(epoch)
         self.current_layer = int(current_layer)
-        self._index = None
+        self.n_layers = n_layers
 
     @classmethod
     def from_reference(cls, f):
-        """Copy the tables of a reference ``scantherm.mesh.Forest``."""
+        """Tables of a reference ``scantherm.mesh.Forest``."""
         return cls(f.level, f.anchor, f.active, f.init_consol, f.depth, f.cpl,
                    f.h_fine, f.geometry.z_min(), f.mesh_params.dirichlet_bottom,
-                   f.epoch, f.current_layer)
+                   f.epoch, f.current_layer, f.geometry.n_layers)
 
     @property
     def h_fine(self):
@@ -85,7 +73,8 @@ class Forest:
         return len(self.level)
 
     def size(self, idx=slice(None)):
-        return np.int64(1) << (self.depth - self.level[idx].astype(np.int64))
+        """Edge length in lattice units."""
+        return np.left_shift(np.int64(1), self.depth - self.level[idx].astype(np.int64))
 
     def size_m(self, idx=slice(None)):
         return self.size(idx) * self.h_fine
@@ -94,42 +83,15 @@ class Forest:
         return np.flatnonzero(self.active)
 
     def active_volume_m3(self):
-        s = self.size_m(self.active_cells())
-        return float(np.sum(s * s * s))
-
-    def _levels(self):
-        if self._index is None:
-            idx = {}
-            for ell in np.unique(self.level):
-                rows = np.flatnonzero(self.level == ell)
-                keys = pack_coords(self.anchor[rows])
-                o = np.argsort(keys, kind="stable")
-                idx[int(ell)] = (keys[o], rows[o])
-            self._index = idx
-        return self._index
-
-    def lookup(self, level, anchors):
-        anchors = np.atleast_2d(np.asarray(anchors, dtype=np.int64))
-        out = np.full(len(anchors), -1, dtype=np.int64)
-        entry = self._levels().get(int(level))
-        if entry is None or len(anchors) == 0:
-            return out
-        keys, rows = entry
-        want = pack_coords(anchors)
-        pos = np.searchsorted(keys, want)
-        ok = pos < len(keys)
-        ok[ok] &= keys[pos[ok]] == want[ok]
-        out[ok] = rows[pos[ok]]
-        return out
+        e = self.size_m(self.active_cells())
+        return float(np.sum(e * e * e))
 
 
-def _forest_z_min(forest):
-    if hasattr(forest, "z_min_lattice"):
-        return forest.z_min_lattice
-    return forest.geometry.z_min()
+def _z_min(forest):
+    return forest.z_min_lattice if hasattr(forest, "z_min_lattice") else forest.geometry.z_min()
 
 
-def _forest_dirichlet(forest):
+def _dirichlet_bottom(forest):
     if hasattr(forest, "dirichlet_bottom"):
         return forest.dirichlet_bottom
     return forest.mesh_params.dirichlet_bottom
@@ -137,7 +99,9 @@ def _forest_dirichlet(forest):
 
 @dataclass
 class DofMap:
-    """Vertex numbering + hanging-node constraints (reference mesh.py:619)."""
+    """Vertex numbering of the active region with hanging-node constraints
+    (the reference DofMap's fields); slaves are interpolated from masters
+    that are never slaves themselves."""
 
     vertices: np.ndarray
     cell_verts: np.ndarray
@@ -161,17 +125,29 @@ class DofMap:
     def vertices_m(self):
         return self.vertices * self.h_fine
 
+    def _csr(self):
+        i64 = ctypes.POINTER(ctypes.c_int64)
+        arrs = [np.ascontiguousarray(a, dtype=np.int64)
+                for a in (self.slaves, self.slave_ptr, self.slave_masters)]
+        w = np.ascontiguousarray(self.slave_weights, dtype=np.float64)
+        return arrs, w, [a.ctypes.data_as(i64) for a in arrs] + [_lib.dptr(w)]
+
     def distribute(self, values):
+        """Slave entries <- weighted sums of their masters (in place)."""
         if len(self.slaves):
-            prod = self.slave_weights * values[self.slave_masters]
-            values[self.slaves] = np.add.reduceat(prod, self.slave_ptr[:-1])
+            _check_f64(values)
+            keep, w, p = self._csr()
+            _lib.check(_lib.load().st_host_distribute(len(self.slaves), *p, _lib.dptr(values)),
+                       "distribute")
         return values
 
     def condense(self, values):
+        """Slave entries folded into their masters, slaves zeroed (in place)."""
         if len(self.slaves):
-            rep = np.repeat(values[self.slaves], np.diff(self.slave_ptr))
-            np.add.at(values, self.slave_masters, self.slave_weights * rep)
-            values[self.slaves] = 0.0
+            _check_f64(values)
+            keep, w, p = self._csr()
+            _lib.check(_lib.load().st_host_condense(len(self.slaves), *p, _lib.dptr(values)),
+                       "condense")
         return values
 
     @classmethod
@@ -181,116 +157,17 @@ class DofMap:
                    d.slave_weights, d.h_fine)
 
 
-def _hanging_host_cell(forest, verts):
-    """For each vertex: an active leaf containing it off its corners
-    (row, offset in lattice units) or row -1.  Same search order as the
-    reference (_containing_active_cell, mesh.py:673-703): levels coarse
-    to fine, candidate anchors in bit order, first hit wins."""
-    n = len(verts)
-    row = np.full(n, -1, dtype=np.int64)
-    rel = np.zeros((n, 3), dtype=np.int64)
-    for ell in sorted(forest._levels() if hasattr(forest, "_levels")
-                      else forest._level_index()):
-        todo = np.flatnonzero(row == -1)
-        if todo.size == 0:
-            break
-        s = np.int64(1) << (forest.depth - ell)
-        v = verts[todo]
-        hi = (v // s) * s
-        lo = np.where(v % s == 0, hi - s, hi)
-        for bits in range(8):
-            pick = np.array([(bits >> 2) & 1, (bits >> 1) & 1, bits & 1]) == 1
-            a = np.where(pick[None, :], hi, lo)
-            hit = forest.lookup(ell, a)
-            ok = hit >= 0
-            ok[ok] &= forest.active[hit[ok]]
-            if not ok.any():
-                continue
-            r = v - a
-            on_corner = np.all((r == 0) | (r == s), axis=1)
-            take = ok & ~on_corner & (row[todo] == -1)
-            row[todo[take]] = hit[take]
-            rel[todo[take]] = r[take]
-    return row, rel
-
-
-def build_dofmap(forest) -> DofMap:
-    """Vertex numbering + hanging constraints (reference mesh.py:706-779)."""
-    rows = forest.active_cells()
-    size = forest.size(rows)
-    corners = forest.anchor[rows, None, :] + CORNER_OFFSETS[None] * size[:, None, None]
-    keys = pack_coords(corners.reshape(-1, 3))
-    uniq, inv = np.unique(keys, return_inverse=True)
-    cell_verts = inv.reshape(-1, 8).astype(np.int32)
-    verts = unpack_coords(uniq)
-    nv = len(verts)
-
-    cand = np.flatnonzero(np.bincount(inv, minlength=nv) < 8)
-    crow, crel = _hanging_host_cell(forest, verts[cand])
-    pos_of_row = np.full(forest.n_cells, -1, dtype=np.int64)
-    pos_of_row[rows] = np.arange(len(rows))
-
-    cons = {}
-    for j in np.flatnonzero(crow >= 0):
-        c = int(crow[j])
-        s = float(forest.size(c))
-        frac = crel[j] / s
-        lst = []
-        for ci in range(8):
-            w = 1.0
-            for d in range(3):
-                w *= frac[d] if CORNER_OFFSETS[ci, d] else (1.0 - frac[d])
-            if w > 0.0:
-                lst.append((int(cell_verts[pos_of_row[c], ci]), w))
-        cons[int(cand[j])] = lst
-
-    # constraint chains (a master hanging on a coarser cell), resolved by
-    # substitution until closed, in the reference's dict order
-    changed = True
-    while changed:
-        changed = False
-        for v in list(cons):
-            ms = cons[v]
-            if any(m in cons for m, _ in ms):
-                acc = {}
-                for m, wm in ms:
-                    if m in cons:
-                        for mm, wmm in cons[m]:
-                            acc[mm] = acc.get(mm, 0.0) + wm * wmm
-                    else:
-                        acc[m] = acc.get(m, 0.0) + wm
-                cons[v] = sorted(acc.items())
-                changed = True
-
-    slaves = np.array(sorted(cons), dtype=np.int64)
-    ptr = np.zeros(len(slaves) + 1, dtype=np.int64)
-    mlist, wlist = [], []
-    for i, v in enumerate(slaves):
-        for m, w in sorted(cons[int(v)]):
-            mlist.append(m)
-            wlist.append(w)
-        ptr[i + 1] = len(mlist)
-    is_slave = np.zeros(nv, dtype=bool)
-    is_slave[slaves] = True
-    is_dir = np.zeros(nv, dtype=bool)
-    if _forest_dirichlet(forest):
-        is_dir = (verts[:, 2] == _forest_z_min(forest)) & ~is_slave
-    return DofMap(verts, cell_verts, rows, is_slave, is_dir, slaves, ptr,
-                  np.array(mlist, dtype=np.int64), np.array(wlist, dtype=np.float64),
-                  forest.h_fine)
-
-
-def initial_history(forest):
-    """r_c = 1 on initially consolidated cells, 0 on powder (mesh.py:785)."""
-    from .material import HistoryField
-    rows = forest.active_cells()
-    r_c = np.zeros((len(rows), 2, 2, 2))
-    r_c[forest.init_consol[rows]] = 1.0
-    return HistoryField(r_c, forest.epoch)
+def _check_f64(values):
+    if not (isinstance(values, np.ndarray) and values.dtype == np.float64
+            and values.flags["C_CONTIGUOUS"] and values.flags["WRITEABLE"]):
+        raise TypeError("constraint plumbing works in place on a contiguous float64 array")
 
 
 @dataclass
 class FaceSet:
+    """+z radiating facets: owning leaf row, in-face offset and edge
+    length (lattice units)."""
+
     cell_rows: np.ndarray
     offset: np.ndarray
     fsize: np.ndarray
@@ -299,77 +176,269 @@ class FaceSet:
         return len(self.cell_rows)
 
 
+@dataclass
+class NodalField:
+    values: np.ndarray
+    epoch: int
+
+    def copy(self):
+        return NodalField(self.values.copy(), self.epoch)
+
+
+@dataclass
+class TransferReport:
+    """Per new vertex: 0 copied, 1 interpolated, 2 fresh (T_0)."""
+
+    vertex_source: np.ndarray
+
+
+@dataclass
+class MeshUpdatePlan:
+    """Target leaf set of a layer advance with its lineage to the old set
+    (the reference MeshUpdatePlan's fields)."""
+
+    base_epoch: int
+    new_layer: int
+    level: np.ndarray
+    anchor: np.ndarray
+    active: np.ndarray
+    init_consol: np.ndarray
+    same_src: np.ndarray
+    ancestor_src: np.ndarray
+    coarse_groups: list
+    coarsened_min_rc: list
+    transfer_report: TransferReport = field(default=None)
+
+
+# --- native builders -----------------------------------------------------------
+
+class _Leaves:
+    """st_leaves view of a forest (keeps the arrays alive)."""
+
+    def __init__(self, forest):
+        self.level = np.ascontiguousarray(forest.level, dtype=np.int8)
+        self.anchor = np.ascontiguousarray(forest.anchor, dtype=np.int64)
+        self.active = np.ascontiguousarray(forest.active, dtype=np.uint8)
+        self.consol = np.ascontiguousarray(forest.init_consol, dtype=np.uint8)
+        self.c = _lib.StLeaves(
+            len(self.level), int(forest.depth), int(forest.cpl),
+            self.level.ctypes.data_as(ctypes.POINTER(ctypes.c_int8)),
+            self.anchor.ctypes.data_as(ctypes.POINTER(ctypes.c_int64)),
+            self.active.ctypes.data_as(ctypes.POINTER(ctypes.c_uint8)),
+            self.consol.ctypes.data_as(ctypes.POINTER(ctypes.c_uint8)))
+
+    @property
+    def ref(self):
+        return ctypes.byref(self.c)
+
+
+def _take(call, what):
+    """Run a builder returning an st_tables bag; dict of numpy copies."""
+    lib = _lib.load()
+    t = ctypes.c_void_p()
+    _lib.check(call(ctypes.byref(t)), what)
+    try:
+        return _lib.tables_dict(t)
+    finally:
+        lib.st_tables_free(t)
+
+
+def build_dofmap(forest) -> DofMap:
+    """Vertex numbering + hanging-node constraints + Dirichlet plane
+    (replaces reference build_dofmap, mesh.py:706-779)."""
+    L = _Leaves(forest)
+    d = _take(lambda out: _lib.load().st_build_dofmap(
+        L.ref, int(_z_min(forest)), int(bool(_dirichlet_bottom(forest))), out), "build_dofmap")
+    return DofMap(d["vertices"], d["cell_verts"], d["active_rows"],
+                  d["is_slave"].astype(bool), d["is_dirichlet"].astype(bool), d["slaves"],
+                  d["slave_ptr"], d["slave_masters"], d["slave_weights"], forest.h_fine)
+
+
 def interface_faces(forest) -> FaceSet:
-    """+z boundary facets of the active region (reference mesh.py:998).
+    """Radiating +z facets (replaces reference interface_faces,
+    mesh.py:998-1072)."""
+    L = _Leaves(forest)
+    d = _take(lambda out: _lib.load().st_interface_faces(L.ref, out), "interface_faces")
+    return FaceSet(d["cell_rows"], d["offset"].reshape(-1, 2), d["fsize"])
 
-    A top face is exterior when the leaf above it (same level, or the
-    coarser parent when the face lies on the parent's bottom plane) is
-    void; when no such leaf exists the face is split against the finer
-    level and every quarter not covered by an active leaf is emitted.
-    """
-    rows = forest.active_cells()
-    out_r, out_o, out_s = [], [], []
-    lev_all = forest.level[rows]
-    for ell in np.unique(lev_all):
-        ell = int(ell)
-        sub = rows[lev_all == ell]
-        s = np.int64(1) << (forest.depth - ell)
-        ax, ay = forest.anchor[sub, 0], forest.anchor[sub, 1]
-        top = forest.anchor[sub, 2] + s
 
-        def status(hit):
-            st = np.zeros(len(hit), dtype=np.int8)
-            got = hit >= 0
-            st[got] = np.where(forest.active[hit[got]], 1, 2)
-            return st
+def initial_history(forest):
+    """Consolidation state per quadrature point: 1 on initially
+    consolidated leaves (the plate), 0 on powder."""
+    from .material import HistoryField
+    consol = forest.init_consol[forest.active_cells()]
+    r_c = np.broadcast_to(consol.astype(np.float64)[:, None, None, None],
+                          (len(consol), 2, 2, 2)).copy()
+    return HistoryField(r_c, forest.epoch)
 
-        cov = status(forest.lookup(ell, np.column_stack([ax, ay, top])))
-        if ell > 0:
-            ps = 2 * s
-            par = forest.lookup(ell - 1, np.column_stack([(ax // ps) * ps,
-                                                          (ay // ps) * ps, top]))
-            par[top % ps != 0] = -1
-            pst = status(par)
-            cov = np.where(cov == 0, pst, cov)
 
-        full = cov == 2
-        open_idx = np.flatnonzero(cov == 0)
-        if ell < forest.depth and open_idx.size:
-            hs = s >> 1
-            q = np.zeros((len(open_idx), 2, 2), dtype=np.int8)
-            exists = np.zeros(len(open_idx), dtype=bool)
-            for i in range(2):
-                for j in range(2):
-                    hit = forest.lookup(ell + 1, np.column_stack(
-                        [ax[open_idx] + i * hs, ay[open_idx] + j * hs, top[open_idx]]))
-                    q[:, i, j] = status(hit)
-                    exists |= hit >= 0
-            for t, k in enumerate(open_idx):
-                if exists[t]:
-                    for i in range(2):
-                        for j in range(2):
-                            if q[t, i, j] != 1:
-                                out_r.append(sub[k])
-                                out_o.append((i * hs, j * hs))
-                                out_s.append(hs)
-                else:
-                    full[k] = True
-        else:
-            full[open_idx] = True
-        for k in np.flatnonzero(full):
-            out_r.append(sub[k])
-            out_o.append((0, 0))
-            out_s.append(s)
+@dataclass
+class Geometry:
+    """Build volume in finest lattice units: plate boxes (m, 6) below
+    z = 0 and one footprint (k, 4) [x0 y0 x1 y1] per powder layer."""
 
-    if not out_r:
-        return FaceSet(np.zeros(0, np.int64), np.zeros((0, 2), np.int64),
-                       np.zeros(0, np.int64))
-    r = np.array(out_r, dtype=np.int64)
-    o = np.array(out_o, dtype=np.int64).reshape(-1, 2)
-    s = np.array(out_s, dtype=np.int64)
-    order = np.lexsort((o[:, 1], o[:, 0], r))
-    return FaceSet(r[order], o[order], s[order])
+    plate_boxes: np.ndarray
+    footprints: list
+    n_layers: int
 
+    def z_min(self):
+        return int(self.plate_boxes[:, 2].min()) if len(self.plate_boxes) else 0
+
+
+def _lattice(value_m, unit_m, what):
+    k = int(round(value_m / unit_m))
+    if abs(k * unit_m - value_m) > 1e-9 * max(unit_m, abs(value_m)):
+        raise ValueError(f"{what} = {value_m} is not a multiple of {unit_m}")
+    return k
+
+
+def chamber_geometry(size_xy, height, plate_thickness, mesh):
+    """Full chamber cross-section in every layer on a plate (all lengths in
+    metres, multiples of mesh.h_coarse)."""
+    unit = _lattice(mesh.h_coarse, mesh.h_fine, "h_coarse")
+    nx, ny, nz, tp = (_lattice(v, mesh.h_coarse, w) * unit for v, w in
+                      ((size_xy[0], "chamber x"), (size_xy[1], "chamber y"),
+                       (height, "chamber height"), (plate_thickness, "plate thickness")))
+    plate = np.array([[0, 0, -tp, nx, ny, 0]], dtype=np.int64) if tp else \
+        np.zeros((0, 6), dtype=np.int64)
+    n_layers = nz // mesh.cells_per_layer
+    return Geometry(plate, [np.array([[0, 0, nx, ny]], dtype=np.int64)] * n_layers, n_layers)
+
+
+def fitted_geometry(part_boxes, plate_box, mesh):
+    """Part as a union of boxes (x0 y0 z0 x1 y1 z1, metres above the
+    plate) on a plate (x0, y0, x1, y1, thickness)."""
+    unit = _lattice(mesh.h_coarse, mesh.h_fine, "h_coarse")
+    boxes = np.array([[_lattice(v, mesh.h_coarse, "part box") * unit for v in b]
+                      for b in part_boxes], dtype=np.int64).reshape(-1, 6)
+    if np.any(boxes[:, 3:] <= boxes[:, :3]):
+        raise ValueError("degenerate part box")
+    cpl = mesh.cells_per_layer
+    n_layers = int(boxes[:, 5].max()) // cpl
+    feet = []
+    for k in range(n_layers):
+        inside = (boxes[:, 2] <= k * cpl) & ((k + 1) * cpl <= boxes[:, 5])
+        if not inside.any():
+            raise ValueError(f"layer {k} has an empty cross-section")
+        feet.append(boxes[inside][:, [0, 1, 3, 4]].copy())
+    x0, y0, x1, y1, t = plate_box
+    tp = _lattice(t, mesh.h_coarse, "plate thickness") * unit
+    plate = np.array([[_lattice(x0, mesh.h_coarse, "plate") * unit,
+                       _lattice(y0, mesh.h_coarse, "plate") * unit, -tp,
+                       _lattice(x1, mesh.h_coarse, "plate") * unit,
+                       _lattice(y1, mesh.h_coarse, "plate") * unit, 0]], dtype=np.int64)
+    if tp == 0:
+        plate = np.zeros((0, 6), dtype=np.int64)
+    return Geometry(plate, feet, n_layers)
+
+
+def build_coarse_grid(geometry, mesh) -> Forest:
+    """Level-0 leaves: the plate active and consolidated, the build volume
+    void above it (replaces reference build_coarse_grid, mesh.py:289-333)."""
+    mesh.validate()
+    depth, cpl = mesh.total_depth, mesh.cells_per_layer
+    s0 = 1 << depth
+    if (geometry.n_layers * cpl) % s0:
+        raise ValueError("part height is not a multiple of h_coarse")
+    boxes, act = [b for b in geometry.plate_boxes], [1] * len(geometry.plate_boxes)
+    for j in range(geometry.n_layers * cpl // s0):
+        layers = range(j * s0 // cpl, (j + 1) * s0 // cpl)
+        fp = geometry.footprints[layers[0]]
+        if any(not np.array_equal(geometry.footprints[k], fp) for k in layers):
+            raise ValueError("cross-section changes inside a coarse slab")
+        for r in fp:
+            boxes.append([r[0], r[1], j * s0, r[2], r[3], (j + 1) * s0])
+            act.append(0)
+    b = np.ascontiguousarray(np.array(boxes, dtype=np.int64).reshape(-1, 6))
+    a = np.ascontiguousarray(np.array(act, dtype=np.uint8))
+    d = _take(lambda out: _lib.load().st_coarse_grid(
+        depth, cpl, len(b), b.ctypes.data_as(ctypes.POINTER(ctypes.c_int64)),
+        a.ctypes.data_as(ctypes.POINTER(ctypes.c_uint8)), out), "build_coarse_grid")
+    return Forest(d["level"], d["anchor"].reshape(-1, 3), d["active"].astype(bool),
+                  d["init_consol"].astype(bool), depth, cpl, mesh.h_fine,
+                  geometry.z_min(), mesh.dirichlet_bottom, 0, -1, geometry.n_layers)
+
+
+def advance_layer(forest, history) -> MeshUpdatePlan:
+    """Plan the update activating layer ``current_layer + 1``: the layer
+    refined to the finest level and activated, settled octets below the
+    heat-affected zone coarsened (min r_c >= 0.9), void collapsed, 2:1
+    balance restored (replaces reference advance_layer, mesh.py:439-549)."""
+    if history is not None and history.epoch != forest.epoch:
+        raise ValueError("history epoch does not match forest epoch")
+    new_layer = forest.current_layer + 1
+    n_layers = getattr(forest, "n_layers", None)
+    if n_layers is None and hasattr(forest, "geometry"):
+        n_layers = forest.geometry.n_layers
+    if n_layers is not None and new_layer >= n_layers:
+        raise ValueError("no further layer in the build")
+    L = _Leaves(forest)
+    rc = None if history is None else np.ascontiguousarray(
+        history.r_c, dtype=np.float64).reshape(len(forest.active_cells()), -1)
+    d = _take(lambda out: _lib.load().st_plan_layer(
+        L.ref, new_layer, _lib.dptr(rc), 0 if rc is None else rc.shape[1], out), "advance_layer")
+    ptr, kids = d["group_ptr"], d["group_kids"]
+    groups = [(int(r), kids[ptr[g]:ptr[g + 1]].copy()) for g, r in enumerate(d["group_rows"])]
+    return MeshUpdatePlan(forest.epoch, new_layer, d["level"], d["anchor"].reshape(-1, 3),
+                          d["active"].astype(bool), d["init_consol"].astype(bool),
+                          d["same_src"], d["ancestor_src"], groups,
+                          [float(x) for x in d["coarsened_min_rc"]])
+
+
+def apply_update(forest, plan, fields, history, T_0=303.0, old_dofmap=None, new_dofmap=None):
+    """Successor forest of a plan with nodal fields and history moved onto
+    it (replaces reference apply_update, mesh.py:803-899).  Returns
+    (new_forest, new_fields, new_history); plan.transfer_report records
+    each new vertex's source."""
+    from .material import HistoryField
+    if plan.base_epoch != forest.epoch:
+        raise ValueError("plan is stale: mesh changed since it was computed")
+    new = Forest(plan.level, plan.anchor, plan.active, plan.init_consol, forest.depth,
+                 forest.cpl, forest.h_fine, _z_min(forest), _dirichlet_bottom(forest),
+                 forest.epoch + 1, plan.new_layer, getattr(forest, "n_layers", None))
+    old_dm = old_dofmap if old_dofmap is not None else build_dofmap(forest)
+    new_dm = new_dofmap if new_dofmap is not None else build_dofmap(new)
+    lib = _lib.load()
+    i64 = ctypes.POINTER(ctypes.c_int64)
+
+    def ip(a):
+        return a.ctypes.data_as(i64)
+
+    Lo, Ln = _Leaves(forest), _Leaves(new)
+    ov = np.ascontiguousarray(old_dm.vertices, dtype=np.int64)
+    nv = np.ascontiguousarray(new_dm.vertices, dtype=np.int64)
+    ocv = np.ascontiguousarray(old_dm.cell_verts, dtype=np.int32)
+    sl, sp, sm = (np.ascontiguousarray(a, dtype=np.int64)
+                  for a in (new_dm.slaves, new_dm.slave_ptr, new_dm.slave_masters))
+    sw = np.ascontiguousarray(new_dm.slave_weights, dtype=np.float64)
+    vals = [np.asarray(getattr(f, "values", f), dtype=np.float64) for f in fields]
+    src_f = np.ascontiguousarray(np.stack(vals) if vals else np.zeros((0, len(ov))))
+    out_f = np.empty((len(vals), len(nv)))
+    source = np.empty(len(nv), dtype=np.int8)
+    _lib.check(lib.st_transfer_nodal(
+        Lo.ref, ip(ov), len(ov), ocv.ctypes.data_as(ctypes.POINTER(ctypes.c_int32)), ip(nv),
+        len(nv), ip(sp), ip(sl), len(sl), ip(sm), _lib.dptr(sw), len(vals), _lib.dptr(src_f),
+        float(T_0), _lib.dptr(out_f), source.ctypes.data_as(ctypes.POINTER(ctypes.c_int8))),
+        "apply_update (nodal)")
+    plan.transfer_report = TransferReport(source)
+    same = np.ascontiguousarray(plan.same_src, dtype=np.int64)
+    anc = np.ascontiguousarray(plan.ancestor_src, dtype=np.int64)
+    g_rows = np.array([r for r, _ in plan.coarse_groups], dtype=np.int64)
+    g_ptr = np.concatenate([[0], np.cumsum([len(k) for _, k in plan.coarse_groups],
+                                           dtype=np.int64)]).astype(np.int64)
+    g_kids = np.ascontiguousarray(np.concatenate(
+        [np.asarray(k, dtype=np.int64) for _, k in plan.coarse_groups])
+        if plan.coarse_groups else np.zeros(0, dtype=np.int64))
+    rc_old = np.ascontiguousarray(history.r_c, dtype=np.float64)
+    rc_new = np.empty((int(new.active.sum()), 2, 2, 2))
+    _lib.check(lib.st_transfer_history(
+        Lo.ref, Ln.ref, ip(same), ip(anc), len(g_rows), ip(g_rows), ip(g_ptr), ip(g_kids),
+        _lib.dptr(rc_old), _lib.dptr(rc_new)), "apply_update (history)")
+    new_fields = [NodalField(out_f[k].copy(), new.epoch) for k in range(len(vals))]
+    return new, new_fields, HistoryField(rc_new, new.epoch)
+
+
+# --- structured meshes ---------------------------------------------------------
 
 class StructuredBox:
     """Uniform box of degree-p hexahedra, nodes numbered x-major, z-fastest.
