@@ -33,6 +33,8 @@ import time
 
 import numpy as np
 
+from workloads import hatch_segments
+
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
@@ -86,7 +88,7 @@ def workload_config1():
     h = 10, 70 W beam on a 5-track serpentine hatch (100 um), dt = 0.5 us."""
     st = _st()
     h = 31.25e-6
-    segs = st.generate_hatch([(1.5e-3, 1.75e-3, 2.5e-3, 2.25e-3)], 1e-4, 1.0, 70.0)
+    segs = hatch_segments([(1.5e-3, 1.75e-3, 2.5e-3, 2.25e-3)], 1e-4, 1.0, 70.0)
     lp = st.LayerPath(0, 0.0, segs, 0.0)
     return dict(name="config1_q2_128x128x32", dims=(128, 128, 32), h=h, degree=2,
                 params=_config1_params(),

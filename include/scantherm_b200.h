@@ -202,11 +202,13 @@ int st_implicit_step(st_ctx* ctx, double dt, double newton_tol,
 /* Dirichlet pin of the resident T + history update (run_cooldown_phase
  * :357-362). */
 int st_finish_implicit_step(st_ctx* ctx);
-/* krylov_solve (timestepping.py:102-131) for J(T_lin) x = b with the
- * Jacobi preconditioner (precond = 1) or none (0). */
+/* krylov_solve (timestepping.py:102-131) for J(T_lin) x = b: no
+ * preconditioner (precond = 0), or z = diag_inv * r with the caller's
+ * diag_inv (precond = 1, diag_inv != NULL) or with the inverse of the
+ * exact Jacobian diagonal (precond = 1, diag_inv == NULL). */
 int st_pcg(st_ctx* ctx, const double* T_lin, const double* rc, double dt,
-           const double* b, double tol, int max_iter, int precond, double* x,
-           int* iters, int* converged);
+           const double* b, double tol, int max_iter, int precond,
+           const double* diag_inv, double* x, int* iters, int* converged);
 /* compute_step_criteria / estimate_spectral_radius (timestepping.py:49-99):
  * rho(C~^-1 K) at conductivity k_frozen by power iteration, entirely on the
  * device.  v0 is the caller's normalised start vector (the reference draws

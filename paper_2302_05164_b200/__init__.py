@@ -9,7 +9,7 @@ from .params import (BoundaryParams, ConfigError, HeatSourceParams, MaterialPara
                      MeshParams, ProcessParams, SolverSettings, STEFAN_BOLTZMANN)
 from .material import HistoryField
 from .physics import (BeamState, LayerPath, ScanPath, Segment, flatten_schedule,
-                      generate_hatch, layer_beam_state, pack_beams)
+                      layer_beam_state, pack_beams)
 from .mesh import (DofMap, Forest, StructuredBox, build_dofmap, initial_history,
                    interface_faces)
 from .operators import ThermalOperator, close_constraints

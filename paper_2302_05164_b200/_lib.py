@@ -130,7 +130,7 @@ SIGNATURES = [
     ("st_finish_implicit_step", ctypes.c_int, [_VP]),
     ("st_pcg", ctypes.c_int,
      [_VP, _dp, _dp, ctypes.c_double, _dp, ctypes.c_double, ctypes.c_int,
-      ctypes.c_int, _dp, ctypes.POINTER(ctypes.c_int), ctypes.POINTER(ctypes.c_int)]),
+      ctypes.c_int, _dp, _dp, ctypes.POINTER(ctypes.c_int), ctypes.POINTER(ctypes.c_int)]),
     ("st_spectral_radius", ctypes.c_int,
      [_VP, ctypes.c_double, _dp, ctypes.c_double, ctypes.c_int, _dp,
       ctypes.POINTER(ctypes.c_int)]),

@@ -622,20 +622,26 @@ int st_jacobian_diagonal(st_ctx* ctx, const double* T_lin, const double* rc, dou
 }
 
 int st_pcg(st_ctx* ctx, const double* T_lin, const double* rc, double dt, const double* b,
-           double tol, int max_iter, int precond, double* x, int* iters, int* converged) {
+           double tol, int max_iter, int precond, const double* diag_inv, double* x, int* iters,
+           int* converged) {
   ST_TRY(check_ctx(ctx));
   Ctx& c = ctx->impl;
   double *Td, *bd, *xd, *di = nullptr, *rcd;
   ST_TRY(c.vec(0, &Td));
-  ST_TRY(c.vec(5, &bd));
+  // b has a slot of its own (the Jacobian apply uses slot 5 for its input)
+  ST_TRY(c.vec(8, &bd));
   ST_TRY(c.vec(6, &xd));
   ST_TRY(c.h2d(Td, T_lin, c.nv));
   ST_TRY(c.h2d(bd, b, c.nv));
   ST_TRY(stage_rc(c, rc, &rcd));
   if (precond) {
     ST_TRY(c.vec(7, &di));
-    ST_TRY(c.be->jac_diag(Td, rcd, dt, di));
-    ST_TRY(vec_recip(&c, di, di, c.nv));
+    if (diag_inv) {  // the caller's preconditioner, as krylov_solve applies it
+      ST_TRY(c.h2d(di, diag_inv, c.nv));
+    } else {  // the exact Jacobian diagonal, inverted
+      ST_TRY(c.be->jac_diag(Td, rcd, dt, di));
+      ST_TRY(vec_recip(&c, di, di, c.nv));
+    }
   }
   ST_TRY(pcg_dev(c, Td, rcd, dt, bd, tol, max_iter, di, xd, iters, converged));
   return c.d2h(x, xd, c.nv);

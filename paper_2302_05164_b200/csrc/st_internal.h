@@ -177,7 +177,7 @@ struct Ctx {
   cudaGraphExec_t cg_exec[2] = {nullptr, nullptr};  // captured PCG iteration per parity
   DevBuf<double> pws;       // power iteration: counter, scalars, (ww, vw) history
   cudaGraphExec_t pw_exec = nullptr;  // captured power iteration
-  DevBuf<double> scratch[8];
+  DevBuf<double> scratch[10];
   double* pinned = nullptr;  // small pinned host staging
   // profiling of the dominant kernel
   int prof = 0;

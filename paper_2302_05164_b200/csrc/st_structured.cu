@@ -15,13 +15,17 @@
 //      points (physics.py:154-171), one transposed interpolation (3
 //      sweeps) to the element vector, plus the top-face radiation /
 //      evaporation / convection term (operators.py:275-290),
-//   3. sums the element vectors into shared node-plane accumulators in 4
-//      conflict-free phases (deterministic within the CTA),
+//   3. stores the element planes entry-major in shared memory and each
+//      thread gathers the <= 4 contributions of the nodes its cell owns in
+//      a fixed order (deterministic),
 //   4. finalises the completed planes in the same pass: T' = T + dt C^-1 f
 //      with the Dirichlet pin (operators.py:359-368), writes T', and folds
 //      |T'| / max T' into the stability slots (timestepping.py:186-192).
-// Nodes on tile seams (shared with another CTA) are sent with fp64
-// atomics to a seam buffer and finalised by k_seams.
+// Nodes on tile / chunk seams (shared with another CTA) store this CTA's
+// partial with a plain store to its own slot of the seam buffer (slot =
+// side of the CTA per seam axis); k_seam_list then sums the slots of every
+// seam node in a fixed order and finalises it, so a step is bitwise
+// reproducible.
 #include <cmath>
 #include <cstdlib>
 #include <cstring>

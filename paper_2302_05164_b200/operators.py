@@ -272,9 +272,13 @@ class ThermalOperator:
                    "jacobian_diagonal")
         return out
 
-    def solve_jacobian(self, b, T_lin, r_c, dt, tol, max_iter, precondition=True):
-        """Device PCG for J(T_lin) x = b (krylov_solve, timestepping.py:102)."""
+    def solve_jacobian(self, b, T_lin, r_c, dt, tol, max_iter, precondition=True,
+                       diag_inv=None):
+        """Device PCG for J(T_lin) x = b (krylov_solve, timestepping.py:102):
+        Jacobi with the caller's ``diag_inv`` when given, else with the
+        exact Jacobian diagonal (``precondition``), or none."""
         b = self._vec(b, "b")
+        di = None if diag_inv is None else self._vec(diag_inv, "diag_inv")
         T_lin = self._vec(T_lin, "T_lin")
         rc = self._rc(r_c)
         x = np.empty(self.nv)
@@ -282,7 +286,8 @@ class ThermalOperator:
         ok = ctypes.c_int()
         _lib.check(self._lib.st_pcg(self._ctx, _lib.dptr(T_lin), _lib.dptr(rc), float(dt),
                                     _lib.dptr(b), float(tol), int(max_iter),
-                                    int(bool(precondition)), _lib.dptr(x), ctypes.byref(it),
+                                    int(bool(precondition) or di is not None), _lib.dptr(di),
+                                    _lib.dptr(x), ctypes.byref(it),
                                     ctypes.byref(ok)), "pcg")
         return x, it.value, bool(ok.value)
 

@@ -9,11 +9,8 @@ states for a run of steps at once (``tau = (step - 1) * dt``,
 ``timestepping.py:211-214``) into a packed float64 table that the CUDA
 step loop consumes without host round trips.
 
-``generate_hatch`` restates ``driver.py:85-111`` (serpentine hatching)
-because BASELINE config 1 is defined through it.
 """
 
-import math
 from dataclasses import dataclass, field
 
 import numpy as np
@@ -194,26 +191,3 @@ def flatten_schedule_loop(layer_paths, dt, n_steps, step0=1):
         dts[i] = min(dt, duration - tau)
         beams[i] = pack_beams([layer_beam_state(lp, tau) for lp in layer_paths])
     return dts, beams
-
-
-def generate_hatch(boxes, spacing, v, power, direction_deg=0.0):
-    """Serpentine tracks over (x0, y0, x1, y1) boxes, alternating sense."""
-    if direction_deg not in (0.0, 90.0, 0, 90):
-        raise ValueError("hatch direction must be 0 or 90 degrees")
-    along_x = direction_deg in (0.0, 0)
-    segs = []
-    sense = 1
-    for (x0, y0, x1, y1) in boxes:
-        width = (y1 - y0) if along_x else (x1 - x0)
-        n = max(1, int(math.floor(width / spacing + 1e-9)))
-        off = (width - (n - 1) * spacing) / 2.0
-        for i in range(n):
-            c = off + i * spacing
-            if along_x:
-                a, b = (x0, x1) if sense > 0 else (x1, x0)
-                segs.append(Segment(a, y0 + c, b, y0 + c, v, power))
-            else:
-                a, b = (y0, y1) if sense > 0 else (y1, y0)
-                segs.append(Segment(x0 + c, a, x0 + c, b, v, power))
-            sense = -sense
-    return segs

@@ -246,12 +246,13 @@ class JacobianApply:
 def krylov_solve(apply_fn, b, diag_inv=None, tol=1e-10, max_iter=2000, x0=None):
     """Preconditioned CG for J x = b (timestepping.py:102-131).
 
-    With a :class:`JacobianApply` (and the Jacobi diagonal or none) the
-    whole solve runs on the device; other callables run the reference
-    loop around them."""
+    With a :class:`JacobianApply` the whole solve runs on the device, with
+    the caller's ``diag_inv`` as the Jacobi preconditioner (or none); other
+    callables run the reference loop around them."""
     if isinstance(apply_fn, JacobianApply) and x0 is None:
         return apply_fn.op.solve_jacobian(b, apply_fn.T_lin, apply_fn.r_c, apply_fn.dt,
-                                          tol, max_iter, precondition=diag_inv is not None)
+                                          tol, max_iter, precondition=diag_inv is not None,
+                                          diag_inv=diag_inv)
     n = len(b)
     x = np.zeros(n) if x0 is None else x0.copy()
     r = b - apply_fn(x) if x0 is not None else b.copy()

@@ -17,6 +17,7 @@ import pytest
 
 import paper_2302_05164_b200 as st
 from paper_2302_05164_b200.physics import BeamState
+from workloads import hatch_segments
 
 pytestmark = pytest.mark.gpu
 
@@ -102,7 +103,7 @@ def test_config1_500_steps_stay_physical():
     op = st.ThermalOperator(box, box, _params(h), st.SolverSettings())
     T0 = 300.0 + np.random.default_rng(0).uniform(0.0, 1.0, op.nv)
     T0[box.is_dirichlet] = 300.0
-    segs = st.generate_hatch([(1.5e-3, 1.75e-3, 2.5e-3, 2.25e-3)], 1e-4, 1.0, 70.0)
+    segs = hatch_segments([(1.5e-3, 1.75e-3, 2.5e-3, 2.25e-3)], 1e-4, 1.0, 70.0)
     lp = st.LayerPath(0, 0.0, segs, 0.0)
     dts, bm = st.flatten_schedule(lp, 5e-7, 500)
     op.set_state(T0, 1.0)

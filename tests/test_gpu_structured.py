@@ -150,8 +150,9 @@ def test_structured_determinism_run_to_run():
     box, op, orc, T, rc, beams, tb = _setup(2, seed=21)
     a = op.evaluate_rhs(T, rc, beams)
     b = op.evaluate_rhs(T, rc, beams)
-    # seams are combined with atomics: order noise only
-    assert rel(a, b) < 1e-15
+    # seam partials are plain stores to per-CTA slots summed by k_seam_list
+    # in a fixed order: bitwise reproducible
+    assert np.array_equal(a, b)
 
 
 @pytest.mark.parametrize("kernel", ["march", "slab"])
