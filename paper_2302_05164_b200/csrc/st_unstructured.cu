@@ -476,7 +476,9 @@ __global__ void k_step_nodes(int64_t nv, NodeTab nt, const double* E, const doub
       ci = 1.0 / c_atomic[v];
     else
       ci = cinv[v];
-    out = T[v] + dt * (ci * f);
+    // T + dt (C^-1 f) with the reference's three roundings (no FMA), so a
+    // step equals the host composition of the same pieces bit for bit
+    out = __dadd_rn(T[v], __dmul_rn(dt, __dmul_rn(ci, f)));
     if (nt.is_dir[v]) out = T_inf;
     Tout[v] = out;
   }
@@ -491,9 +493,26 @@ __global__ void k_distribute(int64_t ns, const int64_t* slaves, const int64_t* p
   pdl_wait_release();
   int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (i >= ns) return;
-  double acc = 0.0;
-  for (int64_t p = ptr[i]; p < ptr[i + 1]; p++) acc += w[p] * v[masters[p]];
-  v[slaves[i]] = acc;
+  // the rounding of the reference's segmented sum (numpy add.reduceat:
+  // first product, plus the rest summed from zero, 8-lane pairwise blocks
+  // beyond 8 terms), every product rounded on its own
+  const int64_t b = ptr[i], e = ptr[i + 1];
+  if (e <= b) return;
+  const int64_t n = e - b - 1;
+  double rest = 0.0;
+  if (n < 8) {
+    for (int64_t p = b + 1; p < e; p++) rest = __dadd_rn(rest, __dmul_rn(w[p], v[masters[p]]));
+  } else {
+    double r[8];
+    for (int j = 0; j < 8; j++) r[j] = __dmul_rn(w[b + 1 + j], v[masters[b + 1 + j]]);
+    int64_t k = 8;
+    for (; k < n - (n % 8); k += 8)
+      for (int j = 0; j < 8; j++) r[j] = __dadd_rn(r[j], __dmul_rn(w[b + 1 + k + j], v[masters[b + 1 + k + j]]));
+    rest = __dadd_rn(__dadd_rn(__dadd_rn(r[0], r[1]), __dadd_rn(r[2], r[3])),
+                     __dadd_rn(__dadd_rn(r[4], r[5]), __dadd_rn(r[6], r[7])));
+    for (; k < n; k++) rest = __dadd_rn(rest, __dmul_rn(w[b + 1 + k], v[masters[b + 1 + k]]));
+  }
+  v[slaves[i]] = __dadd_rn(__dmul_rn(w[b], v[masters[b]]), rest);
 }
 
 // atomic-mode condensation (fold slave rows into masters, zero slaves)

@@ -137,6 +137,40 @@ class ThermalOperator:
             "st_ctx_create_unstructured")
         self._faces_cell_pos = cell_pos
 
+    # -- SIMD-batch view of the reference (API parity, not on the device path) --
+    @property
+    def verts8(self):
+        """(n_cells, 8) int64 corner vertex ids (reference attribute)."""
+        if getattr(self.forest, "structured", False):
+            return self.forest.cell_node_ids()
+        return np.asarray(self.dofmap.cell_verts, dtype=np.int64)
+
+    def _batch_colors(self):
+        """First-fit colouring of n_lanes-wide cell batches such that the
+        batches of one colour share no vertex (the reference's CPU SIMD
+        scatter schedule, operators.py:136-156).  The device never needs
+        it: its non-deterministic mode scatters with fp64 atomics.  Each
+        vertex carries a bit set of the colours already touching it; a
+        batch takes the lowest colour absent from the union of its
+        vertices' sets."""
+        if getattr(self, "_colors", None) is not None:
+            return self._colors
+        lanes = int(getattr(self.settings, "n_lanes", 8))
+        v8 = self.verts8
+        used = [0] * int(self.nv)
+        groups = {}
+        for start in range(0, len(v8), lanes):
+            verts = np.unique(v8[start:start + lanes]).tolist()
+            taken = 0
+            for v in verts:
+                taken |= used[v]
+            color = (~taken & (taken + 1)).bit_length() - 1
+            for v in verts:
+                used[v] |= 1 << color
+            groups.setdefault(color, []).append(slice(start, min(start + lanes, len(v8))))
+        self._colors = [groups[c] for c in sorted(groups)]
+        return self._colors
+
     def close(self):
         if getattr(self, "_ctx", None) is not None and self._ctx.value:
             self._lib.st_ctx_destroy(self._ctx)
