@@ -35,3 +35,117 @@ def hatch_segments(boxes, spacing, v, power, direction_deg=0.0):
             out.append(Segment(s, c, e, c, v, power) if across else Segment(c, s, c, e, v, power))
         parity = (parity + n) % 2
     return out
+
+
+# --- BASELINE configs[3]: growing domain with cool-down ------------------------
+
+def config3_setup(krylov_tol=1e-10):
+    """2 x 2 mm chamber on a 2 mm plate, Q1, h_coarse 80 um / one refinement
+    level / 40 um layers, ten layers; reference default material and
+    boundary, 70 W beam at 1 m/s; backward-Euler cool-down at 1 ms with
+    Jacobi-PCG."""
+    import paper_2302_05164_b200 as st
+    from paper_2302_05164_b200.mesh import chamber_geometry
+    mesh = st.MeshParams(h_coarse=80e-6, n_refine=1, h_powder=40e-6)
+    geo = chamber_geometry((2e-3, 2e-3), 10 * 40e-6, 2e-3, mesh)
+    params = st.ProcessParams(st.MaterialParams(), st.BoundaryParams(),
+                              st.HeatSourceParams(power=70.0, scan_velocity=1.0), mesh)
+    settings = st.SolverSettings(explicit_cooldown_steps=0, dt_implicit=1e-3,
+                                 krylov_tol=krylov_tol, preconditioner="diagonal")
+    return mesh, geo, params, settings
+
+
+def config3_layer_paths(geo, mesh, d_h=1e-4, v=1.0, power=70.0, cool_time=1.0,
+                        rotation=(0, 90)):
+    """Per layer: the footprint hatched at d_h, direction cycling through
+    ``rotation``, the beam at the layer top (the reference's hatch_path,
+    driver.py:114-130)."""
+    from paper_2302_05164_b200.physics import LayerPath
+    out = []
+    for k in range(geo.n_layers):
+        boxes = geo.footprints[k] * mesh.h_fine
+        segs = hatch_segments(boxes, d_h, v, power, rotation[k % len(rotation)])
+        out.append(LayerPath(k, (k + 1) * mesh.h_powder, segs, cool_time))
+    return out
+
+
+def config3_initial_state(mesh, geo, params, settings):
+    import paper_2302_05164_b200 as st
+    from paper_2302_05164_b200.mesh import build_coarse_grid
+    forest = build_coarse_grid(geo, mesh)
+    history = st.initial_history(forest)
+    dofmap = st.build_dofmap(forest)
+    op = st.ThermalOperator(forest, dofmap, params, settings)
+    return st.SimulationState(forest, dofmap, op, np.full(dofmap.n_vertices, params.T_0),
+                              history)
+
+
+def advance_mesh(state, params, settings):
+    """One deposition step: plan, transfer T and r_c, new tables and a new
+    operator (the reference's _advance_mesh + _rebuild_operator,
+    driver.py:162-194)."""
+    import paper_2302_05164_b200 as st
+    from paper_2302_05164_b200.mesh import NodalField, advance_layer, apply_update
+    plan = advance_layer(state.forest, state.history)
+    forest, fields, history = apply_update(state.forest, plan,
+                                           [NodalField(state.T, state.forest.epoch)],
+                                           state.history, T_0=params.T_0)
+    state.op.close()
+    state.forest, state.T, state.history = forest, fields[0].values, history
+    state.dofmap = st.build_dofmap(forest)
+    state.op = st.ThermalOperator(forest, state.dofmap, params, settings)
+    return plan
+
+
+def run_config3_build(n_layers=None, dt=1e-6, scan_steps=None, cool_time=None,
+                      krylov_tol=1e-10, on_layer=None):
+    """The reference's run_build layer loop (driver.py:197-254) for
+    config 3 on the B200 operator: per layer advance the mesh, step
+    criteria, the scan (dt = 1 us) and the backward-Euler cool-down.
+    ``scan_steps`` / ``cool_time`` truncate a layer for quick runs.
+    Returns per-layer records with wall times."""
+    import time
+
+    import paper_2302_05164_b200 as st
+    from paper_2302_05164_b200.physics import LayerPath, Segment
+    mesh, geo, params, settings = config3_setup(krylov_tol)
+    paths = config3_layer_paths(geo, mesh)
+    state = config3_initial_state(mesh, geo, params, settings)
+    recs = []
+    for lp in paths[:n_layers]:
+        rec = {"layer": lp.layer_index}
+        t0 = time.perf_counter()
+        advance_mesh(state, params, settings)
+        rec["wall_amr"] = time.perf_counter() - t0
+        rec["n_dofs"] = int(state.dofmap.n_dofs)
+        rec["n_cells"] = int(state.forest.active.sum())
+        t0 = time.perf_counter()
+        crit = st.compute_step_criteria(state.op, settings)
+        rec["wall_criteria"] = time.perf_counter() - t0
+        rec["dt_stability"] = crit.dt_stability
+        scan_lp = lp
+        if scan_steps is not None:
+            # the same schedule, stopped after scan_steps steps
+            keep, t_left = [], scan_steps * dt
+            for s in lp.segments:
+                if t_left <= 0:
+                    break
+                if s.duration <= t_left + 1e-15:
+                    keep.append(s)
+                    t_left -= s.duration
+                else:
+                    f = t_left / s.duration
+                    keep.append(Segment(s.x0, s.y0, s.x0 + f * (s.x1 - s.x0),
+                                        s.y0 + f * (s.y1 - s.y0), s.v, s.power))
+                    t_left = 0
+            scan_lp = LayerPath(lp.layer_index, lp.z, keep, lp.cool_time)
+        cool_lp = lp if cool_time is None else LayerPath(lp.layer_index, lp.z, [], cool_time)
+        scan = st.run_scan_phase(state, scan_lp, dt)
+        cool = st.run_cooldown_phase(state, cool_lp, dt, settings)
+        rec.update(scan_steps=scan.n_steps, wall_scan=scan.wall_time, t_max=scan.t_max_seen,
+                   cool_steps=cool.n_steps, newton=cool.newton_iters, krylov=cool.krylov_iters,
+                   wall_cool=cool.wall_time)
+        recs.append(rec)
+        if on_layer is not None:
+            on_layer(state, rec)
+    return state, recs
