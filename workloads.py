@@ -37,6 +37,100 @@ def hatch_segments(boxes, spacing, v, power, direction_deg=0.0):
     return out
 
 
+# --- BASELINE configs[0..2] (structured boxes) ---------------------------------
+
+def _st():
+    import paper_2302_05164_b200 as st
+    return st
+
+
+def workload_config0():
+    """configs[0]: 64x64x32 Q1 (139,425 DoFs), k = 6.7 const, 70 W beam at
+    1 m/s along y = 1 mm, dt = 1 us, bottom Dirichlet 300 K."""
+    st = _st()
+    h = 31.25e-6
+    mat = st.MaterialParams(k_p=6.7, k_m=6.7, k_s=6.7, rho=4430.0, c=526.0)
+    bnd = st.BoundaryParams(emissivity=0.0, T_inf=300.0, T_v=1e9)
+    las = st.HeatSourceParams(radius=50e-6, h_powder=40e-6, power=70.0, scan_velocity=1.0)
+    params = st.ProcessParams(mat, bnd, las, st.MeshParams(h_coarse=h, n_refine=0, h_powder=h))
+    lp = st.LayerPath(0, 0.0, [st.Segment(0.0, 1e-3, 2e-3, 1e-3, 1.0, 70.0)], 0.0)
+    return dict(name="config0_q1_64x64x32", dims=(64, 64, 32), h=h, degree=1,
+                params=params, T0=lambda n: 300.0 + np.random.default_rng(0).uniform(0, 1, n),
+                dt=1e-6, paths=[lp], sample=(64, 64, 32),
+                cfg={"mesh": "64x64x32 Q1", "dt": 1e-6, "material": "k=6.7 const",
+                     "beams": 1})
+
+
+def _config1_params():
+    st = _st()
+    h = 31.25e-6
+    # k(T) = g k_m + (1-g) k_s with r_c = 1 (SURVEY §0.1), c_app with latent heat
+    mat = st.MaterialParams(k_p=6.7, k_m=32.0, k_s=6.7, rho=4430.0, c=526.0, T_s=300.0,
+                            T_l=1928.0, latent_heat=2.86e5, T_lat_s=1878.0, T_lat_l=1928.0)
+    bnd = st.BoundaryParams(emissivity=0.3, T_inf=300.0, T_v=1e9, h_conv=10.0)
+    las = st.HeatSourceParams(radius=50e-6, h_powder=40e-6, power=70.0, scan_velocity=1.0)
+    return st.ProcessParams(mat, bnd, las, st.MeshParams(h_coarse=h, n_refine=0, h_powder=h))
+
+
+def workload_config1():
+    """configs[1]: 4x4x1 mm, 128x128x32 Q2 cells (4,293,185 DoFs), k(T)
+    6.7 -> 32 W/mK over 300-1928 K, apparent heat capacity (latent
+    2.86e5 J/kg over 1878-1928 K), top radiation eps 0.3 + convection
+    h = 10, 70 W beam on a 5-track serpentine hatch (100 um), dt = 0.5 us."""
+    st = _st()
+    h = 31.25e-6
+    segs = hatch_segments([(1.5e-3, 1.75e-3, 2.5e-3, 2.25e-3)], 1e-4, 1.0, 70.0)
+    lp = st.LayerPath(0, 0.0, segs, 0.0)
+    return dict(name="config1_q2_128x128x32", dims=(128, 128, 32), h=h, degree=2,
+                params=_config1_params(),
+                T0=lambda n: 300.0 + np.random.default_rng(0).uniform(0, 1, n),
+                dt=0.5e-6, paths=[lp], sample=(32, 32, 32),
+                cfg={"mesh": "128x128x32 Q2", "dt": 0.5e-6,
+                     "material": "k(T) 6.7->32, c_app latent 2.86e5, rad 0.3 + conv 10",
+                     "beams": 1, "hatch": "5 tracks x 1 mm, 100 um"})
+
+
+CELLS_50M = {1: 367, 2: 184, 3: 122, 4: 92}
+
+
+def workload_config2(p):
+    """configs[2]: unit cube, ~50M DoFs at degree p, T ~ U[300, 2500],
+    material as config 1, beam off, dt = 1 ms."""
+    st = _st()
+    n = CELLS_50M[p]
+    h = 1.0 / n
+    lp = st.LayerPath(0, 0.0, [], 0.0)
+    return dict(name=f"config2_q{p}_{n}^3", dims=(n, n, n), h=h, degree=p,
+                params=_config1_params(),
+                T0=lambda m: np.random.default_rng(2).uniform(300.0, 2500.0, m),
+                dt=1e-3, paths=[lp], sample=(24, 24, 24),
+                cfg={"mesh": f"{n}^3 Q{p} unit cube", "dt": 1e-3,
+                     "material": "as config 1", "beams": 0})
+
+
+WORKLOADS = {"config0": workload_config0, "config1": workload_config1,
+             "config2_p1": lambda: workload_config2(1), "config2_p2": lambda: workload_config2(2),
+             "config2_p3": lambda: workload_config2(3), "config2_p4": lambda: workload_config2(4)}
+
+
+def build_problem(w, dims=None):
+    st = _st()
+    nx, ny, nz = dims or w["dims"]
+    box = st.StructuredBox(nx, ny, nz, w["h"], degree=w["degree"])
+    return box
+
+
+def schedule(w, n):
+    from paper_2302_05164_b200.physics import flatten_schedule
+    paths = w["paths"]
+    if not paths[0].segments:       # beam off: an empty layer of n steps
+        dts = np.full(n, w["dt"])
+        from paper_2302_05164_b200.physics import BEAM_DTYPE
+        return dts, np.zeros((n, 0), dtype=BEAM_DTYPE)
+    return flatten_schedule(paths, w["dt"], n)
+
+
+
 # --- BASELINE configs[3]: growing domain with cool-down ------------------------
 
 def config3_setup(krylov_tol=1e-10):
