@@ -112,6 +112,13 @@ typedef struct st_structured_mesh {
    * iface_hi mark local node planes 0 / NX-1 as rank interfaces whose
    * partial sums are exchanged between st_explicit_step_begin/_end. */
   int32_t gx0, gNX, iface_lo, iface_hi;
+  /* Fitted part (BASELINE configs[4]): NULL for the full box, else nz
+   * x extents -- cell row k holds the cells i < xext[k], non-decreasing
+   * in k (a base with overhanging slabs on top; extents may change only at
+   * tile-row boundaries of the kernel).  Nodes are those of the active
+   * cells, numbered by the reference's sorted-key rule: node plane I
+   * holds rows K >= kmin(I) of every J. */
+  const int32_t* xext;
 } st_structured_mesh;
 
 /* evaluate_rhs term flags (operators.py:247 diffusion/faces/source). */

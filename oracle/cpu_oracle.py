@@ -619,3 +619,23 @@ def beam_tuple(b):
     on = int(b["active"]) != 0 and float(b["power"]) > 0.0
     return (float(b["x"]), float(b["y"]), float(b["z_top"]),
             float(b["power"]) if on else 0.0)
+
+
+def fitted_tables(part):
+    """Tables of a paper_2302_05164_b200.mesh.FittedPart (cell rows with
+    x extents, degree p): its node ids (the reference's sorted-key rule on
+    the active nodes), cell anchors, Dirichlet bottom plane, top facets."""
+    p, h = part.degree, part.h
+    ox, oy, oz = part.origin
+    i, j, k = part.cells()
+    nodes = part.cell_node_ids()
+    n = len(i)
+    anchor = np.stack([ox + i * h, oy + j * h, oz + k * h], axis=1)
+    nv = part.n_vertices
+    fc = np.flatnonzero(k == part.nz - 1) if part.top_faces else np.zeros(0, np.int64)
+    return dict(p=p, cell_nodes=nodes, h=np.full(n, float(h)), anchor=anchor,
+                nv=nv, is_slave=np.zeros(nv, bool), is_dirichlet=part.is_dirichlet,
+                slaves=np.zeros(0, np.int64), slave_ptr=np.zeros(1, np.int64),
+                slave_masters=np.zeros(0, np.int64),
+                slave_weights=np.zeros(0), face_cell=fc.astype(np.int64),
+                face_r0=np.zeros((len(fc), 2)), face_rr=np.ones(len(fc)))

@@ -73,7 +73,8 @@ class StStructuredMesh(ctypes.Structure):
                 ("y0", ctypes.c_double), ("z0", ctypes.c_double),
                 ("dirichlet_bottom", ctypes.c_int32), ("top_faces", ctypes.c_int32),
                 ("gx0", ctypes.c_int32), ("gNX", ctypes.c_int32),
-                ("iface_lo", ctypes.c_int32), ("iface_hi", ctypes.c_int32)]
+                ("iface_lo", ctypes.c_int32), ("iface_hi", ctypes.c_int32),
+                ("xext", _i32p)]
 
 
 class StLeaves(ctypes.Structure):

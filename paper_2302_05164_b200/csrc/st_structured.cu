@@ -53,23 +53,15 @@ __device__ __forceinline__ double inv_mass1_rt(const SArgs& A, int P, int L, int
 }
 
 // Seam nodes as a static list (built once per context, st_structured.cu
-// build_seam_list): entry e is node sidx[e] with code bits
-//   0 x seam, 1 y seam, 2 z seam, 3-4 rank-interface side + 1, 5 bottom plane
-// and its inverse lumped capacity sci[e] (k_seam_ci, the hot kernel's
-// expression).  The partials are summed in the fixed order of k_seams: x
-// side outermost, then z side, then y side; a remote x side reads the
-// neighbour rank's pre-summed plane.
-__global__ void k_seam_ci(SArgs A, int P, int64_t n, const int64_t* sidx, double* sci) {
-  const int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (e >= n) return;
-  const int64_t idx = sidx[e], plane = (int64_t)A.NY * A.NZ;
-  const int I = (int)(idx / plane);
-  const int64_t r = idx - (int64_t)I * plane;
-  const int J = (int)(r / A.NZ), K = (int)(r - (int64_t)J * A.NZ);
-  sci[e] = inv_mass1_rt(A, P, K, A.NZ) *
-           (inv_mass1_rt(A, P, J, A.NY) * (inv_mass1_rt(A, P, I + A.gI0, A.gNX) * A.inv_rcdw));
-}
-
+// build_seam_list): entry e is node sidx[e] with a 16-bit code
+//   bits 0-7  the slots (x side + 2 y side + 4 z side of the writing CTA)
+//             this node has partials in,
+//   bits 8-9  rank-interface side + 1 (0: none),
+//   bit 10    bottom plane (Dirichlet),
+// and its inverse lumped capacity sci[e] (host-computed with the hot
+// kernel's expression).  The partials are summed in the fixed order of
+// k_seams: x side outermost, then z side, then y side; a remote x side
+// reads the neighbour rank's pre-summed plane.
 // Seam pass over the static list: for each entry the (up to 8) slot
 // partials are all loaded up front (predicated, 0 for slots the node does
 // not have), then summed in the fixed order of the old per-plane pass: x
@@ -79,7 +71,7 @@ __global__ void k_seam_ci(SArgs A, int P, int64_t n, const int64_t* sidx, double
 template <bool LAT>
 __global__ void __launch_bounds__(256) k_seam_list(SArgs A, int64_t n,
                                                    const int64_t* __restrict__ sidx,
-                                                   const unsigned char* __restrict__ scode,
+                                                   const unsigned short* __restrict__ scode,
                                                    const double* __restrict__ sci) {
   // one entry per thread (measured: maximal parallelism beats batching
   // entries per thread); the loop form keeps U > 1 available
@@ -103,13 +95,11 @@ __global__ void __launch_bounds__(256) k_seam_list(SArgs A, int64_t n,
     for (int u = 0; u < U; u++) {
       const bool in = idx[u] >= 0;
       T[u] = in ? A.T[idx[u]] : 0.0;
-      const bool xs = code[u] & 1u, ys = code[u] & 2u, zs = code[u] & 4u;
-      const int side = (int)((code[u] >> 3) & 3u) - 1;
+      const int side = (int)((code[u] >> 8) & 3u) - 1;
 #pragma unroll
       for (int s = 0; s < 8; s++) {
-        const int xb = s & 1, yb = (s >> 1) & 1, zb = s >> 2;
-        const bool use =
-            in && (xb == 0 || xs) && (yb == 0 || ys) && (zb == 0 || zs) && xb != side;
+        const int xb = s & 1;
+        const bool use = in && ((code[u] >> s) & 1u) && xb != side;
         const int64_t so = (int64_t)s * A.snv + idx[u];
         fv[u][s] = 0.0;
         cv[u][s] = 0.0;
@@ -128,10 +118,10 @@ __global__ void __launch_bounds__(256) k_seam_list(SArgs A, int64_t n,
 #pragma unroll
     for (int u = 0; u < U; u++) {
       if (idx[u] < 0) continue;
-      const int side = (int)((code[u] >> 3) & 3u) - 1;
+      const int side = (int)((code[u] >> 8) & 3u) - 1;
       double rf[2] = {0.0, 0.0}, rc[2] = {0.0, 0.0};
       if (side >= 0) {
-        const int64_t o = side == 0 ? idx[u] : idx[u] - (int64_t)(A.NX - 1) * A.NY * A.NZ;
+        const int64_t o = side == 0 ? idx[u] : idx[u] - A.ioff_hi;
         rf[side] = A.irf[side][o];
         if (LAT) rc[side] = A.irc[side][o];
       }
@@ -149,7 +139,7 @@ __global__ void __launch_bounds__(256) k_seam_list(SArgs A, int64_t n,
         f += sf_;
         dc += sc_;
       }
-      const double o = finalize_node(A, ci[u], (code[u] & 32u) != 0, T[u], f, dc, LAT);
+      const double o = finalize_node(A, ci[u], (code[u] & 1024u) != 0, T[u], f, dc, LAT);
       A.out[idx[u]] = o;
       amax = dmax(amax, fabs(o));
       smax = dmax(smax, o);
@@ -163,14 +153,15 @@ __global__ void __launch_bounds__(256) k_seam_list(SArgs A, int64_t n,
 // (it is the high x side there) or NX-1 (low side), in the same z-then-y
 // slot order k_seams uses, so both ranks add bitwise the same numbers
 __global__ void k_iface_pack(SArgs A, int P, int CY, int CZ, int side, int latent) {
-  const int64_t plane = (int64_t)A.NY * A.NZ;
-  const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (t >= plane) return;
-  const int J = (int)(t / A.NZ), K = (int)(t - (int64_t)J * A.NZ);
   const int I = side == 0 ? 0 : A.NX - 1, xb = side == 0 ? 1 : 0;
+  const int kmI = A.pkmin ? A.pkmin[I] : 0;
+  const int sI = A.NZ - kmI;
+  const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (t >= (int64_t)A.NY * sI) return;
+  const int J = (int)(t / sI), K = kmI + (int)(t - (int64_t)(t / sI) * sI);
   const bool ys = J > 0 && J < A.NY - 1 && (J % (P * CY)) == 0;
-  const bool zs = K > 0 && K < A.NZ - 1 && (K % (P * CZ)) == 0;
-  const int64_t idx = (int64_t)I * plane + t;
+  const bool zs = K > kmI && K < A.NZ - 1 && (K % (P * CZ)) == 0;
+  const int64_t idx = (A.pbase ? A.pbase[I] : (int64_t)I * A.NY * A.NZ) + (int64_t)J * sI + K;
   double sf_ = 0.0, sc_ = 0.0;
   for (int zb = 0; zb <= (zs ? 1 : 0); zb++)
     for (int yb = 0; yb <= (ys ? 1 : 0); yb++) {
@@ -178,6 +169,51 @@ __global__ void k_iface_pack(SArgs A, int P, int CY, int CZ, int side, int laten
     }
   A.ipf[side][t] = sf_;
   if (latent) A.ipc[side][t] = sc_;
+}
+
+// fitted part: inverse constant lumped capacity of every node (row sums
+// over the active cells around it; operators.py:325-339), plane I =
+// blockIdx.y
+template <int P>
+__global__ void k_fit_cinv(SArgs A, const int* xext, double rc_detw, double* out) {
+  const int I = blockIdx.y;
+  const int kmI = A.pkmin[I];
+  const int sI = A.NZ - kmI;
+  const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (t >= (int64_t)A.NY * sI) return;
+  const int J = (int)(t / sI), K = kmI + (int)(t - (int64_t)(t / sI) * sI);
+  auto m1y = [&](int L, int N) {
+    const int a = L % P;
+    if (a != 0) return sM[P - 1][a];
+    double s = 0.0;
+    if (L > 0) s += sM[P - 1][P];
+    if (L < N - 1) s += sM[P - 1][0];
+    return s;
+  };
+  // (x, z) cells around the node, each with the node's 1D masses in it
+  double mxz = 0.0;
+  const int ax = I % P, az = K % P;
+  for (int dx = 0; dx < (ax != 0 ? 1 : 2); dx++) {
+    const int i = ax != 0 ? I / P : I / P - 1 + dx;
+    const double wx = ax != 0 ? sM[P - 1][ax] : sM[P - 1][dx == 0 ? P : 0];
+    for (int dz = 0; dz < (az != 0 ? 1 : 2); dz++) {
+      const int k = az != 0 ? K / P : K / P - 1 + dz;
+      const double wz = az != 0 ? sM[P - 1][az] : sM[P - 1][dz == 0 ? P : 0];
+      if (i >= 0 && k >= 0 && k < A.nz && i < xext[k]) mxz += wx * wz;
+    }
+  }
+  out[A.pbase[I] + (int64_t)J * sI + K] = 1.0 / (rc_detw * (m1y(J, A.NY) * mxz));
+}
+
+// fitted part: bottom node plane (rows K = 0 of the planes that reach it);
+// mode 0: out = val there, mode 1: out = v there
+__global__ void k_fit_pin(SArgs A, int mode, const double* v, double* out, double val) {
+  const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (t >= (int64_t)A.NX * A.NY) return;
+  const int I = (int)(t / A.NY), J = (int)(t - (int64_t)I * A.NY);
+  if (A.pkmin[I] != 0) return;
+  const int64_t idx = A.pbase[I] + (int64_t)J * A.NZ;
+  out[idx] = mode == 0 ? val : v[idx];
 }
 
 // ---------------------------------------------------------------------------
@@ -507,8 +543,25 @@ static int init_struct_constants() {
   return ST_OK;
 }
 
+// 1D lumped mass of local node a at degree p (host)
+static double host_m1(int p, int a) {
+  switch (p) {
+    case 1: return Basis<1>::M(a);
+    case 2: return Basis<2>::M(a);
+    case 3: return Basis<3>::M(a);
+    default: return Basis<4>::M(a);
+  }
+}
+
 struct Structured : Backend {
   st_structured_mesh m{};
+  // fitted part (m.xext != NULL): per cell row x extent, per node plane
+  // lowest row and first-node base, per tile row x extent
+  bool fitted = false;
+  std::vector<int> xext_h, kmin_h, text_h;
+  std::vector<int64_t> base_h;
+  DevBuf<int64_t> pbase_d;
+  DevBuf<int> pkmin_d, text_d, xext_d;
   int p = 1;
   int NX = 0, NY = 0, NZ = 0;
   int Lx = 1, cy = 8, cz = 8;
@@ -517,10 +570,19 @@ struct Structured : Backend {
   long long lx = 0, ly = 0, lz = 0;
   DevBuf<double> cinv, fseam, cseam, lcarry, packf[2], packc[2];
   DevBuf<int64_t> sidx;
-  DevBuf<unsigned char> scode;
+  DevBuf<unsigned short> scode;
   DevBuf<double> sci;
   int64_t n_seam = 0;
   int64_t nv = 0;
+
+  // nodes of node plane I
+  int64_t plane_n(int I) const { return (int64_t)NY * (NZ - (fitted ? kmin_h[I] : 0)); }
+
+  int unsupported_fitted(const char* what) const {
+    set_error(std::string(what) + " is not available on a fitted part (explicit steps and "
+              "evaluate_rhs with a uniform history are)");
+    return ST_EUNSUPPORTED;
+  }
 
   int launched() {
     c->launches++;
@@ -585,6 +647,10 @@ struct Structured : Backend {
     A.gNX = m.gNX > 0 ? m.gNX : NX;
     A.iface_lo = m.iface_lo ? 1 : 0;
     A.iface_hi = m.iface_hi ? 1 : 0;
+    A.pbase = fitted ? pbase_d.p : nullptr;
+    A.pkmin = fitted ? pkmin_d.p : nullptr;
+    A.text = fitted ? text_d.p : nullptr;
+    A.ioff_hi = fitted ? base_h[NX - 1] + kmin_h[NX - 1] : (int64_t)(NX - 1) * NY * NZ;
     for (int a = 0; a < q; a++)
       for (int b = 0; b < q; b++)
         for (int cc = 0; cc < q; cc++) {
@@ -636,50 +702,136 @@ struct Structured : Backend {
     return ST_OK;
   }
 
-  // static seam-node list (see k_seam_list): x-seam planes (chunk
-  // boundaries, rank interfaces), then y-seam planes off x seams, then
-  // z-seam planes off both
+  // static seam-node list (see k_seam_list), in node order.  A node is a
+  // seam when two or more CTAs (tile row t, tile column u, x chunk c)
+  // write it: each CTA owns the closed node box of its cells and stores
+  // its partial of a shared node to slot (first plane of a chunk c > 0
+  // or a low rank interface) + 2 (first column of a tile u > 0) + 4
+  // (first row of a tile row t > 0 with material below), exactly the
+  // hot kernel's rule; the list records which slots each node has.
   int build_seam_list() {
     const int sx = p * Lx, sy = p * cy, sz = p * cz;
-    auto xseam = [&](int I) {
-      return (I > 0 && I < NX - 1 && I % sx == 0) || (I == 0 && m.iface_lo) ||
-             (I == NX - 1 && m.iface_hi);
+    const int nty = (m.ny + cy - 1) / cy, ntz = (m.nz + cz - 1) / cz;
+    auto ext_t = [&](int t) { return fitted ? text_h[t] : m.nx; };
+    auto kmin_of = [&](int I) { return fitted ? kmin_h[I] : 0; };
+    auto base_of = [&](int I) { return fitted ? base_h[I] : (int64_t)I * NY * NZ; };
+    auto ext_row = [&](int k) { return fitted ? xext_h[k] : m.nx; };
+    const SArgs A = sargs();
+    double M1[5] = {};
+    for (int a = 0; a <= p; a++) M1[a] = host_m1(p, a);
+    auto im1 = [&](int L, int N) {  // inverse 1D lumped mass on a full line
+      const int a = L % p;
+      if (a != 0) return A.imr[a];
+      return (L == 0 || L == N - 1) ? A.imv_end : A.imv_int;
     };
-    auto yseam = [&](int J) { return J > 0 && J < NY - 1 && J % sy == 0; };
-    auto zseam = [&](int K) { return K > 0 && K < NZ - 1 && K % sz == 0; };
-    std::vector<int64_t> idx;
-    std::vector<unsigned char> code;
-    auto add = [&](int I, int J, int K) {
-      const bool xs = xseam(I), ys = yseam(J), zs = zseam(K);
-      const int side = (I == 0 && m.iface_lo) ? 0 : ((I == NX - 1 && m.iface_hi) ? 1 : -1);
-      idx.push_back(((int64_t)I * NY + J) * NZ + K);
-      code.push_back((unsigned char)((xs ? 1 : 0) | (ys ? 2 : 0) | (zs ? 4 : 0) |
-                                     ((side + 1) << 3) | (K == 0 ? 32 : 0)));
-    };
+    std::vector<char> xcand(NX, 0);
     for (int I = 0; I < NX; I++)
-      if (xseam(I))
-        for (int J = 0; J < NY; J++)
-          for (int K = 0; K < NZ; K++) add(I, J, K);
-    for (int J = 0; J < NY; J++)
-      if (yseam(J))
-        for (int I = 0; I < NX; I++)
-          if (!xseam(I))
-            for (int K = 0; K < NZ; K++) add(I, J, K);
-    for (int K = 0; K < NZ; K++)
-      if (zseam(K))
-        for (int I = 0; I < NX; I++)
-          if (!xseam(I))
-            for (int J = 0; J < NY; J++)
-              if (!yseam(J)) add(I, J, K);
+      for (int t = 0; t < ntz; t++)
+        if (I > 0 && I % sx == 0 && I < p * ext_t(t)) xcand[I] = 1;
+    if (m.iface_lo) xcand[0] = 1;
+    if (m.iface_hi) xcand[NX - 1] = 1;
+    std::vector<int64_t> idx;
+    std::vector<unsigned short> code;
+    std::vector<double> ci;
+    auto visit = [&](int I, int J, int K, int kmI) {
+      int tl[2], nt = 0, ul[2], nu = 0;
+      for (int t : {K / sz - ((K % sz == 0 && K > 0) ? 1 : 0), K / sz}) {
+        if (t < 0 || t >= ntz || (nt && tl[nt - 1] == t)) continue;
+        if (t * sz <= K && K <= p * std::min((t + 1) * cz, m.nz) && I <= p * ext_t(t)) tl[nt++] = t;
+      }
+      for (int u : {J / sy - ((J % sy == 0 && J > 0) ? 1 : 0), J / sy}) {
+        if (u < 0 || u >= nty || (nu && ul[nu - 1] == u)) continue;
+        if (u * sy <= J && J <= p * std::min((u + 1) * cy, m.ny)) ul[nu++] = u;
+      }
+      unsigned mask = 0;
+      int count = 0;
+      for (int a = 0; a < nt; a++) {
+        const int t = tl[a], ext = ext_t(t);
+        int cl[2], nc = 0;
+        for (int cc : {I / sx - ((I % sx == 0 && I > 0) ? 1 : 0), I / sx}) {
+          if (cc < 0 || (nc && cl[nc - 1] == cc)) continue;
+          if (cc * Lx < ext && cc * sx <= I && I <= p * std::min((cc + 1) * Lx, ext)) cl[nc++] = cc;
+        }
+        for (int b = 0; b < nu; b++)
+          for (int e = 0; e < nc; e++) {
+            const int bit = ((I == cl[e] * sx && (cl[e] > 0 || m.iface_lo)) ? 1 : 0) +
+                            ((J == ul[b] * sy && ul[b] > 0) ? 2 : 0) +
+                            ((K == t * sz && t > 0 && kmI < K) ? 4 : 0);
+            mask |= 1u << bit;
+            count++;
+          }
+      }
+      const int side = (I == 0 && m.iface_lo) ? 0 : ((I == NX - 1 && m.iface_hi) ? 1 : -1);
+      if (count < 2 && side < 0) return;
+      idx.push_back(base_of(I) + (int64_t)J * (NZ - kmI) + K);
+      code.push_back((unsigned short)(mask | ((side + 1) << 8) | (K == 0 ? 1024 : 0)));
+      // inverse lumped capacity: the hot kernel's tensor product where the
+      // active (x, z) cells around the node form a rectangle, else the row
+      // sum over the cells present (re-entrant edge of a fitted part)
+      const int ax = I % p, az = K % p;
+      bool pres[2][2] = {};
+      int npres = 0;
+      for (int dx = 0; dx < (ax ? 1 : 2); dx++)
+        for (int dz = 0; dz < (az ? 1 : 2); dz++) {
+          const int i = ax ? I / p : I / p - 1 + dx, k = az ? K / p : K / p - 1 + dz;
+          bool on = k >= 0 && k < m.nz && i >= 0 && i < ext_row(k);
+          if (k >= 0 && k < m.nz && i < 0 && m.iface_lo) on = true;
+          if (k >= 0 && k < m.nz && i >= m.nx && m.iface_hi && ext_row(k) == m.nx) on = true;
+          pres[dx][dz] = on;
+          npres += on;
+        }
+      const int nxs = ax ? 1 : 2, nzs = az ? 1 : 2;
+      bool rect = true;
+      for (int dx = 0; dx < nxs; dx++)
+        for (int dz = 0; dz < nzs; dz++) {
+          bool anyx = false, anyz = false;
+          for (int e = 0; e < nzs; e++) anyx |= pres[dx][e];
+          for (int e = 0; e < nxs; e++) anyz |= pres[e][dz];
+          if (anyx && anyz && !pres[dx][dz]) rect = false;
+        }
+      const double my = im1(J, NY);
+      if (rect) {
+        auto side_inv = [&](int a, bool lo, bool hi) {
+          if (a) return A.imr[a];
+          return (lo && hi) ? A.imv_int : A.imv_end;
+        };
+        bool xlo = false, xhi = false, zlo = false, zhi = false;
+        for (int dz = 0; dz < nzs; dz++) {
+          xlo |= pres[0][dz];
+          if (nxs == 2) xhi |= pres[1][dz];
+        }
+        for (int dx = 0; dx < nxs; dx++) {
+          zlo |= pres[dx][0];
+          if (nzs == 2) zhi |= pres[dx][1];
+        }
+        const double mx = ax ? A.imr[ax] : side_inv(0, xlo, xhi);
+        const double mz = az ? A.imr[az] : side_inv(0, zlo, zhi);
+        ci.push_back(mz * (my * (mx * A.inv_rcdw)));
+      } else {
+        double mxz = 0.0;
+        for (int dx = 0; dx < nxs; dx++)
+          for (int dz = 0; dz < nzs; dz++)
+            if (pres[dx][dz]) mxz += M1[ax ? ax : (dx ? 0 : p)] * M1[az ? az : (dz ? 0 : p)];
+        ci.push_back((1.0 / mxz) * (my * A.inv_rcdw));
+      }
+      (void)npres;
+    };
+    for (int I = 0; I < NX; I++) {
+      const int kmI = kmin_of(I);
+      for (int J = 0; J < NY; J++) {
+        const bool yc = J > 0 && J < NY - 1 && J % sy == 0;
+        if (xcand[I] || yc) {
+          for (int K = kmI; K < NZ; K++) visit(I, J, K, kmI);
+        } else {
+          for (int K = (kmI / sz + 1) * sz; K < NZ - 1; K += sz) visit(I, J, K, kmI);
+        }
+      }
+    }
     n_seam = (int64_t)idx.size();
     if (n_seam == 0) return ST_OK;
     ST_TRY(sidx.upload(idx.data(), idx.size(), c->stream));
     ST_TRY(scode.upload(code.data(), code.size(), c->stream));
-    ST_TRY(sci.alloc(idx.size()));
-    SArgs A = sargs();
-    k_seam_ci<<<(unsigned)((n_seam + kThreads - 1) / kThreads), kThreads, 0, c->stream>>>(
-        A, p, n_seam, sidx.p, sci.p);
-    ST_LAUNCHED();
+    ST_TRY(sci.upload(ci.data(), ci.size(), c->stream));
     // the host vectors die here: finish the uploads first
     ST_CUDA(cudaStreamSynchronize(c->stream));
     return ST_OK;
@@ -687,6 +839,7 @@ struct Structured : Backend {
 
   int xmarch(SArgs& A, bool rcf, bool with_seams = true) {
     const bool lat = c->dp.latent != 0 && A.mode == 0;
+    if (fitted && rcf) return unsupported_fitted("a stored per-point history");
     if (!slab && p >= 2 && (A.flags & ST_RHS_SOURCE) && A.nb > kMaxTabBeams) {
       set_error("the structured p >= 2 kernel tables at most " + std::to_string(kMaxTabBeams) +
                 " beams per step");
@@ -732,9 +885,9 @@ struct Structured : Backend {
     A.red = reinterpret_cast<unsigned long long*>(red);
     ST_TRY(xmarch(A, rc != nullptr, false));
     const bool lat = c->dp.latent != 0;
-    const int64_t plane = (int64_t)NY * NZ;
     for (int sd = 0; sd < 2; sd++) {
       if (!(sd == 0 ? m.iface_lo : m.iface_hi)) continue;
+      const int64_t plane = plane_n(sd == 0 ? 0 : NX - 1);
       k_iface_pack<<<(unsigned)((plane + kThreads - 1) / kThreads), kThreads, 0, c->stream>>>(
           A, p, cy, cz, sd, lat ? 1 : 0);
       ST_TRY(launched());
@@ -747,7 +900,7 @@ struct Structured : Backend {
   int iface_ptrs(int side, double** f, double** cp, int64_t* n) override {
     *f = packf[side].p;
     *cp = c->dp.latent ? packc[side].p : nullptr;
-    *n = (int64_t)NY * NZ;
+    *n = plane_n(side == 0 ? 0 : NX - 1);
     return ST_OK;
   }
 
@@ -821,6 +974,7 @@ struct Structured : Backend {
 
   int history(const double* T, double* rc) override {
     if (!rc) return ST_OK;
+    if (fitted) return unsupported_fitted("a stored per-point history");
     return generic(0, T, nullptr, rc, 0.0, nullptr);
   }
 
@@ -829,6 +983,7 @@ struct Structured : Backend {
       ST_TRY(vec_recip(c, cinv.p, out, nv));
       return ST_OK;
     }
+    if (fitted) return unsupported_fitted("the apparent lumped capacity");
     ST_CUDA(cudaMemsetAsync(out, 0, nv * sizeof(double), c->stream));
     ST_TRY(generic(1, T, nullptr, nullptr, 0.0, out));
     k_cap_floor<<<(unsigned)((nv + 255) / 256), 256, 0, c->stream>>>(nv, cinv.p, out);
@@ -836,12 +991,14 @@ struct Structured : Backend {
   }
 
   int mass(const double* v, double* out) override {
+    if (fitted) return unsupported_fitted("apply_mass");
     ST_CUDA(cudaMemsetAsync(out, 0, nv * sizeof(double), c->stream));
     return generic(2, nullptr, v, nullptr, 0.0, out);
   }
 
   int jacobian(const double* v, const double* Tl, const double* rc, double dt,
                double* out) override {
+    if (fitted) return unsupported_fitted("apply_jacobian");
     double* vd;
     ST_TRY(c->vec(5, &vd));
     ST_CUDA(cudaMemcpyAsync(vd, v, nv * sizeof(double), cudaMemcpyDeviceToDevice, c->stream));
@@ -859,6 +1016,7 @@ struct Structured : Backend {
   }
 
   int jac_diag(const double* Tl, const double* rc, double dt, double* out) override {
+    if (fitted) return unsupported_fitted("jacobian_diagonal");
     ST_CUDA(cudaMemsetAsync(out, 0, nv * sizeof(double), c->stream));
     ST_TRY(generic(4, Tl, nullptr, const_cast<double*>(rc), dt, out));
     if (m.dirichlet_bottom) ST_TRY(pin_dirichlet(out, 1.0));
@@ -874,6 +1032,11 @@ struct Structured : Backend {
 
   int pin_dirichlet(double* v, double value) override {
     if (!m.dirichlet_bottom) return ST_OK;
+    if (fitted) {
+      const int64_t n = (int64_t)NX * NY;
+      k_fit_pin<<<(unsigned)((n + 255) / 256), 256, 0, c->stream>>>(sargs(), 0, nullptr, v, value);
+      return launched();
+    }
     const int64_t np_ = (int64_t)NX * NY;
     k_pin_bottom<<<(unsigned)((np_ + 255) / 256), 256, 0, c->stream>>>(np_, NZ, v, value);
     return launched();
@@ -934,6 +1097,32 @@ Backend* make_structured(Ctx* c, const st_structured_mesh* m, int* err) {
     if (!strcmp(e, "slab")) s->slab = true;
     if (!strcmp(e, "march")) s->slab = false;
   }
+  if (m->xext) {
+    // fitted part: node plane I holds rows K >= kmin(I) (the first cell row
+    // whose extent reaches the plane), numbered plane by plane (the
+    // reference's sorted-key rule on the active nodes); k_xmarch only
+    s->fitted = true;
+    s->slab = false;
+    s->xext_h.assign(m->xext, m->xext + m->nz);
+    for (int k = 0; k < m->nz; k++)
+      if (s->xext_h[k] < 1 || s->xext_h[k] > m->nx || (k && s->xext_h[k] < s->xext_h[k - 1])) {
+        set_error("fitted part: xext must be non-decreasing extents in [1, nx]");
+        delete s;
+        *err = ST_EINVAL;
+        return nullptr;
+      }
+    s->kmin_h.resize(s->NX);
+    s->base_h.resize(s->NX);
+    int64_t off = 0;
+    for (int I = 0; I < s->NX; I++) {
+      const int need = std::max((I + s->p - 1) / s->p, 1);
+      const int k = (int)(std::lower_bound(s->xext_h.begin(), s->xext_h.end(), need) - s->xext_h.begin());
+      s->kmin_h[I] = s->p * k;
+      s->base_h[I] = off - s->kmin_h[I];
+      off += (int64_t)s->NY * (s->NZ - s->kmin_h[I]);
+    }
+    s->nv = off;
+  }
   if (s->slab) {
     switch (s->p) {
       case 1: s->cy = SlabTile<1>::CY; s->cz = SlabTile<1>::CZ; break;
@@ -952,7 +1141,24 @@ Backend* make_structured(Ctx* c, const st_structured_mesh* m, int* err) {
   // x chunk length: the CTAs (yz tiles x chunks) run in waves of
   // (resident per SM) x (SMs); pick the chunking with the smallest
   // waves x (layers per CTA + overhead) (ties: fewer chunks, fewer x seams)
-  const int64_t nyz = (int64_t)((m->ny + s->cy - 1) / s->cy) * ((m->nz + s->cz - 1) / s->cz);
+  const int64_t nty = (m->ny + s->cy - 1) / s->cy, ntz = (m->nz + s->cz - 1) / s->cz;
+  const int64_t nyz = nty * ntz;
+  if (s->fitted) {
+    // a tile row must not straddle an extent change
+    s->text_h.resize(ntz);
+    for (int t = 0; t < ntz; t++) {
+      s->text_h[t] = s->xext_h[t * s->cz];
+      for (int k = t * s->cz; k < std::min((t + 1) * s->cz, m->nz); k++)
+        if (s->xext_h[k] != s->text_h[t]) {
+          set_error("fitted part: the x extent may change only at multiples of " +
+                    std::to_string(s->cz) + " cell rows (tile rows of the degree-" +
+                    std::to_string(s->p) + " kernel)");
+          delete s;
+          *err = ST_EUNSUPPORTED;
+          return nullptr;
+        }
+    }
+  }
   int sms = 148;
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c->device);
   const int64_t slots = (int64_t)s->resident(c->dp.latent != 0) * std::max(sms, 1);
@@ -961,8 +1167,14 @@ Backend* make_structured(Ctx* c, const st_structured_mesh* m, int* err) {
   for (int L = m->nx; L >= std::min(2, m->nx); L--) {
     const int64_t ch = (m->nx + L - 1) / L;
     if ((m->nx + ch - 1) / ch != L) continue;  // same chunking as a longer L
+    // work items: tiles x chunks (a fitted part's short rows have fewer)
+    int64_t items = nyz * ch;
+    if (s->fitted) {
+      items = 0;
+      for (int t = 0; t < ntz; t++) items += nty * ((s->text_h[t] + L - 1) / L);
+    }
     // + 2 layers per CTA for its prologue planes, tail plane and x seam
-    const int64_t cost = ((nyz * ch + slots - 1) / slots) * (int64_t)(L + 2);
+    const int64_t cost = ((items + slots - 1) / slots) * (int64_t)(L + 2);
     if (best < 0 || cost < best) {
       best = cost;
       s->Lx = L;
@@ -973,8 +1185,19 @@ Backend* make_structured(Ctx* c, const st_structured_mesh* m, int* err) {
                lattice_origin(m->z0, m->h, &s->lz);
   c->nv = s->nv;
   c->n_cells = (int64_t)m->nx * m->ny * m->nz;
+  if (s->fitted) {
+    int64_t cells = 0;
+    for (int k = 0; k < m->nz; k++) cells += s->xext_h[k];
+    c->n_cells = cells * m->ny;
+  }
   c->qpc = (s->p + 1) * (s->p + 1) * (s->p + 1);
   rc = s->cinv.alloc(s->nv);
+  if (rc == ST_OK && s->fitted) {
+    rc = s->pbase_d.upload(s->base_h.data(), s->base_h.size(), c->stream);
+    if (rc == ST_OK) rc = s->pkmin_d.upload(s->kmin_h.data(), s->kmin_h.size(), c->stream);
+    if (rc == ST_OK) rc = s->text_d.upload(s->text_h.data(), s->text_h.size(), c->stream);
+    if (rc == ST_OK) rc = s->xext_d.upload(s->xext_h.data(), s->xext_h.size(), c->stream);
+  }
   // seam slots (see SArgs::fseam / seam_pair)
   const bool pair = s->slab && c->dp.latent;
   const size_t nseam = (size_t)(pair ? 16 : 8) * s->nv;
@@ -993,12 +1216,22 @@ Backend* make_structured(Ctx* c, const st_structured_mesh* m, int* err) {
     rc = ST_ECUDA;
   for (int sd = 0; sd < 2 && rc == ST_OK; sd++) {
     if (!(sd == 0 ? m->iface_lo : m->iface_hi)) continue;
-    rc = s->packf[sd].alloc((size_t)s->NY * s->NZ);
-    if (rc == ST_OK && c->dp.latent) rc = s->packc[sd].alloc((size_t)s->NY * s->NZ);
+    rc = s->packf[sd].alloc((size_t)s->plane_n(sd == 0 ? 0 : s->NX - 1));
+    if (rc == ST_OK && c->dp.latent) rc = s->packc[sd].alloc((size_t)s->plane_n(sd == 0 ? 0 : s->NX - 1));
   }
   if (rc == ST_OK) {
     const double rc_detw = c->dp.rhoc * std::pow(m->h / 2.0, 3.0);
     const unsigned blocks = (unsigned)((s->nv + 255) / 256);
+    if (s->fitted) {
+      const SArgs A = s->sargs();
+      const dim3 g((unsigned)(((int64_t)s->NY * s->NZ + 255) / 256), (unsigned)s->NX);
+      switch (s->p) {
+        case 1: k_fit_cinv<1><<<g, 256, 0, c->stream>>>(A, s->xext_d.p, rc_detw, s->cinv.p); break;
+        case 2: k_fit_cinv<2><<<g, 256, 0, c->stream>>>(A, s->xext_d.p, rc_detw, s->cinv.p); break;
+        case 3: k_fit_cinv<3><<<g, 256, 0, c->stream>>>(A, s->xext_d.p, rc_detw, s->cinv.p); break;
+        default: k_fit_cinv<4><<<g, 256, 0, c->stream>>>(A, s->xext_d.p, rc_detw, s->cinv.p); break;
+      }
+    } else
     switch (s->p) {
       case 1: k_cinv<1><<<blocks, 256, 0, c->stream>>>(s->NX, s->NY, s->NZ, rc_detw, s->cinv.p); break;
       case 2: k_cinv<2><<<blocks, 256, 0, c->stream>>>(s->NX, s->NY, s->NZ, rc_detw, s->cinv.p); break;

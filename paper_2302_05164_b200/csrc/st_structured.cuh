@@ -67,6 +67,14 @@ struct SArgs {
   double imv_int, imv_end;  // cell vertex inside / at the end of the line
   // x-slab of a larger box: global plane offset / count, rank interfaces
   int gI0, gNX, iface_lo, iface_hi;
+  // fitted part (cell row k holds cells i < xext[k], non-decreasing in k;
+  // nullptrs for a full box): node (I, J, K) lives at pbase[I] + J (NZ -
+  // pkmin[I]) + K; text[t] = x extent (cells) of tile row t; ioff_hi = id
+  // of the first node of plane NX-1
+  const int64_t* pbase;
+  const int* pkmin;
+  const int* text;
+  int64_t ioff_hi;
 };
 
 // seam slot access (see SArgs::fseam)

@@ -59,8 +59,10 @@ __global__ void __launch_bounds__(CY* CZ, MinBlocks<P>::v) k_xmarch(SArgs A) {
   const int kl = ZMAJ ? tid / CY : tid % CZ, jl = ZMAJ ? tid % CY : tid / CZ;
   constexpr int SY = ZMAJ ? 1 : CZ, SZ = ZMAJ ? CY : 1;  // tid stride of the y / z neighbour
   const int j0 = blockIdx.x * CY, k0 = blockIdx.y * CZ, i0 = blockIdx.z * A.Lx;
-  if (i0 >= A.nx) return;
-  const int i1 = min(i0 + A.Lx, A.nx);
+  // x extent of this tile row (a fitted part's base rows end early)
+  const int ext = A.text ? A.text[blockIdx.y] : A.nx;
+  if (i0 >= ext) return;
+  const int i1 = min(i0 + A.Lx, ext);
   const int j = j0 + jl, k = k0 + kl;
   const bool live = j < A.ny && k < A.nz;
   const bool hiY = live && (jl == CY - 1 || j == A.ny - 1);
@@ -73,9 +75,10 @@ __global__ void __launch_bounds__(CY* CZ, MinBlocks<P>::v) k_xmarch(SArgs A) {
   const CellFlags F{(A.flags & ST_RHS_DIFFUSION) != 0, (A.flags & ST_RHS_FACES) != 0,
                     (A.flags & ST_RHS_SOURCE) != 0 && A.nb > 0, (A.flags & ST_RHS_FROZEN_K) != 0};
   const int64_t plane_stride = (int64_t)A.NY * A.NZ;
-  const int64_t tile0 = (int64_t)P * j0 * A.NZ + (int64_t)P * k0;
-  // this thread's node origin within a plane (global offset and smem slot)
-  const int64_t my0 = (int64_t)P * j * A.NZ + (int64_t)P * k;
+  // node plane I: first node id (minus its lowest row) and lowest row
+  auto pl_base = [&](int I) -> int64_t { return A.pbase ? A.pbase[I] : (int64_t)I * plane_stride; };
+  auto pl_kmin = [&](int I) -> int { return A.pkmin ? A.pkmin[I] : 0; };
+  // this thread's node origin within a plane (smem slot)
   const int ms0 = P * jl * NZT + P * kl;
   if (tid < 3) lat_any[tid] = 0;
 
@@ -86,12 +89,14 @@ __global__ void __launch_bounds__(CY* CZ, MinBlocks<P>::v) k_xmarch(SArgs A) {
   auto load_planes = [&](int Ib, int n) {
 #pragma unroll 1
     for (int pa = 0; pa < n; pa++) {
-      const double* srcT = A.T + (int64_t)(Ib + pa) * plane_stride + tile0 + lane;
-      double* dT = Tr + ((Ib + pa) % NR) * PL + lane;
+      const int I = Ib + pa;
+      const int64_t sI = A.NZ - pl_kmin(I);  // row stride of plane I
+      const double* srcT = A.T + pl_base(I) + (int64_t)P * j0 * sI + P * k0 + lane;
+      double* dT = Tr + (I % NR) * PL + lane;
 #pragma unroll 1
       for (int r = warp; r < Jn; r += NW) {
-        if (c_lo) cp_async8(dT + r * NZT, srcT + (int64_t)r * A.NZ);
-        if (c_hi) cp_async8(dT + r * NZT + 32, srcT + (int64_t)r * A.NZ + 32);
+        if (c_lo) cp_async8(dT + r * NZT, srcT + (int64_t)r * sI);
+        if (c_hi) cp_async8(dT + r * NZT + 32, srcT + (int64_t)r * sI + 32);
       }
     }
   };
@@ -148,15 +153,16 @@ __global__ void __launch_bounds__(CY* CZ, MinBlocks<P>::v) k_xmarch(SArgs A) {
   // on the low side (the chunk's last plane), 2 = on the high side (the
   // chunk's first plane)
   auto finalize_node3 = [&](auto bb, auto cc, const double* pe, const double* pc,
-                            const double* tpl, int64_t g0, int xc, bool latn, double imIs) {
+                            const double* tpl, int64_t g0, int64_t sI, bool zlo, double mz0,
+                            int xc, bool latn, double imIs) {
     constexpr int b = decltype(bb)::value, c = decltype(cc)::value;
     // own cell, then the y-, z- and yz-neighbour below (fixed order)
     double f = pe[(b * Q + c) * NT];
     if (b == 0 && jl > 0) f += pe[(P * Q + c) * NT - SY];
     if (c == 0 && kl > 0) f += pe[(b * Q + P) * NT - SZ];
     if (b == 0 && c == 0 && jl > 0 && kl > 0) f += pe[(P * Q + P) * NT - SY - SZ];
-    const int64_t idx = g0 + b * A.NZ + c;
-    const bool ys_lo = b == 0 && sy_lo, zs_lo = c == 0 && sz_lo;
+    const int64_t idx = g0 + b * sI + c;
+    const bool ys_lo = b == 0 && sy_lo, zs_lo = c == 0 && zlo;
     const bool seam = xc || ys_lo || (b == P && sy_hi) || zs_lo || (c == P && sz_hi);
     double dc = 0.0;
     if (LATENT && latn) {
@@ -167,7 +173,7 @@ __global__ void __launch_bounds__(CY* CZ, MinBlocks<P>::v) k_xmarch(SArgs A) {
     }
     // branch-free: a seam node stores its partial to this CTA's slot (side
     // code per seam axis), any other node its update
-    const double mzc = c == 0 ? mz_0 : (c == P ? mz_P : A.imr[c]);
+    const double mzc = c == 0 ? mz0 : (c == P ? mz_P : A.imr[c]);
     const double myb = b == 0 ? my_0 : (b == P ? my_P : A.imr[b]);
     const double ci = mzc * (myb * imIs);
     const double o = finalize_node(A, ci, c == 0 && k == 0, tpl[b * NZT + c], f, dc, LATENT);
@@ -185,19 +191,30 @@ __global__ void __launch_bounds__(CY* CZ, MinBlocks<P>::v) k_xmarch(SArgs A) {
   // every node of plane I owned by this thread (element plane a)
   auto finalize_owned = [&](int I, int a, int xc, bool latn) {
     if (!live) return;
-    const double imIs = inv_mass1<P>(A, I + A.gI0, A.gNX) * A.inv_rcdw;
+    // x factor of the inverse lumped mass: a line end at the box ends and
+    // where this tile row's extent stops inside the box
+    const int G = I + A.gI0;
+    const bool xend = G == 0 || G == A.gNX - 1 || (ext < A.nx && I == P * ext);
+    const double imx = (I % P) != 0 ? A.imr[I % P] : (xend ? A.imv_end : A.imv_int);
+    const double imIs = imx * A.inv_rcdw;
     const double* pe = E + a * Q * Q * NT + tid;
     const double* pc = Ec + a * Q * Q * NT + tid;
     const double* tpl = Tr + (I % NR) * PL + ms0;
-    const int64_t g0 = (int64_t)I * plane_stride + my0;
+    // plane I's row layout; its lowest node row is a z line end, and the
+    // tile's bottom nodes are a seam only where material lies below
+    const int kmI = pl_kmin(I);
+    const int64_t sI = A.NZ - kmI;
+    const int64_t g0 = pl_base(I) + (int64_t)P * j * sI + P * k;
+    const bool zlo = sz_lo && kmI < P * k0;
+    const double mz0 = P * k == kmI ? A.imv_end : mz_0;
     static_for<P>([&](auto bb) {
-      static_for<P>([&](auto cc) { finalize_node3(bb, cc, pe, pc, tpl, g0, xc, latn, imIs); });
+      static_for<P>([&](auto cc) { finalize_node3(bb, cc, pe, pc, tpl, g0, sI, zlo, mz0, xc, latn, imIs); });
     });
     if (hiZ)
-      static_for<P>([&](auto bb) { finalize_node3(bb, IC<P>{}, pe, pc, tpl, g0, xc, latn, imIs); });
+      static_for<P>([&](auto bb) { finalize_node3(bb, IC<P>{}, pe, pc, tpl, g0, sI, zlo, mz0, xc, latn, imIs); });
     if (hiY) {
-      static_for<P>([&](auto cc) { finalize_node3(IC<P>{}, cc, pe, pc, tpl, g0, xc, latn, imIs); });
-      if (hiZ) finalize_node3(IC<P>{}, IC<P>{}, pe, pc, tpl, g0, xc, latn, imIs);
+      static_for<P>([&](auto cc) { finalize_node3(IC<P>{}, cc, pe, pc, tpl, g0, sI, zlo, mz0, xc, latn, imIs); });
+      if (hiZ) finalize_node3(IC<P>{}, IC<P>{}, pe, pc, tpl, g0, sI, zlo, mz0, xc, latn, imIs);
     }
   };
 
@@ -295,7 +312,7 @@ __global__ void __launch_bounds__(CY* CZ, MinBlocks<P>::v) k_xmarch(SArgs A) {
       for (int q = 0; q < Q * Q; q++) Ec[q * NT + tid] = lat_had ? lcar[q * NT] : 0.0;
   }
   __syncthreads();
-  finalize_owned(P * i1, 0, (i1 < A.nx || A.iface_hi) ? 1 : 0,
+  finalize_owned(P * i1, 0, (i1 < ext || (A.iface_hi && ext == A.nx)) ? 1 : 0,
                  LATENT && lat_any[(i1 - 1) % 3] != 0);
   block_max2(__longlong_as_double((long long)amaxb), smax, A.red);
 }

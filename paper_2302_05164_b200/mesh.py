@@ -554,3 +554,96 @@ class StructuredBox:
                    np.ones(n, bool), 0, 1, self.h, -nz, self.dirichlet_bottom,
                    self.epoch)
         return f, build_dofmap(f)
+
+
+class FittedPart(StructuredBox):
+    """A boundary-fitted part on a uniform degree-p lattice: cell row k (z)
+    holds the cells i < xext[k] (x), all y; ``xext`` is non-decreasing in
+    k, so the part is a base of the full height with overhanging slabs on
+    top (BASELINE configs[4]: a 12 mm base plus a thin 75 mm overhang).
+
+    Nodes are those of the active cells, numbered by the reference rule
+    (sorted lattice key: x-major, then y, z fastest, mesh.py:712-715): node
+    plane I holds rows K >= kmin(I) of every J, so node (I, J, K) has id
+    base(I) + J (NZ - kmin(I)) + K with base(I) = offset(I) - kmin(I).
+    The bottom node plane z = z0 is Dirichlet, the top cell faces
+    radiate; the overhang's underside and the base's side faces are
+    adiabatic (the reference's boundary model)."""
+
+    def __init__(self, nx, ny, nz, h, xext, degree=2, origin=(0.0, 0.0, None),
+                 dirichlet_bottom=True, top_faces=True, epoch=0):
+        super().__init__(nx, ny, nz, h, degree, origin, dirichlet_bottom, top_faces, epoch)
+        x = np.asarray(xext, dtype=np.int32).reshape(-1)
+        if len(x) != self.nz or x.min() < 1 or x.max() > self.nx or np.any(np.diff(x) < 0):
+            raise ValueError("xext: nz non-decreasing extents in [1, nx]")
+        self.xext = np.ascontiguousarray(x)
+        p = self.degree
+        NX, NY, NZ = super().node_dims
+        I = np.arange(NX)
+        need = np.maximum(-(-I // p), 1)          # cells a row needs to touch plane I
+        first = np.searchsorted(self.xext, need)  # first row reaching plane I
+        self.kmin = (p * first).astype(np.int64)
+        counts = NY * (NZ - self.kmin)
+        self.plane_offset = np.concatenate([[0], np.cumsum(counts)[:-1]]).astype(np.int64)
+
+    @property
+    def n_vertices(self):
+        NX, NY, NZ = self.node_dims
+        return int(np.sum(NY * (NZ - self.kmin)))
+
+    @property
+    def n_dofs(self):
+        return self.n_vertices
+
+    @property
+    def n_cells(self):
+        return int(self.ny * np.sum(self.xext))
+
+    def active_volume_m3(self):
+        return self.n_cells * self.h ** 3
+
+    def node_id(self, I, J, K):
+        NZ = self.node_dims[2]
+        I = np.asarray(I)
+        km = self.kmin[I]
+        return self.plane_offset[I] + np.asarray(J) * (NZ - km) + (np.asarray(K) - km)
+
+    def node_lattice(self):
+        """(I, J, K) of every node in id order."""
+        NX, NY, NZ = self.node_dims
+        out = []
+        for I in range(NX):
+            J, K = np.meshgrid(np.arange(NY), np.arange(self.kmin[I], NZ), indexing="ij")
+            out.append(np.stack([np.full(J.size, I), J.ravel(), K.ravel()], axis=1))
+        return np.concatenate(out)
+
+    @property
+    def is_dirichlet(self):
+        m = np.zeros(self.n_vertices, dtype=bool)
+        if self.dirichlet_bottom:
+            lat = self.node_lattice()
+            m[lat[:, 2] == 0] = True
+        return m
+
+    def cells(self):
+        """(i, j, k) of the active cells in (i, j, k) lexicographic order."""
+        i, j, k = np.meshgrid(np.arange(self.nx), np.arange(self.ny), np.arange(self.nz),
+                              indexing="ij")
+        keep = i < self.xext[k]
+        return i[keep], j[keep], k[keep]
+
+    def cell_node_ids(self, cells=None):
+        """(m, (p+1)^3) node ids of active cells (the cells() order)."""
+        p = self.degree
+        i, j, k = self.cells()
+        if cells is not None:
+            i, j, k = i[cells], j[cells], k[cells]
+        l = np.arange(p + 1)
+        I = (p * i)[:, None, None, None] + l[None, :, None, None]
+        J = (p * j)[:, None, None, None] + l[None, None, :, None]
+        K = (p * k)[:, None, None, None] + l[None, None, None, :]
+        I, J, K = np.broadcast_arrays(I, J, K)
+        return self.node_id(I, J, K).reshape(len(i), -1)
+
+    def to_forest_dofmap(self):
+        raise ValueError("FittedPart runs on the structured backend only")

@@ -63,6 +63,7 @@ class ThermalOperator:
         self._lib = _lib.load()
         self._ctx = ctypes.c_void_p()
         self._cinv = None
+        self._uniform_rc = 1.0  # the context's uniform r_c (st_set_uniform_rc)
         pst = _lib.params_struct(params)
         if getattr(forest, "structured", False):
             self.structured = True
@@ -73,6 +74,10 @@ class ThermalOperator:
                                       int(getattr(forest, "gNX", 0)),
                                       int(bool(getattr(forest, "iface_lo", False))),
                                       int(bool(getattr(forest, "iface_hi", False))))
+            xext = getattr(forest, "xext", None)
+            if xext is not None:
+                self._xext = np.ascontiguousarray(xext, dtype=np.int32)
+                m.xext = self._xext.ctypes.data_as(ctypes.POINTER(ctypes.c_int32))
             _lib.check(self._lib.st_ctx_create_structured(
                 device, ctypes.byref(m), ctypes.byref(pst), ctypes.byref(self._ctx)),
                 "st_ctx_create_structured")
@@ -197,6 +202,17 @@ class ThermalOperator:
             raise ValueError("r_c does not match the active cells of this operator")
         return r.reshape(-1)
 
+    def _call_rc(self, r_c):
+        """r_c for a per-call entry point: a structured context evaluates a
+        uniform consolidated history (every entry equal to the context's
+        uniform value, 1 unless set_state set another) without a per-point
+        array (NULL), which a fitted part requires; else the array."""
+        r = self._rc(r_c)
+        if (r is not None and self.structured and r.size and r[0] >= 1.0
+                and r[0] == self._uniform_rc and np.all(r == r[0])):
+            return None, True
+        return r, False
+
     @property
     def launches(self):
         """Kernels launched by this operator so far."""
@@ -212,6 +228,10 @@ class ThermalOperator:
         T = self._vec(T, "T")
         rc = np.ascontiguousarray(history.r_c, dtype=np.float64)
         flat = rc.reshape(-1)
+        if self.structured and flat.size and flat[0] >= 1.0 and np.all(flat == flat[0]):
+            # max(r_c, g) with g <= 1 <= r_c: a consolidated history is a
+            # fixed point (and a fitted part stores none)
+            return history
         _lib.check(self._lib.st_update_history(self._ctx, _lib.dptr(T), _lib.dptr(flat)),
                    "update_history")
         history.r_c[...] = rc.reshape(history.r_c.shape)
@@ -232,7 +252,7 @@ class ThermalOperator:
             flags |= _lib.ST_RHS_FACES
         if source:
             flags |= _lib.ST_RHS_SOURCE
-        rc = self._rc(r_c) if (diffusion and frozen_k is None) else None
+        rc = self._call_rc(r_c)[0] if (diffusion and frozen_k is None) else None
         b = _beams(beam if source else None)
         bp, nb = _lib.beams_array(b)
         out = np.empty(self.nv)
@@ -268,9 +288,9 @@ class ThermalOperator:
         ``fused`` is accepted for interface parity: the device kernel
         always evaluates T + dt * (cinv * f) in one pass."""
         T = self._vec(T, "T")
-        rc = self._rc(r_c)
-        if rc is None:
+        if r_c is None:
             raise ValueError("explicit step needs r_c")
+        rc, _ = self._call_rc(r_c)
         b = _beams(beam)
         bp, nb = _lib.beams_array(b)
         out = np.empty(self.nv)
@@ -350,10 +370,12 @@ class ThermalOperator:
                    "set T")
         if np.isscalar(r_c):
             _lib.check(self._lib.st_set_uniform_rc(self._ctx, float(r_c)), "set r_c")
+            self._uniform_rc = float(r_c)
             return
         rc = self._rc(r_c)
         if np.all(rc >= 1.0) and np.all(rc == rc[0]) if rc.size else False:
             _lib.check(self._lib.st_set_uniform_rc(self._ctx, float(rc[0])), "set r_c")
+            self._uniform_rc = float(rc[0])
         else:
             _lib.check(self._lib.st_set_field(self._ctx, _lib.ST_FIELD_RC, _lib.dptr(rc),
                                               rc.size), "set r_c")

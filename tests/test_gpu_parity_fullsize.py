@@ -116,3 +116,39 @@ def test_config2_48cube_vs_oracle(p):
     rc = rng.uniform(0.0, 1.0, (op.n_cells, q, q, q))
     assert rel(op.evaluate_rhs(T, rc, None), orc.evaluate_rhs(T, rc, [])) <= 1e-12
     op.close()
+
+
+@pytest.mark.timeout(900)
+def test_config4_replica_vs_oracle():
+    """configs[4] at 1/64 of the volume (h = 100 um: 750 x 50 x 120 lattice,
+    15.2M DoFs, the same 20 mm base + 2.4 mm overhang and four spots): two
+    resident steps vs the oracle on the same numbering, from a state with
+    four melt pools."""
+    from cpu_oracle import fitted_tables
+    wl = w.workload_config4(scale=4)
+    part = w.build_part(wl)
+    params = wl["params"]
+    op = st.ThermalOperator(part, part, params, st.SolverSettings())
+    dts, beams = w.schedule(wl, 2)
+    lat = part.node_lattice()
+    xyz = np.stack([part.node_coords_1d(a)[lat[:, a]] for a in range(3)], axis=1)
+    T0 = wl["T0"](op.nv)
+    for b in beams[0]:
+        r2 = (xyz[:, 0] - b["x"]) ** 2 + (xyz[:, 1] - b["y"]) ** 2 + (xyz[:, 2] / 0.5) ** 2
+        T0 = T0 + 2800.0 * np.exp(-r2 / (300e-6) ** 2)
+    T0[part.is_dirichlet] = 300.0
+    op.set_state(T0, 1.0)
+    fail, _, _ = op.run_explicit(dts, beams)
+    assert fail == 0
+    T_gpu, _ = op.get_state()
+    op.close()
+    orc = OracleOperator(fitted_tables(part), params)
+    ones = np.ones((part.n_cells, 3, 3, 3))
+    T = T0.copy()
+    for i in range(2):
+        tb = [(float(b["x"]), float(b["y"]), float(b["z_top"]), float(b["power"]))
+              for b in beams[i] if b["active"]]
+        T = orc.explicit_step(T, float(dts[i]), ones, tb)
+    assert T.max() > 1928.0
+    assert rel(T_gpu, T) <= 1e-9
+    assert rel(T_gpu - T0, T - T0) <= 1e-9

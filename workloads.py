@@ -131,6 +131,51 @@ def schedule(w, n):
 
 
 
+# --- BASELINE configs[4]: partitioned large part -------------------------------
+
+def workload_config4(scale=1, steps_hint=100):
+    """configs[4]: a cantilever-like part of 75 x 5 x 12 mm -- a 20 mm base
+    of the full 12 mm height plus a 2.4 mm thin overhang slab on top that
+    reaches out to 75 mm -- Q2 at h = 25 um (scale 1: 3000 x 200 x 480 cell
+    lattice, 957,492,161 DoFs; ``scale`` coarsens h by that factor for the
+    replicas, 4 = the 1/64-volume replica), material as config 1 (k(T),
+    latent heat, radiation + convection), r_c = 1, T0 = 300 K + U[0, 1]
+    (seed 0), four 70 W spots at 1 m/s each hatching its own 10 x 4 mm
+    patch of the top surface (tracks along x, 100 um apart), dt = 2 us."""
+    from paper_2302_05164_b200.mesh import FittedPart
+    from paper_2302_05164_b200.physics import LayerPath
+    h = 25e-6 * scale
+    nx, ny, nz = 3000 // scale, 200 // scale, 480 // scale
+    base, over = 800 // scale, 96 // scale
+    xext = [base] * (nz - over) + [nx] * over
+    paths = []
+    for x0 in (2e-3, 22e-3, 42e-3, 62e-3):
+        segs = hatch_segments([(x0, 0.5e-3, x0 + 10e-3, 4.5e-3)], 1e-4, 1.0, 70.0)
+        paths.append(LayerPath(0, 0.0, segs, 0.0))
+    return dict(name=f"config4_q2_cantilever{'' if scale == 1 else f'_1:{scale ** 3}'}",
+                dims=(nx, ny, nz), h=h, degree=2, xext=xext,
+                params=_config1_params(),
+                T0=lambda n: 300.0 + np.random.default_rng(0).uniform(0, 1, n),
+                dt=2e-6, paths=paths, sample=(32, 32, 32),
+                cfg={"mesh": f"{nx}x{ny}x{nz} Q2 lattice, 20 mm base + 2.4 mm overhang to 75 mm",
+                     "h_um": 25.0 * scale, "dt": 2e-6,
+                     "material": "as config 1 (k(T), latent 2.86e5, rad 0.3 + conv 10)",
+                     "beams": 4, "hatch": "4 patches 10 x 4 mm, 100 um, 1 m/s"})
+
+
+def build_part(w):
+    """The mesh object of a workload (box or fitted part)."""
+    import paper_2302_05164_b200 as st
+    from paper_2302_05164_b200.mesh import FittedPart
+    nx, ny, nz = w["dims"]
+    if w.get("xext") is not None:
+        return FittedPart(nx, ny, nz, w["h"], w["xext"], degree=w["degree"])
+    return st.StructuredBox(nx, ny, nz, w["h"], degree=w["degree"])
+
+
+WORKLOADS["config4"] = workload_config4
+
+
 # --- BASELINE configs[3]: growing domain with cool-down ------------------------
 
 def config3_setup(krylov_tol=1e-10):
