@@ -166,7 +166,9 @@ double* st_field_device_ptr(st_ctx* ctx, int field);
 
 /* --- per-call operator methods on host arrays (drop-in API) --------- */
 /* evaluate_rhs (operators.py:318): condensed f, Dirichlet rows kept.
- * rc may be NULL only with ST_RHS_FROZEN_K or without ST_RHS_DIFFUSION. */
+ * rc may be NULL with ST_RHS_FROZEN_K, without ST_RHS_DIFFUSION, or on a
+ * structured context (then the context's uniform history, 1 unless
+ * st_set_uniform_rc set another value). */
 int st_evaluate_rhs(st_ctx* ctx, const double* T, const double* rc, int flags,
                     double frozen_k, const st_beam* beams, int n_beams,
                     double* out);

@@ -523,7 +523,7 @@ int st_evaluate_rhs(st_ctx* ctx, const double* T, const double* rc, int flags, d
                     const st_beam* beams, int n_beams, double* out) {
   ST_TRY(check_ctx(ctx));
   Ctx& c = ctx->impl;
-  if ((flags & ST_RHS_DIFFUSION) && !(flags & ST_RHS_FROZEN_K) && !rc) {
+  if ((flags & ST_RHS_DIFFUSION) && !(flags & ST_RHS_FROZEN_K) && !rc && !c.be->uniform_rc_ok()) {
     set_error("evaluate_rhs needs r_c unless the conductivity is frozen");
     return ST_EINVAL;
   }
@@ -566,7 +566,7 @@ int st_explicit_step(st_ctx* ctx, const double* T, double dt, const double* rc,
                      const st_beam* beams, int n_beams, double* out) {
   ST_TRY(check_ctx(ctx));
   Ctx& c = ctx->impl;
-  if (!rc) {
+  if (!rc && !c.be->uniform_rc_ok()) {
     set_error("explicit step needs r_c");
     return ST_EINVAL;
   }

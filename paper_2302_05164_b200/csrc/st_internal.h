@@ -130,6 +130,8 @@ struct Backend {
   virtual int pin_dirichlet(double* v, double value) = 0;
   virtual double bytes_per_dof() const = 0;
   virtual const char* main_kernel() const = 0;
+  // r_c == NULL means "the context's uniform history" (structured only)
+  virtual bool uniform_rc_ok() const { return false; }
   // multi-GPU slab step (structured backend only)
   virtual int step_begin(const double* T, double* rc, double dt, int nb, const DevBeam* beams,
                          double* Tout, int pending, double* red) {

@@ -1055,6 +1055,7 @@ struct Structured : Backend {
     return b;
   }
   const char* main_kernel() const override { return slab ? "k_xslab" : "k_xmarch"; }
+  bool uniform_rc_ok() const override { return true; }
 };
 
 static bool lattice_origin(double o, double h, long long* l) {

@@ -157,6 +157,7 @@ def workload_config4(scale=1, steps_hint=100):
                 params=_config1_params(),
                 T0=lambda n: 300.0 + np.random.default_rng(0).uniform(0, 1, n),
                 dt=2e-6, paths=paths, sample=(32, 32, 32),
+                sample_origin=(2e-3 - 16 * h, 0.5e-3 - 16 * h, -32 * h),
                 cfg={"mesh": f"{nx}x{ny}x{nz} Q2 lattice, 20 mm base + 2.4 mm overhang to 75 mm",
                      "h_um": 25.0 * scale, "dt": 2e-6,
                      "material": "as config 1 (k(T), latent 2.86e5, rad 0.3 + conv 10)",
