@@ -33,7 +33,7 @@ import time
 
 import numpy as np
 
-from workloads import (CELLS_50M, WORKLOADS, build_part, build_problem,  # noqa: F401
+from workloads import (CELLS_50M, WORKLOADS, _st, build_part, build_problem,  # noqa: F401
                        schedule, workload_config0, workload_config1, workload_config2)
 
 ROOT = os.path.dirname(os.path.abspath(__file__))

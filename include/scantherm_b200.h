@@ -243,7 +243,17 @@ int st_iface_partials(st_ctx* ctx, int side, double** f_plane, double** c_plane,
 int st_explicit_step_end(st_ctx* ctx, const double* recv_lo_f, const double* recv_lo_c,
                          const double* recv_hi_f, const double* recv_hi_c);
 /* max |T| and max T over the steps committed since the last call */
+/* max |T'| and max T' over the split steps since the last read */
 int st_step_maxima(st_ctx* ctx, double* absmax, double* tmax);
+/* per-step maxima of the n oldest unread split steps (n <= 64; read at
+ * least every 64 split steps) -- the rank-local half of the cross-rank
+ * stability check (timestepping.py:186-192) */
+int st_step_maxima_history(st_ctx* ctx, int n, double* absmax, double* tmax);
+/* make `stream` (a cudaStream_t) wait until this step's rank-interface
+ * partials are packed: the exchange may start while the interior chunks
+ * of the sweep still run (st_explicit_step_begin launches the interface
+ * chunks first) */
+int st_iface_wait(st_ctx* ctx, void* stream);
 
 /* --- measurement ------------------------------------------------------ */
 /* When enabled, the step loop brackets its dominant kernel with CUDA

@@ -145,6 +145,8 @@ SIGNATURES = [
      [_VP, ctypes.c_int, ctypes.POINTER(_dp), ctypes.POINTER(_dp), _i64p]),
     ("st_explicit_step_end", ctypes.c_int, [_VP, _VP, _VP, _VP, _VP]),
     ("st_step_maxima", ctypes.c_int, [_VP, _dp, _dp]),
+    ("st_step_maxima_history", ctypes.c_int, [_VP, ctypes.c_int, _dp, _dp]),
+    ("st_iface_wait", ctypes.c_int, [_VP, _VP]),
     ("st_bench_explicit", ctypes.c_int,
      [_VP, ctypes.c_int, _dp, ctypes.POINTER(StBeam), ctypes.c_int, ctypes.c_int64,
       ctypes.POINTER(ctypes.c_float), ctypes.POINTER(ctypes.c_float)]),

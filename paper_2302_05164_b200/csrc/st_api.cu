@@ -76,6 +76,12 @@ int Ctx::upload_beams(const st_beam* b, int64_t count) {
   return ST_OK;
 }
 
+int Ctx::iface_event_record() {
+  if (!ev_iface) ST_CUDA(cudaEventCreateWithFlags(&ev_iface, cudaEventDisableTiming));
+  ST_CUDA(cudaEventRecord(ev_iface, stream));
+  return ST_OK;
+}
+
 int Ctx::vec(int i, double** out) {
   if ((int64_t)scratch[i].n < nv) ST_TRY(scratch[i].alloc(nv));
   *out = scratch[i].p;
@@ -190,6 +196,8 @@ static void ctx_free(st_ctx* c) {
   x.beams.free();
   x.red.free();
   for (auto& s : x.scratch) s.free();
+  x.split_ring.free();
+  if (x.ev_iface) cudaEventDestroy(x.ev_iface);
   if (x.stream) cudaStreamDestroy(x.stream);
   delete c;
 }
@@ -961,24 +969,49 @@ double st_algorithmic_bytes_per_dof(const st_ctx* ctx) {
 // ---------------------------------------------------------------------------
 // multi-GPU slab step
 // ---------------------------------------------------------------------------
-static unsigned long long* split_slot(Ctx& c) {
-  return reinterpret_cast<unsigned long long*>(c.red.p + kRedBlocks + 64 + 2 * 1020);
+// per-step stability maxima of split steps: a ring of kSplitRing slot pairs
+static int split_slot(Ctx& c, unsigned long long** out) {
+  if (!c.split_ring.p) {
+    ST_TRY(c.split_ring.alloc(2 * kSplitRing));
+    ST_CUDA(cudaMemsetAsync(c.split_ring.p, 0, 2 * kSplitRing * sizeof(double), c.stream));
+  }
+  *out = reinterpret_cast<unsigned long long*>(c.split_ring.p) + 2 * (c.split_count % kSplitRing);
+  return ST_OK;
 }
 
 int st_explicit_step_begin(st_ctx* ctx, double dt, const st_beam* beams, int n_beams) {
   ST_TRY(check_ctx(ctx));
   Ctx& c = ctx->impl;
   ST_TRY(need_state(c));
+  if (c.split_count - c.split_read >= kSplitRing) {
+    set_error("st_step_maxima / st_step_maxima_history must be read at least every " +
+              std::to_string(kSplitRing) + " split steps");
+    return ST_EINVAL;
+  }
   const int nb = beams ? n_beams : 0;
   ST_TRY(c.upload_beams(beams, nb));
   if ((int64_t)c.T_alt.n < c.nv) ST_TRY(c.T_alt.alloc(c.nv));
+  unsigned long long* slot;
+  ST_TRY(split_slot(c, &slot));
+  ST_CUDA(cudaMemsetAsync(slot, 0, 2 * sizeof(unsigned long long), c.stream));
   return c.be->step_begin(c.T.p, rc_ptr(c), dt, nb, c.beams.p, c.T_alt.p, c.history_pending,
-                          reinterpret_cast<double*>(split_slot(c)));
+                          reinterpret_cast<double*>(slot));
 }
 
 int st_iface_partials(st_ctx* ctx, int side, double** f_plane, double** c_plane, int64_t* n) {
   ST_TRY(check_ctx(ctx));
   return ctx->impl.be->iface_ptrs(side, f_plane, c_plane, n);
+}
+
+int st_iface_wait(st_ctx* ctx, void* stream) {
+  ST_TRY(check_ctx(ctx));
+  Ctx& c = ctx->impl;
+  if (!c.ev_iface) {
+    set_error("st_iface_wait before st_explicit_step_begin");
+    return ST_EINVAL;
+  }
+  ST_CUDA(cudaStreamWaitEvent((cudaStream_t)stream, c.ev_iface, 0));
+  return ST_OK;
 }
 
 int st_explicit_step_end(st_ctx* ctx, const double* recv_lo_f, const double* recv_lo_c,
@@ -989,20 +1022,50 @@ int st_explicit_step_end(st_ctx* ctx, const double* recv_lo_f, const double* rec
   std::swap(c.T.p, c.T_alt.p);
   std::swap(c.T.n, c.T_alt.n);
   c.history_pending = 1;
+  c.split_count++;
+  return ST_OK;
+}
+
+int st_step_maxima_history(st_ctx* ctx, int n, double* absmax, double* tmax) {
+  ST_TRY(check_ctx(ctx));
+  Ctx& c = ctx->impl;
+  const int64_t avail = c.split_count - c.split_read;
+  if (n < 0 || n > avail) {
+    set_error("st_step_maxima_history: " + std::to_string(avail) + " unread steps");
+    return ST_EINVAL;
+  }
+  if (n == 0 || !c.split_ring.p) return ST_OK;
+  std::vector<unsigned long long> h(2 * kSplitRing);
+  ST_CUDA(cudaMemcpyAsync(h.data(), c.split_ring.p, h.size() * 8, cudaMemcpyDeviceToHost, c.stream));
+  ST_CUDA(cudaStreamSynchronize(c.stream));
+  // the oldest n unread steps, in step order
+  for (int i = 0; i < n; i++) {
+    const int64_t s = c.split_read + i;
+    const unsigned long long* e = h.data() + 2 * (s % kSplitRing);
+    double am;
+    std::memcpy(&am, &e[0], 8);
+    if (absmax) absmax[i] = am;
+    if (tmax) tmax[i] = key_to_double(e[1]);
+  }
+  c.split_read += n;
   return ST_OK;
 }
 
 int st_step_maxima(st_ctx* ctx, double* absmax, double* tmax) {
   ST_TRY(check_ctx(ctx));
   Ctx& c = ctx->impl;
-  unsigned long long h[2];
-  ST_CUDA(cudaMemcpyAsync(h, split_slot(c), sizeof(h), cudaMemcpyDeviceToHost, c.stream));
-  ST_CUDA(cudaStreamSynchronize(c.stream));
-  ST_CUDA(cudaMemsetAsync(split_slot(c), 0, sizeof(h), c.stream));
-  double am;
-  std::memcpy(&am, &h[0], 8);
-  if (absmax) *absmax = am;
-  if (tmax) *tmax = key_to_double(h[1]);
+  const int n = (int)(c.split_count - c.split_read);
+  std::vector<double> a(n), t(n);
+  ST_TRY(st_step_maxima_history(ctx, n, a.data(), t.data()));
+  double am = 0.0, tm = -INFINITY;
+  bool bad = false;
+  for (int i = 0; i < n; i++) {
+    bad |= !(a[i] == a[i]);
+    am = std::max(am, a[i]);
+    tm = std::max(tm, t[i]);
+  }
+  if (absmax) *absmax = bad ? NAN : am;
+  if (tmax) *tmax = tm;
   return ST_OK;
 }
 

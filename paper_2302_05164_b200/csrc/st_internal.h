@@ -192,6 +192,12 @@ struct Ctx {
 
   int upload_beams(const st_beam* b, int64_t count);
   int vec(int i, double** out);  // nv-sized scratch vector i
+  // multi-GPU split step: event after the rank-interface planes are packed
+  // (st_iface_wait), per-step stability maxima ring (st_step_maxima_history)
+  cudaEvent_t ev_iface = nullptr;
+  int iface_event_record();
+  DevBuf<double> split_ring;  // 2 x kSplitRing (|T|max bits, T max key) per step
+  int64_t split_count = 0, split_read = 0;
   int h2d(double* dst, const double* src, int64_t n);
   int d2h(double* dst, const double* src, int64_t n);
   int sync();
@@ -231,6 +237,7 @@ int pw_div(Ctx* c, const double* x, const double* pws, double* y, int64_t n);
 int dot_to_device(Ctx* c, const double* a, const double* b, int64_t n, double* part, double* out);
 
 constexpr int kRedBlocks = 296;  // 2 x 148 SMs
+constexpr int kSplitRing = 64;   // split steps between two maxima reads
 constexpr int kThreads = 256;
 constexpr int kCgsSize = 3 * kRedBlocks + 16;
 

@@ -837,7 +837,9 @@ struct Structured : Backend {
     return ST_OK;
   }
 
-  int xmarch(SArgs& A, bool rcf, bool with_seams = true) {
+  int n_chunks() const { return (m.nx + Lx - 1) / Lx; }
+
+  int xmarch(SArgs& A, bool rcf, bool with_seams = true, int z0 = 0, int z1 = -1) {
     const bool lat = c->dp.latent != 0 && A.mode == 0;
     if (fitted && rcf) return unsupported_fitted("a stored per-point history");
     if (!slab && p >= 2 && (A.flags & ST_RHS_SOURCE) && A.nb > kMaxTabBeams) {
@@ -845,8 +847,11 @@ struct Structured : Backend {
                 " beams per step");
       return ST_EUNSUPPORTED;
     }
+    if (z1 < 0) z1 = n_chunks();
+    if (z1 <= z0) return with_seams ? seams(A) : ST_OK;
     c->prof_begin();
-    const dim3 grid((m.ny + cy - 1) / cy, (m.nz + cz - 1) / cz, (m.nx + Lx - 1) / Lx);
+    const dim3 grid((m.ny + cy - 1) / cy, (m.nz + cz - 1) / cz, z1 - z0);
+    A.zoff = z0;
     cudaError_t e;
     switch (p) {
       case 1: e = hot_launch<1>(A, slab, lat, rcf, grid, c->stream); break;
@@ -883,7 +888,20 @@ struct Structured : Backend {
     A.beams = beams;
     A.dt = dt;
     A.red = reinterpret_cast<unsigned long long*>(red);
-    ST_TRY(xmarch(A, rc != nullptr, false));
+    // the chunks that touch a rank interface first, then the packed
+    // interface planes (event ev_iface: the exchange may start), then the
+    // interior chunks, which the exchange overlaps (ST_NO_OVERLAP=1: one
+    // launch for all chunks, then the pack)
+    const int nch = n_chunks();
+    const int a = m.iface_lo ? 1 : 0, b = m.iface_hi ? nch - 1 : nch;
+    static const bool no_overlap = getenv("ST_NO_OVERLAP") && atoi(getenv("ST_NO_OVERLAP"));
+    const bool overlap = !no_overlap && a < b && (m.iface_lo || m.iface_hi);
+    if (overlap) {
+      if (m.iface_lo) ST_TRY(xmarch(A, rc != nullptr, false, 0, 1));
+      if (m.iface_hi) ST_TRY(xmarch(A, rc != nullptr, false, nch - 1, nch));
+    } else {
+      ST_TRY(xmarch(A, rc != nullptr, false));
+    }
     const bool lat = c->dp.latent != 0;
     for (int sd = 0; sd < 2; sd++) {
       if (!(sd == 0 ? m.iface_lo : m.iface_hi)) continue;
@@ -892,6 +910,8 @@ struct Structured : Backend {
           A, p, cy, cz, sd, lat ? 1 : 0);
       ST_TRY(launched());
     }
+    ST_TRY(c->iface_event_record());
+    if (overlap) ST_TRY(xmarch(A, rc != nullptr, false, a, b));
     split = A;
     split_open = true;
     return ST_OK;

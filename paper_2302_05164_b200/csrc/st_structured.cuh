@@ -75,6 +75,9 @@ struct SArgs {
   const int* pkmin;
   const int* text;
   int64_t ioff_hi;
+  // first x chunk of this launch (a step may be launched as chunk ranges:
+  // rank-interface chunks first, interior after, st_explicit_step_begin)
+  int zoff;
 };
 
 // seam slot access (see SArgs::fseam)

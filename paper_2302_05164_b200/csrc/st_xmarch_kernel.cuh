@@ -58,7 +58,8 @@ __global__ void __launch_bounds__(CY* CZ, MinBlocks<P>::v) k_xmarch(SArgs A) {
   constexpr bool ZMAJ = P >= 2;
   const int kl = ZMAJ ? tid / CY : tid % CZ, jl = ZMAJ ? tid % CY : tid / CZ;
   constexpr int SY = ZMAJ ? 1 : CZ, SZ = ZMAJ ? CY : 1;  // tid stride of the y / z neighbour
-  const int j0 = blockIdx.x * CY, k0 = blockIdx.y * CZ, i0 = blockIdx.z * A.Lx;
+  const int chunk = blockIdx.z + A.zoff;  // x chunk (launches may cover a chunk range)
+  const int j0 = blockIdx.x * CY, k0 = blockIdx.y * CZ, i0 = chunk * A.Lx;
   // x extent of this tile row (a fitted part's base rows end early)
   const int ext = A.text ? A.text[blockIdx.y] : A.nx;
   if (i0 >= ext) return;
@@ -109,7 +110,7 @@ __global__ void __launch_bounds__(CY* CZ, MinBlocks<P>::v) k_xmarch(SArgs A) {
 #pragma unroll
   for (int q = 0; q < Q * Q; q++) Cx[q * NT + tid] = 0.0;
   // latent x-face carry of this thread (global scratch, valid when lat_had)
-  double* lcar = LATENT ? A.lcarry + (((int64_t)blockIdx.z * gridDim.y + blockIdx.y) * gridDim.x +
+  double* lcar = LATENT ? A.lcarry + (((int64_t)chunk * gridDim.y + blockIdx.y) * gridDim.x +
                                       blockIdx.x) * (Q * Q * NT) + tid
                         : nullptr;
   bool lat_had = false;

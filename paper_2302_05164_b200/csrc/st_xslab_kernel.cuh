@@ -85,7 +85,8 @@ __global__ void __launch_bounds__((P + 1) * CY * CZ, SlabTile<P>::MINB) k_xslab(
   const int tid = threadIdx.x;
   const int s = tid / NC, cl = tid - (tid / NC) * NC;
   const int jl = cl / CZ, kl = cl - (cl / CZ) * CZ;
-  const int j0 = blockIdx.x * CY, k0 = blockIdx.y * CZ, i0 = blockIdx.z * A.Lx;
+  const int chunk = blockIdx.z + A.zoff;  // x chunk (launches may cover a chunk range)
+  const int j0 = blockIdx.x * CY, k0 = blockIdx.y * CZ, i0 = chunk * A.Lx;
   if (i0 >= A.nx) return;
   const int i1 = min(i0 + A.Lx, A.nx);
   const int j = j0 + jl, k = k0 + kl;

@@ -621,8 +621,9 @@ class FittedPart(StructuredBox):
     def is_dirichlet(self):
         m = np.zeros(self.n_vertices, dtype=bool)
         if self.dirichlet_bottom:
-            lat = self.node_lattice()
-            m[lat[:, 2] == 0] = True
+            NX, NY, NZ = self.node_dims
+            for I in np.flatnonzero(self.kmin == 0):   # planes reaching z = z0
+                m[self.plane_offset[I] + np.arange(NY) * NZ] = True
         return m
 
     def cells(self):

@@ -15,8 +15,11 @@ import torch.multiprocessing as mp
 from cpu_oracle import OracleOperator, structured_tables
 
 import paper_2302_05164_b200 as st
-from paper_2302_05164_b200.distributed import (Partials, SlabBox, SlabDriver, gather_global,
-                                               partition, torch_exchange)
+from paper_2302_05164_b200.distributed import (Partials, SlabBox, SlabDriver,
+                                               balanced_partition, gather_global, layer_dofs,
+                                               partition, slab_of, torch_exchange,
+                                               torch_max_reducer)
+from paper_2302_05164_b200.mesh import FittedPart
 
 H = 40e-6
 
@@ -44,6 +47,9 @@ class OracleSlabStepper:
         self.plane = box.node_dims[1] * box.node_dims[2]
         self.sides = [s for s, on in ((0, box.iface_lo), (1, box.iface_hi)) if on]
         self.params = params
+        self.hist = []          # per-step (max |T|, max T), unchecked
+        self.poison_at = None   # step number at which this rank diverges (tests)
+        self.n = 0
 
     def _planes(self, v):
         return {0: v[:self.plane], 1: v[-self.plane:]}
@@ -66,8 +72,17 @@ class OracleSlabStepper:
             C[-self.plane:] = C[-self.plane:] + recv[1].c.numpy()
         out = self.T + self.dt * ((1.0 / C) * f)
         out[self.M["is_dirichlet"]] = self.params.boundary.T_inf
+        self.n += 1
+        if self.poison_at is not None and self.n >= self.poison_at:
+            out[len(out) // 2] = np.nan
         self.T = out
-        self.rc = self.orc.update_history(self.rc, self.T)
+        self.hist.append((float(np.max(np.abs(out))) if np.all(np.isfinite(out)) else np.nan,
+                          float(np.max(out))))
+        self.rc = self.orc.update_history(self.rc, np.nan_to_num(self.T, nan=300.0))
+
+    def maxima_history(self, n):
+        h, self.hist = self.hist[:n], self.hist[n:]
+        return np.array([a for a, _ in h]), np.array([b for _, b in h])
 
 
 def _problem(p=2):
@@ -98,6 +113,27 @@ def _worker(rank, world, port, q):
     if rank == 0:
         q.put(gather_global([SlabBox(glob, *partition(glob.nx, world)[r], r, world)
                              for r in range(world)], [t for _, t in sorted(out)]))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def _diverge_worker(rank, world, port, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    glob, T0, dts, beams = _problem()
+    c0, c1 = partition(glob.nx, world)[rank]
+    box = SlabBox(glob, c0, c1, rank, world)
+    qd = glob.degree + 1
+    stepper = OracleSlabStepper(box, _params(), box.local_of(T0), np.ones((box.n_cells, qd, qd, qd)))
+    if rank == world - 1:
+        stepper.poison_at = 4          # only the last rank diverges
+    drv = SlabDriver(stepper, torch_exchange(rank, world), reduce_max=torch_max_reducer())
+    from cpu_oracle import beam_tuple
+    try:
+        drv.run(dts, [[beam_tuple(b) for b in row] for row in beams], check_every=3)
+        q.put((rank, None))
+    except st.InstabilityError as e:
+        q.put((rank, e.step))
     dist.barrier()
     dist.destroy_process_group()
 
@@ -140,6 +176,44 @@ def test_slab_decomposition_matches_single_domain(world):
     T, _ = run_explicit(orc, T0, np.ones((glob.n_cells, qd, qd, qd)), dts,
                         [[beam_tuple(b) for b in row] for row in beams])
     assert np.max(np.abs(got - T)) / np.max(np.abs(T)) < 1e-13
+
+
+def _spawn(target, world):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=target, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    out = [q.get(timeout=300) for _ in range(world)]
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    return out
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_cross_rank_stability_check(world):
+    """One rank diverges at step 4; the MAX all-reduce of the per-step
+    maxima makes every rank raise InstabilityError at step 4."""
+    got = _spawn(_diverge_worker, world)
+    assert sorted(got) == [(r, 4) for r in range(world)]
+
+
+def test_fitted_balanced_partition_and_gather():
+    g = FittedPart(36, 9, 24, H, [10] * 16 + [36] * 8, degree=2)
+    ld = layer_dofs(g)
+    assert ld.sum() + g.node_dims[1] * (g.node_dims[2] - g.kmin[-1]) == g.n_vertices
+    for w in (2, 3, 4):
+        parts = balanced_partition(g, w)
+        assert parts[0][0] == 0 and parts[-1][1] == g.nx
+        boxes = [slab_of(g, *parts[r], r, w) for r in range(w)]
+        T = np.arange(g.n_vertices, dtype=float)
+        assert np.array_equal(gather_global(boxes, [b.local_of(T) for b in boxes]), T)
+        for b in boxes:  # each slab's own numbering is the global one, shifted
+            assert b.n_vertices == len(b.local_of(T))
+    with pytest.raises(ValueError):
+        slab_of(g, 0, 10, 0, 2)  # a cut exactly where the base ends
 
 
 def test_partition_is_balanced_and_contiguous():
