@@ -291,57 +291,63 @@ def gpu_measure(w, steps, warmup, device, clocks=True):
 
 
 def run_slabs(args):
-    """N > 1: the global box is the workload box repeated N times along x
-    (weak scaling, one workload-sized x-slab per GPU); every step exchanges
-    the rank-interface partial sums over NCCL on the library's stream."""
+    """N > 1, one x-slab per GPU.  Default (config 4): strong scaling -- the
+    957M-DoF part cut into N slabs balanced by cumulative DoFs
+    (distributed.balanced_partition); ``--scaling weak`` repeats a box
+    workload N times along x instead.  Every step: interface chunks, packed
+    interface planes, NCCL exchange on a communication stream overlapping
+    the interior chunks, seam pass; a cross-rank MAX stability check every
+    32 steps.  The timed region is the whole K-step loop (checks included)
+    between CUDA events on every rank, max over ranks; the per-rank inputs
+    (>= 1.2e8 DoFs of T) are larger than L2, no flush."""
     import torch
     import torch.distributed as dist
-    from paper_2302_05164_b200.distributed import (GpuSlabStepper, SlabBox, SlabDriver,
-                                                   partition, torch_exchange)
+    from paper_2302_05164_b200.distributed import (GpuSlabStepper, SlabDriver,
+                                                   balanced_partition, partition, slab_of,
+                                                   torch_exchange, torch_max_reducer)
     st = _st()
     ws, rank, local = dist_env()
     torch.cuda.set_device(local)
     dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     w = dict(WORKLOADS[args.workload](), key=args.workload)
-    nx, ny, nz = w["dims"]
-    glob = st.StructuredBox(nx * ws, ny, nz, w["h"], degree=w["degree"])
-    c0, c1 = partition(glob.nx, ws)[rank]
-    box = SlabBox(glob, c0, c1, rank, ws)
+    weak = args.scaling == "weak" or w.get("xext") is None
+    if weak:
+        nx, ny, nz = w["dims"]
+        glob = st.StructuredBox(nx * ws, ny, nz, w["h"], degree=w["degree"])
+        parts = partition(glob.nx, ws)
+    else:
+        glob = build_part(w)
+        parts = balanced_partition(glob, ws)
+    box = slab_of(glob, *parts[rank], rank, ws)
     op = st.ThermalOperator(box, box, w["params"], st.SolverSettings(), device=local)
-    T0 = w["T0"](glob.n_vertices)
-    op.set_state(box.local_of(T0), 1.0)
+    if hasattr(box, "g_lo") and "T0_slice" in w:
+        T_loc = w["T0_slice"](box.g_lo, box.g_hi)
+    else:
+        T_loc = box.local_of(w["T0"](glob.n_vertices))
+    op.set_state(T_loc, 1.0)
     stepper = GpuSlabStepper(op)
-    drv = SlabDriver(stepper, torch_exchange(rank, ws))
+    drv = SlabDriver(stepper, torch_exchange(rank, ws), reduce_max=torch_max_reducer())
     dts, beams = schedule(w, args.warmup + args.steps)
-    flush = torch.empty(L2_FLUSH_BYTES // 8, dtype=torch.float64, device="cuda")
-    sweep = torch.zeros(L2_FLUSH_BYTES // 8, dtype=torch.float64, device="cuda")
-    evs = []
     with torch.cuda.stream(stepper.stream):
-        for i in range(args.warmup):
-            drv.step(float(dts[i]), beams[i])
+        drv.run(dts[:args.warmup], beams[:args.warmup], check_every=32)
         torch.cuda.synchronize()
         dist.barrier()
         launches0 = op.launches
         clk = Clocks(local)
         clk.__enter__()
-        for i in range(args.warmup, args.warmup + args.steps):
-            flush.fill_(float(i))
-            sweep.sum()  # read: leaves L2 with clean lines only (L2_NOTE)
-            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            e0.record()
-            drv.step(float(dts[i]), beams[i])
-            e1.record()
-            evs.append((e0, e1))
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        tmax = drv.run(dts[args.warmup:], beams[args.warmup:], check_every=32)
+        e1.record()
         torch.cuda.synchronize()
         clk.__exit__()
     launches = op.launches - launches0
-    total_ms = sum(a.elapsed_time(b) for a, b in evs)
+    total_ms = e0.elapsed_time(e1)
     t = torch.tensor([total_ms], device="cuda")
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     total_ms = float(t.item())
     # end to end: host slab in -> K split steps with the exchange -> host out
     # (pinned host buffers, as in the single-GPU line)
-    T_loc = box.local_of(T0)
     T_host = torch.empty(len(T_loc), dtype=torch.float64, pin_memory=True).numpy()
     T_host[:] = T_loc
     T_buf = torch.empty(len(T_loc), dtype=torch.float64, pin_memory=True).numpy()
@@ -349,36 +355,36 @@ def run_slabs(args):
     t0 = time.perf_counter()
     op.set_state(T_host, 1.0)
     with torch.cuda.stream(stepper.stream):
-        for i in range(args.warmup, args.warmup + args.steps):
-            drv.step(float(dts[i]), beams[i])
+        drv.run(dts[args.warmup:], beams[args.warmup:], check_every=32)
     T_out, rc_out = op.get_state(out=T_buf)
     e2e_s = torch.tensor([time.perf_counter() - t0], device="cuda")
     dist.all_reduce(e2e_s, op=dist.ReduceOp.MAX)
     nb = beams.shape[1]
-    e2e = {"value": glob.n_dofs * args.steps / float(e2e_s.item()), "unit": "DoF-updates/s",
+    dofs_total = glob.n_dofs
+    e2e = {"value": dofs_total * args.steps / float(e2e_s.item()), "unit": "DoF-updates/s",
            "h2d_bytes_per_step": (T_host.nbytes + args.steps * nb * 40) / args.steps,
            "d2h_bytes_per_step": (T_out.nbytes + (0 if rc_out.strides == (0,) else rc_out.nbytes))
            / args.steps,
-           "api": "per rank: set_state + split steps (NCCL exchange) + get_state; max over ranks"}
-    am, _ = stepper.maxima()
-    amt = torch.tensor([am], device="cuda")
-    dist.all_reduce(amt, op=dist.ReduceOp.MAX)
-    if not np.isfinite(amt.item()) or amt.item() > 1e7:
-        raise RuntimeError("slab run diverged")
-    dofs_total = glob.n_dofs
+           "api": "per rank: set_state + split steps (NCCL exchange, stability check every "
+                  "32 steps) + get_state; max over ranks"}
     value = dofs_total * args.steps / (total_ms * 1e-3)
     dist.barrier()
     if rank == 0:
         out = {"metric": METRIC, "value": value, "unit": "DoF-updates/s", "n_gpus": ws,
                "steps": args.steps, "warmup": args.warmup,
                "ms_per_step": total_ms / args.steps, "higher_is_better": True,
-               "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-               "config": dict(workload=w["name"] + f"_x{ws}", dofs=dofs_total,
+               "scaling": "weak" if weak else "strong", "vs_baseline": None, "dtype": "f64",
+               "data": "synthetic",
+               "config": dict(workload=w["name"] + (f"_x{ws}" if weak else ""), dofs=dofs_total,
                               backend="structured x-slabs",
-                              parallelism=f"x-slab dp{ws}, NCCL partial-sum interface exchange",
-                              l2=L2_NOTE, **w["cfg"]),
-               "e2e": e2e, "gpu_launches": int(launches), "clocks": clk.summary()}
+                              partition=[list(p) for p in parts],
+                              parallelism=f"x-slab dp{ws}, NCCL partial-sum interface exchange "
+                                          "overlapped with the interior chunks",
+                              l2="inputs larger than L2 (no flush)", **w["cfg"]),
+               "e2e": e2e, "gpu_launches": int(launches), "clocks": clk.summary(),
+               "t_max": tmax}
         print(json.dumps(out), flush=True)
+    op.close()
     dist.destroy_process_group()
 
 
@@ -681,6 +687,8 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--sweep", type=int, default=1, help="also measure configs[2], p=1..4")
     ap.add_argument("--sweep-steps", type=int, default=10)
+    ap.add_argument("--scaling", default="strong", choices=["strong", "weak"],
+                    help="N > 1: strong (config 4 split by DoFs) or weak (box per GPU)")
     args = ap.parse_args()
     args.warmup = max(3, args.warmup)
     if args.impl == "reference":

@@ -21,6 +21,17 @@ __device__ __forceinline__ double clamp01_int(double x) {
   const long long one = 0x3FF0000000000000LL;
   return __longlong_as_double(b < 0 ? 0LL : (b > one ? one : b));
 }
+// the same result from the high word alone (4 SASS instructions instead of
+// 8: ISETP, 2 VIMNMX, SEL): x < 0 (sign bit) -> +0, x >= 1 (high word >=
+// 0x3FF00000; 1 + tiny has the same high word and clamps to 1) -> 1.0,
+// else x unchanged; NaNs go to 0 / 1 by sign like clamp01_int
+__device__ __forceinline__ double clamp01_hi(double x) {
+  const int hi = __double2hiint(x);
+  const unsigned lo = (unsigned)__double2loint(x);
+  const int h = min(max(hi, 0), 0x3FF00000);
+  const unsigned l = ((unsigned)hi < 0x3FF00000u) ? lo : 0u;
+  return __hiloint2double(h, (int)l);
+}
 
 
 // any(|x_i - mid| < half) over N values as one chain of predicated

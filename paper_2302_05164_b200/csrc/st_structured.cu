@@ -628,6 +628,9 @@ struct Structured : Backend {
     const DevParams& d = c->dp;
     A.kA = (1.0 - c->rc_value) * d.k_p + c->rc_value * d.k_s;
     A.kB = d.k_m - d.k_s;
+    A.mhh = -(m.h / 2.0);
+    A.kAh = A.mhh * A.kA;
+    A.kBh = A.mhh * A.kB;
     A.glo = -d.T_s * d.inv_dT_l;
     A.lat_mid = 0.5 * (d.T_lat_s + d.T_lat_l);
     A.lat_half = 0.5 * (d.T_lat_l - d.T_lat_s);
@@ -948,6 +951,10 @@ struct Structured : Backend {
     A.mode = 1;
     A.flags = flags;
     A.frozen_k = frozen_k;
+    if (flags & ST_RHS_FROZEN_K) {  // k_xmarch: the frozen value through the uniform law
+      A.kAh = A.mhh * frozen_k;
+      A.kBh = 0.0;
+    }
     A.T = T;
     A.out = f;
     A.rc = rc;

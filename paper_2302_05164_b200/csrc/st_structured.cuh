@@ -55,6 +55,9 @@ struct SArgs {
   // uniform consolidated history (r_c = rc_value >= 1 >= g): the law
   // k = (r_p k_p + g k_m) + r_s k_s collapses to k = kA + g kB
   double kA, kB;
+  // k_xmarch: -(h/2) kA, -(h/2) kB (a frozen conductivity: -(h/2) k, 0)
+  // and -(h/2) for the stored-history law
+  double kAh, kBh, mhh;
   double glo;     // -T_s / (T_l - T_s): g = clamp(T * inv_dT_l + glo)
   double lat_mid, lat_half;  // latent interval as |T - mid| < half
   double hw3[125];  // (h/2) W_qa W_qb W_qc      (diffusion weight)

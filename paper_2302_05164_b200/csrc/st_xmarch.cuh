@@ -240,40 +240,26 @@ __device__ __forceinline__ void cell_element(const SArgs& A, const CellFlags& F,
               iz = true;
             }
           }
-          double kq;
-          if (P >= 2) {
-            // branch-free: the law always, the frozen value selected
-            // (measured: p = 2 faster, p = 1 slightly slower)
-            const double g = clamp01_int(fma(t[q], PP.inv_dT_l, A.glo));
-            if (RCF) {
-              double r = A.rc[cell * Q3 + q];
-              if (A.pending && !F.frozen) {
-                r = dmax(r, g);
-                A.rc[cell * Q3 + q] = r;
-              }
-              kq = conductivity(PP, g, r);
-            } else {
-              kq = fma(g, A.kB, A.kA);
+          // -(h/2) k(T, r_c) at the Gauss point: g(T) (material.py:46-57) as
+          // a clamped ramp; with a uniform consolidated history the law is
+          // one FMA with -(h/2) folded into its constants (kAh, kBh; a
+          // frozen conductivity is kAh = -(h/2) k_frozen, kBh = 0), so
+          // c = W3 (-(h/2) k) takes a compile-time weight
+          const double g = clamp01_hi(fma(t[q], PP.inv_dT_l, A.glo));
+          double kh;
+          if (RCF) {
+            double r = A.rc[cell * Q3 + q];
+            if (A.pending && !F.frozen) {
+              r = dmax(r, g);
+              A.rc[cell * Q3 + q] = r;
             }
-            kq = F.frozen ? A.frozen_k : kq;
-          } else if (F.frozen) {
-            kq = A.frozen_k;
+            kh = A.mhh * conductivity(PP, g, r);
           } else {
-            // g(T) (material.py:46-57) as a clamped ramp
-            const double g = clamp01(fma(t[q], PP.inv_dT_l, A.glo));
-            if (RCF) {
-              double r = A.rc[cell * Q3 + q];
-              if (A.pending) {
-                r = dmax(r, g);
-                A.rc[cell * Q3 + q] = r;
-              }
-              kq = conductivity(PP, g, r);
-            } else {
-              kq = fma(g, A.kB, A.kA);
-            }
+            kh = fma(g, A.kBh, A.kAh);
           }
           // -(w detJ (2/h)^2) k = -(h/2) W3 k ;  f_diff = sum_d Dq_d^T (c grad_d)
-          const double c = -A.hw3[q] * kq;
+          const double W3 = B::W(qa) * B::W(qb) * B::W(qc);  // folded after unrolling
+          const double c = W3 * kh;
           const double fx = c * gx, fy = c * gy, fz = c * gz;
 #pragma unroll
           for (int m = 0; m < Q; m++) {

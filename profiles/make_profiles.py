@@ -29,30 +29,36 @@ def launch_means(path):
     return {k: {"n": len(v), "mean_us": sum(v) / len(v)} for k, v in t.items()}
 
 
-def main(r):
-    traffic = {}
-    for w in ["config1", "config2_p1", "config2_p2", "config2_p3", "config2_p4", "config1_seams"]:
+def main(r, workloads=None):
+    try:
+        traffic = json.load(open(os.path.join(HERE, "traffic.json")))
+    except (OSError, ValueError):
+        traffic = {}
+    for w in workloads or ["config1", "config2_p1", "config2_p2", "config2_p3", "config2_p4",
+                           "config1_seams"]:
         tag = f"{r}_{w}"
         raw = os.path.join(OUT, f"raw_{tag}.csv")
         if not os.path.exists(raw):
             print("missing", raw)
             continue
         s = summarize(raw)
-        with open(os.path.join(HERE, f"{tag}_ncu_summary.json"), "w") as f:
+        dst = os.path.join(HERE, r) if os.path.isdir(os.path.join(HERE, r)) else HERE
+        with open(os.path.join(dst, f"{tag}_ncu_summary.json"), "w") as f:
             json.dump(s, f, indent=1)
         det = os.path.join(OUT, f"details_{tag}.txt")
         if os.path.exists(det):
-            shutil.copy(det, os.path.join(HERE, f"{tag}_ncu_details.txt"))
+            shutil.copy(det, os.path.join(dst, f"{tag}_ncu_details.txt"))
         lc = os.path.join(OUT, f"launches_{tag}.csv")
         if os.path.exists(lc):
-            shutil.copy(lc, os.path.join(HERE, f"{tag}_launches.csv"))
-            with open(os.path.join(HERE, f"{tag}_launches_summary.json"), "w") as f:
+            shutil.copy(lc, os.path.join(dst, f"{tag}_launches.csv"))
+            with open(os.path.join(dst, f"{tag}_launches_summary.json"), "w") as f:
                 json.dump(launch_means(lc), f, indent=1)
-        if w != "config1_seams":
+        if not w.endswith("_seams"):
             traffic[w] = {k: s[k] for k in ("kernel", "dram_bytes", "duration_us", "fp64_pipe_pct",
                                             "issue_active_pct", "fp64_flop",
                                             "fp64_peak_flop_per_cycle") if k in s}
-            traffic[w]["source"] = (f"profiles/{tag}_ncu_summary.json (ncu --set full "
+            rel = os.path.relpath(dst, os.path.dirname(HERE))
+            traffic[w]["source"] = (f"{rel}/{tag}_ncu_summary.json (ncu --set full "
                                     f"--clock-control none, one launch)")
         print(tag, {k: s.get(k) for k in ("kernel", "duration_us", "dram_bytes", "fp64_pipe_pct")})
     with open(os.path.join(HERE, "traffic.json"), "w") as f:
@@ -60,4 +66,4 @@ def main(r):
 
 
 if __name__ == "__main__":
-    main(sys.argv[1] if len(sys.argv) > 1 else "r1")
+    main(sys.argv[1] if len(sys.argv) > 1 else "r1", sys.argv[2:] or None)

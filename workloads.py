@@ -156,12 +156,22 @@ def workload_config4(scale=1, steps_hint=100):
                 dims=(nx, ny, nz), h=h, degree=2, xext=xext,
                 params=_config1_params(),
                 T0=lambda n: 300.0 + np.random.default_rng(0).uniform(0, 1, n),
+                T0_slice=lambda lo, hi: 300.0 + _uniform_slice(0, lo, hi),
                 dt=2e-6, paths=paths, sample=(32, 32, 32),
                 sample_origin=(2e-3 - 16 * h, 0.5e-3 - 16 * h, -32 * h),
                 cfg={"mesh": f"{nx}x{ny}x{nz} Q2 lattice, 20 mm base + 2.4 mm overhang to 75 mm",
                      "h_um": 25.0 * scale, "dt": 2e-6,
                      "material": "as config 1 (k(T), latent 2.86e5, rad 0.3 + conv 10)",
                      "beams": 4, "hatch": "4 patches 10 x 4 mm, 100 um, 1 m/s"})
+
+
+def _uniform_slice(seed, lo, hi):
+    """Entries [lo, hi) of default_rng(seed).uniform(0, 1, n) for any n >= hi
+    without drawing the prefix (PCG64 jump-ahead: one 64-bit draw per
+    double), so every rank builds only its slab of the global T0."""
+    g = np.random.default_rng(seed)
+    g.bit_generator.advance(lo)
+    return g.uniform(0.0, 1.0, hi - lo)
 
 
 def build_part(w):
@@ -175,6 +185,7 @@ def build_part(w):
 
 
 WORKLOADS["config4"] = workload_config4
+WORKLOADS["config4_s2"] = lambda: workload_config4(2)  # 1/8 volume (1.2e8 DoFs)
 
 
 # --- BASELINE configs[3]: growing domain with cool-down ------------------------
