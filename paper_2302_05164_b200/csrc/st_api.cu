@@ -339,6 +339,13 @@ static int pcg_dev(Ctx& c, const double* Tl, const double* rc, double dt, const 
   if (bnorm == 0.0) return ST_OK;
   ST_CUDA(cudaMemcpyAsync(r, b, nv * sizeof(double), cudaMemcpyDeviceToDevice, c.stream));
   if (bnorm <= tol * bnorm) return ST_OK;
+  // the whole solve as one persistent cooperative launch where the backend
+  // has one (unstructured; ST_CG_PERSISTENT=0 turns it off)
+  {
+    const int prc = c.be->pcg_persistent(Tl, rc, dt, b, tol * bnorm, max_iter, diag_inv, x,
+                                         iters, converged);
+    if (prc != ST_EUNSUPPORTED) return prc;
+  }
   // scalars stay on the device; the host reads r.r of iteration it while
   // iteration it + 1 is already queued (its kernels turn into no-ops once
   // the device-side copy of the stopping rule has fired)

@@ -132,6 +132,15 @@ struct Backend {
   virtual const char* main_kernel() const = 0;
   // r_c == NULL means "the context's uniform history" (structured only)
   virtual bool uniform_rc_ok() const { return false; }
+  // the whole Jacobi-PCG solve of J(Tlin) x = b as one persistent launch
+  // (thr = tol ||b||); ST_EUNSUPPORTED: the caller runs its kernel loop
+  virtual int pcg_persistent(const double* Tl, const double* rc, double dt, const double* b,
+                             double thr, int max_iter, const double* dinv, double* x,
+                             int* iters, int* converged) {
+    (void)Tl, (void)rc, (void)dt, (void)b, (void)thr, (void)max_iter, (void)dinv, (void)x,
+        (void)iters, (void)converged;
+    return ST_EUNSUPPORTED;
+  }
   // multi-GPU slab step (structured backend only)
   virtual int step_begin(const double* T, double* rc, double dt, int nb, const DevBeam* beams,
                          double* Tout, int pending, double* red) {

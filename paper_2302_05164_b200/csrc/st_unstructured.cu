@@ -19,7 +19,11 @@
 #include <map>
 #include <vector>
 
+#include <cooperative_groups.h>
+
 #include "st_common.cuh"
+
+namespace cg = cooperative_groups;
 
 namespace st {
 
@@ -300,13 +304,10 @@ __device__ __forceinline__ void tangent(const DevParams& P, const double* tl, co
   }
 }
 
-// J v element vectors: D + L + C/dt (operators.py:380-410)
-__global__ void k_jac_cells(int64_t n, CellGeo g, DevParams P, const double* vd,
-                            const double* Tl, const double* rc, double rc_value,
-                            double dt, double* E) {
-  pdl_wait_release();  // see st_common.cuh
-  int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (c >= n) return;
+// J v element vectors: D + L + C/dt (operators.py:380-410), cell c
+__device__ __forceinline__ void jac_cell(int64_t c, const CellGeo& g, const DevParams& P,
+                                         const double* vd, const double* Tl, const double* rc,
+                                         double rc_value, double dt, double* E) {
   double v[8], tl[8], k[8], dk[8], gx[8], gy[8], gz[8], e[8], tmp[8], pr[8];
   gather8(g.cv, c, vd, v);
   gather8(g.cv, c, Tl, tl);
@@ -357,6 +358,15 @@ __global__ void k_jac_cells(int64_t n, CellGeo g, DevParams P, const double* vd,
   project<0, 0, 0>(vq, pr);
 #pragma unroll
   for (int i = 0; i < 8; i++) E[c * 8 + i] = e[i] + pr[i] / dt;
+}
+
+__global__ void k_jac_cells(int64_t n, CellGeo g, DevParams P, const double* vd,
+                            const double* Tl, const double* rc, double rc_value,
+                            double dt, double* E) {
+  pdl_wait_release();  // see st_common.cuh
+  int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (c >= n) return;
+  jac_cell(c, g, P, vd, Tl, rc, rc_value, dt, E);
 }
 
 // element Jacobian entry A[a][b] (operators.py:412-424)
@@ -440,20 +450,181 @@ __device__ __forceinline__ double gather_condensed(const NodeTab& nt, const doub
   return f;
 }
 
+// condensed(E) at v; slave rows 0 (or slave_val); Dirichlet rows <- dir_src
+__device__ __forceinline__ double gather_row(int64_t v, const NodeTab& nt, const double* E,
+                                             const double* dir_src, int set_slave,
+                                             double slave_val) {
+  if (nt.is_slave[v]) return set_slave ? slave_val : 0.0;
+  double r = gather_condensed(nt, E, v);
+  if (dir_src && nt.is_dir[v]) r = dir_src[v];
+  return r;
+}
+
 // out = condensed(E); slave rows 0; optional: dirichlet rows <- dir_src, slave rows <- slave_val
 __global__ void k_gather(int64_t nv, NodeTab nt, const double* E, double* out,
                          const double* dir_src, int set_slave, double slave_val) {
   pdl_wait_release();  // see st_common.cuh
   int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (v >= nv) return;
-  double r;
-  if (nt.is_slave[v]) {
-    r = set_slave ? slave_val : 0.0;
-  } else {
-    r = gather_condensed(nt, E, v);
-    if (dir_src && nt.is_dir[v]) r = dir_src[v];
+  out[v] = gather_row(v, nt, E, dir_src, set_slave, slave_val);
+}
+
+// ---------------------------------------------------------------------------
+// persistent PCG (krylov_solve, timestepping.py:102-131) for the Newton
+// step of the cool-down: one cooperative launch runs the whole solve with
+// grid-wide barriers instead of kernel boundaries.  Per iteration:
+//   1. p = z + beta p (beta = 0 on the first iteration) and the Jacobian
+//      input vd (Dirichlet rows zeroed, slaves interpolated from the same
+//      z + beta p of their masters, operators.py:380-410),
+//   2. element vectors J vd (cells),
+//   3. Ap = condensed gather (Dirichlet rows identity, slave rows 0) and
+//      the p.Ap block partials,
+//   4. alpha = rz / p.Ap, x += alpha p, r -= alpha Ap, z = D^-1 r and the
+//      r.r / r.z block partials; every block sums the partials in the same
+//      fixed order, so all blocks take the same stopping decision
+//      (||r|| <= tol ||b||, x0 = 0) and the same beta.
+// The result (iterations, converged) is written to the device; the host
+// reads it once after the solve.
+// ---------------------------------------------------------------------------
+constexpr int kPcgThreads = 256;
+
+struct PcgArgs {
+  int64_t n, nv, ns;
+  CellGeo g;
+  NodeTab nt;
+  DevParams P;
+  const double* Tl;
+  const double* rc;
+  double rc_value, dt;
+  const int64_t* slaves;
+  const int64_t* sptr;
+  const int64_t* smast;
+  const double* sw;
+  const double* b;
+  const double* dinv;  // nullable: no preconditioner
+  double *x, *r, *z, *p0, *p1, *Ap, *vd, *E;
+  double* part;        // 4 x gridDim.x block partials
+  double thr;          // tol * ||b||
+  int max_iter;
+  int* out;            // [iterations, converged]
+};
+
+// deterministic block sum (fixed tree); the total is returned to every thread
+__device__ __forceinline__ double block_sum(double v, double* red) {
+  const int t = threadIdx.x;
+  __syncthreads();
+  red[t] = v;
+  __syncthreads();
+#pragma unroll
+  for (int s = kPcgThreads / 2; s > 0; s >>= 1) {
+    if (t < s) red[t] += red[t + s];
+    __syncthreads();
   }
-  out[v] = r;
+  return red[0];
+}
+
+// sum of the nb block partials at part[0..nb), the same order in every block
+__device__ __forceinline__ double sum_partials(const double* part, int nb, double* red) {
+  double v = 0.0;
+  for (int i = threadIdx.x; i < nb; i += kPcgThreads) v += part[i];
+  return block_sum(v, red);
+}
+
+__global__ void __launch_bounds__(kPcgThreads) k_pcg_persistent(PcgArgs a) {
+  cg::grid_group grid = cg::this_grid();
+  __shared__ double red[kPcgThreads];
+  const int nb = gridDim.x;
+  const int64_t tid = blockIdx.x * (int64_t)kPcgThreads + threadIdx.x;
+  const int64_t nth = (int64_t)nb * kPcgThreads;
+  double* pa = a.part;
+  // x = 0, r = b, z = D^-1 r, p = z, rz = r.z
+  double l = 0.0;
+  for (int64_t i = tid; i < a.nv; i += nth) {
+    const double ri = a.b[i];
+    const double zi = a.dinv ? ri * a.dinv[i] : ri;
+    a.x[i] = 0.0;
+    a.r[i] = ri;
+    a.z[i] = zi;
+    a.p0[i] = zi;
+    l += ri * zi;
+  }
+  l = block_sum(l, red);
+  if (threadIdx.x == 0) pa[blockIdx.x] = l;
+  grid.sync();
+  double rz = sum_partials(pa, nb, red);
+  double beta = 0.0;
+  double* p = a.p0;
+  double* pn = a.p1;
+  for (int it = 1; it <= a.max_iter; it++) {
+    // 1. p_new = z + beta p and the Jacobian input
+    for (int64_t i = tid; i < a.nv + a.ns; i += nth) {
+      if (i < a.nv) {
+        const double q = fma(beta, p[i], a.z[i]);
+        pn[i] = q;
+        if (!a.nt.is_slave[i]) a.vd[i] = a.nt.is_dir[i] ? 0.0 : q;
+      } else {
+        const int64_t s = i - a.nv;
+        double acc = 0.0;
+        for (int64_t k = a.sptr[s]; k < a.sptr[s + 1]; k++) {
+          const int64_t m = a.smast[k];
+          acc += a.sw[k] * fma(beta, p[m], a.z[m]);
+        }
+        a.vd[a.slaves[s]] = acc;
+      }
+    }
+    {
+      double* t = p;
+      p = pn;
+      pn = t;
+    }
+    grid.sync();
+    // 2. element vectors of J vd
+    for (int64_t c = tid; c < a.n; c += nth)
+      jac_cell(c, a.g, a.P, a.vd, a.Tl, a.rc, a.rc_value, a.dt, a.E);
+    grid.sync();
+    // 3. Ap and p.Ap
+    l = 0.0;
+    for (int64_t v = tid; v < a.nv; v += nth) {
+      const double ap = gather_row(v, a.nt, a.E, p, 0, 0.0);
+      a.Ap[v] = ap;
+      l += p[v] * ap;
+    }
+    l = block_sum(l, red);
+    if (threadIdx.x == 0) pa[nb + blockIdx.x] = l;
+    grid.sync();
+    const double alpha = rz / sum_partials(pa + nb, nb, red);
+    // 4. x, r, z and r.r / r.z
+    double lrr = 0.0, lrz = 0.0;
+    for (int64_t i = tid; i < a.nv; i += nth) {
+      a.x[i] += alpha * p[i];
+      const double ri = a.r[i] - alpha * a.Ap[i];
+      const double zi = a.dinv ? ri * a.dinv[i] : ri;
+      a.r[i] = ri;
+      a.z[i] = zi;
+      lrr += ri * ri;
+      lrz += ri * zi;
+    }
+    lrr = block_sum(lrr, red);
+    if (threadIdx.x == 0) pa[2 * nb + blockIdx.x] = lrr;
+    lrz = block_sum(lrz, red);
+    if (threadIdx.x == 0) pa[3 * nb + blockIdx.x] = lrz;
+    grid.sync();
+    const double rr = sum_partials(pa + 2 * nb, nb, red);
+    const double rzn = sum_partials(pa + 3 * nb, nb, red);
+    if (sqrt(rr) <= a.thr) {
+      if (tid == 0) {
+        a.out[0] = it;
+        a.out[1] = 1;
+      }
+      return;
+    }
+    beta = rzn / rz;
+    rz = rzn;
+  }
+  if (tid == 0) {
+    a.out[0] = a.max_iter;
+    a.out[1] = 0;
+  }
 }
 
 // forward Euler with the lumped capacity (operators.py:352-369)
@@ -745,6 +916,67 @@ struct Unstructured : Backend {
     ST_CUDA(launch_pdl(pdl, k_gather, dim3(nblk(nv)), dim3(kThreads), c->stream, nv, nodes(),
                        (const double*)E.p, out, v, 0, 0.0));
     return launched();
+  }
+
+  DevBuf<double> pcg_part;
+  DevBuf<int> pcg_out;
+  int pcg_blocks = 0;
+
+  int pcg_persistent(const double* Tl, const double* rc, double dt, const double* b, double thr,
+                     int max_iter, const double* dinv, double* x, int* iters,
+                     int* converged) override {
+    static const bool off = getenv("ST_CG_PERSISTENT") && getenv("ST_CG_PERSISTENT")[0] == '0';
+    if (off) return ST_EUNSUPPORTED;
+    if (!pcg_blocks) {
+      int per_sm = 0, sms = 0;
+      ST_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_pcg_persistent,
+                                                            kPcgThreads, 0));
+      ST_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c->device));
+      pcg_blocks = std::max(1, std::min(per_sm, 2) * sms);
+      ST_TRY(pcg_part.alloc(4 * (size_t)pcg_blocks));
+      ST_TRY(pcg_out.alloc(2));
+    }
+    PcgArgs a{};
+    a.n = n;
+    a.nv = nv;
+    a.ns = ns;
+    a.g = geo();
+    a.nt = nodes();
+    a.P = c->dp;
+    a.Tl = Tl;
+    a.rc = rc;
+    a.rc_value = c->rc_value;
+    a.dt = dt;
+    a.slaves = slaves.p;
+    a.sptr = sptr.p;
+    a.smast = smast.p;
+    a.sw = sw.p;
+    a.b = b;
+    a.dinv = dinv;
+    a.x = x;
+    ST_TRY(c->vec(1, &a.r));
+    ST_TRY(c->vec(2, &a.z));
+    ST_TRY(c->vec(3, &a.p0));
+    ST_TRY(c->vec(9, &a.p1));
+    ST_TRY(c->vec(4, &a.Ap));
+    ST_TRY(c->vec(5, &a.vd));
+    a.E = E.p;
+    a.part = pcg_part.p;
+    a.thr = thr;
+    a.max_iter = max_iter;
+    a.out = pcg_out.p;
+    void* args[] = {&a};
+    c->prof_begin();
+    ST_CUDA(cudaLaunchCooperativeKernel((const void*)k_pcg_persistent, dim3(pcg_blocks),
+                                        dim3(kPcgThreads), args, 0, c->stream));
+    c->prof_end();
+    ST_TRY(launched());
+    int h[2];
+    ST_CUDA(cudaMemcpyAsync(h, pcg_out.p, sizeof(h), cudaMemcpyDeviceToHost, c->stream));
+    ST_CUDA(cudaStreamSynchronize(c->stream));
+    *iters = h[0];
+    *converged = h[1];
+    return ST_OK;
   }
 
   int jac_diag(const double* Tl, const double* rc, double dt, double* out) override {

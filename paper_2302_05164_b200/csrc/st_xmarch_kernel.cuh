@@ -49,6 +49,8 @@ __global__ void __launch_bounds__(CY* CZ, MinBlocks<P>::v) k_xmarch(SArgs A) {
   double* Fq = Sx + (COOP ? MB * Q : 0);       // [CY][Q * Q] facet fluxes
   double* Fo = Fq + (COOP ? CY * Q * Q : 0);   // [CY][Q * Q] facet node terms
   __shared__ int lat_any[3];  // latent increments per layer (slot i % 3)
+  __shared__ long long pinfo_b[NR];  // ring: first node id (- lowest row) of a staged plane
+  __shared__ int pinfo_k[NR];        // ring: lowest node row of a staged plane
   const int tid = threadIdx.x;
   const int lane = tid & 31, warp = tid >> 5;
   // P >= 2: z-major cell order inside the CTA (tid = kl * CY + jl), so the
@@ -91,13 +93,23 @@ __global__ void __launch_bounds__(CY* CZ, MinBlocks<P>::v) k_xmarch(SArgs A) {
 #pragma unroll 1
     for (int pa = 0; pa < n; pa++) {
       const int I = Ib + pa;
-      const int64_t sI = A.NZ - pl_kmin(I);  // row stride of plane I
-      const double* srcT = A.T + pl_base(I) + (int64_t)P * j0 * sI + P * k0 + lane;
+      const int kmI = pl_kmin(I);
+      const int64_t bI = pl_base(I);
+      const int64_t sI = A.NZ - kmI;  // row stride of plane I
+      // the plane's layout rides along in the ring for its finalisation
+      if (tid == 0) {
+        pinfo_b[I % NR] = bI;
+        pinfo_k[I % NR] = kmI;
+      }
+      const double* srcT = A.T + bI + (int64_t)P * j0 * sI + P * k0 + lane;
       double* dT = Tr + (I % NR) * PL + lane;
-#pragma unroll 1
-      for (int r = warp; r < Jn; r += NW) {
-        if (c_lo) cp_async8(dT + r * NZT, srcT + (int64_t)r * sI);
-        if (c_hi) cp_async8(dT + r * NZT + 32, srcT + (int64_t)r * sI + 32);
+#pragma unroll
+      for (int it = 0; it < (NYT + NW - 1) / NW; it++) {
+        const int r = warp + it * NW;
+        if (r < Jn) {
+          if (c_lo) cp_async8(dT + r * NZT, srcT + (int64_t)r * sI);
+          if (c_hi) cp_async8(dT + r * NZT + 32, srcT + (int64_t)r * sI + 32);
+        }
       }
     }
   };
@@ -201,11 +213,12 @@ __global__ void __launch_bounds__(CY* CZ, MinBlocks<P>::v) k_xmarch(SArgs A) {
     const double* pe = E + a * Q * Q * NT + tid;
     const double* pc = Ec + a * Q * Q * NT + tid;
     const double* tpl = Tr + (I % NR) * PL + ms0;
-    // plane I's row layout; its lowest node row is a z line end, and the
-    // tile's bottom nodes are a seam only where material lies below
-    const int kmI = pl_kmin(I);
+    // plane I's row layout (staged with its T plane); its lowest node row
+    // is a z line end, and the tile's bottom nodes are a seam only where
+    // material lies below
+    const int kmI = pinfo_k[I % NR];
     const int64_t sI = A.NZ - kmI;
-    const int64_t g0 = pl_base(I) + (int64_t)P * j * sI + P * k;
+    const int64_t g0 = pinfo_b[I % NR] + (int64_t)P * j * sI + P * k;
     const bool zlo = sz_lo && kmI < P * k0;
     const double mz0 = P * k == kmI ? A.imv_end : mz_0;
     static_for<P>([&](auto bb) {

@@ -378,10 +378,11 @@ class GpuSlabStepper:
             done = torch.cuda.Event()
             done.record(self.comm)
         self.stream.wait_event(done)
-        for p in recv.values():  # consumed on the library stream
-            p.f.record_stream(self.stream)
-            if p.c is not None:
-                p.c.record_stream(self.stream)
+        # the received planes are read by this step's seam pass on the
+        # library stream: keep them until the next exchange, whose comm-stream
+        # work is ordered after that seam pass (it waits for the next step's
+        # packed-planes event); no record_stream on the library's stream,
+        # which the context destroys before torch frees these buffers
         self._keep = recv
         return recv
 
