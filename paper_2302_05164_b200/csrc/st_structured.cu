@@ -217,8 +217,9 @@ __global__ void k_fit_pin(SArgs A, int mode, const double* v, double* out, doubl
 }
 
 // ---------------------------------------------------------------------------
-// generic one-thread-per-cell kernels with fp64 atomics (per-call API and
-// the implicit path on structured meshes; not the explicit hot loop)
+// generic one-thread-per-cell kernels (per-call API and the implicit path
+// on structured meshes; not the explicit hot loop): element vectors to a
+// buffer, then a fixed-order node gather (k_sgather) -- deterministic
 // ---------------------------------------------------------------------------
 
 struct GArgs {
@@ -230,6 +231,7 @@ struct GArgs {
   double rc_value;
   double dt;
   double* out;
+  double* E;  // element vectors (n_cells x (p+1)^3), gathered per node by k_sgather
   DevParams P;
 };
 
@@ -295,7 +297,7 @@ __global__ void k_sgeneric(GArgs A, int mode) {
         }
     project3<P>(G);
 #pragma unroll
-    for (int q = 0; q < Q3; q++) atomicAdd(A.out + ids[q], G[q]);
+    for (int q = 0; q < Q3; q++) A.E[cell * Q3 + q] = G[q];
     return;
   }
   // tangent at the Gauss points
@@ -347,7 +349,7 @@ __global__ void k_sgeneric(GArgs A, int mode) {
         }
     project3<P>(G);
 #pragma unroll
-    for (int q = 0; q < Q3; q++) atomicAdd(A.out + ids[q], G[q]);
+    for (int q = 0; q < Q3; q++) A.E[cell * Q3 + q] = G[q];
     return;
   }
   // mode 4: element diagonal
@@ -378,8 +380,39 @@ __global__ void k_sgeneric(GArgs A, int mode) {
       l_ += w3 * dkq[q] * phi * (g0 * gt[0][q] + g1 * gt[1][q] + g2 * gt[2][q]);
     }
     const double val = (PP.rhoc / A.dt) * A.detw0 * m_ + A.hh * d_ + A.detw0 * gs * gs * l_;
-    atomicAdd(A.out + ids[nd], val);
+    A.E[cell * Q3 + nd] = val;
   }
+}
+
+// node sums of the element vectors of k_sgeneric in a fixed order (cells
+// low before high in x, then y, then z): deterministic, no atomics
+template <int P>
+__global__ void k_sgather(GArgs A, const double* __restrict__ E, double* out) {
+  constexpr int Q = P + 1;
+  const int64_t id = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (id >= (int64_t)A.NX * A.NY * A.NZ) return;
+  const int I = (int)(id / ((int64_t)A.NY * A.NZ));
+  const int r = (int)(id - (int64_t)I * A.NY * A.NZ);
+  const int J = r / A.NZ, K = r - (r / A.NZ) * A.NZ;
+  double acc = 0.0;
+#pragma unroll
+  for (int dx = 0; dx < 2; dx++) {
+    const int i = (I % P) ? I / P : I / P - 1 + dx;
+    if ((I % P && dx) || i < 0 || i >= A.nx) continue;
+#pragma unroll
+    for (int dy = 0; dy < 2; dy++) {
+      const int j = (J % P) ? J / P : J / P - 1 + dy;
+      if ((J % P && dy) || j < 0 || j >= A.ny) continue;
+#pragma unroll
+      for (int dz = 0; dz < 2; dz++) {
+        const int k = (K % P) ? K / P : K / P - 1 + dz;
+        if ((K % P && dz) || k < 0 || k >= A.nz) continue;
+        const int64_t cell = ((int64_t)i * A.ny + j) * A.nz + k;
+        acc += E[cell * (Q * Q * Q) + ((I - P * i) * Q + (J - P * j)) * Q + (K - P * k)];
+      }
+    }
+  }
+  out[id] = acc;
 }
 
 // C^-1 of the constant lumped capacity as a tensor product of 1D lumped
@@ -569,6 +602,7 @@ struct Structured : Backend {
   int use_lat = 0;
   long long lx = 0, ly = 0, lz = 0;
   DevBuf<double> cinv, fseam, cseam, lcarry, packf[2], packc[2];
+  DevBuf<double> Eg;  // element vectors of the generic (implicit-path) kernels
   DevBuf<int64_t> sidx;
   DevBuf<unsigned short> scode;
   DevBuf<double> sci;
@@ -990,11 +1024,23 @@ struct Structured : Backend {
     A.out = out;
     const int64_t n = (int64_t)m.nx * m.ny * m.nz;
     const unsigned blocks = (unsigned)((n + 127) / 128);
+    const int64_t q3 = (int64_t)(p + 1) * (p + 1) * (p + 1);
+    if (mode != 0 && (int64_t)Eg.n < n * q3) ST_TRY(Eg.alloc(n * q3));
+    A.E = Eg.p;
     switch (p) {
       case 1: k_sgeneric<1><<<blocks, 128, 0, c->stream>>>(A, mode); break;
       case 2: k_sgeneric<2><<<blocks, 128, 0, c->stream>>>(A, mode); break;
       case 3: k_sgeneric<3><<<blocks, 128, 0, c->stream>>>(A, mode); break;
       default: k_sgeneric<4><<<blocks, 128, 0, c->stream>>>(A, mode); break;
+    }
+    ST_TRY(launched());
+    if (mode == 0) return ST_OK;
+    const unsigned nb = (unsigned)((nv + 255) / 256);
+    switch (p) {
+      case 1: k_sgather<1><<<nb, 256, 0, c->stream>>>(A, Eg.p, out); break;
+      case 2: k_sgather<2><<<nb, 256, 0, c->stream>>>(A, Eg.p, out); break;
+      case 3: k_sgather<3><<<nb, 256, 0, c->stream>>>(A, Eg.p, out); break;
+      default: k_sgather<4><<<nb, 256, 0, c->stream>>>(A, Eg.p, out); break;
     }
     return launched();
   }
@@ -1011,7 +1057,6 @@ struct Structured : Backend {
       return ST_OK;
     }
     if (fitted) return unsupported_fitted("the apparent lumped capacity");
-    ST_CUDA(cudaMemsetAsync(out, 0, nv * sizeof(double), c->stream));
     ST_TRY(generic(1, T, nullptr, nullptr, 0.0, out));
     k_cap_floor<<<(unsigned)((nv + 255) / 256), 256, 0, c->stream>>>(nv, cinv.p, out);
     return launched();
@@ -1019,7 +1064,6 @@ struct Structured : Backend {
 
   int mass(const double* v, double* out) override {
     if (fitted) return unsupported_fitted("apply_mass");
-    ST_CUDA(cudaMemsetAsync(out, 0, nv * sizeof(double), c->stream));
     return generic(2, nullptr, v, nullptr, 0.0, out);
   }
 
@@ -1030,7 +1074,6 @@ struct Structured : Backend {
     ST_TRY(c->vec(5, &vd));
     ST_CUDA(cudaMemcpyAsync(vd, v, nv * sizeof(double), cudaMemcpyDeviceToDevice, c->stream));
     if (m.dirichlet_bottom) ST_TRY(pin_dirichlet(vd, 0.0));
-    ST_CUDA(cudaMemsetAsync(out, 0, nv * sizeof(double), c->stream));
     c->prof_begin();
     ST_TRY(generic(3, Tl, vd, const_cast<double*>(rc), dt, out));
     c->prof_end();
@@ -1044,7 +1087,6 @@ struct Structured : Backend {
 
   int jac_diag(const double* Tl, const double* rc, double dt, double* out) override {
     if (fitted) return unsupported_fitted("jacobian_diagonal");
-    ST_CUDA(cudaMemsetAsync(out, 0, nv * sizeof(double), c->stream));
     ST_TRY(generic(4, Tl, nullptr, const_cast<double*>(rc), dt, out));
     if (m.dirichlet_bottom) ST_TRY(pin_dirichlet(out, 1.0));
     return ST_OK;
