@@ -426,6 +426,14 @@ def implicit_measure(device, n_steps=10, cpu=True):
         nn += out[0]
         nk += out[1]
     el = time.perf_counter() - t0
+    # the PCG solve alone (st_pcg: one persistent cooperative launch on this
+    # backend), krylov_tol 1e-13 for a longer solve
+    rhs = op.evaluate_rhs(T0, rc0, None, faces=False, source=False)
+    rhs[dm.is_dirichlet] = 0.0
+    op.solve_jacobian(rhs, T0, rc0, 1e-3, 1e-13, 2000)
+    tp = time.perf_counter()
+    _, pcg_it, _ = op.solve_jacobian(rhs, T0, rc0, 1e-3, 1e-13, 2000)
+    el_p = time.perf_counter() - tp
     # the explicit scan steps of the same backend (config 3 integrates 40k
     # of them per layer): 2 x 512 device-resident steps of a 1 m/s track
     lp = st.LayerPath(0, 0.0, [st.Segment(5 * h, 20 * h, 35 * h, 20 * h, 1.0, 70.0)], 0.0)
@@ -447,7 +455,12 @@ def implicit_measure(device, n_steps=10, cpu=True):
     res = {"workload": "config3-sized cool-down: 40x40x14 Q1 box, unstructured backend",
            "dofs": int(n), "be_steps": n_steps, "ms_per_be_step": el / n_steps * 1e3,
            "newton_per_step": nn / n_steps, "cg_per_step": nk / n_steps,
-           "us_per_cg_iteration": el / max(nk, 1) * 1e6, **res_e, **res_c}
+           "us_per_cg_iteration": el / max(nk, 1) * 1e6,
+           "pcg_solve": {"iterations": int(pcg_it), "ms": el_p * 1e3,
+                         "us_per_iteration": el_p / max(pcg_it, 1) * 1e6,
+                         "note": "st_pcg alone (krylov_tol 1e-13), wall clock incl. the "
+                                 "vector copies in and out"},
+           **res_e, **res_c}
     if cpu:
         sys.path.insert(0, os.path.join(ROOT, "oracle"))
         from cpu_oracle import OracleOperator, implicit_step, structured_tables

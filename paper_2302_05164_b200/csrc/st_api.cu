@@ -197,6 +197,7 @@ static void ctx_free(st_ctx* c) {
   x.red.free();
   for (auto& s : x.scratch) s.free();
   x.split_ring.free();
+  for (auto& v : x.imp) v.free();
   if (x.ev_iface) cudaEventDestroy(x.ev_iface);
   if (x.stream) cudaStreamDestroy(x.stream);
   delete c;
@@ -812,14 +813,29 @@ int st_explicit_steps(st_ctx* ctx, int n_steps, const double* dts, const st_beam
     }
     const int pending0 = c.history_pending;
     ST_CUDA(cudaMemsetAsync(slots, 0, 2 * nbatch * sizeof(unsigned long long), c.stream));
-    for (int i = 0; i < nbatch; i++) {
-      const int s = b0 + i;
-      ST_TRY(c.be->explicit_step(c.T.p, rc_ptr(c), dts[s], nb, c.beams.p + (int64_t)s * nb,
-                                 c.T_alt.p, c.history_pending,
-                                 reinterpret_cast<double*>(slots + 2 * i)));
-      std::swap(c.T.p, c.T_alt.p);
-      std::swap(c.T.n, c.T_alt.n);
+    // the whole batch as one persistent launch where the backend has one
+    // (unstructured; ST_SCAN_PERSISTENT=0 turns it off), else step by step
+    const int prc = c.be->explicit_steps_persistent(c.T.p, c.T_alt.p, rc_ptr(c), dts + b0,
+                                                    nbatch, nb, c.beams.p + (int64_t)b0 * nb,
+                                                    c.history_pending, slots);
+    if (prc == ST_OK) {
+      if (nbatch & 1) {
+        std::swap(c.T.p, c.T_alt.p);
+        std::swap(c.T.n, c.T_alt.n);
+      }
       c.history_pending = 1;
+    } else if (prc != ST_EUNSUPPORTED) {
+      return prc;
+    } else {
+      for (int i = 0; i < nbatch; i++) {
+        const int s = b0 + i;
+        ST_TRY(c.be->explicit_step(c.T.p, rc_ptr(c), dts[s], nb, c.beams.p + (int64_t)s * nb,
+                                   c.T_alt.p, c.history_pending,
+                                   reinterpret_cast<double*>(slots + 2 * i)));
+        std::swap(c.T.p, c.T_alt.p);
+        std::swap(c.T.n, c.T_alt.n);
+        c.history_pending = 1;
+      }
     }
     ST_CUDA(cudaMemcpyAsync(hs.data(), slots, 2 * nbatch * sizeof(unsigned long long),
                             cudaMemcpyDeviceToHost, c.stream));
@@ -872,16 +888,13 @@ int st_implicit_step(st_ctx* ctx, double dt, double newton_tol, double newton_ab
   ST_TRY(flush_history(c));
   const int64_t nv = c.nv;
   static_assert(sizeof(DevBuf<double>) > 0, "");
-  // vectors: 8..: allocate extra scratch on demand beyond the 8 slots
-  DevBuf<double> Tn, Ti, fre, f, r, tmp, di, delta;
-  ST_TRY(Tn.alloc(nv));
-  ST_TRY(Ti.alloc(nv));
-  ST_TRY(fre.alloc(nv));
-  ST_TRY(f.alloc(nv));
-  ST_TRY(r.alloc(nv));
-  ST_TRY(tmp.alloc(nv));
-  ST_TRY(di.alloc(nv));
-  ST_TRY(delta.alloc(nv));
+  // the step's vectors live in the context (allocated once: a cudaMalloc /
+  // cudaFree pair per vector and step cost more than the step itself at
+  // cool-down mesh sizes)
+  for (auto& v : c.imp)
+    if ((int64_t)v.n < nv) ST_TRY(v.alloc(nv));
+  DevBuf<double>&Tn = c.imp[0], &Ti = c.imp[1], &fre = c.imp[2], &f = c.imp[3], &r = c.imp[4],
+                 &tmp = c.imp[5], &di = c.imp[6], &delta = c.imp[7];
   double* rc = rc_ptr(c);
   ST_CUDA(cudaMemcpyAsync(Tn.p, c.T.p, nv * sizeof(double), cudaMemcpyDeviceToDevice, c.stream));
   ST_CUDA(cudaMemcpyAsync(Ti.p, c.T.p, nv * sizeof(double), cudaMemcpyDeviceToDevice, c.stream));

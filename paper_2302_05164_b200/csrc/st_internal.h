@@ -132,6 +132,16 @@ struct Backend {
   virtual const char* main_kernel() const = 0;
   // r_c == NULL means "the context's uniform history" (structured only)
   virtual bool uniform_rc_ok() const { return false; }
+  // nsteps explicit steps in one persistent launch, ping-ponging Ta / Tb
+  // (step s reads Ta when s is even), per-step maxima into slots[2 s ..];
+  // ST_EUNSUPPORTED: the caller launches step by step
+  virtual int explicit_steps_persistent(double* Ta, double* Tb, double* rc, const double* dts,
+                                        int nsteps, int nb, const DevBeam* beams, int pending0,
+                                        unsigned long long* slots) {
+    (void)Ta, (void)Tb, (void)rc, (void)dts, (void)nsteps, (void)nb, (void)beams, (void)pending0,
+        (void)slots;
+    return ST_EUNSUPPORTED;
+  }
   // the whole Jacobi-PCG solve of J(Tlin) x = b as one persistent launch
   // (thr = tol ||b||); ST_EUNSUPPORTED: the caller runs its kernel loop
   virtual int pcg_persistent(const double* Tl, const double* rc, double dt, const double* b,
@@ -189,6 +199,7 @@ struct Ctx {
   DevBuf<double> pws;       // power iteration: counter, scalars, (ww, vw) history
   cudaGraphExec_t pw_exec = nullptr;  // captured power iteration
   DevBuf<double> scratch[10];
+  DevBuf<double> imp[8];  // backward-Euler step vectors (st_implicit_step)
   double* pinned = nullptr;  // small pinned host staging
   // profiling of the dominant kernel
   int prof = 0;

@@ -109,17 +109,11 @@ __device__ __forceinline__ void gather8(const int* cv, int64_t c, const double* 
 // ---------------------------------------------------------------------------
 // rhs element vectors: -diffusion + faces + sources   (operators.py:247-316)
 // ---------------------------------------------------------------------------
-__global__ void k_rhs_cells(int64_t n, CellGeo g, FaceTab ft, DevParams P,
-                            const double* __restrict__ T, double* rc,
-                            double rc_value, int flags, double frozen_k,
-                            int pending, int nb, const DevBeam* beams,
-                            double* E, double* Ec, double* f_atomic,
-                            double* c_atomic) {
-  // programmatic dependent launch (explicit scan loop): wait for the
-  // previous kernel of the stream in every CTA, then release the next one
-  pdl_wait_release();
-  int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (c >= n) return;
+__device__ __forceinline__ void rhs_cell(int64_t c, const CellGeo& g, const FaceTab& ft,
+                                         const DevParams& P, const double* __restrict__ T,
+                                         double* rc, double rc_value, int flags, double frozen_k,
+                                         int pending, int nb, const DevBeam* beams, double* E,
+                                         double* Ec, double* f_atomic, double* c_atomic) {
   double t[8], e[8];
   gather8(g.cv, c, T, t);
 #pragma unroll
@@ -237,6 +231,21 @@ __global__ void k_rhs_cells(int64_t n, CellGeo g, FaceTab ft, DevParams P,
 #pragma unroll
       for (int i = 0; i < 8; i++) atomicAdd(c_atomic + g.cv[c * 8 + i], ec[i]);
   }
+}
+
+__global__ void k_rhs_cells(int64_t n, CellGeo g, FaceTab ft, DevParams P,
+                            const double* __restrict__ T, double* rc,
+                            double rc_value, int flags, double frozen_k,
+                            int pending, int nb, const DevBeam* beams,
+                            double* E, double* Ec, double* f_atomic,
+                            double* c_atomic) {
+  // programmatic dependent launch (explicit scan loop): wait for the
+  // previous kernel of the stream in every CTA, then release the next one
+  pdl_wait_release();
+  int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (c >= n) return;
+  rhs_cell(c, g, ft, P, T, rc, rc_value, flags, frozen_k, pending, nb, beams, E, Ec, f_atomic,
+           c_atomic);
 }
 
 // consistent capacity apply / lumped capacity (operators.py:325-348):
@@ -509,30 +518,44 @@ struct PcgArgs {
   int* out;            // [iterations, converged]
 };
 
-// deterministic block sum (fixed tree); the total is returned to every thread
-__device__ __forceinline__ double block_sum(double v, double* red) {
-  const int t = threadIdx.x;
-  __syncthreads();
-  red[t] = v;
-  __syncthreads();
+// deterministic block sums of (a, b): an xor butterfly inside each warp
+// (every lane ends with the same bits: a + b == b + a), then the same over
+// the warp totals; the totals are returned to every thread
+__device__ __forceinline__ double2 block_sum2(double a, double b, double2* red) {
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  constexpr int nw = kPcgThreads / 32;
 #pragma unroll
-  for (int s = kPcgThreads / 2; s > 0; s >>= 1) {
-    if (t < s) red[t] += red[t + s];
-    __syncthreads();
+  for (int o = 16; o > 0; o >>= 1) {
+    a += __shfl_xor_sync(0xffffffffu, a, o);
+    b += __shfl_xor_sync(0xffffffffu, b, o);
   }
-  return red[0];
+  __syncthreads();  // red is free (previous use finished)
+  if (lane == 0) red[w] = make_double2(a, b);
+  __syncthreads();
+  double2 v = lane < nw ? red[lane] : make_double2(0.0, 0.0);
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    v.x += __shfl_xor_sync(0xffffffffu, v.x, o);
+    v.y += __shfl_xor_sync(0xffffffffu, v.y, o);
+  }
+  return v;
 }
 
-// sum of the nb block partials at part[0..nb), the same order in every block
-__device__ __forceinline__ double sum_partials(const double* part, int nb, double* red) {
-  double v = 0.0;
-  for (int i = threadIdx.x; i < nb; i += kPcgThreads) v += part[i];
-  return block_sum(v, red);
+// sums of the nb block partials pa[0..nb) and pb[0..nb), the same order in
+// every block
+__device__ __forceinline__ double2 sum_partials2(const double* pa, const double* pb, int nb,
+                                                 double2* red) {
+  double a = 0.0, b = 0.0;
+  for (int i = threadIdx.x; i < nb; i += kPcgThreads) {
+    a += pa[i];
+    b += pb ? pb[i] : 0.0;
+  }
+  return block_sum2(a, b, red);
 }
 
 __global__ void __launch_bounds__(kPcgThreads) k_pcg_persistent(PcgArgs a) {
   cg::grid_group grid = cg::this_grid();
-  __shared__ double red[kPcgThreads];
+  __shared__ double2 red[32];
   const int nb = gridDim.x;
   const int64_t tid = blockIdx.x * (int64_t)kPcgThreads + threadIdx.x;
   const int64_t nth = (int64_t)nb * kPcgThreads;
@@ -548,10 +571,10 @@ __global__ void __launch_bounds__(kPcgThreads) k_pcg_persistent(PcgArgs a) {
     a.p0[i] = zi;
     l += ri * zi;
   }
-  l = block_sum(l, red);
-  if (threadIdx.x == 0) pa[blockIdx.x] = l;
+  double2 t2 = block_sum2(l, 0.0, red);
+  if (threadIdx.x == 0) pa[blockIdx.x] = t2.x;
   grid.sync();
-  double rz = sum_partials(pa, nb, red);
+  double rz = sum_partials2(pa, nullptr, nb, red).x;
   double beta = 0.0;
   double* p = a.p0;
   double* pn = a.p1;
@@ -589,10 +612,10 @@ __global__ void __launch_bounds__(kPcgThreads) k_pcg_persistent(PcgArgs a) {
       a.Ap[v] = ap;
       l += p[v] * ap;
     }
-    l = block_sum(l, red);
-    if (threadIdx.x == 0) pa[nb + blockIdx.x] = l;
+    t2 = block_sum2(l, 0.0, red);
+    if (threadIdx.x == 0) pa[nb + blockIdx.x] = t2.x;
     grid.sync();
-    const double alpha = rz / sum_partials(pa + nb, nb, red);
+    const double alpha = rz / sum_partials2(pa + nb, nullptr, nb, red).x;
     // 4. x, r, z and r.r / r.z
     double lrr = 0.0, lrz = 0.0;
     for (int64_t i = tid; i < a.nv; i += nth) {
@@ -604,13 +627,14 @@ __global__ void __launch_bounds__(kPcgThreads) k_pcg_persistent(PcgArgs a) {
       lrr += ri * ri;
       lrz += ri * zi;
     }
-    lrr = block_sum(lrr, red);
-    if (threadIdx.x == 0) pa[2 * nb + blockIdx.x] = lrr;
-    lrz = block_sum(lrz, red);
-    if (threadIdx.x == 0) pa[3 * nb + blockIdx.x] = lrz;
+    t2 = block_sum2(lrr, lrz, red);
+    if (threadIdx.x == 0) {
+      pa[2 * nb + blockIdx.x] = t2.x;
+      pa[3 * nb + blockIdx.x] = t2.y;
+    }
     grid.sync();
-    const double rr = sum_partials(pa + 2 * nb, nb, red);
-    const double rzn = sum_partials(pa + 3 * nb, nb, red);
+    t2 = sum_partials2(pa + 2 * nb, pa + 3 * nb, nb, red);
+    const double rr = t2.x, rzn = t2.y;
     if (sqrt(rr) <= a.thr) {
       if (tid == 0) {
         a.out[0] = it;
@@ -627,7 +651,29 @@ __global__ void __launch_bounds__(kPcgThreads) k_pcg_persistent(PcgArgs a) {
   }
 }
 
-// forward Euler with the lumped capacity (operators.py:352-369)
+// forward Euler with the lumped capacity (operators.py:352-369) at a
+// non-slave vertex v; returns T'(v)
+__device__ __forceinline__ double step_node(int64_t v, const NodeTab& nt, const double* E,
+                                            const double* Ec, const double* f_atomic,
+                                            const double* c_atomic, const double* cinv,
+                                            const double* T, double dt, double T_inf,
+                                            double* Tout) {
+  double f = E ? gather_condensed(nt, E, v) : f_atomic[v];
+  double ci;
+  if (Ec)
+    ci = 1.0 / gather_condensed(nt, Ec, v);
+  else if (c_atomic)
+    ci = 1.0 / c_atomic[v];
+  else
+    ci = cinv[v];
+  // T + dt (C^-1 f) with the reference's three roundings (no FMA), so a
+  // step equals the host composition of the same pieces bit for bit
+  double out = __dadd_rn(T[v], __dmul_rn(dt, __dmul_rn(ci, f)));
+  if (nt.is_dir[v]) out = T_inf;
+  Tout[v] = out;
+  return out;
+}
+
 __global__ void k_step_nodes(int64_t nv, NodeTab nt, const double* E, const double* Ec,
                              const double* f_atomic, const double* c_atomic,
                              const double* cinv, const double* T, double dt, double T_inf,
@@ -638,32 +684,14 @@ __global__ void k_step_nodes(int64_t nv, NodeTab nt, const double* E, const doub
   int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   double out = 0.0;
   bool live = v < nv && !nt.is_slave[v];
-  if (live) {
-    double f = E ? gather_condensed(nt, E, v) : f_atomic[v];
-    double ci;
-    if (Ec)
-      ci = 1.0 / gather_condensed(nt, Ec, v);
-    else if (c_atomic)
-      ci = 1.0 / c_atomic[v];
-    else
-      ci = cinv[v];
-    // T + dt (C^-1 f) with the reference's three roundings (no FMA), so a
-    // step equals the host composition of the same pieces bit for bit
-    out = __dadd_rn(T[v], __dmul_rn(dt, __dmul_rn(ci, f)));
-    if (nt.is_dir[v]) out = T_inf;
-    Tout[v] = out;
-  }
+  if (live) out = step_node(v, nt, E, Ec, f_atomic, c_atomic, cinv, T, dt, T_inf, Tout);
   block_max2(live ? out : 0.0, live ? out : -INFINITY, red);
 }
 
 // hanging-vertex closure (mesh.py:652-661)
-__global__ void k_distribute(int64_t ns, const int64_t* slaves, const int64_t* ptr,
-                             const int64_t* masters, const double* w, double* v) {
-  // programmatic dependent launch (explicit scan loop): wait for the
-  // previous kernel of the stream in every CTA, then release the next one
-  pdl_wait_release();
-  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (i >= ns) return;
+__device__ __forceinline__ void distribute_slave(int64_t i, const int64_t* slaves,
+                                                 const int64_t* ptr, const int64_t* masters,
+                                                 const double* w, double* v) {
   // the rounding of the reference's segmented sum (numpy add.reduceat:
   // first product, plus the rest summed from zero, 8-lane pairwise blocks
   // beyond 8 terms), every product rounded on its own
@@ -684,6 +712,84 @@ __global__ void k_distribute(int64_t ns, const int64_t* slaves, const int64_t* p
     for (; k < n; k++) rest = __dadd_rn(rest, __dmul_rn(w[b + 1 + k], v[masters[b + 1 + k]]));
   }
   v[slaves[i]] = __dadd_rn(__dmul_rn(w[b], v[masters[b]]), rest);
+}
+
+__global__ void k_distribute(int64_t ns, const int64_t* slaves, const int64_t* ptr,
+                             const int64_t* masters, const double* w, double* v) {
+  // programmatic dependent launch (explicit scan loop): wait for the
+  // previous kernel of the stream in every CTA, then release the next one
+  pdl_wait_release();
+  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= ns) return;
+  distribute_slave(i, slaves, ptr, masters, w, v);
+}
+
+// ---------------------------------------------------------------------------
+// persistent explicit scan (run_scan_phase's step loop, timestepping.py:211-
+// 221) for the unstructured backend: one cooperative launch integrates a
+// batch of steps; per step the cell phase (element vectors, the owed history
+// update first), a grid barrier, the node phase (condensed gather, forward
+// Euler with the lumped capacity, Dirichlet pin, the step's |T| / T maxima
+// into its own slot pair), a grid barrier, the slave closure and a barrier.
+// The same device functions as the per-kernel path, so a step is bitwise the
+// one k_rhs_cells -> k_step_nodes -> k_distribute computes.
+// ---------------------------------------------------------------------------
+constexpr int kScanThreads = 128;
+
+struct ScanArgs {
+  int64_t n, nv, ns;
+  CellGeo g;
+  FaceTab ft;
+  NodeTab nt;
+  DevParams P;
+  double* Ta;  // step s reads Ta when s is even, Tb when odd, writes the other
+  double* Tb;
+  double* rc;
+  double rc_value;
+  int pending0, nsteps, nb, latent;
+  const double* dts;
+  const DevBeam* beams;  // nb per step
+  double* E;
+  double* Ec;
+  const double* cinv;
+  const int64_t* slaves;
+  const int64_t* sptr;
+  const int64_t* smast;
+  const double* sw;
+  unsigned long long* slots;  // 2 per step
+};
+
+__global__ void __launch_bounds__(kScanThreads) k_scan_persistent(ScanArgs a) {
+  cg::grid_group grid = cg::this_grid();
+  const int64_t tid = blockIdx.x * (int64_t)kScanThreads + threadIdx.x;
+  const int64_t nth = (int64_t)gridDim.x * kScanThreads;
+  const int flags = ST_RHS_DIFFUSION | ST_RHS_FACES | ST_RHS_SOURCE;
+  for (int s = 0; s < a.nsteps; s++) {
+    const double* T = (s & 1) ? a.Tb : a.Ta;
+    double* Tout = (s & 1) ? a.Ta : a.Tb;
+    for (int64_t c = tid; c < a.n; c += nth)
+      rhs_cell(c, a.g, a.ft, a.P, T, a.rc, a.rc_value, flags, 0.0, s ? 1 : a.pending0, a.nb,
+               a.beams + (int64_t)s * a.nb, a.E, a.latent ? a.Ec : nullptr, nullptr, nullptr);
+    grid.sync();
+    unsigned long long ka = 0ull;
+    double tm = -INFINITY;
+    const double dt = a.dts[s];
+    for (int64_t v = tid; v < a.nv; v += nth) {
+      if (a.nt.is_slave[v]) continue;
+      const double o = step_node(v, a.nt, a.E, a.latent ? a.Ec : nullptr, nullptr, nullptr,
+                                 a.cinv, T, dt, a.P.T_inf, Tout);
+      const unsigned long long b = (unsigned long long)__double_as_longlong(o) & 0x7fffffffffffffffull;
+      ka = b > ka ? b : ka;
+      tm = o > tm ? o : tm;
+    }
+    block_max2(__longlong_as_double((long long)ka), tm, a.slots + 2 * s);
+    grid.sync();
+    if (a.ns) {
+      for (int64_t i = tid; i < a.ns; i += nth)
+        distribute_slave(i, a.slaves, a.sptr, a.smast, a.sw, Tout);
+      grid.sync();
+    }
+  }
 }
 
 // atomic-mode condensation (fold slave rows into masters, zero slaves)
@@ -875,6 +981,60 @@ struct Unstructured : Backend {
                        dt, c->dp.T_inf, Tout, reinterpret_cast<unsigned long long*>(red)));
     ST_TRY(launched());
     return distribute_pdl(Tout, pdl);
+  }
+
+  DevBuf<double> scan_dts;
+  int scan_blocks = 0;
+
+  int explicit_steps_persistent(double* Ta, double* Tb, double* rc, const double* dts,
+                                int nsteps, int nb, const DevBeam* beams, int pending0,
+                                unsigned long long* slots) override {
+    static const bool off = getenv("ST_SCAN_PERSISTENT") && getenv("ST_SCAN_PERSISTENT")[0] == '0';
+    if (off || !c->deterministic) return ST_EUNSUPPORTED;
+    if (!scan_blocks) {
+      int per_sm = 0, sms = 0;
+      ST_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_scan_persistent,
+                                                            kScanThreads, 0));
+      ST_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c->device));
+      scan_blocks = std::max(1, std::min(per_sm, 4) * sms);
+    }
+    if ((int64_t)scan_dts.n < nsteps) ST_TRY(scan_dts.alloc(std::max(nsteps, 512)));
+    ST_CUDA(cudaMemcpyAsync(scan_dts.p, dts, nsteps * sizeof(double), cudaMemcpyHostToDevice,
+                            c->stream));
+    ScanArgs a{};
+    a.n = n;
+    a.nv = nv;
+    a.ns = ns;
+    a.g = geo();
+    a.ft = faces();
+    a.nt = nodes();
+    a.P = c->dp;
+    a.Ta = Ta;
+    a.Tb = Tb;
+    a.rc = rc;
+    a.rc_value = c->rc_value;
+    a.pending0 = pending0;
+    a.nsteps = nsteps;
+    a.nb = nb;
+    a.latent = c->dp.latent != 0;
+    a.dts = scan_dts.p;
+    a.beams = beams;
+    a.E = E.p;
+    a.Ec = Ec.p;
+    a.cinv = cinv.p;
+    a.slaves = slaves.p;
+    a.sptr = sptr.p;
+    a.smast = smast.p;
+    a.sw = sw.p;
+    a.slots = slots;
+    void* args[] = {&a};
+    c->prof_begin();
+    ST_CUDA(cudaLaunchCooperativeKernel((const void*)k_scan_persistent, dim3(scan_blocks),
+                                        dim3(kScanThreads), args, 0, c->stream));
+    c->prof_end();
+    // the host copy of dts must outlive the async upload
+    ST_CUDA(cudaStreamSynchronize(c->stream));
+    return launched();
   }
 
   int history(const double* T, double* rc) override {
