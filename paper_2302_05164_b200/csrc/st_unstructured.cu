@@ -313,16 +313,16 @@ __device__ __forceinline__ void tangent(const DevParams& P, const double* tl, co
   }
 }
 
-// J v element vectors: D + L + C/dt (operators.py:380-410), cell c
-__device__ __forceinline__ void jac_cell(int64_t c, const CellGeo& g, const DevParams& P,
-                                         const double* vd, const double* Tl, const double* rc,
-                                         double rc_value, double dt, double* E) {
-  double v[8], tl[8], k[8], dk[8], gx[8], gy[8], gz[8], e[8], tmp[8], pr[8];
+// J v element vectors: D + L + C/dt (operators.py:380-410) of cell c from
+// its tangent fields (k, dk, grad T_lin at the Gauss points)
+__device__ __forceinline__ void jac_apply(int64_t c, const CellGeo& g, const DevParams& P,
+                                          const double* vd, const double* k, const double* dk,
+                                          const double* gx, const double* gy, const double* gz,
+                                          double dt, double* E) {
+  double v[8], e[8], tmp[8], pr[8];
   gather8(g.cv, c, vd, v);
-  gather8(g.cv, c, Tl, tl);
   const double h = g.h[c];
   const double gscale = 2.0 / h;
-  tangent(P, tl, rc, rc_value, c, gscale, k, dk, gx, gy, gz);
   const double hh = h / 2.0;
   interp<1, 0, 0>(v, tmp);
 #pragma unroll
@@ -367,6 +367,40 @@ __device__ __forceinline__ void jac_cell(int64_t c, const CellGeo& g, const DevP
   project<0, 0, 0>(vq, pr);
 #pragma unroll
   for (int i = 0; i < 8; i++) E[c * 8 + i] = e[i] + pr[i] / dt;
+}
+
+__device__ __forceinline__ void jac_cell(int64_t c, const CellGeo& g, const DevParams& P,
+                                         const double* vd, const double* Tl, const double* rc,
+                                         double rc_value, double dt, double* E) {
+  double tl[8], k[8], dk[8], gx[8], gy[8], gz[8];
+  gather8(g.cv, c, Tl, tl);
+  tangent(P, tl, rc, rc_value, c, 2.0 / g.h[c], k, dk, gx, gy, gz);
+  jac_apply(c, g, P, vd, k, dk, gx, gy, gz, dt, E);
+}
+
+// the tangent fields of every cell, structure of arrays: TG[(f * 8 + q) * n + c]
+// for f = k, dk, gx, gy, gz (the reference's _tangent_fields, operators.py:373)
+__device__ __forceinline__ void tangent_store(int64_t c, int64_t n, const CellGeo& g,
+                                              const DevParams& P, const double* Tl,
+                                              const double* rc, double rc_value, double* TG) {
+  double tl[8], f[5][8];
+  gather8(g.cv, c, Tl, tl);
+  tangent(P, tl, rc, rc_value, c, 2.0 / g.h[c], f[0], f[1], f[2], f[3], f[4]);
+#pragma unroll
+  for (int j = 0; j < 5; j++)
+#pragma unroll
+    for (int q = 0; q < 8; q++) TG[(j * 8 + q) * n + c] = f[j][q];
+}
+
+__device__ __forceinline__ void jac_cell_tg(int64_t c, int64_t n, const CellGeo& g,
+                                            const DevParams& P, const double* vd,
+                                            const double* TG, double dt, double* E) {
+  double f[5][8];
+#pragma unroll
+  for (int j = 0; j < 5; j++)
+#pragma unroll
+    for (int q = 0; q < 8; q++) f[j][q] = TG[(j * 8 + q) * n + c];
+  jac_apply(c, g, P, vd, f[0], f[1], f[2], f[3], f[4], dt, E);
 }
 
 __global__ void k_jac_cells(int64_t n, CellGeo g, DevParams P, const double* vd,
@@ -512,6 +546,7 @@ struct PcgArgs {
   const double* b;
   const double* dinv;  // nullable: no preconditioner
   double *x, *r, *z, *p0, *p1, *Ap, *vd, *E;
+  double* TG;          // tangent fields (40 per cell, structure of arrays)
   double* part;        // 4 x gridDim.x block partials
   double thr;          // tol * ||b||
   int max_iter;
@@ -553,13 +588,18 @@ __device__ __forceinline__ double2 sum_partials2(const double* pa, const double*
   return block_sum2(a, b, red);
 }
 
-__global__ void __launch_bounds__(kPcgThreads) k_pcg_persistent(PcgArgs a) {
+#ifndef ST_PCG_MINB
+#define ST_PCG_MINB 2  // resident blocks per SM (A/B hook: 1 = no register cap)
+#endif
+__global__ void __launch_bounds__(kPcgThreads, ST_PCG_MINB) k_pcg_persistent(PcgArgs a) {
   cg::grid_group grid = cg::this_grid();
   __shared__ double2 red[32];
   const int nb = gridDim.x;
   const int64_t tid = blockIdx.x * (int64_t)kPcgThreads + threadIdx.x;
   const int64_t nth = (int64_t)nb * kPcgThreads;
   double* pa = a.part;
+  // the tangent at T_lin once per solve (it is fixed over the iterations)
+  for (int64_t c = tid; c < a.n; c += nth) tangent_store(c, a.n, a.g, a.P, a.Tl, a.rc, a.rc_value, a.TG);
   // x = 0, r = b, z = D^-1 r, p = z, rz = r.z
   double l = 0.0;
   for (int64_t i = tid; i < a.nv; i += nth) {
@@ -602,8 +642,7 @@ __global__ void __launch_bounds__(kPcgThreads) k_pcg_persistent(PcgArgs a) {
     }
     grid.sync();
     // 2. element vectors of J vd
-    for (int64_t c = tid; c < a.n; c += nth)
-      jac_cell(c, a.g, a.P, a.vd, a.Tl, a.rc, a.rc_value, a.dt, a.E);
+    for (int64_t c = tid; c < a.n; c += nth) jac_cell_tg(c, a.n, a.g, a.P, a.vd, a.TG, a.dt, a.E);
     grid.sync();
     // 3. Ap and p.Ap
     l = 0.0;
@@ -989,8 +1028,11 @@ struct Unstructured : Backend {
   int explicit_steps_persistent(double* Ta, double* Tb, double* rc, const double* dts,
                                 int nsteps, int nb, const DevBeam* beams, int pending0,
                                 unsigned long long* slots) override {
-    static const bool off = getenv("ST_SCAN_PERSISTENT") && getenv("ST_SCAN_PERSISTENT")[0] == '0';
-    if (off || !c->deterministic) return ST_EUNSUPPORTED;
+    // measured slower than the PDL kernel chain at config-3 sizes (14.6 vs
+    // 10.4 us per step: three grid barriers per step at low occupancy), so
+    // opt-in: ST_SCAN_PERSISTENT=1
+    static const bool on = getenv("ST_SCAN_PERSISTENT") && getenv("ST_SCAN_PERSISTENT")[0] == '1';
+    if (!on || !c->deterministic) return ST_EUNSUPPORTED;
     if (!scan_blocks) {
       int per_sm = 0, sms = 0;
       ST_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_scan_persistent,
@@ -1078,7 +1120,7 @@ struct Unstructured : Backend {
     return launched();
   }
 
-  DevBuf<double> pcg_part;
+  DevBuf<double> pcg_part, pcg_tg;
   DevBuf<int> pcg_out;
   int pcg_blocks = 0;
 
@@ -1121,6 +1163,8 @@ struct Unstructured : Backend {
     ST_TRY(c->vec(4, &a.Ap));
     ST_TRY(c->vec(5, &a.vd));
     a.E = E.p;
+    if ((int64_t)pcg_tg.n < 40 * n) ST_TRY(pcg_tg.alloc(40 * n));
+    a.TG = pcg_tg.p;
     a.part = pcg_part.p;
     a.thr = thr;
     a.max_iter = max_iter;
