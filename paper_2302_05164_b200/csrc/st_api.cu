@@ -325,6 +325,7 @@ static int stage_rc(Ctx& c, const double* rc_host, double** out) {
 static int pcg_dev(Ctx& c, const double* Tl, const double* rc, double dt, const double* b,
                    double tol, int max_iter, const double* diag_inv, double* x, int* iters,
                    int* converged) {
+  NvtxScope nvtx_scope("pcg");
   const int64_t nv = c.nv;
   double *r, *z, *p, *Ap;
   ST_TRY(c.vec(1, &r));
@@ -674,6 +675,7 @@ int st_pcg(st_ctx* ctx, const double* T_lin, const double* rc, double dt, const 
 // launches directly).
 int st_spectral_radius(st_ctx* ctx, double k_frozen, const double* v0, double tol, int max_iter,
                        double* rho, int* iters) {
+  NvtxScope nvtx_scope("st_spectral_radius");
   ST_TRY(check_ctx(ctx));
   Ctx& c = ctx->impl;
   if (!v0 || !rho || !iters || max_iter < 0) {
@@ -787,6 +789,7 @@ static const double kDiverged = 1.0e7;  // timestepping.py:183
 
 int st_explicit_steps(st_ctx* ctx, int n_steps, const double* dts, const st_beam* beams,
                       int n_beams, int* fail_step, double* t_extreme, double* t_max) {
+  NvtxScope nvtx_scope("st_explicit_steps");
   ST_TRY(check_ctx(ctx));
   Ctx& c = ctx->impl;
   ST_TRY(need_state(c));
@@ -882,6 +885,7 @@ int st_explicit_steps(st_ctx* ctx, int n_steps, const double* dts, const st_beam
 int st_implicit_step(st_ctx* ctx, double dt, double newton_tol, double newton_abs_tol,
                      int newton_max_iter, double krylov_tol, int krylov_max_iter, int precond,
                      int* newton_iters, int* krylov_iters, int* converged) {
+  NvtxScope nvtx_scope("st_implicit_step");
   ST_TRY(check_ctx(ctx));
   Ctx& c = ctx->impl;
   ST_TRY(need_state(c));
@@ -1000,6 +1004,7 @@ static int split_slot(Ctx& c, unsigned long long** out) {
 }
 
 int st_explicit_step_begin(st_ctx* ctx, double dt, const st_beam* beams, int n_beams) {
+  NvtxScope nvtx_scope("st_explicit_step_begin");
   ST_TRY(check_ctx(ctx));
   Ctx& c = ctx->impl;
   ST_TRY(need_state(c));
@@ -1036,6 +1041,7 @@ int st_iface_wait(st_ctx* ctx, void* stream) {
 
 int st_explicit_step_end(st_ctx* ctx, const double* recv_lo_f, const double* recv_lo_c,
                          const double* recv_hi_f, const double* recv_hi_c) {
+  NvtxScope nvtx_scope("st_explicit_step_end");
   ST_TRY(check_ctx(ctx));
   Ctx& c = ctx->impl;
   ST_TRY(c.be->step_end(recv_lo_f, recv_lo_c, recv_hi_f, recv_hi_c));

@@ -1,6 +1,7 @@
 // Internal definitions shared by the scantherm_b200 translation units.
 #pragma once
 
+#include <nvtx3/nvToolsExt.h>
 #include <cuda_runtime.h>
 
 #include <cstdint>
@@ -8,6 +9,13 @@
 #include <vector>
 
 #include "../../include/scantherm_b200.h"
+
+// NVTX range for the duration of a scope (header-only NVTX 3: no library to
+// link; free when no profiler is attached)
+struct NvtxScope {
+  explicit NvtxScope(const char* name) { nvtxRangePushA(name); }
+  ~NvtxScope() { nvtxRangePop(); }
+};
 
 namespace st {
 
