@@ -51,6 +51,8 @@ __global__ void __launch_bounds__(CY* CZ, MinBlocks<P>::v) k_xmarch(SArgs A) {
   __shared__ int lat_any[3];  // latent increments per layer (slot i % 3)
   __shared__ long long pinfo_b[NR];  // ring: first node id (- lowest row) of a staged plane
   __shared__ int pinfo_k[NR];        // ring: lowest node row of a staged plane
+  __shared__ long long pf_b[2][P];   // fitted layout of the next layer's planes (prefetch)
+  __shared__ int pf_k[2][P];
   const int tid = threadIdx.x;
   const int lane = tid & 31, warp = tid >> 5;
   // P >= 2: z-major cell order inside the CTA (tid = kl * CY + jl), so the
@@ -89,12 +91,22 @@ __global__ void __launch_bounds__(CY* CZ, MinBlocks<P>::v) k_xmarch(SArgs A) {
   // lane l the row entries l and l + 32 (rows run along z, contiguous)
   static_assert(NZT <= 64, "tile row wider than two warp passes");
   const bool c_lo = lane < Kn, c_hi = NZT > 32 && lane + 32 < Kn;
-  auto load_planes = [&](int Ib, int n) {
+  // a fitted part's plane layout is read from global one layer ahead of the
+  // staging that needs it (pf[layer parity]), so the table loads do not sit
+  // in front of the cp.async issue
+  auto prefetch_layout = [&](int Ib, int buf) {
+    if (A.pbase && tid < P) {
+      pf_b[buf][tid] = A.pbase[Ib + tid];
+      pf_k[buf][tid] = A.pkmin[Ib + tid];
+    }
+  };
+  auto load_planes = [&](int Ib, int n, int buf) {
 #pragma unroll 1
     for (int pa = 0; pa < n; pa++) {
       const int I = Ib + pa;
-      const int kmI = pl_kmin(I);
-      const int64_t bI = pl_base(I);
+      const bool pre = buf >= 0 && A.pbase;
+      const int kmI = pre ? pf_k[buf][pa] : pl_kmin(I);
+      const int64_t bI = pre ? pf_b[buf][pa] : pl_base(I);
       const int64_t sI = A.NZ - kmI;  // row stride of plane I
       // the plane's layout rides along in the ring for its finalisation
       if (tid == 0) {
@@ -233,7 +245,8 @@ __global__ void __launch_bounds__(CY* CZ, MinBlocks<P>::v) k_xmarch(SArgs A) {
   };
 
   // prologue: the first layer's P+1 planes (and its COOP side work)
-  load_planes(P * i0, P + 1);
+  load_planes(P * i0, P + 1, -1);
+  if (i0 + 1 < i1) prefetch_layout(P * (i0 + 1) + 1, (i0 + 1) & 1);
   cp_commit();
   if (COOP) {
     cp_wait<0>();
@@ -252,7 +265,8 @@ __global__ void __launch_bounds__(CY* CZ, MinBlocks<P>::v) k_xmarch(SArgs A) {
     // publishes the facet terms / x factors made during it
     cp_wait<0>();
     __syncthreads();
-    if (i + 1 < i1) load_planes(P * (i + 1) + 1, P);
+    if (i + 1 < i1) load_planes(P * (i + 1) + 1, P, (i + 1) & 1);
+    if (i + 2 < i1) prefetch_layout(P * (i + 2) + 1, i & 1);
     cp_commit();
     if (LATENT && tid == 0) lat_any[(i + 1) % 3] = 0;  // last read by layer i-1
     if (live) {
