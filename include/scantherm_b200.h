@@ -161,6 +161,15 @@ int st_set_uniform_rc(st_ctx* ctx, double value);
  * value >= 1: the history is a fixed point and is never stored), else 0;
  * < 0 on error.  Lets a caller read the state without expanding r_c. */
 int st_get_uniform_rc(st_ctx* ctx, double* value);
+/* Asynchronous snapshot of the resident state (the output / checkpoint
+ * phase, driver.py:275-337, io/vtu.py:58-145, without stalling the step
+ * loop): T (and r_c, after the owed history update; host_rc nullable) is
+ * copied on the device on the context stream and drained to the (pinned)
+ * host buffers on a separate copy stream while later steps run.
+ * st_snapshot_wait returns 1 when the snapshot is on the host (wait != 0
+ * blocks until then), 0 while it is in flight. */
+int st_snapshot_begin(st_ctx* ctx, double* host_T, double* host_rc);
+int st_snapshot_wait(st_ctx* ctx, int wait);
 /* raw device pointer of a resident field (for zero-copy interop) */
 double* st_field_device_ptr(st_ctx* ctx, int field);
 

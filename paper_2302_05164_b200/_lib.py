@@ -111,6 +111,8 @@ SIGNATURES = [
     ("st_set_uniform_rc", ctypes.c_int, [_VP, ctypes.c_double]),
     ("st_get_uniform_rc", ctypes.c_int, [_VP, ctypes.POINTER(ctypes.c_double)]),
     ("st_field_device_ptr", _VP, [_VP, ctypes.c_int]),
+    ("st_snapshot_begin", ctypes.c_int, [_VP, _dp, _dp]),
+    ("st_snapshot_wait", ctypes.c_int, [_VP, ctypes.c_int]),
     ("st_evaluate_rhs", ctypes.c_int,
      [_VP, _dp, _dp, ctypes.c_int, ctypes.c_double, ctypes.POINTER(StBeam),
       ctypes.c_int, _dp]),

@@ -196,6 +196,12 @@ static void ctx_free(st_ctx* c) {
   x.beams.free();
   x.red.free();
   for (auto& s : x.scratch) s.free();
+  if (x.snap_busy && x.ev_snap_done) cudaEventSynchronize(x.ev_snap_done);
+  x.snap_T.free();
+  x.snap_rc.free();
+  if (x.ev_snap_src) cudaEventDestroy(x.ev_snap_src);
+  if (x.ev_snap_done) cudaEventDestroy(x.ev_snap_done);
+  if (x.copy_stream) cudaStreamDestroy(x.copy_stream);
   x.split_ring.free();
   for (auto& v : x.imp) v.free();
   if (x.ev_iface) cudaEventDestroy(x.ev_iface);
@@ -525,6 +531,71 @@ int st_get_field(st_ctx* ctx, int field, double* host, int64_t n) {
   }
   set_error("unknown field");
   return ST_EINVAL;
+}
+
+// Asynchronous snapshot of the resident state (the output / checkpoint
+// phase of run_build, driver.py:275-337, without stalling the step loop): a
+// device-to-device copy of T (and of a stored r_c, after the owed history
+// update) on the context stream, then the device-to-host drain on a separate
+// copy stream that overlaps the steps queued after it.  host_T / host_rc
+// should be pinned for the drain to be asynchronous; host_rc may be NULL; a
+// uniform r_c is written on the host directly.
+int st_snapshot_begin(st_ctx* ctx, double* host_T, double* host_rc) {
+  ST_TRY(check_ctx(ctx));
+  Ctx& c = ctx->impl;
+  ST_TRY(need_state(c));
+  if (!host_T) {
+    set_error("st_snapshot_begin: host_T is NULL");
+    return ST_EINVAL;
+  }
+  if (!c.copy_stream) {
+    ST_CUDA(cudaStreamCreateWithFlags(&c.copy_stream, cudaStreamNonBlocking));
+    ST_CUDA(cudaEventCreateWithFlags(&c.ev_snap_src, cudaEventDisableTiming));
+    ST_CUDA(cudaEventCreateWithFlags(&c.ev_snap_done, cudaEventDisableTiming));
+  }
+  if (c.snap_busy) ST_CUDA(cudaEventSynchronize(c.ev_snap_done));  // one in flight
+  c.snap_busy = 0;
+  const bool want_rc = host_rc != nullptr;
+  const int64_t nrc = c.n_cells * c.qpc;
+  if (want_rc) ST_TRY(flush_history(c));
+  if ((int64_t)c.snap_T.n < c.nv) ST_TRY(c.snap_T.alloc(c.nv));
+  ST_CUDA(cudaMemcpyAsync(c.snap_T.p, c.T.p, c.nv * sizeof(double), cudaMemcpyDeviceToDevice,
+                          c.stream));
+  const bool rc_dev = want_rc && !c.rc_uniform;
+  if (rc_dev) {
+    if ((int64_t)c.snap_rc.n < nrc) ST_TRY(c.snap_rc.alloc(nrc));
+    ST_CUDA(cudaMemcpyAsync(c.snap_rc.p, c.rc.p, nrc * sizeof(double), cudaMemcpyDeviceToDevice,
+                            c.stream));
+  }
+  ST_CUDA(cudaEventRecord(c.ev_snap_src, c.stream));
+  ST_CUDA(cudaStreamWaitEvent(c.copy_stream, c.ev_snap_src, 0));
+  ST_CUDA(cudaMemcpyAsync(host_T, c.snap_T.p, c.nv * sizeof(double), cudaMemcpyDeviceToHost,
+                          c.copy_stream));
+  if (rc_dev)
+    ST_CUDA(cudaMemcpyAsync(host_rc, c.snap_rc.p, nrc * sizeof(double), cudaMemcpyDeviceToHost,
+                            c.copy_stream));
+  if (want_rc && c.rc_uniform)
+    for (int64_t i = 0; i < nrc; i++) host_rc[i] = c.rc_value;
+  ST_CUDA(cudaEventRecord(c.ev_snap_done, c.copy_stream));
+  c.snap_busy = 1;
+  return ST_OK;
+}
+
+// 1 when the last snapshot has reached the host (wait != 0: block until it
+// has), 0 while it is in flight
+int st_snapshot_wait(st_ctx* ctx, int wait) {
+  ST_TRY(check_ctx(ctx));
+  Ctx& c = ctx->impl;
+  if (!c.snap_busy) return 1;
+  if (wait) {
+    ST_CUDA(cudaEventSynchronize(c.ev_snap_done));
+  } else {
+    const cudaError_t e = cudaEventQuery(c.ev_snap_done);
+    if (e == cudaErrorNotReady) return 0;
+    ST_CUDA(e);
+  }
+  c.snap_busy = 0;
+  return 1;
 }
 
 double* st_field_device_ptr(st_ctx* ctx, int field) {

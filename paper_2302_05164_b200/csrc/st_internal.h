@@ -208,6 +208,12 @@ struct Ctx {
   cudaGraphExec_t pw_exec = nullptr;  // captured power iteration
   DevBuf<double> scratch[10];
   DevBuf<double> imp[8];  // backward-Euler step vectors (st_implicit_step)
+  // asynchronous snapshot (st_snapshot_begin / _wait): device copies of T
+  // and r_c, drained to the host on a copy stream while stepping continues
+  DevBuf<double> snap_T, snap_rc;
+  cudaStream_t copy_stream = nullptr;
+  cudaEvent_t ev_snap_src = nullptr, ev_snap_done = nullptr;
+  int snap_busy = 0;
   double* pinned = nullptr;  // small pinned host staging
   // profiling of the dominant kernel
   int prof = 0;

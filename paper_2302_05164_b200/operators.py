@@ -405,6 +405,32 @@ class ThermalOperator:
                                                                           r_c_shape)
         return T, rc
 
+    def snapshot(self, T_out, r_c_out=None):
+        """Start an asynchronous snapshot of the resident state into the
+        caller's arrays (pinned host memory keeps it asynchronous): the
+        device copy is ordered after the steps queued so far, the drain to
+        the host overlaps the steps queued after it.  Complete it with
+        :meth:`snapshot_wait` before reading the arrays."""
+        if T_out.dtype != np.float64 or T_out.shape != (self.nv,) or \
+                not T_out.flags["C_CONTIGUOUS"]:
+            raise ValueError("T_out must be a contiguous float64 array of n_vertices")
+        rc = None
+        if r_c_out is not None:
+            if r_c_out.dtype != np.float64 or r_c_out.size != self.n_cells * self.qpc or \
+                    not r_c_out.flags["C_CONTIGUOUS"]:
+                raise ValueError("r_c_out must be a contiguous float64 array of n_cells * qp")
+            rc = r_c_out.reshape(-1)
+        self._snap = (T_out, r_c_out)  # keep the buffers alive until the drain ends
+        _lib.check(self._lib.st_snapshot_begin(self._ctx, _lib.dptr(T_out), _lib.dptr(rc)),
+                   "snapshot")
+
+    def snapshot_wait(self, block=True):
+        """True when the last snapshot is on the host (block: wait for it)."""
+        r = self._lib.st_snapshot_wait(self._ctx, int(bool(block)))
+        if r < 0:
+            _lib.check(r, "snapshot_wait")
+        return bool(r)
+
     def run_explicit(self, dts, beams):
         """Forward-Euler steps on the resident state (timestepping.py:211-221).
 
