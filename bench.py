@@ -558,6 +558,44 @@ def config3_build_measure(cpu=True):
     return res
 
 
+def snapshot_measure(device, steps=60):
+    """the output / checkpoint phase as an asynchronous
+    snapshot.  Config 1, K device-resident steps in one st_explicit_steps
+    call, with and without a snapshot of T (into pinned host memory) taken
+    after the first third: wall clock of the whole call sequence (the
+    drain overlaps the steps queued after the snapshot)."""
+    import torch
+    st = _st()
+    w = workload_config1()
+    box = build_part(w)
+    op = st.ThermalOperator(box, box, w["params"], st.SolverSettings(), device=device)
+    dts, beams = schedule(w, steps)
+    T0 = w["T0"](box.n_vertices)
+    buf = torch.empty(op.nv, dtype=torch.float64, pin_memory=True).numpy()
+    k = steps // 3
+    res = {}
+    for with_snap in (False, True, False, True):
+        op.set_state(T0, 1.0)
+        t0 = time.perf_counter()
+        op.run_explicit(dts[:k], beams[:k])
+        if with_snap:
+            op.snapshot(buf)
+        op.run_explicit(dts[k:], beams[k:])
+        if with_snap:
+            op.snapshot_wait()
+        res["with_snapshot" if with_snap else "without"] = (time.perf_counter() - t0) * 1e3
+    Tk = None
+    op.set_state(T0, 1.0)
+    op.run_explicit(dts[:k], beams[:k])
+    Tk, _ = op.get_state()
+    op.close()
+    return {"workload": w["name"], "steps": steps, "snapshot_after": k,
+            "ms_without": res["without"], "ms_with_snapshot": res["with_snapshot"],
+            "snapshot_bytes": int(buf.nbytes), "snapshot_equals_state": bool(np.array_equal(buf, Tk)),
+            "note": "wall clock of the K-step sequence; the snapshot's D2H drain runs on a copy "
+                    "stream while the later steps run"}
+
+
 def measure_summary(r, steps):
     return {"dofs": r["box"].n_dofs,
             "value": r["box"].n_dofs * steps / (float(np.sum(r["step_ms"])) * 1e-3),
@@ -650,6 +688,7 @@ def run_ours(args):
     if rank == 0 and ws == 1 and args.sweep:
         out["implicit_config3"] = implicit_measure(local, cpu=not args.no_cpu_baseline)
         out["config3_build"] = config3_build_measure(cpu=not args.no_cpu_baseline)
+        out["snapshot_config1"] = snapshot_measure(local)
     if rank == 0 and ws == 1 and not args.no_cpu_baseline:
         out["cpu_baseline"] = cpu_baseline(w, seconds=args.cpu_seconds)
     if rank == 0:
