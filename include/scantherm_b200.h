@@ -77,6 +77,14 @@ typedef struct st_beam {
   int32_t _pad;
 } st_beam;
 
+/* One straight scan segment (reference physics.py:32 Segment) with the
+ * values the reference derives from it: length (np.hypot), duration
+ * (length / v) and the start time within its layer path (the running
+ * sum of the earlier durations), all as the caller's Python computes them. */
+typedef struct st_segment {
+  double x0, y0, x1, y1, v, power, length, duration, t_start;
+} st_segment;
+
 /* Tables of an arbitrary (adaptive, hanging-node) Q1 mesh: reference
  * DofMap (mesh.py:619-638) + per-cell geometry (operators.py:104-112)
  * + facet quadrature (operators.py:118-134, FaceSet mesh.py:980). */
@@ -161,6 +169,20 @@ int st_set_uniform_rc(st_ctx* ctx, double value);
  * value >= 1: the history is a fixed point and is never stored), else 0;
  * < 0 on error.  Lets a caller read the state without expanding r_c. */
 int st_get_uniform_rc(st_ctx* ctx, double* value);
+/* A layer's scan phase (run_scan_phase, timestepping.py:195-226) with the
+ * beam schedule evaluated on the device: n_paths concurrently scanned
+ * layer paths (seg_count[k] segments each, concatenated in segs; beam z
+ * z_top[k]), steps step0 .. step0+n_steps-1 at tau = (step-1) dt with
+ * dt_step = min(dt, duration - tau); layer_beam_state's closed windows
+ * (physics.py:135-151).  Otherwise as st_explicit_steps. */
+int st_scan_layer(st_ctx* ctx, int n_steps, int step0, double dt, double duration, int n_paths,
+                  const int32_t* seg_count, const st_segment* segs, const double* z_top,
+                  int* fail_step, double* t_extreme, double* t_max);
+/* the device-evaluated beam records of those steps (n_steps x n_paths) */
+int st_beam_schedule(st_ctx* ctx, int n_steps, int step0, double dt, int n_paths,
+                     const int32_t* seg_count, const st_segment* segs, const double* z_top,
+                     st_beam* out);
+
 /* Asynchronous snapshot of the resident state (the output / checkpoint
  * phase, driver.py:275-337, io/vtu.py:58-145, without stalling the step
  * loop): T (and r_c, after the owed history update; host_rc nullable) is

@@ -77,6 +77,11 @@ class StStructuredMesh(ctypes.Structure):
                 ("xext", _i32p)]
 
 
+class StSegment(ctypes.Structure):
+    _fields_ = [(n, ctypes.c_double) for n in
+                ("x0", "y0", "x1", "y1", "v", "power", "length", "duration", "t_start")]
+
+
 class StLeaves(ctypes.Structure):
     _fields_ = [("n", ctypes.c_int64), ("depth", ctypes.c_int32), ("cpl", ctypes.c_int32),
                 ("level", ctypes.POINTER(ctypes.c_int8)), ("anchor", _i64p),
@@ -112,6 +117,12 @@ SIGNATURES = [
     ("st_get_uniform_rc", ctypes.c_int, [_VP, ctypes.POINTER(ctypes.c_double)]),
     ("st_field_device_ptr", _VP, [_VP, ctypes.c_int]),
     ("st_snapshot_begin", ctypes.c_int, [_VP, _dp, _dp]),
+    ("st_scan_layer", ctypes.c_int,
+     [_VP, ctypes.c_int, ctypes.c_int, ctypes.c_double, ctypes.c_double, ctypes.c_int, _i32p,
+      ctypes.POINTER(StSegment), _dp, ctypes.POINTER(ctypes.c_int), _dp, _dp]),
+    ("st_beam_schedule", ctypes.c_int,
+     [_VP, ctypes.c_int, ctypes.c_int, ctypes.c_double, ctypes.c_int, _i32p,
+      ctypes.POINTER(StSegment), _dp, ctypes.POINTER(StBeam)]),
     ("st_snapshot_wait", ctypes.c_int, [_VP, ctypes.c_int]),
     ("st_evaluate_rhs", ctypes.c_int,
      [_VP, _dp, _dp, ctypes.c_int, ctypes.c_double, ctypes.POINTER(StBeam),

@@ -858,6 +858,9 @@ int st_spectral_radius(st_ctx* ctx, double k_frozen, const double* v0, double to
 // ---------------------------------------------------------------------------
 static const double kDiverged = 1.0e7;  // timestepping.py:183
 
+static int explicit_steps_resident(Ctx& c, int n_steps, const double* dts, int nb,
+                                   int* fail_step, double* t_extreme, double* t_max);
+
 int st_explicit_steps(st_ctx* ctx, int n_steps, const double* dts, const st_beam* beams,
                       int n_beams, int* fail_step, double* t_extreme, double* t_max) {
   NvtxScope nvtx_scope("st_explicit_steps");
@@ -868,6 +871,136 @@ int st_explicit_steps(st_ctx* ctx, int n_steps, const double* dts, const st_beam
   if (n_steps <= 0) return ST_OK;
   const int nb = beams ? n_beams : 0;
   ST_TRY(c.upload_beams(beams, (int64_t)n_steps * nb));
+  return explicit_steps_resident(c, n_steps, dts, nb, fail_step, t_extreme, t_max);
+}
+
+// ---------------------------------------------------------------------------
+// device beam schedule (physics.py:135-151 layer_beam_state at tau = (step-1)
+// dt for every step of a scan phase, several concurrently scanned paths):
+// one thread per (step, path); closed segment windows, first match, the
+// reference's float expressions with explicit roundings (no FMA), so the
+// records equal the host expansion (flatten_schedule) bit for bit.
+// ---------------------------------------------------------------------------
+struct SegDev {
+  double x0, y0, x1, y1, v, power, length, duration, t_start;
+};
+
+__global__ void k_beam_schedule(const SegDev* __restrict__ segs, const int* __restrict__ seg_off,
+                                const double* __restrict__ z_top, int n_paths, int step0,
+                                int n_steps, double dt, double denom, st_beam* recs,
+                                DevBeam* dev) {
+  const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (t >= (int64_t)n_steps * n_paths) return;
+  const int i = (int)(t / n_paths), k = (int)(t - (int64_t)i * n_paths);
+  const double tau = __dmul_rn((double)(step0 + i - 1), dt);
+  st_beam r;
+  r.x = 0.0;
+  r.y = 0.0;
+  r.z_top = z_top[k];
+  r.power = 0.0;
+  r.active = 0;
+  r._pad = 0;
+  for (int sg = seg_off[k]; sg < seg_off[k + 1]; sg++) {
+    const SegDev g = segs[sg];
+    if (g.t_start <= tau && tau <= __dadd_rn(g.t_start, g.duration)) {
+      const double sv = __dmul_rn(__dsub_rn(tau, g.t_start), g.v);
+      const double frac = g.length > 0.0 ? __ddiv_rn(sv, g.length) : 0.0;
+      r.x = __dadd_rn(g.x0, __dmul_rn(frac, __dsub_rn(g.x1, g.x0)));
+      r.y = __dadd_rn(g.y0, __dmul_rn(frac, __dsub_rn(g.y1, g.y0)));
+      r.power = g.power;
+      r.active = g.power > 0.0 ? 1 : 0;
+      break;
+    }
+  }
+  if (recs) recs[t] = r;
+  if (dev) {
+    DevBeam b;
+    b.x = r.x;
+    b.y = r.y;
+    b.z_top = r.z_top;
+    b.peak = r.active ? __ddiv_rn(__dmul_rn(2.0, r.power), denom) : 0.0;
+    dev[t] = b;
+  }
+}
+
+static int beam_schedule(Ctx& c, int n_steps, int step0, double dt, int n_paths,
+                         const int32_t* seg_count, const st_segment* segs, const double* z_top,
+                         st_beam* recs_dev) {
+  if (n_paths < 0 || (n_paths > 0 && (!seg_count || !z_top))) {
+    set_error("beam schedule: invalid paths");
+    return ST_EINVAL;
+  }
+  std::vector<int> off(n_paths + 1, 0);
+  for (int k = 0; k < n_paths; k++) off[k + 1] = off[k] + seg_count[k];
+  std::vector<SegDev> hs(std::max(off[n_paths], 1));
+  for (int q = 0; q < off[n_paths]; q++) {
+    const st_segment& g = segs[q];
+    hs[q] = SegDev{g.x0, g.y0, g.x1, g.y1, g.v, g.power, g.length, g.duration, g.t_start};
+  }
+  DevBuf<SegDev> dsegs;
+  DevBuf<int> doff;
+  DevBuf<double> dz;
+  ST_TRY(dsegs.upload(hs.data(), hs.size(), c.stream));
+  ST_TRY(doff.upload(off.data(), off.size(), c.stream));
+  ST_TRY(dz.upload(z_top, std::max(n_paths, 1), c.stream));
+  const int64_t n = (int64_t)n_steps * n_paths;
+  if (!recs_dev && (int64_t)c.beams.n < n) ST_TRY(c.beams.alloc(n));
+  const double R = c.params.las.radius, hp = c.params.las.h_powder;
+  const double denom = M_PI * R * R * hp;
+  if (n > 0) {
+    k_beam_schedule<<<(unsigned)((n + 255) / 256), 256, 0, c.stream>>>(
+        dsegs.p, doff.p, dz.p, n_paths, step0, n_steps, dt, denom, recs_dev,
+        recs_dev ? nullptr : c.beams.p);
+    ST_LAUNCHED();
+    c.launches++;
+  }
+  // the staging buffers die here
+  ST_CUDA(cudaStreamSynchronize(c.stream));
+  return ST_OK;
+}
+
+int st_beam_schedule(st_ctx* ctx, int n_steps, int step0, double dt, int n_paths,
+                     const int32_t* seg_count, const st_segment* segs, const double* z_top,
+                     st_beam* out) {
+  ST_TRY(check_ctx(ctx));
+  Ctx& c = ctx->impl;
+  if (!out || n_steps < 0) {
+    set_error("st_beam_schedule: invalid arguments");
+    return ST_EINVAL;
+  }
+  const int64_t n = (int64_t)n_steps * n_paths;
+  DevBuf<st_beam> recs;
+  ST_TRY(recs.alloc(std::max<int64_t>(n, 1)));
+  ST_TRY(beam_schedule(c, n_steps, step0, dt, n_paths, seg_count, segs, z_top, recs.p));
+  if (n) ST_CUDA(cudaMemcpyAsync(out, recs.p, n * sizeof(st_beam), cudaMemcpyDeviceToHost, c.stream));
+  ST_CUDA(cudaStreamSynchronize(c.stream));
+  return ST_OK;
+}
+
+int st_scan_layer(st_ctx* ctx, int n_steps, int step0, double dt, double duration, int n_paths,
+                  const int32_t* seg_count, const st_segment* segs, const double* z_top,
+                  int* fail_step, double* t_extreme, double* t_max) {
+  NvtxScope nvtx_scope("st_scan_layer");
+  ST_TRY(check_ctx(ctx));
+  Ctx& c = ctx->impl;
+  ST_TRY(need_state(c));
+  if (fail_step) *fail_step = 0;
+  if (n_steps <= 0) return ST_OK;
+  // the step sizes on the host (the last step is clipped to the scan end,
+  // timestepping.py:210-213): dt = min(dt, duration - tau)
+  std::vector<double> dts(n_steps);
+  for (int i = 0; i < n_steps; i++) {
+    const double tau = (double)(step0 + i - 1) * dt;
+    dts[i] = std::min(dt, duration - tau);
+  }
+  ST_TRY(beam_schedule(c, n_steps, step0, dt, n_paths, seg_count, segs, z_top, nullptr));
+  return explicit_steps_resident(c, n_steps, dts.data(), n_paths, fail_step, t_extreme, t_max);
+}
+
+// the step loop over beams already resident in c.beams (nb per step)
+static int explicit_steps_resident(Ctx& c, int n_steps, const double* dts, int nb,
+                                   int* fail_step, double* t_extreme, double* t_max) {
+  if (fail_step) *fail_step = 0;
   if ((int64_t)c.T_alt.n < c.nv) ST_TRY(c.T_alt.alloc(c.nv));
   const int64_t nrc = c.rc_uniform ? 0 : c.n_cells * c.qpc;
   const int kBatch = 512;

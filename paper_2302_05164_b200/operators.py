@@ -405,6 +405,39 @@ class ThermalOperator:
                                                                           r_c_shape)
         return T, rc
 
+    def _seg_args(self, layer_paths):
+        from .physics import segment_table
+        counts, segs, z = segment_table(layer_paths)
+        keep = (counts, segs if len(segs) else np.zeros((1, 9)), z)
+        return keep, (len(counts), keep[0].ctypes.data_as(ctypes.POINTER(ctypes.c_int32)),
+                      keep[1].ctypes.data_as(ctypes.POINTER(_lib.StSegment)), _lib.dptr(keep[2]))
+
+    def run_scan(self, layer_paths, dt, n_steps, step0=1):
+        """Forward-Euler steps step0 .. step0+n_steps-1 of a scan phase on
+        the resident state with the beams of ``layer_paths`` (one or several
+        concurrently scanned LayerPaths) evaluated on the device
+        (st_scan_layer).  Returns (fail_step, t_extreme, t_max)."""
+        paths = layer_paths if isinstance(layer_paths, (list, tuple)) else [layer_paths]
+        keep, (np_, cnt, seg, z) = self._seg_args(paths)
+        fail, ext, tmax = ctypes.c_int(), ctypes.c_double(), ctypes.c_double()
+        _lib.check(self._lib.st_scan_layer(self._ctx, int(n_steps), int(step0), float(dt),
+                                           float(paths[0].scan_duration()), np_, cnt, seg, z,
+                                           ctypes.byref(fail), ctypes.byref(ext),
+                                           ctypes.byref(tmax)), "scan_layer")
+        return fail.value, ext.value, tmax.value
+
+    def beam_schedule(self, layer_paths, dt, n_steps, step0=1):
+        """The device-evaluated beam records (n_steps, n_paths) BEAM_DTYPE."""
+        from .physics import BEAM_DTYPE
+        paths = layer_paths if isinstance(layer_paths, (list, tuple)) else [layer_paths]
+        keep, (np_, cnt, seg, z) = self._seg_args(paths)
+        out = np.zeros((int(n_steps), np_), dtype=BEAM_DTYPE)
+        _lib.check(self._lib.st_beam_schedule(self._ctx, int(n_steps), int(step0), float(dt), np_,
+                                              cnt, seg, z,
+                                              out.ctypes.data_as(ctypes.POINTER(_lib.StBeam))),
+                   "beam_schedule")
+        return out
+
     def snapshot(self, T_out, r_c_out=None):
         """Start an asynchronous snapshot of the resident state into the
         caller's arrays (pinned host memory keeps it asynchronous): the

@@ -191,3 +191,24 @@ def flatten_schedule_loop(layer_paths, dt, n_steps, step0=1):
         dts[i] = min(dt, duration - tau)
         beams[i] = pack_beams([layer_beam_state(lp, tau) for lp in layer_paths])
     return dts, beams
+
+
+def segment_table(layer_paths):
+    """Device beam schedule input (st_scan_layer / st_beam_schedule): per
+    path the segment count, then every segment with the length, duration
+    and start time the reference derives for it (Segment.length /
+    .duration and layer_beam_state's running t_seg, physics.py:135-151),
+    computed here in Python so the device sees the same doubles."""
+    if not isinstance(layer_paths, (list, tuple)):
+        layer_paths = [layer_paths]
+    counts = np.array([len(lp.segments) for lp in layer_paths], dtype=np.int32)
+    rows = []
+    for lp in layer_paths:
+        t_seg = 0.0
+        for seg in lp.segments:
+            d = seg.duration
+            rows.append((seg.x0, seg.y0, seg.x1, seg.y1, seg.v, seg.power, seg.length, d, t_seg))
+            t_seg += d
+    segs = np.array(rows, dtype=np.float64).reshape(-1, 9)
+    z = np.array([float(lp.z) for lp in layer_paths], dtype=np.float64)
+    return counts, np.ascontiguousarray(segs), z

@@ -22,7 +22,7 @@ from dataclasses import dataclass, field
 
 import numpy as np
 
-from .physics import flatten_schedule
+from .physics import ScheduleError, flatten_schedule
 
 
 class InstabilityError(RuntimeError):
@@ -88,9 +88,16 @@ def run_scan_phase(state, layer_path, dt, on_step=None) -> PhaseStats:
     duration = _scan_duration(layer_path)
     n_steps = max(0, math.ceil(duration / dt - 1e-9))
     if on_step is None and n_steps:
-        dts, beams = flatten_schedule(layer_path, dt, n_steps)
+        dts, _ = flatten_schedule(layer_path, dt, 1)  # validates the schedule's start
+        paths = layer_path if isinstance(layer_path, (list, tuple)) else [layer_path]
+        for lp in paths:   # layer_beam_state raises past the layer (physics.py:150)
+            if (n_steps - 1) * dt > lp.duration():
+                raise ScheduleError(f"tau = {(n_steps - 1) * dt} beyond the layer duration "
+                                    f"{lp.duration()}")
+        dts = np.minimum(dt, duration - np.arange(n_steps, dtype=np.float64) * dt)
         op.set_state(state.T, state.history.r_c)
-        fail, ext, tmax = op.run_explicit(dts, beams)
+        # the whole layer on the device, beams evaluated there per step
+        fail, ext, tmax = op.run_scan(layer_path, dt, n_steps)
         T, rc = op.get_state()
         state.T = T
         state.history.r_c[...] = rc.reshape(state.history.r_c.shape)
