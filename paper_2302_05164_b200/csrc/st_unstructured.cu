@@ -477,6 +477,11 @@ struct NodeTab {
   const double* cond_w;
   const uint8_t* is_slave;
   const uint8_t* is_dir;
+  // the condensation flattened per master: the incident entries of its
+  // slaves in cond order (cfe_ptr / cfe) and each slave's entry count (cgl)
+  const int* cfe_ptr;
+  const int* cfe;
+  const int* cgl;
 };
 
 // sum of the element entries incident to vertex v, in incidence order
@@ -499,11 +504,36 @@ __device__ __forceinline__ double gather_v(const NodeTab& nt, const double* E, i
   return acc;
 }
 
-// condensed sum at a non-slave vertex (bincount then np.add.at order)
+// condensed sum at a non-slave vertex (bincount then np.add.at order):
+// f = own entries, then f + w * (the slave's entries) per folded slave.  The
+// slaves' entries come from the flattened table, all indices then all
+// entries loaded up front (up to 32), the same sums in the same order.
 __device__ __forceinline__ double gather_condensed(const NodeTab& nt, const double* E, int64_t v) {
   double f = gather_v(nt, E, v);
-  for (int i = nt.cond_ptr[v]; i < nt.cond_ptr[v + 1]; i++)
-    f = f + nt.cond_w[i] * gather_v(nt, E, nt.cond_s[i]);
+  const int ga = nt.cond_ptr[v], gb = nt.cond_ptr[v + 1];
+  if (ga == gb) return f;
+  const int e0 = nt.cfe_ptr[v], ne = nt.cfe_ptr[v + 1] - e0;
+  constexpr int kMax = 32;
+  if (ne <= kMax) {
+    int ix[kMax];
+    double e[kMax];
+#pragma unroll
+    for (int k = 0; k < kMax; k++) ix[k] = k < ne ? nt.cfe[e0 + k] : 0;
+#pragma unroll
+    for (int k = 0; k < kMax; k++) e[k] = k < ne ? E[ix[k]] : 0.0;
+    int k = 0;
+    for (int g = ga; g < gb; g++) {
+      const int len = nt.cgl[g];
+      double sv = 0.0;
+#pragma unroll
+      for (int q = 0; q < kMax; q++)
+        if (q >= k && q < k + len) sv += e[q];
+      k += len;
+      f = f + nt.cond_w[g] * sv;
+    }
+    return f;
+  }
+  for (int i = ga; i < gb; i++) f = f + nt.cond_w[i] * gather_v(nt, E, nt.cond_s[i]);
   return f;
 }
 
@@ -926,6 +956,7 @@ static inline unsigned nblk_cells(int64_t n) {
 struct Unstructured : Backend {
   int64_t n = 0, nv = 0, ns = 0, nf = 0;
   DevBuf<int> cv, inc_ptr, inc_ent, cond_ptr, cond_s, face_ptr, touched_pos, fold_ptr, fold_ent;
+  DevBuf<int> cfe_ptr, cfe, cgl;
   DevBuf<double> h, anc, detw, cond_w, fvx, fvy, farea, cinv, E, Ec, Ae, fold_w;
   DevBuf<uint8_t> is_slave, is_dir;
   DevBuf<int64_t> slaves, sptr, smast;
@@ -935,7 +966,8 @@ struct Unstructured : Backend {
   CellGeo geo() const { return CellGeo{cv.p, h.p, anc.p, detw.p}; }
   FaceTab faces() const { return FaceTab{nf ? face_ptr.p : nullptr, fvx.p, fvy.p, farea.p}; }
   NodeTab nodes() const {
-    return NodeTab{inc_ptr.p, inc_ent.p, cond_ptr.p, cond_s.p, cond_w.p, is_slave.p, is_dir.p};
+    return NodeTab{inc_ptr.p, inc_ent.p, cond_ptr.p, cond_s.p, cond_w.p, is_slave.p, is_dir.p,
+                   cfe_ptr.p, cfe.p, cgl.p};
   }
 
   int launched() {
@@ -1313,6 +1345,20 @@ static int build_unstructured(Unstructured* u, Ctx* c, const st_unstructured_mes
     cs.push_back(0);
     cw.push_back(0.0);
   }
+  // the condensation flattened per master (gather_condensed): each folded
+  // slave's incident entries in cond order, and the entry count per slave
+  std::vector<int> cfp(nv + 1, 0), cfe, cgl(cs.size(), 0);
+  for (int64_t v = 0; v < nv; v++) {
+    cfp[v + 1] = cfp[v];
+    if (!ns) continue;
+    for (int i = cp[v]; i < cp[v + 1]; i++) {
+      const int sl = cs[i];
+      cgl[i] = ip[sl + 1] - ip[sl];
+      for (int q = ip[sl]; q < ip[sl + 1]; q++) cfe.push_back(ie[q]);
+      cfp[v + 1] += cgl[i];
+    }
+  }
+  if (cfe.empty()) cfe.push_back(0);
   // per-cell face CSR (faces sorted by cell)
   std::vector<int> fp(n + 1, 0);
   for (int64_t f = 0; f < nf; f++) {
@@ -1414,6 +1460,9 @@ static int build_unstructured(Unstructured* u, Ctx* c, const st_unstructured_mes
   ST_TRY(u->cond_ptr.upload(cp.data(), nv + 1, s));
   ST_TRY(u->cond_s.upload(cs.data(), cs.size(), s));
   ST_TRY(u->cond_w.upload(cw.data(), cw.size(), s));
+  ST_TRY(u->cfe_ptr.upload(cfp.data(), nv + 1, s));
+  ST_TRY(u->cfe.upload(cfe.data(), cfe.size(), s));
+  ST_TRY(u->cgl.upload(cgl.data(), cgl.size(), s));
   ST_TRY(u->face_ptr.upload(fp.data(), n + 1, s));
   if (nf) {
     ST_TRY(u->fvx.upload(m->face_vx, 4 * nf, s));
