@@ -18,6 +18,44 @@
 // interval in this or the previous layer.
 #pragma once
 
+#ifndef ST_LAT_NOINLINE
+#define ST_LAT_NOINLINE 0  // A/B hook: the rare latent projection out of line (measured: the call saves
+                           // ~170 live registers, 2.7 KB of stack, and the code grows 6.2k -> 7.2k)
+#endif
+
+// apparent-capacity increments rho L/dT_lat of one cell, projected from its
+// Gauss points inside the latent interval (the rare path of k_xmarch, kept
+// out of line so the hot loop's code stays small): the Gauss-point
+// temperatures are recomputed from the staged node planes, the x face is
+// carried in lcar, the element planes a < P go to ec[q * NT]
+template <int P, int NT, int NZT, int PL, int NR>
+__device__ __noinline__ void latent_cell(const SArgs& A, const double* Tr, int ib, int ms0,
+                                         double* lcar, bool lat_had, double* ec) {
+  constexpr int Q = P + 1;
+  constexpr int Q3 = Q * Q * Q;
+  constexpr int EW = P * Q * Q;
+  double t[Q3];
+#pragma unroll
+  for (int a = 0; a < Q; a++) {
+    const double* tp = Tr + ((ib + a) % NR) * PL + ms0;
+#pragma unroll
+    for (int b = 0; b < Q; b++)
+#pragma unroll
+      for (int c = 0; c < Q; c++) t[(a * Q + b) * Q + c] = tp[b * NZT + c];
+  }
+  interp3<P>(t);
+#pragma unroll
+  for (int q = 0; q < Q3; q++) t[q] = fabs(t[q] - A.lat_mid) < A.lat_half ? A.lw3[q] : 0.0;
+  project3<P>(t);
+#pragma unroll
+  for (int q = 0; q < Q * Q; q++) {
+    if (lat_had) t[q] += lcar[q * NT];
+    lcar[q * NT] = t[P * Q * Q + q];
+  }
+#pragma unroll
+  for (int q = 0; q < EW; q++) ec[q * NT] = t[q];
+}
+
 template <int P>
 struct MinBlocks {
   static constexpr int v = P == 1 ? 2 : (P == 2 ? 3 : 1);
@@ -299,7 +337,10 @@ __global__ void __launch_bounds__(CY* CZ, MinBlocks<P>::v) k_xmarch(SArgs A) {
         // points inside the latent interval (G is dead here, so t can be
         // reused); a predicate pass first, most cells have none
         const bool lat = any_abs_lt<Q3>(t, A.lat_mid, A.lat_half);
-        if (lat) {
+        if (ST_LAT_NOINLINE && lat) {
+          lat_any[i % 3] = 1;
+          latent_cell<P, NT, NZT, PL, NR>(A, Tr, P * i, ms0, lcar, lat_had, Ec + tid);
+        } else if (lat) {
           lat_any[i % 3] = 1;
 #pragma unroll
           for (int q = 0; q < Q3; q++) t[q] = fabs(t[q] - A.lat_mid) < A.lat_half ? A.lw3[q] : 0.0;
@@ -315,9 +356,11 @@ __global__ void __launch_bounds__(CY* CZ, MinBlocks<P>::v) k_xmarch(SArgs A) {
 #pragma unroll
           for (int q = Q * Q; q < EW; q++) t[q] = 0.0;
         }
-        lat_had = lat;
+        if (!(ST_LAT_NOINLINE && lat)) {  // (the out-of-line path stored its own)
 #pragma unroll
-        for (int q = 0; q < EW; q++) Ec[q * NT + tid] = t[q];
+          for (int q = 0; q < EW; q++) Ec[q * NT + tid] = t[q];
+        }
+        lat_had = lat;
       }
     }
     cp_wait<0>();  // the next layer's planes (prefetched at the top) have landed
