@@ -56,6 +56,10 @@ __device__ __noinline__ void latent_cell(const SArgs& A, const double* Tr, int i
   for (int q = 0; q < EW; q++) ec[q * NT] = t[q];
 }
 
+#ifndef ST_ROWSTORE
+#define ST_ROWSTORE 1  // A/B hook: T' staged in the ring and written out as whole rows
+#endif
+
 template <int P>
 struct MinBlocks {
   static constexpr int v = P == 1 ? 2 : (P == 2 ? 3 : 1);
@@ -242,14 +246,47 @@ __global__ void __launch_bounds__(CY* CZ, MinBlocks<P>::v) k_xmarch(SArgs A) {
     const double o = finalize_node(A, ci, c == 0 && k == 0, tpl[b * NZT + c], f, dc, LATENT);
     const int slot = (xc == 2 ? 1 : 0) + (ys_lo ? 2 : 0) + (zs_lo ? 4 : 0);
     const int64_t so = (int64_t)slot * A.snv + idx;
-    *(seam ? A.fseam + so : A.out + idx) = seam ? f : o;
-    if (LATENT && seam) A.cseam[so] = dc;
+    if (ST_ROWSTORE) {
+      // the update goes back into the staged plane (T of this node is no
+      // longer needed); the plane leaves as whole coalesced rows
+      // (store_planes) -- a seam node's row entry is then a stale T that the
+      // seam pass overwrites
+      if (seam) {
+        A.fseam[so] = f;
+        if (LATENT) A.cseam[so] = dc;
+      } else {
+        const_cast<double*>(tpl)[b * NZT + c] = o;
+      }
+    } else {
+      *(seam ? A.fseam + so : A.out + idx) = seam ? f : o;
+      if (LATENT && seam) A.cseam[so] = dc;
+    }
     if (!seam) {
       const unsigned long long ab = (unsigned long long)__double_as_longlong(o) & 0x7fffffffffffffffull;
       amaxb = ab > amaxb ? ab : amaxb;
       smax = dmax(smax, o);
     }
   };
+
+  // a finished plane from the ring to T' as whole rows, the
+  // staging's own row / lane mapping (so the prefetch that reuses a slot
+  // next is ordered after these reads in every thread, no barrier needed);
+  // cb / ck: the planes' layout, read from the ring before it is rewritten
+  auto store_plane = [&](int I, long long base, int km) {
+    const int64_t sI = A.NZ - km;
+    double* dst = A.out + base + (int64_t)P * j0 * sI + P * k0 + lane;
+    const double* src = Tr + (I % NR) * PL + lane;
+#pragma unroll
+    for (int it = 0; it < (NYT + NW - 1) / NW; it++) {
+      const int r = warp + it * NW;
+      if (r < Jn) {
+        if (c_lo) dst[(int64_t)r * sI] = src[r * NZT];
+        if (c_hi) dst[(int64_t)r * sI + 32] = src[r * NZT + 32];
+      }
+    }
+  };
+  long long cb[P];  // layout of the planes finalised in the previous layer
+  int ck[P];
 
   // every node of plane I owned by this thread (element plane a)
   auto finalize_owned = [&](int I, int a, int xc, bool latn) {
@@ -303,6 +340,9 @@ __global__ void __launch_bounds__(CY* CZ, MinBlocks<P>::v) k_xmarch(SArgs A) {
     // publishes the facet terms / x factors made during it
     cp_wait<0>();
     __syncthreads();
+    if (ST_ROWSTORE && i > i0)
+#pragma unroll
+      for (int a = 0; a < P; a++) store_plane(P * (i - 1) + a, cb[a], ck[a]);
     if (i + 1 < i1) load_planes(P * (i + 1) + 1, P, (i + 1) & 1);
     if (i + 2 < i1) prefetch_layout(P * (i + 2) + 1, i & 1);
     cp_commit();
@@ -368,12 +408,22 @@ __global__ void __launch_bounds__(CY* CZ, MinBlocks<P>::v) k_xmarch(SArgs A) {
     if (COOP && i + 1 < i1) side_work(i + 1);
     // latent increments of this layer or carried from the previous one
     const bool latn = LATENT && (lat_any[i % 3] | lat_any[(i + 2) % 3]);
+#pragma unroll
+    for (int a = 0; a < P; a++) {
+      cb[a] = pinfo_b[(P * i + a) % NR];
+      ck[a] = pinfo_k[(P * i + a) % NR];
+    }
 #pragma unroll 1
     for (int a = 0; a < P; a++)
       finalize_owned(P * i + a, a, (a == 0 && i == i0 && (i0 > 0 || A.iface_lo)) ? 2 : 0, latn);
   }
   cp_wait<0>();
   __syncthreads();  // the last layer's finalisation is done with E
+  const long long cbl = pinfo_b[(P * i1) % NR];
+  const int ckl = pinfo_k[(P * i1) % NR];
+  if (ST_ROWSTORE)
+#pragma unroll
+    for (int a = 0; a < P; a++) store_plane(P * (i1 - 1) + a, cb[a], ck[a]);
   // last node plane of the chunk: the carried x face (as element plane 0)
   if (live) {
 #pragma unroll
@@ -385,5 +435,9 @@ __global__ void __launch_bounds__(CY* CZ, MinBlocks<P>::v) k_xmarch(SArgs A) {
   __syncthreads();
   finalize_owned(P * i1, 0, (i1 < ext || (A.iface_hi && ext == A.nx)) ? 1 : 0,
                  LATENT && lat_any[(i1 - 1) % 3] != 0);
+  if (ST_ROWSTORE) {
+    __syncthreads();
+    store_plane(P * i1, cbl, ckl);
+  }
   block_max2(__longlong_as_double((long long)amaxb), smax, A.red);
 }
