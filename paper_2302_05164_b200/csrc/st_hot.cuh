@@ -49,8 +49,37 @@ static constexpr size_t march_smem() {
          sizeof(double);
 }
 
+// the lean Q2 explicit-step kernel (k_xmarch2) replaces k_xmarch<2> for
+// explicit steps with a uniform history (ST_XMARCH2=0: the general kernel)
+static inline bool use_xmarch2() {
+  const char* e = getenv("ST_XMARCH2");  // read per launch: tests toggle it
+  return !(e && e[0] == '0');
+}
+static constexpr size_t march2_smem() {
+  constexpr int P = 2, CY = 8, CZ = 16, Q = 3;
+  return (size_t)((2 * P + 1) * (P * CY + 1) * (P * CZ + 1) + P * Q * Q * (CY + 2) * (CZ + 2) +
+                  Q * Q * CY * CZ + (CY + CZ + 1) * kMaxTabBeams * Q + 2 * CY * Q * Q) *
+         sizeof(double);
+}
+
 template <int P, bool LAT>
-static cudaError_t hot_kernel(bool slab, bool rcf, const void** fn, size_t* smem, int* threads) {
+static cudaError_t hot_kernel(bool slab, bool rcf, bool x2, const void** fn, size_t* smem,
+                              int* threads) {
+#if ST_HOT_P == 2
+  {
+    if (x2) {
+      *fn = (const void*)k_xmarch2<LAT>;
+      *smem = march2_smem();
+      *threads = 128;
+      static bool attr2 = false;
+      if (attr2) return cudaSuccess;
+      cudaError_t e =
+          cudaFuncSetAttribute(*fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)*smem);
+      attr2 = e == cudaSuccess;
+      return e;
+    }
+  }
+#endif
   if (slab) {
     constexpr int CY = SlabTile<P>::CY, CZ = SlabTile<P>::CZ;
     *fn = rcf ? (const void*)k_xslab<P, CY, CZ, LAT, true> : (const void*)k_xslab<P, CY, CZ, LAT, false>;
@@ -75,8 +104,9 @@ int hot_resident(bool slab, bool lat) {
   const void* fn;
   size_t smem;
   int threads, nb = 0;
-  cudaError_t e = lat ? hot_kernel<P, true>(slab, false, &fn, &smem, &threads)
-                      : hot_kernel<P, false>(slab, false, &fn, &smem, &threads);
+  const bool x2 = P == 2 && !slab && use_xmarch2();
+  cudaError_t e = lat ? hot_kernel<P, true>(slab, false, x2, &fn, &smem, &threads)
+                      : hot_kernel<P, false>(slab, false, x2, &fn, &smem, &threads);
   if (e == cudaSuccess) cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, fn, threads, smem);
   cudaGetLastError();
   return nb > 0 ? nb : 1;
@@ -88,8 +118,10 @@ cudaError_t hot_launch(const SArgs& A, bool slab, bool lat, bool rcf, dim3 grid,
   const void* fn;
   size_t smem;
   int threads;
-  cudaError_t e = lat ? hot_kernel<P, true>(slab, rcf, &fn, &smem, &threads)
-                      : hot_kernel<P, false>(slab, rcf, &fn, &smem, &threads);
+  const bool x2 = P == 2 && !slab && !rcf && A.mode == 0 &&
+                  A.flags == (ST_RHS_DIFFUSION | ST_RHS_FACES | ST_RHS_SOURCE) && use_xmarch2();
+  cudaError_t e = lat ? hot_kernel<P, true>(slab, rcf, x2, &fn, &smem, &threads)
+                      : hot_kernel<P, false>(slab, rcf, x2, &fn, &smem, &threads);
   if (e != cudaSuccess) return e;
   void* args[] = {const_cast<SArgs*>(&A)};
   return cudaLaunchKernel(fn, grid, dim3(threads), args, smem, stream);

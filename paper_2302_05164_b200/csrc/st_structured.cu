@@ -601,7 +601,7 @@ struct Structured : Backend {
   bool slab = false;  // k_xslab (p+1 threads per cell) instead of k_xmarch
   int use_lat = 0;
   long long lx = 0, ly = 0, lz = 0;
-  DevBuf<double> cinv, fseam, cseam, lcarry, packf[2], packc[2];
+  DevBuf<double> cinv, fseam, cseam, lcarry, ecg, packf[2], packc[2];
   DevBuf<double> Eg;  // element vectors of the generic (implicit-path) kernels
   DevBuf<int64_t> sidx;
   DevBuf<unsigned short> scode;
@@ -651,6 +651,7 @@ struct Structured : Backend {
     A.cseam = cseam.p;
     A.seam_pair = slab && c->dp.latent ? 1 : 0;
     A.lcarry = lcarry.p;
+    A.ecg = ecg.p;
     A.snv = nv;
     for (int sd = 0; sd < 2; sd++) {
       A.ipf[sd] = packf[sd].p;
@@ -668,6 +669,17 @@ struct Structured : Backend {
     A.glo = -d.T_s * d.inv_dT_l;
     A.lat_mid = 0.5 * (d.T_lat_s + d.T_lat_l);
     A.lat_half = 0.5 * (d.T_lat_l - d.T_lat_s);
+    {
+      // high words of the interval ends, widened by one (k_xmarch2's
+      // candidate window; positive temperatures)
+      auto hiword = [](double x) {
+        long long b;
+        memcpy(&b, &x, 8);
+        return (int)(b >> 32);
+      };
+      A.lat_hi0 = hiword(A.lat_mid - A.lat_half) - 1;
+      A.lat_hiw = hiword(A.lat_mid + A.lat_half) + 1 - A.lat_hi0;
+    }
     const int q = p + 1;
     std::vector<double> w(q), m1(q);
     switch (p) {
@@ -1277,6 +1289,8 @@ Backend* make_structured(Ctx* c, const st_structured_mesh* m, int* err) {
     const size_t ctas = (size_t)((m->ny + s->cy - 1) / s->cy) * ((m->nz + s->cz - 1) / s->cz) *
                         ((m->nx + s->Lx - 1) / s->Lx);
     rc = s->lcarry.alloc(ctas * s->cy * s->cz * (s->p + 1) * (s->p + 1));
+    if (rc == ST_OK && s->p == 2)
+      rc = s->ecg.alloc(ctas * s->cy * s->cz * s->p * (s->p + 1) * (s->p + 1));
   }
   if (rc == ST_OK &&
       cudaMemsetAsync(s->fseam.p, 0, nseam * sizeof(double), c->stream) != cudaSuccess)

@@ -40,6 +40,11 @@ struct SArgs {
   // k_xmarch latent x-face carry, per (CTA, thread) slot (Q^2 doubles
   // entry-major); only touched by cells with latent Gauss points
   double* lcarry;
+  // k_xmarch2: latent increments of the cells that have any, per (CTA,
+  // entry, thread) (global scratch, L2 resident), and the latent interval as
+  // a window of high words (candidates for the exact test)
+  double* ecg;
+  int lat_hi0, lat_hiw;
   int64_t snv;
   // rank interfaces: own pre-summed plane (packed after the sweep) and the
   // neighbour's, per side (0: local plane 0, 1: local plane NX-1)

@@ -394,6 +394,9 @@ __device__ __forceinline__ void static_for(F&& f) {
   static_for_(f, std::make_integer_sequence<int, N>{});
 }
 #include "st_xmarch_kernel.cuh"
+#if ST_HOT_P == 2
+#include "st_xmarch2_kernel.cuh"
+#endif
 #include "st_xslab_kernel.cuh"
 
 }  // namespace st

@@ -1,0 +1,502 @@
+// k_xmarch2: the lean Q2 explicit-step kernel (included from st_xmarch.cuh).
+//
+// Same scheme and the same arithmetic as k_xmarch<2, 8, 16, LATENT, false> in
+// explicit-step mode (one CTA = an 8 x 16 cell (y, z) tile marching over an x
+// chunk, one thread per cell, cell_element in registers, element planes in
+// shared memory, fixed-order gathers, seam partials to the CTA's slots), with
+// the per-layer work around the cell evaluation rebuilt for instruction
+// count (the kernel is issue bound: ncu of k_xmarch showed 28 % of all warp
+// instructions in the node finalisation and 11 % in the plane staging):
+//   * element entries are stored with a ring of zero ghost cells around the
+//     tile, so the <= 4 contributions of a node are summed without
+//     neighbour tests;
+//   * every thread finalises the four nodes (b, c < 2) of its cell with no
+//     seam logic: T' is stored unconditionally (a seam node's value there
+//     is overwritten by the seam pass, which runs after this kernel) and
+//     only the stability maxima are predicated;
+//   * the tile's perimeter nodes (seam partials of the low edges, the high
+//     edges) are a dense second pass, one node per lane, instead of
+//     divergent per-thread branches in every warp;
+//   * the staging keeps one running row pointer per plane and copies the
+//     33rd column with one instruction of one warp;
+//   * the stability maxima are only updated by nodes whose high word
+//     reaches the running maximum's;
+//   * the latent check is an integer window test on the high words (exact
+//     test only for candidates); the rare latent increments live in an
+//     L2-resident global scratch instead of 18 KB of shared memory.
+// Results are bitwise those of k_xmarch (except the sign of exact zeros).
+#pragma once
+
+template <bool LATENT>
+__global__ void __launch_bounds__(128, 3) k_xmarch2(SArgs A) {
+  constexpr int P = 2, Q = 3, Q3 = 27, CY = 8, CZ = 16, NT = 128, NW = 4;
+  constexpr int NYT = P * CY + 1, NZT = P * CZ + 1, PL = NYT * NZT;
+  constexpr int NR = 2 * P + 1;
+  constexpr int EW = P * Q * Q;
+  // padded cell index of the element arrays: (kl + 1) * ES + jl + 1, ghost
+  // cells at jl = -1, CY and kl = -1, CZ stay zero
+  constexpr int ES = CY + 2, EN = ES * (CZ + 2);
+  constexpr int MB = kMaxTabBeams;
+  constexpr int NPER = 2 * NZT + 2 * (NYT - 2);
+  extern __shared__ double sm[];
+  double* Tr = sm;              // NR planes of T
+  double* E = Tr + NR * PL;     // E[q * EN + cp]
+  double* Cx = E + EW * EN;     // x face carried to the next layer, Cx[q * NT + tid]
+  double* Sy = Cx + Q * Q * NT;          // [CY][MB][Q]
+  double* Sz = Sy + CY * MB * Q;         // [CZ][MB][Q]
+  double* Sx = Sz + CZ * MB * Q;         // [MB][Q], current layer
+  double* Fq = Sx + MB * Q;              // [CY][Q * Q] facet fluxes
+  double* Fo = Fq + CY * Q * Q;          // [CY][Q * Q] facet node terms
+  __shared__ long long pinfo_b[NR];  // ring: first node id (- lowest row) of a staged plane
+  __shared__ int pinfo_k[NR];        // ring: lowest node row of a staged plane
+  __shared__ long long pf_b[2][P];   // fitted layout of the next layer's planes (prefetch)
+  __shared__ int pf_k[2][P];
+  __shared__ unsigned short peri[NPER];  // perimeter nodes of the tile, J << 8 | K
+  // per-thread constants and running maxima, kept out of the register
+  // budget of the cell evaluation: inverse 1D masses of the cell's low
+  // corner, max |T'| (bit pattern) and max T'
+  __shared__ double rec_my[NT], rec_mz[NT], rec_smax[NT];
+  __shared__ unsigned long long rec_amax[NT];
+  __shared__ unsigned char latf[LATENT ? EN : 1];  // cell has latent increments this layer
+
+  const int tid = threadIdx.x;
+  const int lane = tid & 31, warp = tid >> 5;
+  const int kl = tid / CY, jl = tid % CY;  // z-major cell order
+  const int chunk = blockIdx.z + A.zoff;
+  const int j0 = blockIdx.x * CY, k0 = blockIdx.y * CZ, i0 = chunk * A.Lx;
+  const int ext = A.text ? A.text[blockIdx.y] : A.nx;
+  if (i0 >= ext) return;
+  const int i1 = min(i0 + A.Lx, ext);
+  const int j = j0 + jl, k = k0 + kl;
+  const bool live = j < A.ny && k < A.nz;
+  const int Jn = min(P * CY, P * (A.ny - j0)) + 1;
+  const int Kn = min(P * CZ, P * (A.nz - k0)) + 1;
+  const int nper = 2 * Kn + 2 * (Jn - 2);
+  // tile-edge node lines are seams unless they are the domain boundary
+  const bool ty_lo = j0 > 0, ty_hi = j0 + CY < A.ny;
+  const bool tz_lo = k0 > 0, tz_hi = k0 + CZ < A.nz;
+  const CellFlags F{true, true, A.nb > 0, false};
+  const int64_t plane_stride = (int64_t)A.NY * A.NZ;
+  const int ms0 = P * jl * NZT + P * kl;
+  const int cp = (kl + 1) * ES + jl + 1;
+
+  // zero the element arrays once (ghost and dead cells are never written)
+  for (int e = tid; e < EW * EN; e += NT) E[e] = 0.0;
+  if (LATENT)
+    for (int e = tid; e < EN; e += NT) latf[e] = 0;
+  // perimeter list: rows J = 0 and Jn-1, then columns K = 0 and Kn-1
+  for (int e = tid; e < nper; e += NT) {
+    int J, K;
+    if (e < Kn) {
+      J = 0, K = e;
+    } else if (e < 2 * Kn) {
+      J = Jn - 1, K = e - Kn;
+    } else if (e < 2 * Kn + Jn - 2) {
+      J = e - 2 * Kn + 1, K = 0;
+    } else {
+      J = e - (2 * Kn + Jn - 2) + 1, K = Kn - 1;
+    }
+    peri[e] = (unsigned short)((J << 8) | K);
+  }
+
+  // (asynchronous copies in the staging's commit group: no load sits in
+  // front of the barrier)
+  auto prefetch_layout = [&](int Ib, int buf) {
+    if (A.pbase && tid < P) {
+      asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(
+                       (unsigned)__cvta_generic_to_shared(&pf_b[buf][tid])),
+                   "l"(A.pbase + Ib + tid)
+                   : "memory");
+      asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(
+                       (unsigned)__cvta_generic_to_shared(&pf_k[buf][tid])),
+                   "l"(A.pkmin + Ib + tid)
+                   : "memory");
+    }
+  };
+  // stage plane I into ring slot rs: warp w copies tile rows w, w + 4, ...
+  // (lane l the row entry l), one running row pointer; the 33rd column goes
+  // with one instruction of warp 1 (lane l the row l)
+  const bool c_lo = lane < Kn;
+  const unsigned tr_s = (unsigned)__cvta_generic_to_shared(Tr);
+  auto load_plane = [&](int I, int rs, long long bI, int kmI) {
+    const int sI = A.NZ - kmI;
+    if (tid == 0) {
+      pinfo_b[rs] = bI;
+      pinfo_k[rs] = kmI;
+    }
+    const double* src = A.T + bI + (int64_t)(P * j0 + warp) * sI + P * k0 + lane;
+    const unsigned dst = tr_s + (unsigned)((rs * PL + warp * NZT + lane) * 8);
+#pragma unroll
+    for (int it = 0; it < (NYT + NW - 1) / NW; it++) {
+      if (c_lo && warp + it * NW < Jn)
+        asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(dst + it * NW * NZT * 8),
+                     "l"(src)
+                     : "memory");
+      src += NW * sI;
+    }
+    if (warp == 1 && Kn == NZT && lane < Jn) {
+      const double* s2 = A.T + bI + (int64_t)(P * j0 + lane) * sI + P * k0 + (NZT - 1);
+      asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(
+                       tr_s + (unsigned)((rs * PL + lane * NZT + NZT - 1) * 8)),
+                   "l"(s2)
+                   : "memory");
+    }
+  };
+  auto plane_layout = [&](int I, long long& bI, int& kmI) {
+    bI = A.pbase ? A.pbase[I] : (int64_t)I * plane_stride;
+    kmI = A.pkmin ? A.pkmin[I] : 0;
+  };
+
+  // 1D lumped inverse-mass factors of this thread's cell corner in y and z
+  rec_my[tid] = inv_mass1<P>(A, P * j, A.NY);
+  rec_mz[tid] = inv_mass1<P>(A, P * k, A.NZ);
+  rec_amax[tid] = 0ull;
+  rec_smax[tid] = -INFINITY;
+  const double imr1 = A.imr[1];
+
+#pragma unroll
+  for (int q = 0; q < Q * Q; q++) Cx[q * NT + tid] = 0.0;
+  const int64_t cta = ((int64_t)chunk * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x;
+  double* lcar = LATENT ? A.lcarry + cta * (Q * Q * NT) + tid : nullptr;
+  double* ecg = LATENT ? A.ecg + cta * (EW * NT) : nullptr;  // [q * NT + cell]
+  bool lat_had = false;
+  const unsigned ymask = F.source && live ? beam_column_mask<P>(A, j, k) : 0u;
+  const int nbt = (F.source && __syncthreads_or(ymask != 0u)) ? min(A.nb, MB) : 0;
+  for (int e = tid; e < nbt * CY; e += NT) {
+    const int b = e / CY, r = e - (e / CY) * CY;
+    src_factor_xy<P>(A, anchor<P>(A, 1, j0 + r), A.beams[b].y, Sy + (r * MB + b) * Q);
+  }
+  for (int e = tid; e < nbt * CZ; e += NT) {
+    const int b = e / CZ, r = e - (e / CZ) * CZ;
+    src_factor_z<P>(A, anchor<P>(A, 2, k0 + r), A.beams[b], Sz + (r * MB + b) * Q);
+  }
+  const int kl_top = A.nz - 1 - k0;
+  const bool has_top = A.top_faces && kl_top < CZ;
+  constexpr int CPW = (CY + NW - 1) / NW;
+  auto side_work = [&](int il, int rs0) {
+    if (has_top) {
+      face_phase<P>(A, lane, min(warp * CPW, CY), min(warp * CPW + CPW, CY), Fq, Fo,
+                    [&](int r, int a, int b) {
+                      int rs = rs0 + a;
+                      rs = rs >= NR ? rs - NR : rs;
+                      return Tr[rs * PL + P * r * NZT + P * kl_top + b * NZT + P];
+                    });
+    }
+    if (tid < nbt) src_factor_xy<P>(A, anchor<P>(A, 0, il), A.beams[tid].x, Sx + tid * Q);
+  };
+
+  // stability maxima (rec_amax: |T'| as its bit pattern, rec_smax: max T'):
+  // thr = high word a node must reach to be able to raise either (smax <=
+  // amax), so the exact update is a rare branch
+  int thr = 0;
+  auto track_exact = [&](double o) {
+    const unsigned long long ab =
+        (unsigned long long)__double_as_longlong(o) & 0x7fffffffffffffffull;
+    const unsigned long long am = rec_amax[tid];
+    const double sm_ = rec_smax[tid];
+    rec_amax[tid] = ab > am ? ab : am;
+    const double s2 = dmax(sm_, o);
+    rec_smax[tid] = s2;
+    thr = max(__double2hiint(s2), 0);
+  };
+  auto habs = [](double o) { return __double2hiint(o) & 0x7fffffff; };
+  auto track = [&](double o) {
+    if (habs(o) >= thr) track_exact(o);
+  };
+
+  // latent increment of a node: the contributions of the (<= 4) cells around
+  // it in the gather's order; cells without increments count as zero
+  auto latent_sum = [&](int cpn, int tn, int a, int b, int c) {
+    // tn: thread (cell) id of the own cell of the node (may be a ghost)
+    double dc = 0.0;
+    if (latf[cpn]) dc = __ldcg(ecg + (a * 9 + b * 3 + c) * NT + tn);
+    if (b == 0 && latf[cpn - 1]) dc += __ldcg(ecg + (a * 9 + 6 + c) * NT + tn - 1);
+    if (c == 0 && latf[cpn - ES]) dc += __ldcg(ecg + (a * 9 + b * 3 + 2) * NT + tn - CY);
+    if (b == 0 && c == 0 && latf[cpn - ES - 1]) dc += __ldcg(ecg + (a * 9 + 8) * NT + tn - CY - 1);
+    return dc;
+  };
+
+  // x factor of the inverse lumped mass of plane I (times 1 / (rho c detw))
+  auto plane_imx = [&](int I) {
+    const int G = I + A.gI0;
+    const bool xend = G == 0 || G == A.gNX - 1 || (ext < A.nx && I == P * ext);
+    const double imx = (I & 1) ? imr1 : (xend ? A.imv_end : A.imv_int);
+    return imx * A.inv_rcdw;
+  };
+
+  // the four nodes (b, c < 2) of this thread's cell in plane I (element
+  // plane a, ring slot rs); xc: 0 = ordinary plane, 1 / 2 = x seam with this
+  // CTA on the low / high side (every node of the plane is a seam then)
+  auto finalize_cell = [&](int I, int a, int rs, int xc, bool latn) {
+    if (!live) return;
+    const double imIs = plane_imx(I);
+    const int kmI = pinfo_k[rs];
+    const int sI = A.NZ - kmI;
+    const int64_t g0 = pinfo_b[rs] + (int64_t)(P * j * sI + P * k);
+    const bool s_y = jl == 0 && ty_lo;                      // b = 0 nodes on a y seam
+    const bool s_z = kl == 0 && tz_lo && kmI < P * k0;      // c = 0 nodes on a z seam
+    const double* e = E + a * 9 * EN + cp;
+    double f00 = e[0 * EN];
+    f00 += e[6 * EN - 1];
+    f00 += e[2 * EN - ES];
+    f00 += e[8 * EN - ES - 1];
+    double f01 = e[1 * EN];
+    f01 += e[7 * EN - 1];
+    double f10 = e[3 * EN];
+    f10 += e[5 * EN - ES];
+    const double f11 = e[4 * EN];
+    double d00 = 0.0, d01 = 0.0, d10 = 0.0, d11 = 0.0;
+    if (LATENT && latn) {
+      d00 = latent_sum(cp, tid, a, 0, 0);
+      d01 = latent_sum(cp, tid, a, 0, 1);
+      d10 = latent_sum(cp, tid, a, 1, 0);
+      d11 = latent_sum(cp, tid, a, 1, 1);
+    }
+    if (xc != 0) {
+      // x seam plane: partials to this CTA's slots
+      const int xb = xc == 2 ? 1 : 0;
+      const int64_t s00 = (int64_t)(xb + (s_y ? 2 : 0) + (s_z ? 4 : 0)) * A.snv + g0;
+      const int64_t s01 = (int64_t)(xb + (s_y ? 2 : 0)) * A.snv + g0 + 1;
+      const int64_t s10 = (int64_t)(xb + (s_z ? 4 : 0)) * A.snv + g0 + sI;
+      const int64_t s11 = (int64_t)xb * A.snv + g0 + sI + 1;
+      A.fseam[s00] = f00;
+      A.fseam[s01] = f01;
+      A.fseam[s10] = f10;
+      A.fseam[s11] = f11;
+      if (LATENT) {
+        A.cseam[s00] = d00;
+        A.cseam[s01] = d01;
+        A.cseam[s10] = d10;
+        A.cseam[s11] = d11;
+      }
+      return;
+    }
+    const double* tp = Tr + rs * PL + ms0;
+    const double mz0e = P * k == kmI ? A.imv_end : rec_mz[tid];
+    const double yb0 = rec_my[tid] * imIs, yb1 = imr1 * imIs;
+    double c00 = mz0e * yb0, c01 = imr1 * yb0, c10 = mz0e * yb1, c11 = imr1 * yb1;
+    if (LATENT && latn) {
+      if (d00 > 0.0) c00 = c00 / fma(c00, d00, 1.0);
+      if (d01 > 0.0) c01 = c01 / fma(c01, d01, 1.0);
+      if (d10 > 0.0) c10 = c10 / fma(c10, d10, 1.0);
+      if (d11 > 0.0) c11 = c11 / fma(c11, d11, 1.0);
+    }
+    double o00 = tp[0] + A.dt * (c00 * f00);
+    double o01 = tp[1] + A.dt * (c01 * f01);
+    double o10 = tp[NZT] + A.dt * (c10 * f10);
+    double o11 = tp[NZT + 1] + A.dt * (c11 * f11);
+    if (A.dir_bottom && k == 0) {
+      o00 = A.P.T_inf;
+      o10 = A.P.T_inf;
+    }
+    // a seam node's entry is overwritten by the seam pass (after this kernel)
+    double* po = A.out + g0;
+    po[0] = o00;
+    po[1] = o01;
+    po[sI] = o10;
+    po[sI + 1] = o11;
+    if (s_y || s_z) {
+      // low-edge seam partials of this cell
+      if (s_y || s_z) {
+        const int64_t s00 = (int64_t)((s_y ? 2 : 0) + (s_z ? 4 : 0)) * A.snv + g0;
+        A.fseam[s00] = f00;
+        if (LATENT) A.cseam[s00] = d00;
+      }
+      if (s_y) {
+        const int64_t s01 = (int64_t)2 * A.snv + g0 + 1;
+        A.fseam[s01] = f01;
+        if (LATENT) A.cseam[s01] = d01;
+      }
+      if (s_z) {
+        const int64_t s10 = (int64_t)4 * A.snv + g0 + sI;
+        A.fseam[s10] = f10;
+        if (LATENT) A.cseam[s10] = d10;
+      }
+      if (!s_y) track(o01);
+      if (!s_z) track(o10);
+      track(o11);
+    } else if (max(max(habs(o00), habs(o01)), max(habs(o10), habs(o11))) >= thr) {
+      track_exact(o00);
+      track_exact(o01);
+      track_exact(o10);
+      track_exact(o11);
+    }
+  };
+
+  // the tile's high-edge nodes of plane I (J = Jn-1 or K = Kn-1), one per
+  // lane: a seam partial to the slot where the edge is shared with the next
+  // tile, the finished node where it is the domain boundary
+  auto finalize_edges = [&](int I, int a, int rs, int xc, bool latn) {
+    const double imIs = plane_imx(I);
+    const int kmI = pinfo_k[rs];
+    const int sI = A.NZ - kmI;
+    const int64_t gb = pinfo_b[rs] + (int64_t)(P * j0) * sI + P * k0;
+    const bool z_lo = tz_lo && kmI < P * k0;
+    for (int it = tid; it < nper; it += NT) {
+      const int J = peri[it] >> 8, K = peri[it] & 255;
+      const bool hiJ = J == Jn - 1, hiK = K == Kn - 1;
+      if (!(hiJ || hiK)) continue;
+      const int bj = J >> 1, b = J & 1, bk = K >> 1, c = K & 1;
+      const int cpn = (bk + 1) * ES + bj + 1;
+      const double* e = E + a * 9 * EN + cpn;
+      double f = e[(b * 3 + c) * EN];
+      if (b == 0) f += e[(6 + c) * EN - 1];
+      if (c == 0) f += e[(b * 3 + 2) * EN - ES];
+      if (b == 0 && c == 0) f += e[8 * EN - ES - 1];
+      double dc = 0.0;
+      if (LATENT && latn) dc = latent_sum(cpn, bk * CY + bj, a, b, c);
+      const int64_t idx = gb + (int64_t)J * sI + K;
+      const bool loJ = J == 0, loK = K == 0;
+      const bool seam = xc != 0 || (loJ && ty_lo) || (hiJ && ty_hi) || (loK && z_lo) || (hiK && tz_hi);
+      if (seam) {
+        const int slot = (xc == 2 ? 1 : 0) + ((loJ && ty_lo) ? 2 : 0) + ((loK && z_lo) ? 4 : 0);
+        const int64_t so = (int64_t)slot * A.snv + idx;
+        A.fseam[so] = f;
+        if (LATENT) A.cseam[so] = dc;
+      } else {
+        const int Jg = P * j0 + J, Kg = P * k0 + K;
+        const double my = b ? imr1 : ((Jg == 0 || Jg == A.NY - 1) ? A.imv_end : A.imv_int);
+        const double mz = c ? imr1 : ((Kg == kmI || Kg == A.NZ - 1) ? A.imv_end : A.imv_int);
+        double ci = mz * (my * imIs);
+        if (LATENT && dc > 0.0) ci = ci / fma(ci, dc, 1.0);
+        double o = Tr[rs * PL + J * NZT + K] + A.dt * (ci * f);
+        if (A.dir_bottom && Kg == 0) o = A.P.T_inf;
+        A.out[idx] = o;
+        track(o);
+      }
+    }
+  };
+
+  // prologue: the first layer's P+1 planes (and its side work)
+  int rs0 = (P * i0) % NR;  // ring slot of the layer's first plane
+  {
+    int rs = rs0;
+    for (int pa = 0; pa <= P; pa++) {
+      long long bI;
+      int kmI;
+      plane_layout(P * i0 + pa, bI, kmI);
+      load_plane(P * i0 + pa, rs, bI, kmI);
+      rs = rs + 1 >= NR ? 0 : rs + 1;
+    }
+  }
+  if (i0 + 1 < i1) prefetch_layout(P * (i0 + 1) + 1, (i0 + 1) & 1);
+  cp_commit();
+  cp_wait<0>();
+  __syncthreads();
+  side_work(i0, rs0);
+
+  // one loop body for the layers and the chunk's last plane (tail: i == i1,
+  // the carried x face as element plane 0), so the finalisation code exists
+  // once (instruction cache)
+  const int xc1 = (i1 < ext || (A.iface_hi && ext == A.nx)) ? 1 : 0;
+#pragma unroll 1
+  for (int i = i0; i <= i1; i++) {
+    const bool tail = i == i1;
+    cp_wait<0>();
+    __syncthreads();
+    if (i + 1 < i1) {
+      const int buf = (i + 1) & 1;
+      int rs = rs0 + P + 1;
+      rs = rs >= NR ? rs - NR : rs;
+#pragma unroll
+      for (int pa = 0; pa < P; pa++) {
+        long long bI;
+        int kmI;
+        if (A.pbase) {
+          bI = pf_b[buf][pa];
+          kmI = pf_k[buf][pa];
+        } else {
+          bI = (int64_t)(P * (i + 1) + 1 + pa) * plane_stride;
+          kmI = 0;
+        }
+        load_plane(P * (i + 1) + 1 + pa, rs, bI, kmI);
+        rs = rs + 1 >= NR ? 0 : rs + 1;
+      }
+    }
+    if (i + 2 < i1) prefetch_layout(P * (i + 2) + 1, i & 1);
+    cp_commit();
+    bool lf = false;
+    if (live && !tail) {
+      double t[Q3], G[Q3];
+      {
+        int rs = rs0;
+#pragma unroll
+        for (int a = 0; a < Q; a++) {
+          const double* tp = Tr + rs * PL + ms0;
+#pragma unroll
+          for (int b = 0; b < Q; b++)
+#pragma unroll
+            for (int c = 0; c < Q; c++) t[(a * Q + b) * Q + c] = tp[b * NZT + c];
+          rs = rs + 1 >= NR ? 0 : rs + 1;
+        }
+      }
+      interp3<P>(t);
+      cell_element<P, false, true>(
+          A, F, i, j, k, 0, t, G, ymask, [&](int, int, int) { return 0.0; }, Sx, Sy + jl * MB * Q,
+          Sz + kl * MB * Q, Fo + jl * Q * Q);
+#pragma unroll
+      for (int q = 0; q < Q * Q; q++) {
+        G[q] += Cx[q * NT + tid];
+        Cx[q * NT + tid] = G[P * Q * Q + q];
+      }
+#pragma unroll
+      for (int q = 0; q < EW; q++) E[q * EN + cp] = G[q];
+      if (LATENT) {
+        // candidates by the high words (a superset of the open interval),
+        // then the exact test
+        bool cand = false;
+#pragma unroll
+        for (int q = 0; q < Q3; q++)
+          cand |= (unsigned)(__double2hiint(t[q]) - A.lat_hi0) <= (unsigned)A.lat_hiw;
+        bool lat = false;
+        if (cand) lat = any_abs_lt<Q3>(t, A.lat_mid, A.lat_half);
+        lf = lat || lat_had;
+        if (lat) {
+#pragma unroll
+          for (int q = 0; q < Q3; q++) t[q] = fabs(t[q] - A.lat_mid) < A.lat_half ? A.lw3[q] : 0.0;
+          project3<P>(t);
+#pragma unroll
+          for (int q = 0; q < Q * Q; q++) {
+            if (lat_had) t[q] += lcar[q * NT];
+            lcar[q * NT] = t[P * Q * Q + q];
+          }
+#pragma unroll
+          for (int q = 0; q < EW; q++) ecg[q * NT + tid] = t[q];
+        } else if (lat_had) {
+#pragma unroll
+          for (int q = 0; q < Q * Q; q++) ecg[q * NT + tid] = lcar[q * NT];
+#pragma unroll
+          for (int q = Q * Q; q < EW; q++) ecg[q * NT + tid] = 0.0;
+        }
+        latf[cp] = lf ? 1 : 0;
+        lat_had = lat;
+      }
+    } else if (live) {
+#pragma unroll
+      for (int q = 0; q < Q * Q; q++) E[q * EN + cp] = Cx[q * NT + tid];
+      if (LATENT) {
+        lf = lat_had;
+        if (lat_had)
+#pragma unroll
+          for (int q = 0; q < Q * Q; q++) ecg[q * NT + tid] = lcar[q * NT];
+        latf[cp] = lat_had ? 1 : 0;
+      }
+    }
+    cp_wait<0>();
+    const bool latn = LATENT ? __syncthreads_or(lf) != 0 : (__syncthreads(), false);
+    int rs1 = rs0 + P;  // first plane of the next layer
+    rs1 = rs1 >= NR ? rs1 - NR : rs1;
+    if (i + 1 < i1) side_work(i + 1, rs1);
+    const int na = tail ? 1 : P;
+    int rs = rs0;
+#pragma unroll 1
+    for (int a = 0; a < na; a++) {
+      const int xc = tail ? xc1 : ((a == 0 && i == i0 && (i0 > 0 || A.iface_lo)) ? 2 : 0);
+      finalize_cell(P * i + a, a, rs, xc, latn);
+      finalize_edges(P * i + a, a, rs, xc, latn);
+      rs = rs + 1 >= NR ? 0 : rs + 1;
+    }
+    rs0 = rs1;
+  }
+  block_max2(__longlong_as_double((long long)rec_amax[tid]), rec_smax[tid], A.red);
+}

@@ -57,7 +57,7 @@ __device__ __noinline__ void latent_cell(const SArgs& A, const double* Tr, int i
 }
 
 #ifndef ST_ROWSTORE
-#define ST_ROWSTORE 1  // A/B hook: T' staged in the ring and written out as whole rows
+#define ST_ROWSTORE 0  // A/B hook: T' staged in the ring and written out as whole rows
 #endif
 
 template <int P>

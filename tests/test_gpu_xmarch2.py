@@ -1,0 +1,70 @@
+"""k_xmarch2 (the lean Q2 explicit-step kernel) against k_xmarch<2> (the
+general kernel, ST_XMARCH2=0): the same arithmetic in the same order, so the
+fields after several steps are bitwise equal (zeros may differ in sign) --
+boxes with full and ragged tiles, several x chunks, a fitted part with its
+re-entrant edge, latent heat on and off, a melt pool that crosses the latent
+interval, and the stability maxima."""
+
+import numpy as np
+import pytest
+
+import paper_2302_05164_b200 as st
+from paper_2302_05164_b200.mesh import FittedPart
+from paper_2302_05164_b200.physics import BEAM_DTYPE, BeamState, pack_beams
+
+pytestmark = pytest.mark.gpu
+
+H = 40e-6
+
+
+def _params(latent):
+    mat = st.MaterialParams(k_p=0.3, k_m=30.0, k_s=22.0, T_s=1450.0, T_l=1900.0,
+                            latent_heat=2.86e5 if latent else 0.0, T_lat_s=1878.0,
+                            T_lat_l=1928.0)
+    bnd = st.BoundaryParams(emissivity=0.4, T_inf=300.0, T_v=2900.0, h_conv=10.0)
+    las = st.HeatSourceParams(radius=60e-6, h_powder=40e-6, power=90.0)
+    return st.ProcessParams(mat, bnd, las, st.MeshParams(h_coarse=H, n_refine=0, h_powder=H))
+
+
+def _run(mesh, latent, lx, x2, monkeypatch, steps=6):
+    monkeypatch.setenv("ST_XMARCH2", "1" if x2 else "0")
+    if lx:
+        monkeypatch.setenv("ST_LX", lx)
+    else:
+        monkeypatch.delenv("ST_LX", raising=False)
+    op = st.ThermalOperator(mesh, mesh, _params(latent), st.SolverSettings())
+    rng = np.random.default_rng(7)
+    # a field that crosses the latent interval (1878-1928 K) in many cells
+    T = rng.uniform(1700.0, 2100.0, op.nv)
+    T[rng.random(op.nv) < 0.5] = rng.uniform(300.0, 600.0)
+    op.set_state(T, 1.0)
+    lx_m, ly_m = mesh.nx * H, mesh.ny * H
+    recs = np.zeros((steps, 2), dtype=BEAM_DTYPE)
+    for s in range(steps):
+        recs[s] = pack_beams([
+            BeamState(np.array([lx_m * 0.3 + s * 4e-6, ly_m * 0.5]), 0.0, 90.0, True),
+            BeamState(np.array([lx_m * 0.7, ly_m * 0.3 + s * 2e-6]), 0.0, 60.0, s % 2 == 0)])
+    fail, amax, tmax = op.run_explicit(np.full(steps, 2e-8), recs)
+    Tout, _ = op.get_state()
+    op.close()
+    return fail, amax, tmax, Tout
+
+
+CASES = {
+    "box_full": lambda: st.StructuredBox(12, 16, 32, H, degree=2),
+    "box_ragged": lambda: st.StructuredBox(9, 11, 19, H, degree=2),
+    "box_single_tile": lambda: st.StructuredBox(5, 7, 9, H, degree=2),
+    "fitted": lambda: FittedPart(13, 11, 40, H, [5] * 16 + [9] * 16 + [13] * 8, degree=2),
+}
+
+
+@pytest.mark.parametrize("lx", [None, "3"])
+@pytest.mark.parametrize("latent", [True, False])
+@pytest.mark.parametrize("case", list(CASES))
+def test_lean_kernel_equals_general_kernel_bitwise(case, latent, lx, monkeypatch):
+    mesh = CASES[case]()
+    f0, a0, t0, T0 = _run(mesh, latent, lx, False, monkeypatch)
+    f1, a1, t1, T1 = _run(mesh, latent, lx, True, monkeypatch)
+    assert f0 == f1
+    assert a0 == a1 and t0 == t1
+    assert np.array_equal(T0, T1)
