@@ -5,25 +5,33 @@
 // chunk, one thread per cell, cell_element in registers, element planes in
 // shared memory, fixed-order gathers, seam partials to the CTA's slots), with
 // the per-layer work around the cell evaluation rebuilt for instruction
-// count (the kernel is issue bound: ncu of k_xmarch showed 28 % of all warp
-// instructions in the node finalisation and 11 % in the plane staging):
+// count and stalls (ncu of k_xmarch: 28 % of all warp instructions in the
+// node finalisation, 11 % in the plane staging, 5 % re-deriving per-thread
+// constants the cell evaluation had pushed out of the registers):
 //   * element entries are stored with a ring of zero ghost cells around the
 //     tile, so the <= 4 contributions of a node are summed without
 //     neighbour tests;
 //   * every thread finalises the four nodes (b, c < 2) of its cell with no
 //     seam logic: T' is stored unconditionally (a seam node's value there
 //     is overwritten by the seam pass, which runs after this kernel) and
-//     only the stability maxima are predicated;
-//   * the tile's perimeter nodes (seam partials of the low edges, the high
-//     edges) are a dense second pass, one node per lane, instead of
-//     divergent per-thread branches in every warp;
+//     only the stability maxima skip seam nodes;
+//   * the tile's perimeter nodes (high edges; low edges where they are
+//     seams) are a dense second pass, one node per lane, from a per-CTA
+//     table of gather offsets (absent contributions point at a zero ghost
+//     entry), instead of divergent per-thread branches in every warp;
+//   * per-thread constants (shared-memory offsets, node coordinates, flags)
+//     and per-plane constants (layout, x factor of the lumped mass) are
+//     records in shared memory, loaded where a phase starts;
 //   * the staging keeps one running row pointer per plane and copies the
-//     33rd column with one instruction of one warp;
-//   * the stability maxima are only updated by nodes whose high word
-//     reaches the running maximum's;
+//     33rd column with one instruction of one warp; the fitted layout of
+//     the next planes arrives by cp.async in the same group;
+//   * the stability maxima live in shared memory and are only updated by
+//     nodes whose high word reaches the running maximum's;
 //   * the latent check is an integer window test on the high words (exact
 //     test only for candidates); the rare latent increments live in an
-//     L2-resident global scratch instead of 18 KB of shared memory.
+//     L2-resident global scratch instead of 18 KB of shared memory;
+//   * one loop body serves the layers and the chunk's last plane, so the
+//     finalisation code exists once (instruction cache).
 // Results are bitwise those of k_xmarch (except the sign of exact zeros).
 #pragma once
 
@@ -47,58 +55,100 @@ __global__ void __launch_bounds__(128, 3) k_xmarch2(SArgs A) {
   double* Sx = Sz + CZ * MB * Q;         // [MB][Q], current layer
   double* Fq = Sx + MB * Q;              // [CY][Q * Q] facet fluxes
   double* Fo = Fq + CY * Q * Q;          // [CY][Q * Q] facet node terms
-  __shared__ long long pinfo_b[NR];  // ring: first node id (- lowest row) of a staged plane
-  __shared__ int pinfo_k[NR];        // ring: lowest node row of a staged plane
+  // ring: per staged plane, first node id (- lowest row), lowest node row,
+  // x factor of the inverse lumped mass times 1 / (rho c detw)
+  __shared__ long long pinfo_b[NR];
+  __shared__ int pinfo_k[NR];
+  __shared__ double pinfo_im[NR];
   __shared__ long long pf_b[2][P];   // fitted layout of the next layer's planes (prefetch)
   __shared__ int pf_k[2][P];
-  __shared__ unsigned short peri[NPER];  // perimeter nodes of the tile, J << 8 | K
-  // per-thread constants and running maxima, kept out of the register
-  // budget of the cell evaluation: inverse 1D masses of the cell's low
-  // corner, max |T'| (bit pattern) and max T'
+  // perimeter nodes of the tile (high edges first): x = gather offsets 0, 1
+  // (u16 each, into an element plane), y = offsets 2, 3, z = J | K << 8 |
+  // flags << 16, w = J * NZT + K
+  __shared__ int4 peri[NPER];
+  // per-thread record: x = ms0 (plane offset of the cell's low corner), y =
+  // cp (padded cell index), z = flags, w = 2 j | 2 k << 16
+  __shared__ int4 rec4[NT];
+  // inverse 1D masses of the cell's low corner, running max |T'| (bit
+  // pattern) and max T'
   __shared__ double rec_my[NT], rec_mz[NT], rec_smax[NT];
   __shared__ unsigned long long rec_amax[NT];
   __shared__ unsigned char latf[LATENT ? EN : 1];  // cell has latent increments this layer
+  // record flags
+  constexpr int RF_LIVE = 1, RF_SY = 2, RF_SZ = 4, RF_DIR = 8;
+  // perimeter flags
+  constexpr int PF_LOJ = 1, PF_LOK = 2, PF_HI = 4, PF_SEAM = 8, PF_SLOT2 = 16;
 
   const int tid = threadIdx.x;
-  const int lane = tid & 31, warp = tid >> 5;
-  const int kl = tid / CY, jl = tid % CY;  // z-major cell order
   const int chunk = blockIdx.z + A.zoff;
   const int j0 = blockIdx.x * CY, k0 = blockIdx.y * CZ, i0 = chunk * A.Lx;
   const int ext = A.text ? A.text[blockIdx.y] : A.nx;
   if (i0 >= ext) return;
   const int i1 = min(i0 + A.Lx, ext);
-  const int j = j0 + jl, k = k0 + kl;
-  const bool live = j < A.ny && k < A.nz;
   const int Jn = min(P * CY, P * (A.ny - j0)) + 1;
   const int Kn = min(P * CZ, P * (A.nz - k0)) + 1;
-  const int nper = 2 * Kn + 2 * (Jn - 2);
+  const int nhi = Kn + Jn - 1, nper = 2 * Kn + 2 * (Jn - 2);
   // tile-edge node lines are seams unless they are the domain boundary
   const bool ty_lo = j0 > 0, ty_hi = j0 + CY < A.ny;
   const bool tz_lo = k0 > 0, tz_hi = k0 + CZ < A.nz;
   const CellFlags F{true, true, A.nb > 0, false};
   const int64_t plane_stride = (int64_t)A.NY * A.NZ;
-  const int ms0 = P * jl * NZT + P * kl;
-  const int cp = (kl + 1) * ES + jl + 1;
+  const double imr1 = A.imr[1];
 
+  {
+    const int kl = tid / CY, jl = tid % CY;  // z-major cell order
+    const int j = j0 + jl, k = k0 + kl;
+    const bool live = j < A.ny && k < A.nz;
+    rec4[tid] = make_int4(P * jl * NZT + P * kl, (kl + 1) * ES + jl + 1,
+                          (live ? RF_LIVE : 0) | ((jl == 0 && ty_lo) ? RF_SY : 0) |
+                              ((kl == 0 && tz_lo) ? RF_SZ : 0) |
+                              ((k == 0 && A.dir_bottom) ? RF_DIR : 0),
+                          (P * j) | ((P * k) << 16));
+    rec_my[tid] = inv_mass1<P>(A, P * j, A.NY);
+    rec_mz[tid] = inv_mass1<P>(A, P * k, A.NZ);
+    rec_amax[tid] = 0ull;
+    rec_smax[tid] = -INFINITY;
+  }
   // zero the element arrays once (ghost and dead cells are never written)
   for (int e = tid; e < EW * EN; e += NT) E[e] = 0.0;
   if (LATENT)
     for (int e = tid; e < EN; e += NT) latf[e] = 0;
-  // perimeter list: rows J = 0 and Jn-1, then columns K = 0 and Kn-1
+  // perimeter table: row J = Jn-1, column K = Kn-1 (high edges), then row
+  // J = 0 and column K = 0 (low edges)
   for (int e = tid; e < nper; e += NT) {
     int J, K;
     if (e < Kn) {
-      J = 0, K = e;
-    } else if (e < 2 * Kn) {
-      J = Jn - 1, K = e - Kn;
-    } else if (e < 2 * Kn + Jn - 2) {
-      J = e - 2 * Kn + 1, K = 0;
+      J = Jn - 1, K = e;
+    } else if (e < nhi) {
+      J = e - Kn, K = Kn - 1;
+    } else if (e < nhi + Kn - 1) {
+      J = 0, K = e - nhi;
     } else {
-      J = e - (2 * Kn + Jn - 2) + 1, K = Kn - 1;
+      J = e - (nhi + Kn - 1) + 1, K = 0;
     }
-    peri[e] = (unsigned short)((J << 8) | K);
+    const int bj = J >> 1, b = J & 1, bk = K >> 1, c = K & 1;
+    const int cpn = (bk + 1) * ES + bj + 1;
+    // own cell, y-, z-, yz-neighbour below (the gather's order); entry 0 of
+    // the ghost corner cell is always zero
+    const int o0 = (b * 3 + c) * EN + cpn;
+    const int o1 = b == 0 ? (6 + c) * EN + cpn - 1 : 0;
+    const int o2 = c == 0 ? (b * 3 + 2) * EN + cpn - ES : 0;
+    const int o3 = (b == 0 && c == 0) ? 8 * EN + cpn - ES - 1 : 0;
+    const bool loJ = J == 0, loK = K == 0, hiJ = J == Jn - 1, hiK = K == Kn - 1;
+    // seams fixed over the march (the z-low seam depends on the plane)
+    const bool seam = (loJ && ty_lo) || (hiJ && ty_hi) || (hiK && tz_hi);
+    const int fl = (loJ ? PF_LOJ : 0) | (loK ? PF_LOK : 0) | ((hiJ || hiK) ? PF_HI : 0) |
+                   (seam ? PF_SEAM : 0) | ((loJ && ty_lo) ? PF_SLOT2 : 0);
+    peri[e] = make_int4(o0 | (o1 << 16), o2 | (o3 << 16), J | (K << 8) | (fl << 16), J * NZT + K);
   }
 
+  // x factor of the inverse lumped mass of plane I (times 1 / (rho c detw))
+  auto plane_imx = [&](int I) {
+    const int G = I + A.gI0;
+    const bool xend = G == 0 || G == A.gNX - 1 || (ext < A.nx && I == P * ext);
+    const double imx = (I & 1) ? imr1 : (xend ? A.imv_end : A.imv_int);
+    return imx * A.inv_rcdw;
+  };
   // (asynchronous copies in the staging's commit group: no load sits in
   // front of the barrier)
   auto prefetch_layout = [&](int Ib, int buf) {
@@ -116,51 +166,66 @@ __global__ void __launch_bounds__(128, 3) k_xmarch2(SArgs A) {
   // stage plane I into ring slot rs: warp w copies tile rows w, w + 4, ...
   // (lane l the row entry l), one running row pointer; the 33rd column goes
   // with one instruction of warp 1 (lane l the row l)
-  const bool c_lo = lane < Kn;
   const unsigned tr_s = (unsigned)__cvta_generic_to_shared(Tr);
+  const bool full = Jn == NYT && Kn == NZT;
   auto load_plane = [&](int I, int rs, long long bI, int kmI) {
+    const int lane = tid & 31, warp = tid >> 5;
     const int sI = A.NZ - kmI;
     if (tid == 0) {
       pinfo_b[rs] = bI;
       pinfo_k[rs] = kmI;
+      pinfo_im[rs] = plane_imx(I);
     }
-    const double* src = A.T + bI + (int64_t)(P * j0 + warp) * sI + P * k0 + lane;
+    const double* src = A.T + (bI + ((P * j0 + warp) * sI + P * k0 + lane));
     const unsigned dst = tr_s + (unsigned)((rs * PL + warp * NZT + lane) * 8);
+    const int64_t step = (int64_t)(NW * sI) * 8;
+    if (full) {
 #pragma unroll
-    for (int it = 0; it < (NYT + NW - 1) / NW; it++) {
-      if (c_lo && warp + it * NW < Jn)
+      for (int it = 0; it < NYT / NW; it++) {
         asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(dst + it * NW * NZT * 8),
                      "l"(src)
                      : "memory");
-      src += NW * sI;
+        src = (const double*)((const char*)src + step);
+      }
+      if (warp == 0)
+        asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(dst + (NYT - 1) * NZT * 8),
+                     "l"(src)
+                     : "memory");
+    } else {
+      const bool c_lo = lane < Kn;
+#pragma unroll
+      for (int it = 0; it < (NYT + NW - 1) / NW; it++) {
+        if (c_lo && warp + it * NW < Jn)
+          asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(dst + it * NW * NZT * 8),
+                       "l"(src)
+                       : "memory");
+        src = (const double*)((const char*)src + step);
+      }
     }
     if (warp == 1 && Kn == NZT && lane < Jn) {
-      const double* s2 = A.T + bI + (int64_t)(P * j0 + lane) * sI + P * k0 + (NZT - 1);
+      const double* s2 = A.T + (bI + ((P * j0 + lane) * sI + P * k0 + (NZT - 1)));
       asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(
                        tr_s + (unsigned)((rs * PL + lane * NZT + NZT - 1) * 8)),
                    "l"(s2)
                    : "memory");
     }
   };
-  auto plane_layout = [&](int I, long long& bI, int& kmI) {
-    bI = A.pbase ? A.pbase[I] : (int64_t)I * plane_stride;
-    kmI = A.pkmin ? A.pkmin[I] : 0;
-  };
-
-  // 1D lumped inverse-mass factors of this thread's cell corner in y and z
-  rec_my[tid] = inv_mass1<P>(A, P * j, A.NY);
-  rec_mz[tid] = inv_mass1<P>(A, P * k, A.NZ);
-  rec_amax[tid] = 0ull;
-  rec_smax[tid] = -INFINITY;
-  const double imr1 = A.imr[1];
 
 #pragma unroll
   for (int q = 0; q < Q * Q; q++) Cx[q * NT + tid] = 0.0;
-  const int64_t cta = ((int64_t)chunk * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x;
-  double* lcar = LATENT ? A.lcarry + cta * (Q * Q * NT) + tid : nullptr;
-  double* ecg = LATENT ? A.ecg + cta * (EW * NT) : nullptr;  // [q * NT + cell]
+  // latent scratch of this CTA, addressed where the rare paths need it
+  // (lcar: x-face carry [q * NT + tid]; ecg: increments [q * NT + cell])
+  auto cta_id = [&]() {
+    return ((int64_t)(blockIdx.z + A.zoff) * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x;
+  };
+#define lcar (A.lcarry + cta_id() * (Q * Q * NT) + tid)
+#define ecg (A.ecg + cta_id() * (EW * NT))
   bool lat_had = false;
-  const unsigned ymask = F.source && live ? beam_column_mask<P>(A, j, k) : 0u;
+  unsigned ymask = 0u;
+  if (F.source) {
+    const int kl = tid / CY, jl = tid % CY;
+    if (j0 + jl < A.ny && k0 + kl < A.nz) ymask = beam_column_mask<P>(A, j0 + jl, k0 + kl);
+  }
   const int nbt = (F.source && __syncthreads_or(ymask != 0u)) ? min(A.nb, MB) : 0;
   for (int e = tid; e < nbt * CY; e += NT) {
     const int b = e / CY, r = e - (e / CY) * CY;
@@ -175,6 +240,7 @@ __global__ void __launch_bounds__(128, 3) k_xmarch2(SArgs A) {
   constexpr int CPW = (CY + NW - 1) / NW;
   auto side_work = [&](int il, int rs0) {
     if (has_top) {
+      const int lane = tid & 31, warp = tid >> 5;
       face_phase<P>(A, lane, min(warp * CPW, CY), min(warp * CPW + CPW, CY), Fq, Fo,
                     [&](int r, int a, int b) {
                       int rs = rs0 + a;
@@ -200,9 +266,6 @@ __global__ void __launch_bounds__(128, 3) k_xmarch2(SArgs A) {
     thr = max(__double2hiint(s2), 0);
   };
   auto habs = [](double o) { return __double2hiint(o) & 0x7fffffff; };
-  auto track = [&](double o) {
-    if (habs(o) >= thr) track_exact(o);
-  };
 
   // latent increment of a node: the contributions of the (<= 4) cells around
   // it in the gather's order; cells without increments count as zero
@@ -216,25 +279,19 @@ __global__ void __launch_bounds__(128, 3) k_xmarch2(SArgs A) {
     return dc;
   };
 
-  // x factor of the inverse lumped mass of plane I (times 1 / (rho c detw))
-  auto plane_imx = [&](int I) {
-    const int G = I + A.gI0;
-    const bool xend = G == 0 || G == A.gNX - 1 || (ext < A.nx && I == P * ext);
-    const double imx = (I & 1) ? imr1 : (xend ? A.imv_end : A.imv_int);
-    return imx * A.inv_rcdw;
-  };
-
   // the four nodes (b, c < 2) of this thread's cell in plane I (element
   // plane a, ring slot rs); xc: 0 = ordinary plane, 1 / 2 = x seam with this
   // CTA on the low / high side (every node of the plane is a seam then)
-  auto finalize_cell = [&](int I, int a, int rs, int xc, bool latn) {
-    if (!live) return;
-    const double imIs = plane_imx(I);
+  auto finalize_cell = [&](int a, int rs, int xc, bool latn) {
+    const int4 r = rec4[tid];
+    if (!(r.z & RF_LIVE)) return;
+    const int cp = r.y;
     const int kmI = pinfo_k[rs];
     const int sI = A.NZ - kmI;
-    const int64_t g0 = pinfo_b[rs] + (int64_t)(P * j * sI + P * k);
-    const bool s_y = jl == 0 && ty_lo;                      // b = 0 nodes on a y seam
-    const bool s_z = kl == 0 && tz_lo && kmI < P * k0;      // c = 0 nodes on a z seam
+    const int j2 = r.w & 0xffff, k2 = r.w >> 16;
+    const int64_t g0 = pinfo_b[rs] + (j2 * sI + k2);
+    const bool s_y = (r.z & RF_SY) != 0;                          // b = 0 nodes on a y seam
+    const bool s_z = (r.z & RF_SZ) != 0 && kmI < P * k0;          // c = 0 nodes on a z seam
     const double* e = E + a * 9 * EN + cp;
     double f00 = e[0 * EN];
     f00 += e[6 * EN - 1];
@@ -271,8 +328,9 @@ __global__ void __launch_bounds__(128, 3) k_xmarch2(SArgs A) {
       }
       return;
     }
-    const double* tp = Tr + rs * PL + ms0;
-    const double mz0e = P * k == kmI ? A.imv_end : rec_mz[tid];
+    const double imIs = pinfo_im[rs];
+    const double* tp = Tr + rs * PL + r.x;
+    const double mz0e = k2 == kmI ? A.imv_end : rec_mz[tid];
     const double yb0 = rec_my[tid] * imIs, yb1 = imr1 * imIs;
     double c00 = mz0e * yb0, c01 = imr1 * yb0, c10 = mz0e * yb1, c11 = imr1 * yb1;
     if (LATENT && latn) {
@@ -285,84 +343,71 @@ __global__ void __launch_bounds__(128, 3) k_xmarch2(SArgs A) {
     double o01 = tp[1] + A.dt * (c01 * f01);
     double o10 = tp[NZT] + A.dt * (c10 * f10);
     double o11 = tp[NZT + 1] + A.dt * (c11 * f11);
-    if (A.dir_bottom && k == 0) {
+    if (r.z & RF_DIR) {
       o00 = A.P.T_inf;
       o10 = A.P.T_inf;
     }
-    // a seam node's entry is overwritten by the seam pass (after this kernel)
+    // a seam node's entry (its partial goes out with the perimeter pass) is
+    // overwritten by the seam pass, which runs after this kernel
     double* po = A.out + g0;
     po[0] = o00;
     po[1] = o01;
     po[sI] = o10;
     po[sI + 1] = o11;
-    if (s_y || s_z) {
-      // low-edge seam partials of this cell
-      if (s_y || s_z) {
-        const int64_t s00 = (int64_t)((s_y ? 2 : 0) + (s_z ? 4 : 0)) * A.snv + g0;
-        A.fseam[s00] = f00;
-        if (LATENT) A.cseam[s00] = d00;
-      }
-      if (s_y) {
-        const int64_t s01 = (int64_t)2 * A.snv + g0 + 1;
-        A.fseam[s01] = f01;
-        if (LATENT) A.cseam[s01] = d01;
-      }
-      if (s_z) {
-        const int64_t s10 = (int64_t)4 * A.snv + g0 + sI;
-        A.fseam[s10] = f10;
-        if (LATENT) A.cseam[s10] = d10;
-      }
-      if (!s_y) track(o01);
-      if (!s_z) track(o10);
-      track(o11);
-    } else if (max(max(habs(o00), habs(o01)), max(habs(o10), habs(o11))) >= thr) {
-      track_exact(o00);
-      track_exact(o01);
-      track_exact(o10);
+    const int h00 = (s_y || s_z) ? 0 : habs(o00), h01 = s_y ? 0 : habs(o01);
+    const int h10 = s_z ? 0 : habs(o10), h11 = habs(o11);
+    if (max(max(h00, h01), max(h10, h11)) >= thr) {
+      if (!(s_y || s_z)) track_exact(o00);
+      if (!s_y) track_exact(o01);
+      if (!s_z) track_exact(o10);
       track_exact(o11);
     }
   };
 
-  // the tile's high-edge nodes of plane I (J = Jn-1 or K = Kn-1), one per
-  // lane: a seam partial to the slot where the edge is shared with the next
-  // tile, the finished node where it is the domain boundary
-  auto finalize_edges = [&](int I, int a, int rs, int xc, bool latn) {
-    const double imIs = plane_imx(I);
+  // the tile's perimeter nodes of plane I, one per lane: the high edges (J =
+  // Jn-1 or K = Kn-1: a seam partial to the slot where the edge is shared
+  // with the next tile, the finished node where it is the domain boundary)
+  // and, in an ordinary plane, the low edges that are seams
+  auto finalize_edges = [&](int a, int rs, int xc, bool latn) {
     const int kmI = pinfo_k[rs];
     const int sI = A.NZ - kmI;
-    const int64_t gb = pinfo_b[rs] + (int64_t)(P * j0) * sI + P * k0;
     const bool z_lo = tz_lo && kmI < P * k0;
-    for (int it = tid; it < nper; it += NT) {
-      const int J = peri[it] >> 8, K = peri[it] & 255;
-      const bool hiJ = J == Jn - 1, hiK = K == Kn - 1;
-      if (!(hiJ || hiK)) continue;
-      const int bj = J >> 1, b = J & 1, bk = K >> 1, c = K & 1;
-      const int cpn = (bk + 1) * ES + bj + 1;
-      const double* e = E + a * 9 * EN + cpn;
-      double f = e[(b * 3 + c) * EN];
-      if (b == 0) f += e[(6 + c) * EN - 1];
-      if (c == 0) f += e[(b * 3 + 2) * EN - ES];
-      if (b == 0 && c == 0) f += e[8 * EN - ES - 1];
+    const int n = (xc == 0 && (ty_lo || z_lo)) ? nper : nhi;
+    if (tid >= n) return;
+    const int64_t gb = pinfo_b[rs] + ((P * j0) * sI + P * k0);
+    const double* ea = E + a * 9 * EN;
+#pragma unroll 1
+    for (int it = tid; it < n; it += NT) {
+      const int4 pr = peri[it];
+      const int J = pr.z & 255, K = (pr.z >> 8) & 255, fl = pr.z >> 16;
+      const bool zs = (fl & PF_LOK) && z_lo;
+      const bool seam = xc != 0 || (fl & PF_SEAM) || zs;
+      if (!(fl & PF_HI) && !seam) continue;  // a low edge on the domain boundary: its cells' own
+      double f = ea[pr.x & 0xffff];
+      f += ea[(unsigned)pr.x >> 16];
+      f += ea[pr.y & 0xffff];
+      f += ea[(unsigned)pr.y >> 16];
       double dc = 0.0;
-      if (LATENT && latn) dc = latent_sum(cpn, bk * CY + bj, a, b, c);
-      const int64_t idx = gb + (int64_t)J * sI + K;
-      const bool loJ = J == 0, loK = K == 0;
-      const bool seam = xc != 0 || (loJ && ty_lo) || (hiJ && ty_hi) || (loK && z_lo) || (hiK && tz_hi);
+      if (LATENT && latn) {
+        const int bj = J >> 1, bk = K >> 1;
+        dc = latent_sum((bk + 1) * ES + bj + 1, bk * CY + bj, a, J & 1, K & 1);
+      }
+      const int64_t idx = gb + (J * sI + K);
       if (seam) {
-        const int slot = (xc == 2 ? 1 : 0) + ((loJ && ty_lo) ? 2 : 0) + ((loK && z_lo) ? 4 : 0);
+        const int slot = (xc == 2 ? 1 : 0) + ((fl & PF_SLOT2) ? 2 : 0) + (zs ? 4 : 0);
         const int64_t so = (int64_t)slot * A.snv + idx;
         A.fseam[so] = f;
         if (LATENT) A.cseam[so] = dc;
       } else {
         const int Jg = P * j0 + J, Kg = P * k0 + K;
-        const double my = b ? imr1 : ((Jg == 0 || Jg == A.NY - 1) ? A.imv_end : A.imv_int);
-        const double mz = c ? imr1 : ((Kg == kmI || Kg == A.NZ - 1) ? A.imv_end : A.imv_int);
-        double ci = mz * (my * imIs);
+        const double my = (J & 1) ? imr1 : ((Jg == 0 || Jg == A.NY - 1) ? A.imv_end : A.imv_int);
+        const double mz = (K & 1) ? imr1 : ((Kg == kmI || Kg == A.NZ - 1) ? A.imv_end : A.imv_int);
+        double ci = mz * (my * pinfo_im[rs]);
         if (LATENT && dc > 0.0) ci = ci / fma(ci, dc, 1.0);
-        double o = Tr[rs * PL + J * NZT + K] + A.dt * (ci * f);
+        double o = Tr[rs * PL + pr.w] + A.dt * (ci * f);
         if (A.dir_bottom && Kg == 0) o = A.P.T_inf;
         A.out[idx] = o;
-        track(o);
+        if (habs(o) >= thr) track_exact(o);
       }
     }
   };
@@ -372,10 +417,8 @@ __global__ void __launch_bounds__(128, 3) k_xmarch2(SArgs A) {
   {
     int rs = rs0;
     for (int pa = 0; pa <= P; pa++) {
-      long long bI;
-      int kmI;
-      plane_layout(P * i0 + pa, bI, kmI);
-      load_plane(P * i0 + pa, rs, bI, kmI);
+      const int I = P * i0 + pa;
+      load_plane(I, rs, A.pbase ? A.pbase[I] : (int64_t)I * plane_stride, A.pkmin ? A.pkmin[I] : 0);
       rs = rs + 1 >= NR ? 0 : rs + 1;
     }
   }
@@ -386,9 +429,9 @@ __global__ void __launch_bounds__(128, 3) k_xmarch2(SArgs A) {
   side_work(i0, rs0);
 
   // one loop body for the layers and the chunk's last plane (tail: i == i1,
-  // the carried x face as element plane 0), so the finalisation code exists
-  // once (instruction cache)
+  // the carried x face as element plane 0)
   const int xc1 = (i1 < ext || (A.iface_hi && ext == A.nx)) ? 1 : 0;
+  const int xc0 = (i0 > 0 || A.iface_lo) ? 2 : 0;
 #pragma unroll 1
   for (int i = i0; i <= i1; i++) {
     const bool tail = i == i1;
@@ -416,13 +459,16 @@ __global__ void __launch_bounds__(128, 3) k_xmarch2(SArgs A) {
     if (i + 2 < i1) prefetch_layout(P * (i + 2) + 1, i & 1);
     cp_commit();
     bool lf = false;
+    const int4 r = rec4[tid];
+    const bool live = (r.z & RF_LIVE) != 0;
+    const int cp = r.y;
     if (live && !tail) {
       double t[Q3], G[Q3];
       {
         int rs = rs0;
 #pragma unroll
         for (int a = 0; a < Q; a++) {
-          const double* tp = Tr + rs * PL + ms0;
+          const double* tp = Tr + rs * PL + r.x;
 #pragma unroll
           for (int b = 0; b < Q; b++)
 #pragma unroll
@@ -431,9 +477,12 @@ __global__ void __launch_bounds__(128, 3) k_xmarch2(SArgs A) {
         }
       }
       interp3<P>(t);
-      cell_element<P, false, true>(
-          A, F, i, j, k, 0, t, G, ymask, [&](int, int, int) { return 0.0; }, Sx, Sy + jl * MB * Q,
-          Sz + kl * MB * Q, Fo + jl * Q * Q);
+      {
+        const int kl = tid / CY, jl = tid % CY;
+        cell_element<P, false, true>(
+            A, F, i, j0 + jl, k0 + kl, 0, t, G, ymask, [&](int, int, int) { return 0.0; }, Sx,
+            Sy + jl * MB * Q, Sz + kl * MB * Q, Fo + jl * Q * Q);
+      }
 #pragma unroll
       for (int q = 0; q < Q * Q; q++) {
         G[q] += Cx[q * NT + tid];
@@ -491,12 +540,14 @@ __global__ void __launch_bounds__(128, 3) k_xmarch2(SArgs A) {
     int rs = rs0;
 #pragma unroll 1
     for (int a = 0; a < na; a++) {
-      const int xc = tail ? xc1 : ((a == 0 && i == i0 && (i0 > 0 || A.iface_lo)) ? 2 : 0);
-      finalize_cell(P * i + a, a, rs, xc, latn);
-      finalize_edges(P * i + a, a, rs, xc, latn);
+      const int xc = tail ? xc1 : ((a == 0 && i == i0) ? xc0 : 0);
+      finalize_cell(a, rs, xc, latn);
+      finalize_edges(a, rs, xc, latn);
       rs = rs + 1 >= NR ? 0 : rs + 1;
     }
     rs0 = rs1;
   }
   block_max2(__longlong_as_double((long long)rec_amax[tid]), rec_smax[tid], A.red);
+#undef lcar
+#undef ecg
 }
