@@ -74,6 +74,7 @@ __global__ void __launch_bounds__(128, 3) k_xmarch2(SArgs A) {
   __shared__ double rec_my[NT], rec_mz[NT], rec_smax[NT];
   __shared__ unsigned long long rec_amax[NT];
   __shared__ unsigned char latf[LATENT ? EN : 1];  // cell has latent increments this layer
+  __shared__ double beam_x[MB];  // x of the tabled beams (read per layer for the x factors)
   // record flags
   constexpr int RF_LIVE = 1, RF_SY = 2, RF_SZ = 4, RF_DIR = 8;
   // perimeter flags
@@ -235,6 +236,7 @@ __global__ void __launch_bounds__(128, 3) k_xmarch2(SArgs A) {
     const int b = e / CZ, r = e - (e / CZ) * CZ;
     src_factor_z<P>(A, anchor<P>(A, 2, k0 + r), A.beams[b], Sz + (r * MB + b) * Q);
   }
+  if (tid < nbt) beam_x[tid] = A.beams[tid].x;
   const int kl_top = A.nz - 1 - k0;
   const bool has_top = A.top_faces && kl_top < CZ;
   constexpr int CPW = (CY + NW - 1) / NW;
@@ -248,7 +250,7 @@ __global__ void __launch_bounds__(128, 3) k_xmarch2(SArgs A) {
                       return Tr[rs * PL + P * r * NZT + P * kl_top + b * NZT + P];
                     });
     }
-    if (tid < nbt) src_factor_xy<P>(A, anchor<P>(A, 0, il), A.beams[tid].x, Sx + tid * Q);
+    if (tid < nbt) src_factor_xy<P>(A, anchor<P>(A, 0, il), beam_x[tid], Sx + tid * Q);
   };
 
   // stability maxima (rec_amax: |T'| as its bit pattern, rec_smax: max T'):
@@ -356,7 +358,9 @@ __global__ void __launch_bounds__(128, 3) k_xmarch2(SArgs A) {
     po[sI + 1] = o11;
     const int h00 = (s_y || s_z) ? 0 : habs(o00), h01 = s_y ? 0 : habs(o01);
     const int h10 = s_z ? 0 : habs(o10), h11 = habs(o11);
-    if (max(max(h00, h01), max(h10, h11)) >= thr) {
+    // a warp-uniform branch (the vote keeps it from being if-converted into
+    // always-issued predicated code)
+    if (__any_sync(__activemask(), max(max(h00, h01), max(h10, h11)) >= thr)) {
       if (!(s_y || s_z)) track_exact(o00);
       if (!s_y) track_exact(o01);
       if (!s_z) track_exact(o10);
@@ -407,7 +411,7 @@ __global__ void __launch_bounds__(128, 3) k_xmarch2(SArgs A) {
         double o = Tr[rs * PL + pr.w] + A.dt * (ci * f);
         if (A.dir_bottom && Kg == 0) o = A.P.T_inf;
         A.out[idx] = o;
-        if (habs(o) >= thr) track_exact(o);
+        if (__any_sync(__activemask(), habs(o) >= thr)) track_exact(o);
       }
     }
   };
