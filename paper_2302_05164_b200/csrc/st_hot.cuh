@@ -49,12 +49,6 @@ static constexpr size_t march_smem() {
          sizeof(double);
 }
 
-// the lean Q2 explicit-step kernel (k_xmarch2) replaces k_xmarch<2> for
-// explicit steps with a uniform history (ST_XMARCH2=0: the general kernel)
-static inline bool use_xmarch2() {
-  const char* e = getenv("ST_XMARCH2");  // read per launch: tests toggle it
-  return !(e && e[0] == '0');
-}
 static constexpr size_t march2_smem() {
   constexpr int P = 2, CY = 8, CZ = 16, Q = 3;
   return (size_t)((2 * P + 1) * (P * CY + 1) * (P * CZ + 1) + P * Q * Q * (CY + 2) * (CZ + 2) +
@@ -118,8 +112,7 @@ cudaError_t hot_launch(const SArgs& A, bool slab, bool lat, bool rcf, dim3 grid,
   const void* fn;
   size_t smem;
   int threads;
-  const bool x2 = P == 2 && !slab && !rcf && A.mode == 0 &&
-                  A.flags == (ST_RHS_DIFFUSION | ST_RHS_FACES | ST_RHS_SOURCE) && use_xmarch2();
+  const bool x2 = P == 2 && A.x2 != 0;
   cudaError_t e = lat ? hot_kernel<P, true>(slab, rcf, x2, &fn, &smem, &threads)
                       : hot_kernel<P, false>(slab, rcf, x2, &fn, &smem, &threads);
   if (e != cudaSuccess) return e;

@@ -603,10 +603,20 @@ struct Structured : Backend {
   long long lx = 0, ly = 0, lz = 0;
   DevBuf<double> cinv, fseam, cseam, lcarry, ecg, packf[2], packc[2];
   DevBuf<double> Eg;  // element vectors of the generic (implicit-path) kernels
-  DevBuf<int64_t> sidx;
-  DevBuf<unsigned short> scode;
-  DevBuf<double> sci;
-  int64_t n_seam = 0;
+  // seam lists (k_seam_list): [0] every seam node (the general kernels;
+  // built when first needed), [1] only the nodes k_xmarch2 leaves to the
+  // pass when it completes the ordinary planes' seams itself (x-seam planes
+  // and rank interfaces)
+  struct SeamList {
+    DevBuf<int64_t> sidx;
+    DevBuf<unsigned short> scode;
+    DevBuf<double> sci;
+    int64_t n = 0;
+    bool built = false;
+  } slist[2];
+  DevBuf<int> seamcnt;  // arrival counters of k_xmarch2's in-kernel seam completion
+  int GY = 0, GZ = 0;
+  bool inseam = false;  // k_xmarch2 completes ordinary-plane seams in the kernel
   int64_t nv = 0;
 
   // nodes of node plane I
@@ -652,6 +662,11 @@ struct Structured : Backend {
     A.seam_pair = slab && c->dp.latent ? 1 : 0;
     A.lcarry = lcarry.p;
     A.ecg = ecg.p;
+    A.seamcnt = inseam ? seamcnt.p : nullptr;
+    A.GY = GY;
+    A.GZ = GZ;
+    A.m1_0 = host_m1(p, 0);
+    A.m1_p = host_m1(p, p);
     A.snv = nv;
     for (int sd = 0; sd < 2; sd++) {
       A.ipf[sd] = packf[sd].p;
@@ -738,14 +753,17 @@ struct Structured : Backend {
 
   int seams(SArgs& A) {
     const bool lat = c->dp.latent != 0 && A.mode == 0;
-    if (n_seam > 0) {
+    const int which = (A.x2 && A.seamcnt) ? 1 : 0;
+    if (!slist[which].built) ST_TRY(build_seam_list(which));
+    const SeamList& L = slist[which];
+    if (L.n > 0) {
       // one thread per seam node: the pass is latency bound
       constexpr int kSB = 128;  // measured a hair faster than 256
-      const unsigned grid = (unsigned)((n_seam + kSB - 1) / kSB);
+      const unsigned grid = (unsigned)((L.n + kSB - 1) / kSB);
       if (lat)
-        k_seam_list<true><<<grid, kSB, 0, c->stream>>>(A, n_seam, sidx.p, scode.p, sci.p);
+        k_seam_list<true><<<grid, kSB, 0, c->stream>>>(A, L.n, L.sidx.p, L.scode.p, L.sci.p);
       else
-        k_seam_list<false><<<grid, kSB, 0, c->stream>>>(A, n_seam, sidx.p, scode.p, sci.p);
+        k_seam_list<false><<<grid, kSB, 0, c->stream>>>(A, L.n, L.sidx.p, L.scode.p, L.sci.p);
       ST_TRY(launched());
     }
     return ST_OK;
@@ -758,7 +776,10 @@ struct Structured : Backend {
   // or a low rank interface) + 2 (first column of a tile u > 0) + 4
   // (first row of a tile row t > 0 with material below), exactly the
   // hot kernel's rule; the list records which slots each node has.
-  int build_seam_list() {
+  // which = 1: only the nodes with an x seam among their contributors (a
+  // tile row with two x chunks at the node's plane) or on a rank interface
+  int build_seam_list(int which) {
+    const bool xonly = which == 1;
     const int sx = p * Lx, sy = p * cy, sz = p * cz;
     const int nty = (m.ny + cy - 1) / cy, ntz = (m.nz + cz - 1) / cz;
     auto ext_t = [&](int t) { return fitted ? text_h[t] : m.nx; };
@@ -794,6 +815,7 @@ struct Structured : Backend {
       }
       unsigned mask = 0;
       int count = 0;
+      bool xany = false;
       for (int a = 0; a < nt; a++) {
         const int t = tl[a], ext = ext_t(t);
         int cl[2], nc = 0;
@@ -801,6 +823,7 @@ struct Structured : Backend {
           if (cc < 0 || (nc && cl[nc - 1] == cc)) continue;
           if (cc * Lx < ext && cc * sx <= I && I <= p * std::min((cc + 1) * Lx, ext)) cl[nc++] = cc;
         }
+        xany |= nc == 2;
         for (int b = 0; b < nu; b++)
           for (int e = 0; e < nc; e++) {
             const int bit = ((I == cl[e] * sx && (cl[e] > 0 || m.iface_lo)) ? 1 : 0) +
@@ -812,6 +835,7 @@ struct Structured : Backend {
       }
       const int side = (I == 0 && m.iface_lo) ? 0 : ((I == NX - 1 && m.iface_hi) ? 1 : -1);
       if (count < 2 && side < 0) return;
+      if (xonly && !xany && side < 0) return;
       idx.push_back(base_of(I) + (int64_t)J * (NZ - kmI) + K);
       code.push_back((unsigned short)(mask | ((side + 1) << 8) | (K == 0 ? 1024 : 0)));
       // inverse lumped capacity: the hot kernel's tensor product where the
@@ -866,6 +890,7 @@ struct Structured : Backend {
       (void)npres;
     };
     for (int I = 0; I < NX; I++) {
+      if (xonly && !xcand[I]) continue;
       const int kmI = kmin_of(I);
       for (int J = 0; J < NY; J++) {
         const bool yc = J > 0 && J < NY - 1 && J % sy == 0;
@@ -876,11 +901,13 @@ struct Structured : Backend {
         }
       }
     }
-    n_seam = (int64_t)idx.size();
-    if (n_seam == 0) return ST_OK;
-    ST_TRY(sidx.upload(idx.data(), idx.size(), c->stream));
-    ST_TRY(scode.upload(code.data(), code.size(), c->stream));
-    ST_TRY(sci.upload(ci.data(), ci.size(), c->stream));
+    SeamList& L = slist[which];
+    L.built = true;
+    L.n = (int64_t)idx.size();
+    if (L.n == 0) return ST_OK;
+    ST_TRY(L.sidx.upload(idx.data(), idx.size(), c->stream));
+    ST_TRY(L.scode.upload(code.data(), code.size(), c->stream));
+    ST_TRY(L.sci.upload(ci.data(), ci.size(), c->stream));
     // the host vectors die here: finish the uploads first
     ST_CUDA(cudaStreamSynchronize(c->stream));
     return ST_OK;
@@ -896,6 +923,10 @@ struct Structured : Backend {
                 " beams per step");
       return ST_EUNSUPPORTED;
     }
+    A.x2 = (p == 2 && !slab && !rcf && A.mode == 0 &&
+            A.flags == (ST_RHS_DIFFUSION | ST_RHS_FACES | ST_RHS_SOURCE) && use_xmarch2())
+               ? 1
+               : 0;
     if (z1 < 0) z1 = n_chunks();
     if (z1 <= z0) return with_seams ? seams(A) : ST_OK;
     c->prof_begin();
@@ -1327,7 +1358,27 @@ Backend* make_structured(Ctx* c, const st_structured_mesh* m, int* err) {
       rc = ST_ECUDA;
     }
   }
-  if (rc == ST_OK) rc = s->build_seam_list();
+  // opt-in (ST_INSEAM=1): k_xmarch2 completes the seams of ordinary planes
+  // itself (arrival counters per chunk and seam group).  Measured slower than
+  // the seam pass on config 4 (21.1 ms against 12.8 + 3.6 ms): the completion
+  // is a latency-bound gather that a CTA runs with far fewer loads in flight
+  // than the pass's one thread per node.
+  if (rc == ST_OK && !s->slab && s->p == 2) {
+    const char* e = getenv("ST_INSEAM");
+    s->GY = 2 * (int)nty + 1;
+    s->GZ = 2 * (int)ntz + 1;
+    const int64_t ncnt = (int64_t)s->NX * s->GY * s->GZ;
+    if (e && e[0] == '1' && ncnt < (1ll << 31)) {
+      rc = s->seamcnt.alloc((size_t)ncnt);
+      if (rc == ST_OK &&
+          cudaMemsetAsync(s->seamcnt.p, 0, (size_t)ncnt * sizeof(int), c->stream) != cudaSuccess)
+        rc = ST_ECUDA;
+      s->inseam = rc == ST_OK;
+    }
+  }
+  // the list the context's explicit steps use; the other one is built when a
+  // launch first needs it
+  if (rc == ST_OK) rc = s->build_seam_list(s->inseam ? 1 : 0);
   if (rc != ST_OK) {
     delete s;
     *err = rc;

@@ -45,6 +45,15 @@ struct SArgs {
   // a window of high words (candidates for the exact test)
   double* ecg;
   int lat_hi0, lat_hiw;
+  // k_xmarch2 launches (x2, set by the host per launch); with seamcnt != 0
+  // the kernel completes the seams of ordinary planes itself: one arrival
+  // counter per (plane, seam group), index (I GY + gy) GZ + gz with gy / gz
+  // = 2 line for a tile seam line, 2 tile + 1 inside a tile; m1_0 / m1_p: 1D
+  // lumped masses of a cell's end nodes (re-entrant edge of a fitted part)
+  int x2;
+  int* seamcnt;
+  int GY, GZ;
+  double m1_0, m1_p;
   int64_t snv;
   // rank interfaces: own pre-summed plane (packed after the sweep) and the
   // neighbour's, per side (0: local plane 0, 1: local plane NX-1)
@@ -184,6 +193,14 @@ __device__ __forceinline__ double finalize_node(const SArgs& A, double ci, bool 
   // selects, not branches (measured faster in every hot kernel): rhs mode
   // (mode 1) returns f
   return A.mode == 1 ? f : o;
+}
+
+// the lean Q2 explicit-step kernel (k_xmarch2) replaces k_xmarch<2> for
+// explicit steps with a uniform history (ST_XMARCH2=0: the general kernel);
+// read per launch, tests toggle it
+static inline bool use_xmarch2() {
+  const char* e = getenv("ST_XMARCH2");
+  return !(e && e[0] == '0');
 }
 
 // tile of k_xmarch (CY x CZ cells, one thread per cell)

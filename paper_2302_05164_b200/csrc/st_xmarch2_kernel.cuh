@@ -32,6 +32,17 @@
 //     L2-resident global scratch instead of 18 KB of shared memory;
 //   * one loop body serves the layers and the chunk's last plane, so the
 //     finalisation code exists once (instruction cache).
+// In-kernel seam completion (A.seamcnt != 0): the seams of ordinary planes
+// (y / z tile seams; everything but the x-seam planes at chunk boundaries and
+// rank interfaces, which stay with the seam pass) are finished by the last
+// CTA to arrive.  Every CTA stores its partials to its slots as before; when
+// its chunk is done, one lane per seam group (the tile's 4 faces and 4 corner
+// lines over the chunk) bumps the group's arrival counter (after a barrier,
+// fence + atomicInc that wraps back to zero), and the CTA that sees the last
+// arrival sums the slots of the group's nodes in the seam pass's fixed order
+// and finalises them (a dense loop with several loads in flight per thread).
+// No CTA ever waits for another, and the sums do not depend on the arrival
+// order.
 // Results are bitwise those of k_xmarch (except the sign of exact zeros).
 #pragma once
 
@@ -92,6 +103,10 @@ __global__ void __launch_bounds__(128, 3) k_xmarch2(SArgs A) {
   // tile-edge node lines are seams unless they are the domain boundary
   const bool ty_lo = j0 > 0, ty_hi = j0 + CY < A.ny;
   const bool tz_lo = k0 > 0, tz_hi = k0 + CZ < A.nz;
+  // x extents of the tile rows below / above (in-kernel seam completion)
+  const int ext_lo = (A.text && blockIdx.y > 0) ? A.text[blockIdx.y - 1] : A.nx;
+  const int ext_hi = (A.text && blockIdx.y + 1 < gridDim.y) ? A.text[blockIdx.y + 1] : A.nx;
+  const bool inseam = A.seamcnt != nullptr;
   const CellFlags F{true, true, A.nb > 0, false};
   const int64_t plane_stride = (int64_t)A.NY * A.NZ;
   const double imr1 = A.imr[1];
@@ -349,12 +364,11 @@ __global__ void __launch_bounds__(128, 3) k_xmarch2(SArgs A) {
       o00 = A.P.T_inf;
       o10 = A.P.T_inf;
     }
-    // a seam node's entry (its partial goes out with the perimeter pass) is
-    // overwritten by the seam pass, which runs after this kernel
+    // a seam node's partial goes out with the perimeter pass
     double* po = A.out + g0;
-    po[0] = o00;
-    po[1] = o01;
-    po[sI] = o10;
+    if (!(s_y || s_z)) po[0] = o00;
+    if (!s_y) po[1] = o01;
+    if (!s_z) po[sI] = o10;
     po[sI + 1] = o11;
     const int h00 = (s_y || s_z) ? 0 : habs(o00), h01 = s_y ? 0 : habs(o01);
     const int h10 = s_z ? 0 : habs(o10), h11 = habs(o11);
@@ -550,6 +564,131 @@ __global__ void __launch_bounds__(128, 3) k_xmarch2(SArgs A) {
       rs = rs + 1 >= NR ? 0 : rs + 1;
     }
     rs0 = rs1;
+  }
+  if (inseam) {
+    // ---- seam completion of the chunk's ordinary planes ----
+    // groups: faces y-low, y-high, z-low, z-high (0-3), corner lines (J, K) =
+    // (0, 0), (0, hi), (hi, 0), (hi, hi) (4-7); a group's contributors are the
+    // CTAs of this chunk that share the line / face
+    __shared__ unsigned char glast[8];
+    __syncthreads();  // the chunk's partial stores are issued
+    if (tid < 8) {
+      const int g = tid;
+      const bool ylo = g == 0 || g == 4 || g == 5, yhi = g == 1 || g == 6 || g == 7;
+      const bool zlo = g == 2 || g == 4 || g == 6, zhi = g == 3 || g == 5 || g == 7;
+      const bool ys = (ylo && ty_lo) || (yhi && ty_hi);
+      const bool zs = (zlo && tz_lo && ext_lo > i0) || (zhi && tz_hi);
+      const int need = (ys ? 2 : 1) * (zs ? 2 : 1);
+      bool last = false;
+      if (need > 1) {
+        const int gy = 2 * (int)blockIdx.x + (ylo ? 0 : (yhi ? 2 : 1));
+        const int gz = 2 * (int)blockIdx.y + (zlo ? 0 : (zhi ? 2 : 1));
+        __threadfence();
+        last = atomicInc((unsigned*)A.seamcnt + ((chunk * A.GY + gy) * A.GZ + gz),
+                         (unsigned)need - 1u) == (unsigned)need - 1u;
+        if (last) __threadfence();
+      }
+      glast[g] = last ? 1 : 0;
+    }
+    __syncthreads();
+    // plane range of the chunk without its x-seam planes
+    const int Ia = P * i0 + (xc0 != 0 ? 1 : 0), Ib = P * i1 - (xc1 != 0 ? 1 : 0);
+    auto xplane = [&](int I, int e) { return I > 0 && I % (P * A.Lx) == 0 && I < P * e; };
+#pragma unroll 1
+    for (int g = 0; g < 8; g++) {
+      if (!glast[g]) continue;
+      const bool ylo = g == 0 || g == 4 || g == 5, yhi = g == 1 || g == 6 || g == 7;
+      const bool zlo = g == 2 || g == 4 || g == 6, zhi = g == 3 || g == 5 || g == 7;
+      const bool yn = (ylo && ty_lo) || (yhi && ty_hi);
+      // nodes of the group in a plane: a face's interior line or a corner
+      const int nn = g < 2 ? Kn - 2 : (g < 4 ? Jn - 2 : 1);
+      const int items = (Ib - Ia + 1) * nn;
+      constexpr int U = 4;  // loads of U nodes in flight per thread
+#pragma unroll 1
+      for (int itb = tid; itb < items; itb += U * NT) {
+        double s0[U], s2[U], s4[U], s6[U], c0[U], c2[U], c4[U], c6[U], Tn[U];
+        int64_t idx[U];
+        int Iu[U], JK[U], km[U];
+        bool zn[U], on[U];
+#pragma unroll
+        for (int u = 0; u < U; u++) {
+          const int it = itb + u * NT;
+          on[u] = it < items;
+          s0[u] = s2[u] = s4[u] = s6[u] = c0[u] = c2[u] = c4[u] = c6[u] = Tn[u] = 0.0;
+          idx[u] = 0;
+          Iu[u] = JK[u] = km[u] = 0;
+          zn[u] = false;
+          if (!on[u]) continue;
+          const int pl = it / nn, e = it - pl * nn;
+          const int I = Ia + pl;
+          const int J = g < 2 ? (g == 0 ? 0 : Jn - 1) : (g < 4 ? e + 1 : (yhi ? Jn - 1 : 0));
+          const int K = g < 2 ? e + 1 : (g < 4 ? (g == 2 ? 0 : Kn - 1) : (zhi ? Kn - 1 : 0));
+          const int kmI = A.pkmin ? A.pkmin[I] : 0;
+          const int sI = A.NZ - kmI;
+          const bool z = (zlo && tz_lo && kmI < P * k0 && !xplane(I, ext_lo)) ||
+                         (zhi && tz_hi && !xplane(I, ext_hi));
+          // a z-low line above a row that has ended is no seam at this plane
+          if (!(yn || z) || ((zlo || zhi) && !yn && !z)) {
+            on[u] = false;
+            continue;
+          }
+          // (a corner line whose z seam is with the seam pass at this plane
+          // is with the seam pass as a whole)
+          if ((zlo && tz_lo && kmI < P * k0 && xplane(I, ext_lo)) ||
+              (zhi && tz_hi && xplane(I, ext_hi))) {
+            on[u] = false;
+            continue;
+          }
+          Iu[u] = I;
+          JK[u] = J | (K << 8);
+          km[u] = kmI;
+          zn[u] = z;
+          idx[u] = (A.pbase ? A.pbase[I] : (int64_t)I * plane_stride) +
+                   ((P * j0 + J) * sI + P * k0 + K);
+          const double* fs = A.fseam + idx[u];
+          s0[u] = __ldcg(fs);
+          if (yn) s2[u] = __ldcg(fs + 2 * A.snv);
+          if (z) s4[u] = __ldcg(fs + 4 * A.snv);
+          if (yn && z) s6[u] = __ldcg(fs + 6 * A.snv);
+          if (LATENT) {
+            const double* cs = A.cseam + idx[u];
+            c0[u] = __ldcg(cs);
+            if (yn) c2[u] = __ldcg(cs + 2 * A.snv);
+            if (z) c4[u] = __ldcg(cs + 4 * A.snv);
+            if (yn && z) c6[u] = __ldcg(cs + 6 * A.snv);
+          }
+          Tn[u] = A.T[idx[u]];
+        }
+#pragma unroll
+        for (int u = 0; u < U; u++) {
+          if (!on[u]) continue;
+          const int I = Iu[u], J = JK[u] & 255, K = JK[u] >> 8, kmI = km[u];
+          // the seam pass's order: x side, then z side, then y side
+          const double f = ((s0[u] + s2[u]) + s4[u]) + s6[u];
+          const double dc = LATENT ? ((c0[u] + c2[u]) + c4[u]) + c6[u] : 0.0;
+          const int Jg = P * j0 + J, Kg = P * k0 + K;
+          const double my = (J & 1) ? imr1 : ((Jg == 0 || Jg == A.NY - 1) ? A.imv_end : A.imv_int);
+          // z line of the node: extents of the tile rows below / above it
+          const int e_low = zlo ? ext_lo : ext, e_up = zlo ? ext : ext_hi;
+          double ci;
+          if (zn[u] && e_low < e_up && I == P * e_low) {
+            // re-entrant edge (the lower row ends here, the upper one goes
+            // on): row sum over the three cells present (operators.py:325-339)
+            const double mxz = ((A.m1_p * A.m1_p) + (A.m1_p * A.m1_0)) + (A.m1_0 * A.m1_0);
+            ci = (1.0 / mxz) * (my * A.inv_rcdw);
+          } else {
+            const double mz =
+                (K & 1) ? imr1 : ((Kg == kmI || Kg == A.NZ - 1) ? A.imv_end : A.imv_int);
+            ci = mz * (my * plane_imx(I));
+          }
+          if (LATENT && dc > 0.0) ci = ci / fma(ci, dc, 1.0);
+          double o = Tn[u] + A.dt * (ci * f);
+          if (A.dir_bottom && Kg == 0) o = A.P.T_inf;
+          A.out[idx[u]] = o;
+          if (habs(o) >= thr) track_exact(o);
+        }
+      }
+    }
   }
   block_max2(__longlong_as_double((long long)rec_amax[tid]), rec_smax[tid], A.red);
 #undef lcar

@@ -26,8 +26,9 @@ def _params(latent):
     return st.ProcessParams(mat, bnd, las, st.MeshParams(h_coarse=H, n_refine=0, h_powder=H))
 
 
-def _run(mesh, latent, lx, x2, monkeypatch, steps=6):
+def _run(mesh, latent, lx, x2, monkeypatch, steps=6, inseam=False):
     monkeypatch.setenv("ST_XMARCH2", "1" if x2 else "0")
+    monkeypatch.setenv("ST_INSEAM", "1" if inseam else "0")
     if lx:
         monkeypatch.setenv("ST_LX", lx)
     else:
@@ -58,13 +59,16 @@ CASES = {
 }
 
 
+@pytest.mark.parametrize("inseam", [False, True])
 @pytest.mark.parametrize("lx", [None, "3"])
 @pytest.mark.parametrize("latent", [True, False])
 @pytest.mark.parametrize("case", list(CASES))
-def test_lean_kernel_equals_general_kernel_bitwise(case, latent, lx, monkeypatch):
+def test_lean_kernel_equals_general_kernel_bitwise(case, latent, lx, inseam, monkeypatch):
+    """inseam: the opt-in in-kernel seam completion (last-arriving CTA sums
+    the slots in the seam pass's order) instead of the seam pass."""
     mesh = CASES[case]()
     f0, a0, t0, T0 = _run(mesh, latent, lx, False, monkeypatch)
-    f1, a1, t1, T1 = _run(mesh, latent, lx, True, monkeypatch)
+    f1, a1, t1, T1 = _run(mesh, latent, lx, True, monkeypatch, inseam=inseam)
     assert f0 == f1
     assert a0 == a1 and t0 == t1
     assert np.array_equal(T0, T1)
