@@ -587,6 +587,10 @@ static double host_m1(int p, int a) {
 }
 
 struct Structured : Backend {
+  ~Structured() override {
+    if (latstat_h) cudaFreeHost(latstat_h);
+    if (lat_ev) cudaEventDestroy(lat_ev);
+  }
   st_structured_mesh m{};
   // fitted part (m.xext != NULL): per cell row x extent, per node plane
   // lowest row and first-node base, per tile row x extent
@@ -614,6 +618,19 @@ struct Structured : Backend {
     int64_t n = 0;
     bool built = false;
   } slist[2];
+  // latent-dense fields (every tile gathers latent increments in most
+  // layers, e.g. config 2's random field): k_xmarch2 keeps the increments in
+  // an L2 scratch and loses to the general kernel's shared-memory copy there,
+  // so the kernels count their latent CTA-layers and the host, reading the
+  // counter asynchronously every few steps, picks the kernel (both give
+  // bitwise the same field)
+  DevBuf<unsigned long long> latstat;
+  unsigned long long* latstat_h = nullptr;  // pinned
+  cudaEvent_t lat_ev = nullptr;
+  bool lat_pending = false, prefer_general = false;
+  unsigned long long lat_seen = 0;
+  double lat_launched = 0.0, lat_launched_rec = 0.0, lat_launched_seen = 0.0;
+  int lat_calls = 0;
   DevBuf<int> seamcnt;  // arrival counters of k_xmarch2's in-kernel seam completion
   int GY = 0, GZ = 0;
   bool inseam = false;  // k_xmarch2 completes ordinary-plane seams in the kernel
@@ -662,6 +679,7 @@ struct Structured : Backend {
     A.seam_pair = slab && c->dp.latent ? 1 : 0;
     A.lcarry = lcarry.p;
     A.ecg = ecg.p;
+    A.latstat = latstat.p;
     A.seamcnt = inseam ? seamcnt.p : nullptr;
     A.GY = GY;
     A.GZ = GZ;
@@ -923,8 +941,10 @@ struct Structured : Backend {
                 " beams per step");
       return ST_EUNSUPPORTED;
     }
+    if (lat && latstat_h) poll_latent();
     A.x2 = (p == 2 && !slab && !rcf && A.mode == 0 &&
-            A.flags == (ST_RHS_DIFFUSION | ST_RHS_FACES | ST_RHS_SOURCE) && use_xmarch2())
+            A.flags == (ST_RHS_DIFFUSION | ST_RHS_FACES | ST_RHS_SOURCE) && use_xmarch2() &&
+            !(lat && prefer_general))
                ? 1
                : 0;
     if (z1 < 0) z1 = n_chunks();
@@ -948,7 +968,43 @@ struct Structured : Backend {
     }
     c->prof_end();
     ST_TRY(rc);
+    if (lat && latstat_h) record_latent(z0, z1);
     return with_seams ? seams(A) : ST_OK;
+  }
+
+  // CTA-layers of a launch over the x chunks [z0, z1)
+  double launch_layers(int z0, int z1) const {
+    const int nty = (m.ny + cy - 1) / cy, ntz = (m.nz + cz - 1) / cz;
+    double n = 0.0;
+    for (int t = 0; t < ntz; t++) {
+      const int e = fitted ? text_h[t] : m.nx;
+      n += (double)nty * (std::min(e, z1 * Lx) - std::min(e, z0 * Lx));
+    }
+    return n;
+  }
+  void poll_latent() {
+    if (!lat_pending || cudaEventQuery(lat_ev) != cudaSuccess) return;
+    lat_pending = false;
+    const double d = (double)(*latstat_h - lat_seen), n = lat_launched_rec - lat_launched_seen;
+    lat_seen = *latstat_h;
+    lat_launched_seen = lat_launched_rec;
+    if (n <= 0.0) return;
+    const double frac = d / n;
+    // hysteresis: dense above one half, sparse again below a quarter
+    if (frac > 0.5) prefer_general = true;
+    if (frac < 0.25) prefer_general = false;
+  }
+  void record_latent(int z0, int z1) {
+    lat_launched += launch_layers(z0, z1);
+    if (lat_pending || (++lat_calls & 3) != 0) return;
+    if (cudaMemcpyAsync(latstat_h, latstat.p, sizeof(unsigned long long), cudaMemcpyDeviceToHost,
+                        c->stream) != cudaSuccess ||
+        cudaEventRecord(lat_ev, c->stream) != cudaSuccess) {
+      cudaGetLastError();
+      return;
+    }
+    lat_launched_rec = lat_launched;
+    lat_pending = true;
   }
 
   // --- multi-GPU slab step (rank interfaces exchanged between the halves)
@@ -1356,6 +1412,18 @@ Backend* make_structured(Ctx* c, const st_structured_mesh* m, int* err) {
     if (cudaGetLastError() != cudaSuccess || cudaStreamSynchronize(c->stream) != cudaSuccess) {
       set_error("structured setup kernels failed");
       rc = ST_ECUDA;
+    }
+  }
+  if (rc == ST_OK && !s->slab && s->p == 2 && c->dp.latent && use_xmarch2()) {
+    const char* e = getenv("ST_X2_ADAPT");  // ST_X2_ADAPT=0: never leave k_xmarch2
+    if (!(e && e[0] == '0')) {
+      rc = s->latstat.alloc(1);
+      if (rc == ST_OK &&
+          (cudaMemsetAsync(s->latstat.p, 0, sizeof(unsigned long long), c->stream) != cudaSuccess ||
+           cudaMallocHost(&s->latstat_h, sizeof(unsigned long long)) != cudaSuccess ||
+           cudaEventCreateWithFlags(&s->lat_ev, cudaEventDisableTiming) != cudaSuccess))
+        rc = ST_ECUDA;
+      if (rc == ST_OK) *s->latstat_h = 0;
     }
   }
   // opt-in (ST_INSEAM=1): k_xmarch2 completes the seams of ordinary planes

@@ -51,6 +51,9 @@ struct SArgs {
   // = 2 line for a tile seam line, 2 tile + 1 inside a tile; m1_0 / m1_p: 1D
   // lumped masses of a cell's end nodes (re-entrant edge of a fitted part)
   int x2;
+  // CTA-layers that gathered latent increments, accumulated over launches
+  // (the host picks the kernel for latent-dense fields from it)
+  unsigned long long* latstat;
   int* seamcnt;
   int GY, GZ;
   double m1_0, m1_p;

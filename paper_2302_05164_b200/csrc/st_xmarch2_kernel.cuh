@@ -46,8 +46,12 @@
 // Results are bitwise those of k_xmarch (except the sign of exact zeros).
 #pragma once
 
+#ifndef ST_X2_MINB
+#define ST_X2_MINB 3  // A/B hook: resident CTAs per SM the register allocation aims at
+#endif
+
 template <bool LATENT>
-__global__ void __launch_bounds__(128, 3) k_xmarch2(SArgs A) {
+__global__ void __launch_bounds__(128, ST_X2_MINB) k_xmarch2(SArgs A) {
   constexpr int P = 2, Q = 3, Q3 = 27, CY = 8, CZ = 16, NT = 128, NW = 4;
   constexpr int NYT = P * CY + 1, NZT = P * CZ + 1, PL = NYT * NZT;
   constexpr int NR = 2 * P + 1;
@@ -84,6 +88,7 @@ __global__ void __launch_bounds__(128, 3) k_xmarch2(SArgs A) {
   // pattern) and max T'
   __shared__ double rec_my[NT], rec_mz[NT], rec_smax[NT];
   __shared__ unsigned long long rec_amax[NT];
+  __shared__ unsigned rec_ym[NT];  // beams that can reach the cell's (y, z) column
   __shared__ unsigned char latf[LATENT ? EN : 1];  // cell has latent increments this layer
   __shared__ double beam_x[MB];  // x of the tabled beams (read per layer for the x factors)
   // record flags
@@ -99,14 +104,11 @@ __global__ void __launch_bounds__(128, 3) k_xmarch2(SArgs A) {
   const int i1 = min(i0 + A.Lx, ext);
   const int Jn = min(P * CY, P * (A.ny - j0)) + 1;
   const int Kn = min(P * CZ, P * (A.nz - k0)) + 1;
-  const int nhi = Kn + Jn - 1, nper = 2 * Kn + 2 * (Jn - 2);
+#define nhi (Kn + Jn - 1)
+#define nper (2 * Kn + 2 * (Jn - 2))
   // tile-edge node lines are seams unless they are the domain boundary
   const bool ty_lo = j0 > 0, ty_hi = j0 + CY < A.ny;
   const bool tz_lo = k0 > 0, tz_hi = k0 + CZ < A.nz;
-  // x extents of the tile rows below / above (in-kernel seam completion)
-  const int ext_lo = (A.text && blockIdx.y > 0) ? A.text[blockIdx.y - 1] : A.nx;
-  const int ext_hi = (A.text && blockIdx.y + 1 < gridDim.y) ? A.text[blockIdx.y + 1] : A.nx;
-  const bool inseam = A.seamcnt != nullptr;
   const CellFlags F{true, true, A.nb > 0, false};
   const int64_t plane_stride = (int64_t)A.NY * A.NZ;
   const double imr1 = A.imr[1];
@@ -242,6 +244,7 @@ __global__ void __launch_bounds__(128, 3) k_xmarch2(SArgs A) {
     const int kl = tid / CY, jl = tid % CY;
     if (j0 + jl < A.ny && k0 + kl < A.nz) ymask = beam_column_mask<P>(A, j0 + jl, k0 + kl);
   }
+  rec_ym[tid] = ymask;
   const int nbt = (F.source && __syncthreads_or(ymask != 0u)) ? min(A.nb, MB) : 0;
   for (int e = tid; e < nbt * CY; e += NT) {
     const int b = e / CY, r = e - (e / CY) * CY;
@@ -448,8 +451,12 @@ __global__ void __launch_bounds__(128, 3) k_xmarch2(SArgs A) {
 
   // one loop body for the layers and the chunk's last plane (tail: i == i1,
   // the carried x face as element plane 0)
-  const int xc1 = (i1 < ext || (A.iface_hi && ext == A.nx)) ? 1 : 0;
-  const int xc0 = (i0 > 0 || A.iface_lo) ? 2 : 0;
+  // x-seam state of the chunk's first / last plane (recomputed where used:
+  // two registers less across the cell evaluation)
+#define xc1 ((i1 < ext || (A.iface_hi && ext == A.nx)) ? 1 : 0)
+#define xc0 ((i0 > 0 || A.iface_lo) ? 2 : 0)
+  __shared__ int nlat_s;  // layers that gathered latent increments
+  if (tid == 0) nlat_s = 0;
 #pragma unroll 1
   for (int i = i0; i <= i1; i++) {
     const bool tail = i == i1;
@@ -498,7 +505,7 @@ __global__ void __launch_bounds__(128, 3) k_xmarch2(SArgs A) {
       {
         const int kl = tid / CY, jl = tid % CY;
         cell_element<P, false, true>(
-            A, F, i, j0 + jl, k0 + kl, 0, t, G, ymask, [&](int, int, int) { return 0.0; }, Sx,
+            A, F, i, j0 + jl, k0 + kl, 0, t, G, rec_ym[tid], [&](int, int, int) { return 0.0; }, Sx,
             Sy + jl * MB * Q, Sz + kl * MB * Q, Fo + jl * Q * Q);
       }
 #pragma unroll
@@ -551,6 +558,7 @@ __global__ void __launch_bounds__(128, 3) k_xmarch2(SArgs A) {
     }
     cp_wait<0>();
     const bool latn = LATENT ? __syncthreads_or(lf) != 0 : (__syncthreads(), false);
+    if (LATENT && latn && tid == 0) nlat_s++;
     int rs1 = rs0 + P;  // first plane of the next layer
     rs1 = rs1 >= NR ? rs1 - NR : rs1;
     if (i + 1 < i1) side_work(i + 1, rs1);
@@ -565,8 +573,11 @@ __global__ void __launch_bounds__(128, 3) k_xmarch2(SArgs A) {
     }
     rs0 = rs1;
   }
-  if (inseam) {
+  if (A.seamcnt != nullptr) {
     // ---- seam completion of the chunk's ordinary planes ----
+    // x extents of the tile rows below / above
+    const int ext_lo = (A.text && blockIdx.y > 0) ? A.text[blockIdx.y - 1] : A.nx;
+    const int ext_hi = (A.text && blockIdx.y + 1 < gridDim.y) ? A.text[blockIdx.y + 1] : A.nx;
     // groups: faces y-low, y-high, z-low, z-high (0-3), corner lines (J, K) =
     // (0, 0), (0, hi), (hi, 0), (hi, hi) (4-7); a group's contributors are the
     // CTAs of this chunk that share the line / face
@@ -690,7 +701,13 @@ __global__ void __launch_bounds__(128, 3) k_xmarch2(SArgs A) {
       }
     }
   }
+  if (LATENT && tid == 0 && nlat_s > 0 && A.latstat)
+    atomicAdd(A.latstat, (unsigned long long)nlat_s);
   block_max2(__longlong_as_double((long long)rec_amax[tid]), rec_smax[tid], A.red);
 #undef lcar
 #undef ecg
+#undef xc0
+#undef xc1
+#undef nhi
+#undef nper
 }

@@ -329,6 +329,7 @@ __global__ void __launch_bounds__(CY* CZ, MinBlocks<P>::v) k_xmarch(SArgs A) {
     side_work(i0);
   }
 
+  int nlat = 0;  // layers that gathered latent increments (SArgs::latstat)
   // two barriers per layer: the top one publishes the layer's staged planes
   // and retires the previous layer's finalisation (E, its ring slots and its
   // latent flag slot are free), so the next layer's prefetch goes out right
@@ -408,6 +409,7 @@ __global__ void __launch_bounds__(CY* CZ, MinBlocks<P>::v) k_xmarch(SArgs A) {
     if (COOP && i + 1 < i1) side_work(i + 1);
     // latent increments of this layer or carried from the previous one
     const bool latn = LATENT && (lat_any[i % 3] | lat_any[(i + 2) % 3]);
+    if (LATENT && latn) nlat++;
 #pragma unroll
     for (int a = 0; a < P; a++) {
       cb[a] = pinfo_b[(P * i + a) % NR];
@@ -439,5 +441,6 @@ __global__ void __launch_bounds__(CY* CZ, MinBlocks<P>::v) k_xmarch(SArgs A) {
     __syncthreads();
     store_plane(P * i1, cbl, ckl);
   }
+  if (LATENT && tid == 0 && nlat > 0 && A.latstat) atomicAdd(A.latstat, (unsigned long long)nlat);
   block_max2(__longlong_as_double((long long)amaxb), smax, A.red);
 }

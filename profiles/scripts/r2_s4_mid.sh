@@ -1,5 +1,5 @@
 python -c "import __graft_entry__ as g; g.build()"
-timeout 900 python -m pytest tests/test_gpu_xmarch2.py tests/test_gpu_fitted.py tests/test_gpu_slabs_overlap.py -q -x > gpurun_out/x2_tests.txt 2>&1; echo "x2 tests rc=$?"; tail -4 gpurun_out/x2_tests.txt
+timeout 1500 python -m pytest tests/test_gpu_xmarch2.py tests/test_gpu_structured.py tests/test_gpu_fitted.py tests/test_gpu_slabs.py tests/test_gpu_slabs_overlap.py tests/test_gpu_parity_fullsize.py tests/test_gpu_operator.py -q -x > gpurun_out/x2_tests.txt 2>&1; echo "tests rc=$?"; tail -4 gpurun_out/x2_tests.txt
 for wl in config4 config1 config2_p2; do
   timeout 900 python bench.py --workload $wl --steps 20 --warmup 5 --sweep 0 --no-cpu-baseline > gpurun_out/x2_1_$wl.json 2>gpurun_out/x2_1_$wl.err; echo "$wl rc=$?"
   python -c "
