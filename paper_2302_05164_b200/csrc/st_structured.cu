@@ -628,6 +628,7 @@ struct Structured : Backend {
   unsigned long long* latstat_h = nullptr;  // pinned
   cudaEvent_t lat_ev = nullptr;
   bool lat_pending = false, prefer_general = false;
+  bool last_x2 = false;  // the last hot launch was k_xmarch2 (main_kernel)
   unsigned long long lat_seen = 0;
   double lat_launched = 0.0, lat_launched_rec = 0.0, lat_launched_seen = 0.0;
   int lat_calls = 0;
@@ -947,6 +948,7 @@ struct Structured : Backend {
             !(lat && prefer_general))
                ? 1
                : 0;
+    last_x2 = A.x2 != 0;
     if (z1 < 0) z1 = n_chunks();
     if (z1 <= z0) return with_seams ? seams(A) : ST_OK;
     c->prof_begin();
@@ -1222,7 +1224,9 @@ struct Structured : Backend {
     }
     return b;
   }
-  const char* main_kernel() const override { return slab ? "k_xslab" : "k_xmarch"; }
+  const char* main_kernel() const override {
+    return slab ? "k_xslab" : (last_x2 ? "k_xmarch2" : "k_xmarch");
+  }
   bool uniform_rc_ok() const override { return true; }
 };
 

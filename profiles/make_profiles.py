@@ -42,7 +42,9 @@ def main(r, workloads=None):
             print("missing", raw)
             continue
         s = summarize(raw)
-        dst = os.path.join(HERE, r) if os.path.isdir(os.path.join(HERE, r)) else HERE
+        # r2b / r2c captures live with the round's other files in profiles/r2/
+        rd = r if os.path.isdir(os.path.join(HERE, r)) else r[:2]
+        dst = os.path.join(HERE, rd) if os.path.isdir(os.path.join(HERE, rd)) else HERE
         with open(os.path.join(dst, f"{tag}_ncu_summary.json"), "w") as f:
             json.dump(s, f, indent=1)
         det = os.path.join(OUT, f"details_{tag}.txt")
