@@ -646,6 +646,16 @@ struct Structured : Backend {
     return ST_EUNSUPPORTED;
   }
 
+  // (f, dc) pairs in fseam (one 16-byte access per slot entry): k_xslab and
+  // the degree-2 k_xmarch / k_xmarch2 with latent heat; ST_SEAM_PAIR=0: split
+  // arrays
+  bool seam_pairs() const {
+    if (!c->dp.latent) return false;
+    if (slab) return true;
+    const char* e = getenv("ST_SEAM_PAIR");
+    return p == 2 && !(e && e[0] == '0');
+  }
+
   int launched() {
     c->launches++;
     ST_LAUNCHED();
@@ -677,7 +687,7 @@ struct Structured : Backend {
     A.rc_value = c->rc_value;
     A.fseam = fseam.p;
     A.cseam = cseam.p;
-    A.seam_pair = slab && c->dp.latent ? 1 : 0;
+    A.seam_pair = seam_pairs() ? 1 : 0;
     A.lcarry = lcarry.p;
     A.ecg = ecg.p;
     A.latstat = latstat.p;
@@ -998,7 +1008,8 @@ struct Structured : Backend {
   }
   void record_latent(int z0, int z1) {
     lat_launched += launch_layers(z0, z1);
-    if (lat_pending || (++lat_calls & 3) != 0) return;
+    // the first launch and every fourth after it
+    if (lat_pending || (lat_calls++ & 3) != 0) return;
     if (cudaMemcpyAsync(latstat_h, latstat.p, sizeof(unsigned long long), cudaMemcpyDeviceToHost,
                         c->stream) != cudaSuccess ||
         cudaEventRecord(lat_ev, c->stream) != cudaSuccess) {
@@ -1372,7 +1383,7 @@ Backend* make_structured(Ctx* c, const st_structured_mesh* m, int* err) {
     if (rc == ST_OK) rc = s->xext_d.upload(s->xext_h.data(), s->xext_h.size(), c->stream);
   }
   // seam slots (see SArgs::fseam / seam_pair)
-  const bool pair = s->slab && c->dp.latent;
+  const bool pair = s->seam_pairs();
   const size_t nseam = (size_t)(pair ? 16 : 8) * s->nv;
   if (rc == ST_OK) rc = s->fseam.alloc(nseam);
   if (rc == ST_OK && c->dp.latent && !pair) rc = s->cseam.alloc(nseam);

@@ -299,6 +299,27 @@ __global__ void __launch_bounds__(128, ST_X2_MINB) k_xmarch2(SArgs A) {
     return dc;
   };
 
+  // a seam partial (f, latent increment) to slot entry so: one 16-byte store
+  // where the context keeps (f, dc) pairs (SArgs::seam_pair)
+  auto seam_put = [&](int64_t so, double f, double dc) {
+    if (LATENT && A.seam_pair) {
+      reinterpret_cast<double2*>(A.fseam)[so] = make_double2(f, dc);
+    } else {
+      A.fseam[so] = f;
+      if (LATENT) A.cseam[so] = dc;
+    }
+  };
+  auto seam_get = [&](int64_t so, double& f, double& dc) {
+    if (LATENT && A.seam_pair) {
+      const double2 v = __ldcg(reinterpret_cast<const double2*>(A.fseam) + so);
+      f = v.x;
+      dc = v.y;
+    } else {
+      f = __ldcg(A.fseam + so);
+      dc = LATENT ? __ldcg(A.cseam + so) : 0.0;
+    }
+  };
+
   // the four nodes (b, c < 2) of this thread's cell in plane I (element
   // plane a, ring slot rs); xc: 0 = ordinary plane, 1 / 2 = x seam with this
   // CTA on the low / high side (every node of the plane is a seam then)
@@ -336,16 +357,10 @@ __global__ void __launch_bounds__(128, ST_X2_MINB) k_xmarch2(SArgs A) {
       const int64_t s01 = (int64_t)(xb + (s_y ? 2 : 0)) * A.snv + g0 + 1;
       const int64_t s10 = (int64_t)(xb + (s_z ? 4 : 0)) * A.snv + g0 + sI;
       const int64_t s11 = (int64_t)xb * A.snv + g0 + sI + 1;
-      A.fseam[s00] = f00;
-      A.fseam[s01] = f01;
-      A.fseam[s10] = f10;
-      A.fseam[s11] = f11;
-      if (LATENT) {
-        A.cseam[s00] = d00;
-        A.cseam[s01] = d01;
-        A.cseam[s10] = d10;
-        A.cseam[s11] = d11;
-      }
+      seam_put(s00, f00, d00);
+      seam_put(s01, f01, d01);
+      seam_put(s10, f10, d10);
+      seam_put(s11, f11, d11);
       return;
     }
     const double imIs = pinfo_im[rs];
@@ -416,9 +431,7 @@ __global__ void __launch_bounds__(128, ST_X2_MINB) k_xmarch2(SArgs A) {
       const int64_t idx = gb + (J * sI + K);
       if (seam) {
         const int slot = (xc == 2 ? 1 : 0) + ((fl & PF_SLOT2) ? 2 : 0) + (zs ? 4 : 0);
-        const int64_t so = (int64_t)slot * A.snv + idx;
-        A.fseam[so] = f;
-        if (LATENT) A.cseam[so] = dc;
+        seam_put((int64_t)slot * A.snv + idx, f, dc);
       } else {
         const int Jg = P * j0 + J, Kg = P * k0 + K;
         const double my = (J & 1) ? imr1 : ((Jg == 0 || Jg == A.NY - 1) ? A.imv_end : A.imv_int);
@@ -656,18 +669,10 @@ __global__ void __launch_bounds__(128, ST_X2_MINB) k_xmarch2(SArgs A) {
           zn[u] = z;
           idx[u] = (A.pbase ? A.pbase[I] : (int64_t)I * plane_stride) +
                    ((P * j0 + J) * sI + P * k0 + K);
-          const double* fs = A.fseam + idx[u];
-          s0[u] = __ldcg(fs);
-          if (yn) s2[u] = __ldcg(fs + 2 * A.snv);
-          if (z) s4[u] = __ldcg(fs + 4 * A.snv);
-          if (yn && z) s6[u] = __ldcg(fs + 6 * A.snv);
-          if (LATENT) {
-            const double* cs = A.cseam + idx[u];
-            c0[u] = __ldcg(cs);
-            if (yn) c2[u] = __ldcg(cs + 2 * A.snv);
-            if (z) c4[u] = __ldcg(cs + 4 * A.snv);
-            if (yn && z) c6[u] = __ldcg(cs + 6 * A.snv);
-          }
+          seam_get(idx[u], s0[u], c0[u]);
+          if (yn) seam_get(2 * A.snv + idx[u], s2[u], c2[u]);
+          if (z) seam_get(4 * A.snv + idx[u], s4[u], c4[u]);
+          if (yn && z) seam_get(6 * A.snv + idx[u], s6[u], c6[u]);
           Tn[u] = A.T[idx[u]];
         }
 #pragma unroll

@@ -246,7 +246,13 @@ __global__ void __launch_bounds__(CY* CZ, MinBlocks<P>::v) k_xmarch(SArgs A) {
     const double o = finalize_node(A, ci, c == 0 && k == 0, tpl[b * NZT + c], f, dc, LATENT);
     const int slot = (xc == 2 ? 1 : 0) + (ys_lo ? 2 : 0) + (zs_lo ? 4 : 0);
     const int64_t so = (int64_t)slot * A.snv + idx;
-    if (ST_ROWSTORE) {
+    if (LATENT && A.seam_pair) {
+      // the context keeps (f, dc) pairs (SArgs::seam_pair): one 16-byte store
+      if (seam)
+        reinterpret_cast<double2*>(A.fseam)[so] = make_double2(f, dc);
+      else
+        A.out[idx] = o;
+    } else if (ST_ROWSTORE) {
       // the update goes back into the staged plane (T of this node is no
       // longer needed); the plane leaves as whole coalesced rows
       // (store_planes) -- a seam node's row entry is then a stale T that the
