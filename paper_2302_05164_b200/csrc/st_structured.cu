@@ -26,6 +26,10 @@
 // side of the CTA per seam axis); k_seam_list then sums the slots of every
 // seam node in a fixed order and finalises it, so a step is bitwise
 // reproducible.
+// Explicit steps at p = 2 with a uniform history run k_xmarch2
+// (st_xmarch2_kernel.cuh), the same scheme and arithmetic with the work
+// around the cell evaluation rebuilt for instruction count (bitwise the same
+// fields); Structured::xmarch picks the kernel per launch.
 #include <cmath>
 #include <cstdlib>
 #include <cstring>

@@ -288,7 +288,7 @@ __device__ __forceinline__ void cell_element(const SArgs& A, const CellFlags& F,
         }
   }
   project3<P>(G);
-  if (F.source && (ymask || A.nb > 32)) {
+  if (F.source && __builtin_expect(ymask != 0u || A.nb > 32, 0)) {
     const double ax = anchor<P>(A, 0, i), ay = anchor<P>(A, 1, j), az = anchor<P>(A, 2, k);
 #pragma unroll 1
     for (int b = 0; b < A.nb; b++) {

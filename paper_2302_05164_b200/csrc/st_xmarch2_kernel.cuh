@@ -46,6 +46,10 @@
 // Results are bitwise those of k_xmarch (except the sign of exact zeros).
 #pragma once
 
+// rare paths (latent cells, x-seam planes) off the hot loop's fall-through
+// code (instruction cache)
+#define ST_UNLIKELY(x) __builtin_expect(!!(x), 0)
+
 #ifndef ST_X2_MINB
 #define ST_X2_MINB 3  // A/B hook: resident CTAs per SM the register allocation aims at
 #endif
@@ -344,13 +348,13 @@ __global__ void __launch_bounds__(128, ST_X2_MINB) k_xmarch2(SArgs A) {
     f10 += e[5 * EN - ES];
     const double f11 = e[4 * EN];
     double d00 = 0.0, d01 = 0.0, d10 = 0.0, d11 = 0.0;
-    if (LATENT && latn) {
+    if (LATENT && ST_UNLIKELY(latn)) {
       d00 = latent_sum(cp, tid, a, 0, 0);
       d01 = latent_sum(cp, tid, a, 0, 1);
       d10 = latent_sum(cp, tid, a, 1, 0);
       d11 = latent_sum(cp, tid, a, 1, 1);
     }
-    if (xc != 0) {
+    if (ST_UNLIKELY(xc != 0)) {
       // x seam plane: partials to this CTA's slots
       const int xb = xc == 2 ? 1 : 0;
       const int64_t s00 = (int64_t)(xb + (s_y ? 2 : 0) + (s_z ? 4 : 0)) * A.snv + g0;
@@ -368,7 +372,7 @@ __global__ void __launch_bounds__(128, ST_X2_MINB) k_xmarch2(SArgs A) {
     const double mz0e = k2 == kmI ? A.imv_end : rec_mz[tid];
     const double yb0 = rec_my[tid] * imIs, yb1 = imr1 * imIs;
     double c00 = mz0e * yb0, c01 = imr1 * yb0, c10 = mz0e * yb1, c11 = imr1 * yb1;
-    if (LATENT && latn) {
+    if (LATENT && ST_UNLIKELY(latn)) {
       if (d00 > 0.0) c00 = c00 / fma(c00, d00, 1.0);
       if (d01 > 0.0) c01 = c01 / fma(c01, d01, 1.0);
       if (d10 > 0.0) c10 = c10 / fma(c10, d10, 1.0);
@@ -424,7 +428,7 @@ __global__ void __launch_bounds__(128, ST_X2_MINB) k_xmarch2(SArgs A) {
       f += ea[pr.y & 0xffff];
       f += ea[(unsigned)pr.y >> 16];
       double dc = 0.0;
-      if (LATENT && latn) {
+      if (LATENT && ST_UNLIKELY(latn)) {
         const int bj = J >> 1, bk = K >> 1;
         dc = latent_sum((bk + 1) * ES + bj + 1, bk * CY + bj, a, J & 1, K & 1);
       }
@@ -536,9 +540,9 @@ __global__ void __launch_bounds__(128, ST_X2_MINB) k_xmarch2(SArgs A) {
         for (int q = 0; q < Q3; q++)
           cand |= (unsigned)(__double2hiint(t[q]) - A.lat_hi0) <= (unsigned)A.lat_hiw;
         bool lat = false;
-        if (cand) lat = any_abs_lt<Q3>(t, A.lat_mid, A.lat_half);
+        if (ST_UNLIKELY(cand)) lat = any_abs_lt<Q3>(t, A.lat_mid, A.lat_half);
         lf = lat || lat_had;
-        if (lat) {
+        if (ST_UNLIKELY(lat)) {
 #pragma unroll
           for (int q = 0; q < Q3; q++) t[q] = fabs(t[q] - A.lat_mid) < A.lat_half ? A.lw3[q] : 0.0;
           project3<P>(t);
@@ -549,7 +553,7 @@ __global__ void __launch_bounds__(128, ST_X2_MINB) k_xmarch2(SArgs A) {
           }
 #pragma unroll
           for (int q = 0; q < EW; q++) ecg[q * NT + tid] = t[q];
-        } else if (lat_had) {
+        } else if (ST_UNLIKELY(lat_had)) {
 #pragma unroll
           for (int q = 0; q < Q * Q; q++) ecg[q * NT + tid] = lcar[q * NT];
 #pragma unroll
