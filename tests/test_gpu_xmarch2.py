@@ -29,6 +29,9 @@ def _params(latent):
 def _run(mesh, latent, lx, x2, monkeypatch, steps=6, inseam=False):
     monkeypatch.setenv("ST_XMARCH2", "1" if x2 else "0")
     monkeypatch.setenv("ST_INSEAM", "1" if inseam else "0")
+    # the general kernel runs on the original seam layout (split f / dc slot
+    # arrays), the lean one on the round's layout ((f, dc) pairs)
+    monkeypatch.setenv("ST_SEAM_PAIR", "1" if x2 else "0")
     if lx:
         monkeypatch.setenv("ST_LX", lx)
     else:
@@ -66,6 +69,9 @@ CASES = {
 def test_lean_kernel_equals_general_kernel_bitwise(case, latent, lx, inseam, monkeypatch):
     """inseam: the opt-in in-kernel seam completion (last-arriving CTA sums
     the slots in the seam pass's order) instead of the seam pass."""
+    # (the general kernel on the round's layout is covered by the oracle
+    # comparisons of test_gpu_structured / test_gpu_fitted: rhs mode and
+    # stored histories run it)
     mesh = CASES[case]()
     f0, a0, t0, T0 = _run(mesh, latent, lx, False, monkeypatch)
     f1, a1, t1, T1 = _run(mesh, latent, lx, True, monkeypatch, inseam=inseam)
