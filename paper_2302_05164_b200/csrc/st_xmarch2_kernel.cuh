@@ -54,8 +54,19 @@
 #define ST_X2_MINB 3  // A/B hook: resident CTAs per SM the register allocation aims at
 #endif
 
+#ifdef ST_X2_MAXREG  // A/B hook: an explicit register cap instead of the occupancy target
+#define ST_X2_BOUNDS __maxnreg__(ST_X2_MAXREG)
+#else
+#define ST_X2_BOUNDS __launch_bounds__(128, ST_X2_MINB)
+#endif
+#ifndef ST_X2_FIN_UNROLL
+#define ST_X2_FIN_UNROLL 1  // A/B hook: unroll factor of the per-plane finalisation loop
+#endif
+#define ST_PRAGMA_(x) _Pragma(#x)
+#define ST_UNROLL_N(n) ST_PRAGMA_(unroll n)
+
 template <bool LATENT>
-__global__ void __launch_bounds__(128, ST_X2_MINB) k_xmarch2(SArgs A) {
+__global__ void ST_X2_BOUNDS k_xmarch2(SArgs A) {
   constexpr int P = 2, Q = 3, Q3 = 27, CY = 8, CZ = 16, NT = 128, NW = 4;
   constexpr int NYT = P * CY + 1, NZT = P * CZ + 1, PL = NYT * NZT;
   constexpr int NR = 2 * P + 1;
@@ -506,7 +517,8 @@ __global__ void __launch_bounds__(128, ST_X2_MINB) k_xmarch2(SArgs A) {
     const int cp = r.y;
     if (live && !tail) {
       double t[Q3], G[Q3];
-      {
+      // T at the Gauss points from the layer's three staged planes
+      auto gauss_T = [&](double* tt) {
         int rs = rs0;
 #pragma unroll
         for (int a = 0; a < Q; a++) {
@@ -514,11 +526,28 @@ __global__ void __launch_bounds__(128, ST_X2_MINB) k_xmarch2(SArgs A) {
 #pragma unroll
           for (int b = 0; b < Q; b++)
 #pragma unroll
-            for (int c = 0; c < Q; c++) t[(a * Q + b) * Q + c] = tp[b * NZT + c];
+            for (int c = 0; c < Q; c++) tt[(a * Q + b) * Q + c] = tp[b * NZT + c];
           rs = rs + 1 >= NR ? 0 : rs + 1;
         }
+        interp3<P>(tt);
+      };
+      gauss_T(t);
+      // latent test right away (candidates by the high words, a superset of
+      // the open interval, then the exact test), so that t dies with the
+      // gradients instead of staying live across the projection; the rare
+      // latent cell recomputes it
+#ifndef ST_X2_LAT_EARLY
+#define ST_X2_LAT_EARLY 0  // A/B hook: 1 = test before the cell evaluation, the rare latent cell
+                           // recomputes t (measured slower: 13.2 vs 12.5 ms on config 4)
+#endif
+      bool lat = false;
+      if (LATENT && ST_X2_LAT_EARLY) {
+        bool cand = false;
+#pragma unroll
+        for (int q = 0; q < Q3; q++)
+          cand |= (unsigned)(__double2hiint(t[q]) - A.lat_hi0) <= (unsigned)A.lat_hiw;
+        if (ST_UNLIKELY(cand)) lat = any_abs_lt<Q3>(t, A.lat_mid, A.lat_half);
       }
-      interp3<P>(t);
       {
         const int kl = tid / CY, jl = tid % CY;
         cell_element<P, false, true>(
@@ -532,17 +561,17 @@ __global__ void __launch_bounds__(128, ST_X2_MINB) k_xmarch2(SArgs A) {
       }
 #pragma unroll
       for (int q = 0; q < EW; q++) E[q * EN + cp] = G[q];
-      if (LATENT) {
-        // candidates by the high words (a superset of the open interval),
-        // then the exact test
+      if (LATENT && !ST_X2_LAT_EARLY) {
         bool cand = false;
 #pragma unroll
         for (int q = 0; q < Q3; q++)
           cand |= (unsigned)(__double2hiint(t[q]) - A.lat_hi0) <= (unsigned)A.lat_hiw;
-        bool lat = false;
         if (ST_UNLIKELY(cand)) lat = any_abs_lt<Q3>(t, A.lat_mid, A.lat_half);
+      }
+      if (LATENT) {
         lf = lat || lat_had;
         if (ST_UNLIKELY(lat)) {
+          if (ST_X2_LAT_EARLY) gauss_T(t);
 #pragma unroll
           for (int q = 0; q < Q3; q++) t[q] = fabs(t[q] - A.lat_mid) < A.lat_half ? A.lw3[q] : 0.0;
           project3<P>(t);
@@ -581,7 +610,7 @@ __global__ void __launch_bounds__(128, ST_X2_MINB) k_xmarch2(SArgs A) {
     if (i + 1 < i1) side_work(i + 1, rs1);
     const int na = tail ? 1 : P;
     int rs = rs0;
-#pragma unroll 1
+    ST_UNROLL_N(ST_X2_FIN_UNROLL)
     for (int a = 0; a < na; a++) {
       const int xc = tail ? xc1 : ((a == 0 && i == i0) ? xc0 : 0);
       finalize_cell(a, rs, xc, latn);
@@ -590,7 +619,10 @@ __global__ void __launch_bounds__(128, ST_X2_MINB) k_xmarch2(SArgs A) {
     }
     rs0 = rs1;
   }
-  if (A.seamcnt != nullptr) {
+#ifndef ST_X2_INSEAM
+#define ST_X2_INSEAM 1  // A/B hook: compile the opt-in in-kernel seam completion
+#endif
+  if (ST_X2_INSEAM && A.seamcnt != nullptr) {
     // ---- seam completion of the chunk's ordinary planes ----
     // x extents of the tile rows below / above
     const int ext_lo = (A.text && blockIdx.y > 0) ? A.text[blockIdx.y - 1] : A.nx;
