@@ -554,13 +554,20 @@ __global__ void ST_X2_BOUNDS k_xmarch2(SArgs A) {
             A, F, i, j0 + jl, k0 + kl, 0, t, G, rec_ym[tid], [&](int, int, int) { return 0.0; }, Sx,
             Sy + jl * MB * Q, Sz + kl * MB * Q, Fo + jl * Q * Q);
       }
+#ifndef ST_X2_ESTORE_FIRST
+#define ST_X2_ESTORE_FIRST 0  // A/B hook: plane-1 element stores before the x-carry exchange
+#endif
+      if (ST_X2_ESTORE_FIRST) {
+#pragma unroll
+        for (int q = Q * Q; q < EW; q++) E[q * EN + cp] = G[q];
+      }
 #pragma unroll
       for (int q = 0; q < Q * Q; q++) {
         G[q] += Cx[q * NT + tid];
         Cx[q * NT + tid] = G[P * Q * Q + q];
       }
 #pragma unroll
-      for (int q = 0; q < EW; q++) E[q * EN + cp] = G[q];
+      for (int q = 0; q < (ST_X2_ESTORE_FIRST ? Q * Q : EW); q++) E[q * EN + cp] = G[q];
       if (LATENT && !ST_X2_LAT_EARLY) {
         bool cand = false;
 #pragma unroll
