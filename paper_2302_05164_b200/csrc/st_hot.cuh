@@ -51,7 +51,7 @@ static constexpr size_t march_smem() {
 
 static constexpr size_t march2_smem() {
   constexpr int P = 2, CY = 8, CZ = 16, Q = 3;
-  return (size_t)((2 * P + 1) * (P * CY + 1) * (P * CZ + 1) + P * Q * Q * (CY + 2) * (CZ + 2) +
+  return (size_t)((2 * P + 1) * kX2Plane + P * Q * Q * (CY + 2) * (CZ + 2) +
                   Q * Q * CY * CZ + (CY + CZ + 1) * kMaxTabBeams * Q + 2 * CY * Q * Q) *
          sizeof(double);
 }

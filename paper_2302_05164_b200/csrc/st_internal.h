@@ -79,7 +79,9 @@ struct DevBuf {
   int alloc(size_t count) {
     free();
     if (count == 0) return ST_OK;
-    cudaError_t e = cudaMalloc(&p, count * sizeof(T));
+    // + 16 bytes: the bulk-copy staging of k_xmarch2 rounds a node row up to
+    // whole 16-byte units and may read one element past the array
+    cudaError_t e = cudaMalloc(&p, count * sizeof(T) + 16);
     if (e != cudaSuccess) {
       set_error(std::string("cudaMalloc: ") + cudaGetErrorString(e));
       p = nullptr;

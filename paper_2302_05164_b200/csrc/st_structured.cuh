@@ -198,6 +198,27 @@ __device__ __forceinline__ double finalize_node(const SArgs& A, double ci, bool 
   return A.mode == 1 ? f : o;
 }
 
+// A/B hook (compile time): k_xmarch2 stages its node planes with bulk
+// asynchronous copies (cp.async.bulk + mbarrier, one copy per tile row,
+// UBLKCP / SYNCS in SASS) instead of 8-byte cp.async per lane.  The reference
+// numbering gives node rows an odd length (2 nz + 1 doubles), so a row starts
+// on 8 bytes only: the copy takes the 16-byte aligned superset of the row and
+// the consumers add a per-plane, per-row-parity shift of 0 or 1 doubles.
+// Bitwise the same fields (profiles/scripts/r2_s4_bulk.sh runs the GPU tests
+// on it), measured slower on config 4 (13.7 against 12.5 ms, equal on config
+// 1), so the cp.async staging ships.
+#ifndef ST_X2_BULK
+#define ST_X2_BULK 0
+#endif
+// staged plane of k_xmarch2 (17 tile rows of 33 nodes): offset of tile row J
+// and plane size in doubles.  Bulk rows start on 16 bytes (pitch 34) and every
+// second row is skewed by 2 more, which keeps the threads' row stride an odd
+// multiple of 4 banks as with the odd pitch 33 of the cp.async staging.
+__host__ __device__ constexpr int x2_rowoff(int J) {
+  return ST_X2_BULK ? 34 * J + 2 * (J >> 1) : 33 * J;
+}
+constexpr int kX2Plane = x2_rowoff(16) + (ST_X2_BULK ? 34 : 33);
+
 // the lean Q2 explicit-step kernel (k_xmarch2) replaces k_xmarch<2> for
 // explicit steps with a uniform history (ST_XMARCH2=0: the general kernel);
 // read per launch, tests toggle it

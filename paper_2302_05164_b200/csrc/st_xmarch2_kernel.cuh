@@ -68,7 +68,11 @@
 template <bool LATENT>
 __global__ void ST_X2_BOUNDS k_xmarch2(SArgs A) {
   constexpr int P = 2, Q = 3, Q3 = 27, CY = 8, CZ = 16, NT = 128, NW = 4;
-  constexpr int NYT = P * CY + 1, NZT = P * CZ + 1, PL = NYT * NZT;
+  constexpr int NYT = P * CY + 1, NZT = P * CZ + 1;
+  constexpr bool BULK = ST_X2_BULK != 0;
+  constexpr int NZP = 33;            // row pitch of the cp.async staging
+  constexpr int PL = kX2Plane;       // staged plane (doubles), rows at x2_rowoff(J)
+  constexpr int R1 = x2_rowoff(1) - x2_rowoff(0), R2 = x2_rowoff(2) - x2_rowoff(0);
   constexpr int NR = 2 * P + 1;
   constexpr int EW = P * Q * Q;
   // padded cell index of the element arrays: (kl + 1) * ES + jl + 1, ghost
@@ -90,11 +94,16 @@ __global__ void ST_X2_BOUNDS k_xmarch2(SArgs A) {
   __shared__ long long pinfo_b[NR];
   __shared__ int pinfo_k[NR];
   __shared__ double pinfo_im[NR];
+  // bulk staging: a row lands at its 16-byte aligned position, so its first
+  // node sits 0 or 1 doubles into the slot row; the shift alternates with the
+  // row parity (odd row pitch): bit 0 = even rows, bit 1 = odd rows
+  __shared__ int pinfo_sh[NR];
+  __shared__ unsigned long long mbar[2];  // staging completion, by layer parity
   __shared__ long long pf_b[2][P];   // fitted layout of the next layer's planes (prefetch)
   __shared__ int pf_k[2][P];
   // perimeter nodes of the tile (high edges first): x = gather offsets 0, 1
   // (u16 each, into an element plane), y = offsets 2, 3, z = J | K << 8 |
-  // flags << 16, w = J * NZT + K
+  // flags << 16, w = x2_rowoff(J) + K
   __shared__ int4 peri[NPER];
   // per-thread record: x = ms0 (plane offset of the cell's low corner), y =
   // cp (padded cell index), z = flags, w = 2 j | 2 k << 16
@@ -132,7 +141,7 @@ __global__ void ST_X2_BOUNDS k_xmarch2(SArgs A) {
     const int kl = tid / CY, jl = tid % CY;  // z-major cell order
     const int j = j0 + jl, k = k0 + kl;
     const bool live = j < A.ny && k < A.nz;
-    rec4[tid] = make_int4(P * jl * NZT + P * kl, (kl + 1) * ES + jl + 1,
+    rec4[tid] = make_int4(x2_rowoff(P * jl) + P * kl, (kl + 1) * ES + jl + 1,
                           (live ? RF_LIVE : 0) | ((jl == 0 && ty_lo) ? RF_SY : 0) |
                               ((kl == 0 && tz_lo) ? RF_SZ : 0) |
                               ((k == 0 && A.dir_bottom) ? RF_DIR : 0),
@@ -172,7 +181,7 @@ __global__ void ST_X2_BOUNDS k_xmarch2(SArgs A) {
     const bool seam = (loJ && ty_lo) || (hiJ && ty_hi) || (hiK && tz_hi);
     const int fl = (loJ ? PF_LOJ : 0) | (loK ? PF_LOK : 0) | ((hiJ || hiK) ? PF_HI : 0) |
                    (seam ? PF_SEAM : 0) | ((loJ && ty_lo) ? PF_SLOT2 : 0);
-    peri[e] = make_int4(o0 | (o1 << 16), o2 | (o3 << 16), J | (K << 8) | (fl << 16), J * NZT + K);
+    peri[e] = make_int4(o0 | (o1 << 16), o2 | (o3 << 16), J | (K << 8) | (fl << 16), x2_rowoff(J) + K);
   }
 
   // x factor of the inverse lumped mass of plane I (times 1 / (rho c detw))
@@ -201,27 +210,44 @@ __global__ void ST_X2_BOUNDS k_xmarch2(SArgs A) {
   // with one instruction of warp 1 (lane l the row l)
   const unsigned tr_s = (unsigned)__cvta_generic_to_shared(Tr);
   const bool full = Jn == NYT && Kn == NZT;
-  auto load_plane = [&](int I, int rs, long long bI, int kmI) {
+  // bulk variant: lane r of warp pw copies tile row r with one
+  // cp.async.bulk of (Kn + 1) doubles from the row's 16-byte aligned start
+  // (one double before the row or one after it rides along), completing on
+  // mbar[mslot]
+  auto load_plane = [&](int I, int rs, long long bI, int kmI, int pw, int mslot) {
     const int lane = tid & 31, warp = tid >> 5;
     const int sI = A.NZ - kmI;
     if (tid == 0) {
       pinfo_b[rs] = bI;
       pinfo_k[rs] = kmI;
       pinfo_im[rs] = plane_imx(I);
+      if (BULK) pinfo_sh[rs] = (int)(bI & 1) | ((int)((bI + sI) & 1) << 1);
+    }
+    if (BULK) {
+      if (warp == pw && lane < Jn) {
+        const long long g = bI + ((P * j0 + lane) * sI + P * k0);  // first node of the row
+        const double* src = A.T + (g - (g & 1));
+        const unsigned dst = tr_s + (unsigned)((rs * PL + x2_rowoff(lane)) * 8);
+        asm volatile(
+            "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(dst),
+            "l"(src), "r"((Kn + 1) * 8), "r"((unsigned)__cvta_generic_to_shared(&mbar[mslot]))
+            : "memory");
+      }
+      return;
     }
     const double* src = A.T + (bI + ((P * j0 + warp) * sI + P * k0 + lane));
-    const unsigned dst = tr_s + (unsigned)((rs * PL + warp * NZT + lane) * 8);
+    const unsigned dst = tr_s + (unsigned)((rs * PL + warp * NZP + lane) * 8);
     const int64_t step = (int64_t)(NW * sI) * 8;
     if (full) {
 #pragma unroll
       for (int it = 0; it < NYT / NW; it++) {
-        asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(dst + it * NW * NZT * 8),
+        asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(dst + it * NW * NZP * 8),
                      "l"(src)
                      : "memory");
         src = (const double*)((const char*)src + step);
       }
       if (warp == 0)
-        asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(dst + (NYT - 1) * NZT * 8),
+        asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(dst + (NYT - 1) * NZP * 8),
                      "l"(src)
                      : "memory");
     } else {
@@ -229,7 +255,7 @@ __global__ void ST_X2_BOUNDS k_xmarch2(SArgs A) {
 #pragma unroll
       for (int it = 0; it < (NYT + NW - 1) / NW; it++) {
         if (c_lo && warp + it * NW < Jn)
-          asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(dst + it * NW * NZT * 8),
+          asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(dst + it * NW * NZP * 8),
                        "l"(src)
                        : "memory");
         src = (const double*)((const char*)src + step);
@@ -238,11 +264,46 @@ __global__ void ST_X2_BOUNDS k_xmarch2(SArgs A) {
     if (warp == 1 && Kn == NZT && lane < Jn) {
       const double* s2 = A.T + (bI + ((P * j0 + lane) * sI + P * k0 + (NZT - 1)));
       asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(
-                       tr_s + (unsigned)((rs * PL + lane * NZT + NZT - 1) * 8)),
+                       tr_s + (unsigned)((rs * PL + lane * NZP + NZT - 1) * 8)),
                    "l"(s2)
                    : "memory");
     }
   };
+
+  // one thread arms the layer's barrier with the bytes of its np planes;
+  // every thread waits for the phase (a bounded spin: a miscount traps
+  // instead of hanging the GPU)
+  auto stage_arm = [&](int mslot, int np) {
+    if (BULK && tid == 0)
+      asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(
+                       (unsigned)__cvta_generic_to_shared(&mbar[mslot])),
+                   "r"(np * Jn * (Kn + 1) * 8)
+                   : "memory");
+  };
+  auto stage_wait = [&](int mslot, int parity) {
+    if (!BULK) return;
+    const unsigned mb = (unsigned)__cvta_generic_to_shared(&mbar[mslot]);
+    unsigned done = 0;
+    for (int spin = 0; !done; spin++) {
+      asm volatile(
+          "{\n.reg .pred p;\nmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n"
+          "selp.u32 %0, 1, 0, p;\n}\n"
+          : "=r"(done)
+          : "r"(mb), "r"(parity)
+          : "memory");
+      if (spin > (1 << 24)) __trap();
+    }
+  };
+  if (BULK) {
+    if (tid == 0) {
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(
+          (unsigned)__cvta_generic_to_shared(&mbar[0])));
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(
+          (unsigned)__cvta_generic_to_shared(&mbar[1])));
+      asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+    }
+    __syncthreads();
+  }
 
 #pragma unroll
   for (int q = 0; q < Q * Q; q++) Cx[q * NT + tid] = 0.0;
@@ -280,7 +341,8 @@ __global__ void ST_X2_BOUNDS k_xmarch2(SArgs A) {
                     [&](int r, int a, int b) {
                       int rs = rs0 + a;
                       rs = rs >= NR ? rs - NR : rs;
-                      return Tr[rs * PL + P * r * NZT + P * kl_top + b * NZT + P];
+                      const int sh = BULK ? ((pinfo_sh[rs] >> (b & 1)) & 1) : 0;
+                      return Tr[rs * PL + x2_rowoff(P * r + b) + P * kl_top + P + sh];
                     });
     }
     if (tid < nbt) src_factor_xy<P>(A, anchor<P>(A, 0, il), beam_x[tid], Sx + tid * Q);
@@ -379,7 +441,9 @@ __global__ void ST_X2_BOUNDS k_xmarch2(SArgs A) {
       return;
     }
     const double imIs = pinfo_im[rs];
-    const double* tp = Tr + rs * PL + r.x;
+    const int psh = BULK ? pinfo_sh[rs] : 0;
+    const double* tp = Tr + rs * PL + r.x + (psh & 1);            // even row of the cell
+    const double* tq = Tr + rs * PL + r.x + (psh >> 1) + R1;      // odd row
     const double mz0e = k2 == kmI ? A.imv_end : rec_mz[tid];
     const double yb0 = rec_my[tid] * imIs, yb1 = imr1 * imIs;
     double c00 = mz0e * yb0, c01 = imr1 * yb0, c10 = mz0e * yb1, c11 = imr1 * yb1;
@@ -391,8 +455,8 @@ __global__ void ST_X2_BOUNDS k_xmarch2(SArgs A) {
     }
     double o00 = tp[0] + A.dt * (c00 * f00);
     double o01 = tp[1] + A.dt * (c01 * f01);
-    double o10 = tp[NZT] + A.dt * (c10 * f10);
-    double o11 = tp[NZT + 1] + A.dt * (c11 * f11);
+    double o10 = tq[0] + A.dt * (c10 * f10);
+    double o11 = tq[1] + A.dt * (c11 * f11);
     if (r.z & RF_DIR) {
       o00 = A.P.T_inf;
       o10 = A.P.T_inf;
@@ -453,7 +517,8 @@ __global__ void ST_X2_BOUNDS k_xmarch2(SArgs A) {
         const double mz = (K & 1) ? imr1 : ((Kg == kmI || Kg == A.NZ - 1) ? A.imv_end : A.imv_int);
         double ci = mz * (my * pinfo_im[rs]);
         if (LATENT && dc > 0.0) ci = ci / fma(ci, dc, 1.0);
-        double o = Tr[rs * PL + pr.w] + A.dt * (ci * f);
+        const int sh = BULK ? ((pinfo_sh[rs] >> (J & 1)) & 1) : 0;
+        double o = Tr[rs * PL + pr.w + sh] + A.dt * (ci * f);
         if (A.dir_bottom && Kg == 0) o = A.P.T_inf;
         A.out[idx] = o;
         if (__any_sync(__activemask(), habs(o) >= thr)) track_exact(o);
@@ -465,15 +530,18 @@ __global__ void ST_X2_BOUNDS k_xmarch2(SArgs A) {
   int rs0 = (P * i0) % NR;  // ring slot of the layer's first plane
   {
     int rs = rs0;
+    stage_arm(i0 & 1, P + 1);
     for (int pa = 0; pa <= P; pa++) {
       const int I = P * i0 + pa;
-      load_plane(I, rs, A.pbase ? A.pbase[I] : (int64_t)I * plane_stride, A.pkmin ? A.pkmin[I] : 0);
+      load_plane(I, rs, A.pbase ? A.pbase[I] : (int64_t)I * plane_stride, A.pkmin ? A.pkmin[I] : 0,
+                 pa, i0 & 1);
       rs = rs + 1 >= NR ? 0 : rs + 1;
     }
   }
   if (i0 + 1 < i1) prefetch_layout(P * (i0 + 1) + 1, (i0 + 1) & 1);
   cp_commit();
   cp_wait<0>();
+  stage_wait(i0 & 1, 0);
   __syncthreads();
   side_work(i0, rs0);
 
@@ -494,6 +562,7 @@ __global__ void ST_X2_BOUNDS k_xmarch2(SArgs A) {
       const int buf = (i + 1) & 1;
       int rs = rs0 + P + 1;
       rs = rs >= NR ? rs - NR : rs;
+      stage_arm(buf, P);
 #pragma unroll
       for (int pa = 0; pa < P; pa++) {
         long long bI;
@@ -505,7 +574,7 @@ __global__ void ST_X2_BOUNDS k_xmarch2(SArgs A) {
           bI = (int64_t)(P * (i + 1) + 1 + pa) * plane_stride;
           kmI = 0;
         }
-        load_plane(P * (i + 1) + 1 + pa, rs, bI, kmI);
+        load_plane(P * (i + 1) + 1 + pa, rs, bI, kmI, pa, buf);
         rs = rs + 1 >= NR ? 0 : rs + 1;
       }
     }
@@ -522,11 +591,14 @@ __global__ void ST_X2_BOUNDS k_xmarch2(SArgs A) {
         int rs = rs0;
 #pragma unroll
         for (int a = 0; a < Q; a++) {
-          const double* tp = Tr + rs * PL + r.x;
+          const int psh = BULK ? pinfo_sh[rs] : 0;
+          const double* tpe = Tr + rs * PL + r.x + (psh & 1);   // rows b = 0, 2
+          const double* tpo = Tr + rs * PL + r.x + (psh >> 1);  // row b = 1
 #pragma unroll
           for (int b = 0; b < Q; b++)
 #pragma unroll
-            for (int c = 0; c < Q; c++) tt[(a * Q + b) * Q + c] = tp[b * NZT + c];
+            for (int c = 0; c < Q; c++)
+              tt[(a * Q + b) * Q + c] = ((b & 1) ? tpo : tpe)[(b == 0 ? 0 : (b == 1 ? R1 : R2)) + c];
           rs = rs + 1 >= NR ? 0 : rs + 1;
         }
         interp3<P>(tt);
@@ -610,6 +682,8 @@ __global__ void ST_X2_BOUNDS k_xmarch2(SArgs A) {
       }
     }
     cp_wait<0>();
+    // the next layer's planes (its (i + 1 - i0) / 2-th use of the barrier)
+    if (i + 1 < i1) stage_wait((i + 1) & 1, ((i + 1 - i0) >> 1) & 1);
     const bool latn = LATENT ? __syncthreads_or(lf) != 0 : (__syncthreads(), false);
     if (LATENT && latn && tid == 0) nlat_s++;
     int rs1 = rs0 + P;  // first plane of the next layer
