@@ -1,3 +1,4 @@
+# (the ST_X2_INTERP_PLANES / ST_QP_REV hooks of this sweep were removed after the measurement: no gain)
 python -c "import __graft_entry__ as g; g.build()" || exit 1
 ST_VARIANT=ipl ST_NVCC_EXTRA="-DST_X2_INTERP_PLANES=1" python -m paper_2302_05164_b200._build > /dev/null
 ST_VARIANT=qrev ST_NVCC_EXTRA="-DST_QP_REV=1" python -m paper_2302_05164_b200._build > /dev/null
