@@ -651,13 +651,14 @@ struct Structured : Backend {
   }
 
   // (f, dc) pairs in fseam (one 16-byte access per slot entry): k_xslab and
-  // the degree-2 k_xmarch / k_xmarch2 with latent heat; ST_SEAM_PAIR=0: split
-  // arrays
+  // the k_xmarch / k_xmarch2 contexts (p <= 2) with latent heat (config 4:
+  // step 16.4 -> 15.2 ms, config 2 at p = 1: 2.54 -> 2.47 ms);
+  // ST_SEAM_PAIR=0: split arrays
   bool seam_pairs() const {
     if (!c->dp.latent) return false;
     if (slab) return true;
     const char* e = getenv("ST_SEAM_PAIR");
-    return p == 2 && !(e && e[0] == '0');
+    return p <= 2 && !(e && e[0] == '0');
   }
 
   int launched() {
