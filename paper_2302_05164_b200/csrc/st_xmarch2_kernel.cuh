@@ -305,6 +305,22 @@ __global__ void ST_X2_BOUNDS k_xmarch2(SArgs A) {
     __syncthreads();
   }
 
+  // the first layer's P+1 planes go out now, so that their latency overlaps
+  // the table set-up below (ten-layer chunks: config 1)
+  int rs0 = (P * i0) % NR;  // ring slot of the layer's first plane
+  {
+    int rs = rs0;
+    stage_arm(i0 & 1, P + 1);
+    for (int pa = 0; pa <= P; pa++) {
+      const int I = P * i0 + pa;
+      load_plane(I, rs, A.pbase ? A.pbase[I] : (int64_t)I * plane_stride, A.pkmin ? A.pkmin[I] : 0,
+                 pa, i0 & 1);
+      rs = rs + 1 >= NR ? 0 : rs + 1;
+    }
+  }
+  if (i0 + 1 < i1) prefetch_layout(P * (i0 + 1) + 1, (i0 + 1) & 1);
+  cp_commit();
+
 #pragma unroll
   for (int q = 0; q < Q * Q; q++) Cx[q * NT + tid] = 0.0;
   // latent scratch of this CTA, addressed where the rare paths need it
@@ -526,20 +542,7 @@ __global__ void ST_X2_BOUNDS k_xmarch2(SArgs A) {
     }
   };
 
-  // prologue: the first layer's P+1 planes (and its side work)
-  int rs0 = (P * i0) % NR;  // ring slot of the layer's first plane
-  {
-    int rs = rs0;
-    stage_arm(i0 & 1, P + 1);
-    for (int pa = 0; pa <= P; pa++) {
-      const int I = P * i0 + pa;
-      load_plane(I, rs, A.pbase ? A.pbase[I] : (int64_t)I * plane_stride, A.pkmin ? A.pkmin[I] : 0,
-                 pa, i0 & 1);
-      rs = rs + 1 >= NR ? 0 : rs + 1;
-    }
-  }
-  if (i0 + 1 < i1) prefetch_layout(P * (i0 + 1) + 1, (i0 + 1) & 1);
-  cp_commit();
+  // prologue: the first layer's planes were issued above; wait, then its side work
   cp_wait<0>();
   stage_wait(i0 & 1, 0);
   __syncthreads();
