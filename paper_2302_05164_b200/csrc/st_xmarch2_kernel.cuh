@@ -32,8 +32,9 @@
 //     L2-resident global scratch instead of 18 KB of shared memory;
 //   * one loop body serves the layers and the chunk's last plane, so the
 //     finalisation code exists once (instruction cache).
-// In-kernel seam completion (A.seamcnt != 0): the seams of ordinary planes
-// (y / z tile seams; everything but the x-seam planes at chunk boundaries and
+// Opt-in in-kernel seam completion (ST_INSEAM=1, A.seamcnt != 0; bitwise the
+// seam pass but measured slower than it): the seams of
+// ordinary planes (y / z tile seams; everything but the x-seam planes at chunk boundaries and
 // rank interfaces, which stay with the seam pass) are finished by the last
 // CTA to arrive.  Every CTA stores its partials to its slots as before; when
 // its chunk is done, one lane per seam group (the tile's 4 faces and 4 corner
