@@ -958,7 +958,11 @@ struct Structured : Backend {
       return ST_EUNSUPPORTED;
     }
     if (lat && latstat_h) poll_latent();
-    A.x2 = (p == 2 && !slab && !rcf && A.mode == 0 &&
+    // (k_xmarch2 packs node coordinates in 16 bits and indexes a plane with
+    // 32-bit offsets)
+    const bool x2_fits = 2 * m.ny < 32768 && 2 * m.nz < 32768 &&
+                         (int64_t)(2 * m.ny + 1) * (2 * m.nz + 1) < (1ll << 31);
+    A.x2 = (p == 2 && !slab && !rcf && A.mode == 0 && x2_fits &&
             A.flags == (ST_RHS_DIFFUSION | ST_RHS_FACES | ST_RHS_SOURCE) && use_xmarch2() &&
             !(lat && prefer_general))
                ? 1
