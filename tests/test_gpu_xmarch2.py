@@ -78,3 +78,38 @@ def test_lean_kernel_equals_general_kernel_bitwise(case, latent, lx, inseam, mon
     assert f0 == f1
     assert a0 == a1 and t0 == t1
     assert np.array_equal(T0, T1)
+
+
+def test_adaptive_dispatch_on_a_latent_dense_field(monkeypatch):
+    """A field in which every tile gathers latent increments in most layers
+    (config 2's situation) makes the context fall back to the general kernel
+    (the kernels count their latent CTA-layers, the host reads the counter
+    asynchronously); a field with no latent cell stays on k_xmarch2; the
+    fields are bitwise those of a run pinned to k_xmarch2."""
+    monkeypatch.setenv("ST_XMARCH2", "1")
+    mesh = st.StructuredBox(12, 16, 32, H, degree=2)
+    rng = np.random.default_rng(3)
+    dense = rng.uniform(1700.0, 2100.0, mesh.n_vertices)   # 1/8 of the Gauss points latent
+    cold = rng.uniform(300.0, 600.0, mesh.n_vertices)
+    empty = np.zeros((1, 0), dtype=BEAM_DTYPE)
+
+    def run(T0, adapt):
+        monkeypatch.setenv("ST_X2_ADAPT", "1" if adapt else "0")
+        op = st.ThermalOperator(mesh, mesh, _params(True), st.SolverSettings())
+        op.set_state(T0, 1.0)
+        names = []
+        for _ in range(12):   # one step per call: the counter is read between calls
+            fail, _, _ = op.run_explicit(np.full(1, 2e-8), empty)
+            assert fail == 0
+            names.append(op.profile_read()[2])
+        T, _ = op.get_state()
+        op.close()
+        return T, names
+
+    Td_pinned, n0 = run(dense, False)
+    Td_adapt, n1 = run(dense, True)
+    assert set(n0) == {"k_xmarch2"}
+    assert n1[0] == "k_xmarch2" and n1[-1] == "k_xmarch"
+    assert np.array_equal(Td_pinned, Td_adapt)
+    _, n2 = run(cold, True)
+    assert set(n2) == {"k_xmarch2"}
