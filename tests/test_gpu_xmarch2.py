@@ -26,7 +26,7 @@ def _params(latent):
     return st.ProcessParams(mat, bnd, las, st.MeshParams(h_coarse=H, n_refine=0, h_powder=H))
 
 
-def _run(mesh, latent, lx, x2, monkeypatch, steps=6, inseam=False):
+def _run(mesh, latent, lx, x2, monkeypatch, steps=6, inseam=False, nbeams=2):
     monkeypatch.setenv("ST_XMARCH2", "1" if x2 else "0")
     monkeypatch.setenv("ST_INSEAM", "1" if inseam else "0")
     # the general kernel runs on the original seam layout (split f / dc slot
@@ -43,11 +43,14 @@ def _run(mesh, latent, lx, x2, monkeypatch, steps=6, inseam=False):
     T[rng.random(op.nv) < 0.5] = rng.uniform(300.0, 600.0)
     op.set_state(T, 1.0)
     lx_m, ly_m = mesh.nx * H, mesh.ny * H
-    recs = np.zeros((steps, 2), dtype=BEAM_DTYPE)
+    recs = np.zeros((steps, nbeams), dtype=BEAM_DTYPE)
     for s in range(steps):
-        recs[s] = pack_beams([
-            BeamState(np.array([lx_m * 0.3 + s * 4e-6, ly_m * 0.5]), 0.0, 90.0, True),
-            BeamState(np.array([lx_m * 0.7, ly_m * 0.3 + s * 2e-6]), 0.0, 60.0, s % 2 == 0)])
+        beams = [BeamState(np.array([lx_m * 0.3 + s * 4e-6, ly_m * 0.5]), 0.0, 90.0, True),
+                 BeamState(np.array([lx_m * 0.7, ly_m * 0.3 + s * 2e-6]), 0.0, 60.0, s % 2 == 0)]
+        beams += [BeamState(np.array([lx_m * (0.1 + 0.1 * b), ly_m * (0.9 - 0.1 * b)]), 0.0,
+                            20.0 + 5.0 * b, True) for b in range(2, nbeams)]
+        if nbeams:
+            recs[s] = pack_beams(beams[:nbeams])
     fail, amax, tmax = op.run_explicit(np.full(steps, 2e-8), recs)
     Tout, _ = op.get_state()
     op.close()
@@ -75,6 +78,30 @@ def test_lean_kernel_equals_general_kernel_bitwise(case, latent, lx, inseam, mon
     mesh = CASES[case]()
     f0, a0, t0, T0 = _run(mesh, latent, lx, False, monkeypatch)
     f1, a1, t1, T1 = _run(mesh, latent, lx, True, monkeypatch, inseam=inseam)
+    assert f0 == f1
+    assert a0 == a1 and t0 == t1
+    assert np.array_equal(T0, T1)
+
+
+EDGE_CASES = {
+    # one cell layer (a chunk is its first and last plane only), two layers in
+    # one-layer chunks, no Dirichlet plane and no radiating top, thin in z
+    "one_layer": (lambda: st.StructuredBox(1, 9, 17, H, degree=2), None),
+    "chunks_of_one": (lambda: st.StructuredBox(2, 9, 17, H, degree=2), "1"),
+    "insulated": (lambda: st.StructuredBox(6, 10, 18, H, degree=2, dirichlet_bottom=False,
+                                           top_faces=False), "2"),
+    "one_cell_high": (lambda: st.StructuredBox(7, 20, 1, H, degree=2), "3"),
+}
+
+
+@pytest.mark.parametrize("nbeams", [0, 8])
+@pytest.mark.parametrize("case", list(EDGE_CASES))
+def test_lean_kernel_edge_cases_bitwise(case, nbeams, monkeypatch):
+    """Degenerate extents and boundary switches, without beams and with the
+    eight beams the kernel's source tables hold."""
+    make, lx = EDGE_CASES[case]
+    f0, a0, t0, T0 = _run(make(), True, lx, False, monkeypatch, steps=4, nbeams=nbeams)
+    f1, a1, t1, T1 = _run(make(), True, lx, True, monkeypatch, steps=4, nbeams=nbeams)
     assert f0 == f1
     assert a0 == a1 and t0 == t1
     assert np.array_equal(T0, T1)
