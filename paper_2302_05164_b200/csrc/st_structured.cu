@@ -594,6 +594,12 @@ struct Structured : Backend {
   ~Structured() override {
     if (latstat_h) cudaFreeHost(latstat_h);
     if (lat_ev) cudaEventDestroy(lat_ev);
+    for (auto& e : ev_hot)
+      if (e) cudaEventDestroy(e);
+    if (ev_fork) cudaEventDestroy(ev_fork);
+    if (ev_seams) cudaEventDestroy(ev_seams);
+    if (hot_s) cudaStreamDestroy(hot_s);
+    if (seam_s) cudaStreamDestroy(seam_s);
   }
   st_structured_mesh m{};
   // fitted part (m.xext != NULL): per cell row x extent, per node plane
@@ -621,7 +627,20 @@ struct Structured : Backend {
     DevBuf<double> sci;
     int64_t n = 0;
     bool built = false;
+    // entries on node planes <= I (the list is in node order, so the seam
+    // nodes of a range of planes are a contiguous range of entries)
+    std::vector<int64_t> plane_end;
   } slist[2];
+  // pipelined seam pass (xmarch_piped): the x chunks go out as groups of
+  // launches alternating between the library stream and hot_s, and the seam
+  // entries of a group's planes run on the high-priority seam_s as soon as
+  // the groups that write them are done, under the later groups' cells
+  static constexpr int kMaxPipe = 16;
+  cudaStream_t hot_s = nullptr, seam_s = nullptr;
+  cudaEvent_t ev_fork = nullptr, ev_seams = nullptr, ev_hot[kMaxPipe] = {};
+  int pipe_groups = 0;  // 0: off
+  double pipe_min_waves = 2.0;  // least waves of CTAs per group (ST_SEAM_PIPE_MINWAVES)
+  int64_t hot_slots = 444;  // resident CTAs of the hot kernel on the device
   // latent-dense fields (every tile gathers latent increments in most
   // layers, e.g. config 2's random field): k_xmarch2 keeps the increments in
   // an L2 scratch and loses to the general kernel's shared-memory copy there,
@@ -785,19 +804,25 @@ struct Structured : Backend {
     }
   }
 
-  int seams(SArgs& A) {
+  // seam pass over the entries [e0, e1) of the context's list (e1 < 0: all)
+  int seams(SArgs& A, int64_t e0 = 0, int64_t e1 = -1, cudaStream_t stream = nullptr) {
     const bool lat = c->dp.latent != 0 && A.mode == 0;
     const int which = (A.x2 && A.seamcnt) ? 1 : 0;
     if (!slist[which].built) ST_TRY(build_seam_list(which));
     const SeamList& L = slist[which];
-    if (L.n > 0) {
+    if (e1 < 0) e1 = L.n;
+    if (!stream) stream = c->stream;
+    const int64_t n = e1 - e0;
+    if (n > 0) {
       // one thread per seam node: the pass is latency bound
       constexpr int kSB = 128;  // measured a hair faster than 256
-      const unsigned grid = (unsigned)((L.n + kSB - 1) / kSB);
+      const unsigned grid = (unsigned)((n + kSB - 1) / kSB);
       if (lat)
-        k_seam_list<true><<<grid, kSB, 0, c->stream>>>(A, L.n, L.sidx.p, L.scode.p, L.sci.p);
+        k_seam_list<true><<<grid, kSB, 0, stream>>>(A, n, L.sidx.p + e0, L.scode.p + e0,
+                                                    L.sci.p + e0);
       else
-        k_seam_list<false><<<grid, kSB, 0, c->stream>>>(A, L.n, L.sidx.p, L.scode.p, L.sci.p);
+        k_seam_list<false><<<grid, kSB, 0, stream>>>(A, n, L.sidx.p + e0, L.scode.p + e0,
+                                                     L.sci.p + e0);
       ST_TRY(launched());
     }
     return ST_OK;
@@ -923,7 +948,9 @@ struct Structured : Backend {
       }
       (void)npres;
     };
+    std::vector<int64_t> plane_end(NX, 0);
     for (int I = 0; I < NX; I++) {
+      if (I > 0) plane_end[I] = plane_end[I - 1];
       if (xonly && !xcand[I]) continue;
       const int kmI = kmin_of(I);
       for (int J = 0; J < NY; J++) {
@@ -934,9 +961,11 @@ struct Structured : Backend {
           for (int K = (kmI / sz + 1) * sz; K < NZ - 1; K += sz) visit(I, J, K, kmI);
         }
       }
+      plane_end[I] = (int64_t)idx.size();
     }
     SeamList& L = slist[which];
     L.built = true;
+    L.plane_end = std::move(plane_end);
     L.n = (int64_t)idx.size();
     if (L.n == 0) return ST_OK;
     ST_TRY(L.sidx.upload(idx.data(), idx.size(), c->stream));
@@ -968,29 +997,98 @@ struct Structured : Backend {
                ? 1
                : 0;
     last_x2 = A.x2 != 0;
+    const bool whole = z0 == 0 && (z1 < 0 || z1 == n_chunks());
     if (z1 < 0) z1 = n_chunks();
     if (z1 <= z0) return with_seams ? seams(A) : ST_OK;
+    if (with_seams && whole && A.x2 && !A.seamcnt && pipe_groups >= 2) {
+      int nb = 0, bounds[kMaxPipe + 1];
+      pipe_bounds(bounds, &nb);
+      if (nb >= 2) return xmarch_piped(A, lat, bounds, nb);
+    }
     c->prof_begin();
-    const dim3 grid((m.ny + cy - 1) / cy, (m.nz + cz - 1) / cz, z1 - z0);
-    A.zoff = z0;
-    cudaError_t e;
-    switch (p) {
-      case 1: e = hot_launch<1>(A, slab, lat, rcf, grid, c->stream); break;
-      case 2: e = hot_launch<2>(A, slab, lat, rcf, grid, c->stream); break;
-      case 3: e = hot_launch<3>(A, slab, lat, rcf, grid, c->stream); break;
-      default: e = hot_launch<4>(A, slab, lat, rcf, grid, c->stream); break;
-    }
-    int rc = ST_OK;
-    if (e != cudaSuccess) {
-      set_error(std::string("hot kernel launch: ") + cudaGetErrorString(e));
-      rc = ST_ECUDA;
-    } else {
-      rc = launched();
-    }
+    int rc = hot(A, lat, rcf, z0, z1, c->stream);
     c->prof_end();
     ST_TRY(rc);
     if (lat && latstat_h) record_latent(z0, z1);
     return with_seams ? seams(A) : ST_OK;
+  }
+
+  // the hot kernel over the x chunks [z0, z1)
+  int hot(SArgs& A, bool lat, bool rcf, int z0, int z1, cudaStream_t stream) {
+    const dim3 grid((m.ny + cy - 1) / cy, (m.nz + cz - 1) / cz, z1 - z0);
+    A.zoff = z0;
+    cudaError_t e;
+    switch (p) {
+      case 1: e = hot_launch<1>(A, slab, lat, rcf, grid, stream); break;
+      case 2: e = hot_launch<2>(A, slab, lat, rcf, grid, stream); break;
+      case 3: e = hot_launch<3>(A, slab, lat, rcf, grid, stream); break;
+      default: e = hot_launch<4>(A, slab, lat, rcf, grid, stream); break;
+    }
+    if (e != cudaSuccess) {
+      set_error(std::string("hot kernel launch: ") + cudaGetErrorString(e));
+      return ST_ECUDA;
+    }
+    return launched();
+  }
+
+  // chunk groups of the pipelined step, balanced by CTA-layers; a part with
+  // less than pipe_min_waves waves of CTAs per group stays on the single launch
+  void pipe_bounds(int* bounds, int* nb) const {
+    const int nch = n_chunks();
+    const double total = launch_layers(0, nch);
+    int G = std::min(std::min(pipe_groups, (int)kMaxPipe), nch);
+    // live CTAs (a CTA marches Lx layers) against the resident ones
+    const double waves = total / Lx / (double)hot_slots;
+    G = std::min(G, pipe_min_waves > 0.0 ? (int)(waves / pipe_min_waves) : G);
+    *nb = 0;
+    if (G < 2) return;
+    bounds[0] = 0;
+    int g = 1;
+    for (int z = 1; z < nch && g < G; z++)
+      if (launch_layers(0, z) >= total * g / G) bounds[g++] = z;
+    bounds[g] = nch;
+    *nb = g;
+  }
+
+  // One explicit step of k_xmarch2 with the seam pass under the cells: the
+  // chunk groups alternate between the library stream and hot_s (a group's
+  // CTAs fill the SMs the previous group's tail leaves idle), and the seam
+  // entries of the node planes (first plane of group g, first plane of group
+  // g + 1] (plane 0 with group 0) run on seam_s once groups g and g + 1 are
+  // done.  The pass is bandwidth bound and the cells fp64 bound, so only the
+  // last group's entries stay exposed.  Same kernels, same partials, same
+  // summation order as the single launch: bitwise the same field.
+  int xmarch_piped(SArgs& A, bool lat, const int* bounds, int nb) {
+    const int which = 0;
+    if (!slist[which].built) ST_TRY(build_seam_list(which));
+    const SeamList& L = slist[which];
+    const int sx = p * Lx;
+    auto entries_to = [&](int g) {  // entries on the planes <= first plane of group g
+      if (g >= nb) return L.n;
+      return L.plane_end[std::min(bounds[g] * sx, NX - 1)];
+    };
+    ST_CUDA(cudaEventRecord(ev_fork, c->stream));
+    ST_CUDA(cudaStreamWaitEvent(hot_s, ev_fork, 0));
+    ST_CUDA(cudaStreamWaitEvent(seam_s, ev_fork, 0));
+    c->prof_begin();
+    for (int g = 0; g < nb; g++) {
+      cudaStream_t hs = (g & 1) ? hot_s : c->stream;
+      ST_TRY(hot(A, lat, false, bounds[g], bounds[g + 1], hs));
+      ST_CUDA(cudaEventRecord(ev_hot[g], hs));
+      ST_CUDA(cudaStreamWaitEvent(seam_s, ev_hot[g], 0));
+      if (g >= 1)
+        ST_TRY(seams(A, g == 1 ? 0 : entries_to(g - 1), entries_to(g), seam_s));
+    }
+    // the hot kernel's time for the bench: until the last group of either
+    // stream is done
+    ST_CUDA(cudaStreamWaitEvent(c->stream, ev_hot[nb - 1], 0));
+    if (nb >= 2) ST_CUDA(cudaStreamWaitEvent(c->stream, ev_hot[nb - 2], 0));
+    c->prof_end();
+    ST_TRY(seams(A, entries_to(nb - 1), L.n, seam_s));
+    ST_CUDA(cudaEventRecord(ev_seams, seam_s));
+    ST_CUDA(cudaStreamWaitEvent(c->stream, ev_seams, 0));
+    if (lat && latstat_h) record_latent(0, n_chunks());
+    return ST_OK;
   }
 
   // CTA-layers of a launch over the x chunks [z0, z1)
@@ -1355,6 +1453,7 @@ Backend* make_structured(Ctx* c, const st_structured_mesh* m, int* err) {
   int sms = 148;
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c->device);
   const int64_t slots = (int64_t)s->resident(c->dp.latent != 0) * std::max(sms, 1);
+  s->hot_slots = std::max<int64_t>(slots, 1);
   int64_t best = -1;
   s->Lx = m->nx;
   for (int L = m->nx; L >= std::min(2, m->nx); L--) {
@@ -1466,6 +1565,35 @@ Backend* make_structured(Ctx* c, const st_structured_mesh* m, int* err) {
           cudaMemsetAsync(s->seamcnt.p, 0, (size_t)ncnt * sizeof(int), c->stream) != cudaSuccess)
         rc = ST_ECUDA;
       s->inseam = rc == ST_OK;
+    }
+  }
+  // pipelined seam pass of the k_xmarch2 step (xmarch_piped): ST_SEAM_PIPE=n
+  // chunk groups (0 / 1: the single launch followed by the whole pass)
+  if (rc == ST_OK && !s->slab && s->p == 2 && !s->inseam && !m->iface_lo && !m->iface_hi) {
+    // off by default: measured slower on config 4 (15.9 ms per step with 4
+    // groups, 16.2 with 12, against 15.2): both kernels are bound by resident
+    // threads (the cells by registers, the pass by loads in flight), so the
+    // pass under the cells takes from them what it gains
+    int G = 0;
+    if (const char* e = getenv("ST_SEAM_PIPE")) G = atoi(e);
+    G = std::max(0, std::min(G, (int)Structured::kMaxPipe));
+    if (G >= 2) {
+      int lo = 0, hi = 0;
+      cudaDeviceGetStreamPriorityRange(&lo, &hi);
+      bool ok = cudaStreamCreateWithFlags(&s->hot_s, cudaStreamNonBlocking) == cudaSuccess &&
+                cudaStreamCreateWithPriority(&s->seam_s, cudaStreamNonBlocking, hi) ==
+                    cudaSuccess &&
+                cudaEventCreateWithFlags(&s->ev_fork, cudaEventDisableTiming) == cudaSuccess &&
+                cudaEventCreateWithFlags(&s->ev_seams, cudaEventDisableTiming) == cudaSuccess;
+      for (int g = 0; ok && g < G; g++)
+        ok = cudaEventCreateWithFlags(&s->ev_hot[g], cudaEventDisableTiming) == cudaSuccess;
+      if (!ok) {
+        set_error("structured context: streams / events of the pipelined seam pass");
+        rc = ST_ECUDA;
+      } else {
+        s->pipe_groups = G;
+        if (const char* e = getenv("ST_SEAM_PIPE_MINWAVES")) s->pipe_min_waves = atof(e);
+      }
     }
   }
   // the list the context's explicit steps use; the other one is built when a

@@ -26,8 +26,14 @@ def _params(latent):
     return st.ProcessParams(mat, bnd, las, st.MeshParams(h_coarse=H, n_refine=0, h_powder=H))
 
 
-def _run(mesh, latent, lx, x2, monkeypatch, steps=6, inseam=False, nbeams=2):
+def _run(mesh, latent, lx, x2, monkeypatch, steps=6, inseam=False, nbeams=2, pipe=0):
     monkeypatch.setenv("ST_XMARCH2", "1" if x2 else "0")
+    # the pipelined seam pass is for parts of many waves of CTAs: off here
+    # unless a test forces it on (groups of any size)
+    monkeypatch.setenv("ST_SEAM_PIPE", str(pipe))
+    if pipe:
+        monkeypatch.setenv("ST_X2_ADAPT", "0")   # stay on k_xmarch2 on this latent-dense field
+    monkeypatch.setenv("ST_SEAM_PIPE_MINWAVES", "0")
     monkeypatch.setenv("ST_INSEAM", "1" if inseam else "0")
     # the general kernel runs on the original seam layout (split f / dc slot
     # arrays), the lean one on the round's layout ((f, dc) pairs)
@@ -53,6 +59,7 @@ def _run(mesh, latent, lx, x2, monkeypatch, steps=6, inseam=False, nbeams=2):
             recs[s] = pack_beams(beams[:nbeams])
     fail, amax, tmax = op.run_explicit(np.full(steps, 2e-8), recs)
     Tout, _ = op.get_state()
+    _run.launches = op.launches
     op.close()
     return fail, amax, tmax, Tout
 
@@ -81,6 +88,37 @@ def test_lean_kernel_equals_general_kernel_bitwise(case, latent, lx, inseam, mon
     assert f0 == f1
     assert a0 == a1 and t0 == t1
     assert np.array_equal(T0, T1)
+
+
+PIPE_CASES = {
+    # (mesh, x chunk length): 12 / 5 / 3 chunks of a box, a fitted part whose
+    # tile rows end inside different groups, two chunks (two groups of one)
+    "box_12_chunks": (lambda: st.StructuredBox(12, 16, 32, H, degree=2), "1"),
+    "box_ragged": (lambda: st.StructuredBox(9, 11, 19, H, degree=2), "2"),
+    "box_3_chunks": (lambda: st.StructuredBox(9, 11, 19, H, degree=2), "3"),
+    "fitted": (lambda: FittedPart(13, 11, 40, H, [5] * 16 + [9] * 16 + [13] * 8, degree=2), "2"),
+    "two_chunks": (lambda: st.StructuredBox(4, 9, 17, H, degree=2), "2"),
+}
+
+
+@pytest.mark.parametrize("groups", [2, 3, 16])
+@pytest.mark.parametrize("latent", [True, False])
+@pytest.mark.parametrize("case", list(PIPE_CASES))
+def test_pipelined_seam_pass_bitwise(case, latent, groups, monkeypatch):
+    """The step with the x chunks launched as groups on two streams and the
+    seam entries of each group's planes on a third (xmarch_piped) against the
+    single launch followed by the whole pass: same kernels and summation
+    order, so the fields, the stability maxima and the sign of zeros agree."""
+    make, lx = PIPE_CASES[case]
+    monkeypatch.setenv("ST_X2_ADAPT", "0")
+    f0, a0, t0, T0 = _run(make(), latent, lx, True, monkeypatch, steps=8)
+    n0 = _run.launches
+    f1, a1, t1, T1 = _run(make(), latent, lx, True, monkeypatch, steps=8, pipe=groups)
+    assert _run.launches >= n0 + 8 * 2   # at least two groups per step ran
+    assert f0 == f1
+    assert a0 == a1 and t0 == t1
+    assert np.array_equal(T0, T1)
+    assert np.array_equal(np.signbit(T0), np.signbit(T1))
 
 
 EDGE_CASES = {
