@@ -307,8 +307,18 @@ def run_slabs(args):
                                                    torch_exchange, torch_max_reducer)
     st = _st()
     ws, rank, local = dist_env()
+    # ST_DIST_BACKEND=gloo: functional check of this path where the ranks
+    # cannot have a GPU each (the exchange is staged through the host and
+    # the ranks share the visible GPUs round-robin); never a measurement
+    backend = os.environ.get("ST_DIST_BACKEND", "nccl")
+    if backend == "gloo":
+        local = local % torch.cuda.device_count()
     torch.cuda.set_device(local)
-    dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    if backend == "gloo":
+        dist.init_process_group("gloo")
+    else:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    red_dev = "cpu" if backend == "gloo" else "cuda"
     w = dict(WORKLOADS[args.workload](), key=args.workload)
     weak = args.scaling == "weak" or w.get("xext") is None
     if weak:
@@ -343,7 +353,7 @@ def run_slabs(args):
         clk.__exit__()
     launches = op.launches - launches0
     total_ms = e0.elapsed_time(e1)
-    t = torch.tensor([total_ms], device="cuda")
+    t = torch.tensor([total_ms], device=red_dev)
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     total_ms = float(t.item())
     # end to end: host slab in -> K split steps with the exchange -> host out
@@ -357,7 +367,7 @@ def run_slabs(args):
     with torch.cuda.stream(stepper.stream):
         drv.run(dts[args.warmup:], beams[args.warmup:], check_every=32)
     T_out, rc_out = op.get_state(out=T_buf)
-    e2e_s = torch.tensor([time.perf_counter() - t0], device="cuda")
+    e2e_s = torch.tensor([time.perf_counter() - t0], device=red_dev)
     dist.all_reduce(e2e_s, op=dist.ReduceOp.MAX)
     nb = beams.shape[1]
     dofs_total = glob.n_dofs
@@ -368,6 +378,14 @@ def run_slabs(args):
            "api": "per rank: set_state + split steps (NCCL exchange, stability check every "
                   "32 steps) + get_state; max over ranks"}
     value = dofs_total * args.steps / (total_ms * 1e-3)
+    # per GPU, over the whole split step (cells, exchange, seam pass, stability
+    # checks) -- the kernel alone is the N = 1 line's roofline
+    peak, peak_kind = measured_hbm_peak()
+    ach = B_ALG * value / ws / 1e9
+    roofline = {"bound": "hbm", "achieved": ach, "peak": peak, "unit": "GB/s",
+                "frac": ach / peak, "traffic": None, "bytes_per_dof": B_ALG,
+                "peak_source": peak_kind,
+                "scope": "per GPU, whole split step (max over ranks), not the kernel alone"}
     dist.barrier()
     if rank == 0:
         out = {"metric": METRIC, "value": value, "unit": "DoF-updates/s", "n_gpus": ws,
@@ -379,10 +397,13 @@ def run_slabs(args):
                               backend="structured x-slabs",
                               partition=[list(p) for p in parts],
                               parallelism=f"x-slab dp{ws}, NCCL partial-sum interface exchange "
-                                          "overlapped with the interior chunks",
+                                          "overlapped with the interior chunks"
+                                          + (" [ST_DIST_BACKEND=gloo: host-staged functional "
+                                             "check, not a measurement]"
+                                             if backend == "gloo" else ""),
                               l2="inputs larger than L2 (no flush)", **w["cfg"]),
-               "e2e": e2e, "gpu_launches": int(launches), "clocks": clk.summary(),
-               "t_max": tmax}
+               "e2e": e2e, "roofline": roofline, "gpu_launches": int(launches),
+               "clocks": clk.summary(), "t_max": tmax}
         print(json.dumps(out), flush=True)
     op.close()
     dist.destroy_process_group()

@@ -298,23 +298,31 @@ def torch_exchange(rank, world, group=None):
     import torch.distributed as dist
 
     def ex(parts):
+        # gloo has no device point-to-point: device planes are staged through
+        # the host there (functional checks on a box without a GPU per rank)
+        staged = dist.get_backend(group) != "nccl"
+        host = lambda t: t.cpu() if staged and torch.is_tensor(t) and t.is_cuda else t
         ops, recv = [], {}
         for side, peer in ((0, rank - 1), (1, rank + 1)):
             if side not in parts or not (0 <= peer < world):
                 continue
             mine = parts[side]
-            rf = torch.empty_like(mine.f)
-            rc = torch.empty_like(mine.c) if mine.c is not None else None
-            ops.append(dist.P2POp(dist.isend, mine.f, peer, group))
+            sf, sc = host(mine.f), (host(mine.c) if mine.c is not None else None)
+            rf = torch.empty_like(sf)
+            rc = torch.empty_like(sc) if sc is not None else None
+            ops.append(dist.P2POp(dist.isend, sf, peer, group))
             ops.append(dist.P2POp(dist.irecv, rf, peer, group))
-            if mine.c is not None:
-                ops.append(dist.P2POp(dist.isend, mine.c, peer, group))
+            if sc is not None:
+                ops.append(dist.P2POp(dist.isend, sc, peer, group))
                 ops.append(dist.P2POp(dist.irecv, rc, peer, group))
-            recv[side] = Partials(rf, rc)
+            recv[side] = (Partials(rf, rc), mine)
         if ops:
             for w in dist.batch_isend_irecv(ops):
                 w.wait()
-        return recv
+        back = lambda t, like: (t.to(like.device) if torch.is_tensor(like) and like.is_cuda
+                                and not t.is_cuda else t)
+        return {s: Partials(back(r.f, m.f), back(r.c, m.c) if r.c is not None else None)
+                for s, (r, m) in recv.items()}
 
     return ex
 
