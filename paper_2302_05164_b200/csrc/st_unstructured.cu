@@ -505,45 +505,88 @@ __device__ __forceinline__ double gather_v(const NodeTab& nt, const double* E, i
 }
 
 // condensed sum at a non-slave vertex (bincount then np.add.at order):
-// f = own entries, then f + w * (the slave's entries) per folded slave.  The
-// slaves' entries come from the flattened table, all indices then all
-// entries loaded up front (up to 32), the same sums in the same order.
+// f = own entries, then f + w * (the slave's entries) per folded slave, one
+// thread per vertex (the opt-in persistent scan; the kernels below use the
+// warp version)
 __device__ __forceinline__ double gather_condensed(const NodeTab& nt, const double* E, int64_t v) {
   double f = gather_v(nt, E, v);
-  const int ga = nt.cond_ptr[v], gb = nt.cond_ptr[v + 1];
-  if (ga == gb) return f;
-  const int e0 = nt.cfe_ptr[v], ne = nt.cfe_ptr[v + 1] - e0;
-  constexpr int kMax = 32;
-  if (ne <= kMax) {
-    int ix[kMax];
-    double e[kMax];
-#pragma unroll
-    for (int k = 0; k < kMax; k++) ix[k] = k < ne ? nt.cfe[e0 + k] : 0;
-#pragma unroll
-    for (int k = 0; k < kMax; k++) e[k] = k < ne ? E[ix[k]] : 0.0;
-    int k = 0;
-    for (int g = ga; g < gb; g++) {
-      const int len = nt.cgl[g];
-      double sv = 0.0;
-#pragma unroll
-      for (int q = 0; q < kMax; q++)
-        if (q >= k && q < k + len) sv += e[q];
-      k += len;
-      f = f + nt.cond_w[g] * sv;
-    }
-    return f;
-  }
-  for (int i = ga; i < gb; i++) f = f + nt.cond_w[i] * gather_v(nt, E, nt.cond_s[i]);
+  for (int i = nt.cond_ptr[v]; i < nt.cond_ptr[v + 1]; i++)
+    f = f + nt.cond_w[i] * gather_v(nt, E, nt.cond_s[i]);
   return f;
 }
 
-// condensed(E) at v; slave rows 0 (or slave_val); Dirichlet rows <- dir_src
-__device__ __forceinline__ double gather_row(int64_t v, const NodeTab& nt, const double* E,
-                                             const double* dir_src, int set_slave,
-                                             double slave_val) {
-  if (nt.is_slave[v]) return set_slave ? slave_val : 0.0;
-  double r = gather_condensed(nt, E, v);
-  if (dir_src && nt.is_dir[v]) r = dir_src[v];
+// The same sum with the condensation done by the whole warp.  Every warp of a
+// 2:1 mesh holds about one vertex with slaves folding into it (config 3,
+// layer 0: 616 of 691 warps have one or two), and a thread doing that
+// vertex's up to 32 extra entries alone makes its 31 neighbours wait (the
+// node kernels ran ~1000 warp instructions per vertex that way).  Here each
+// thread gathers its own entries, then the warp takes the vertices with
+// slaves one at a time: lane q loads entry q of the flattened table (cfe),
+// lane j the entry count and weight of slave j; lane j sums slave j's entries
+// in order (shuffles from the lanes that hold them), and the weighted slave
+// sums are added in slave order -- the same additions in the same order as
+// the plain loops.  All 32 lanes call this together; ``live`` marks the lanes
+// with a (non-slave) vertex.
+__device__ __forceinline__ double gather_condensed_warp(const NodeTab& nt, const double* E,
+                                                        int64_t v, bool live) {
+  constexpr unsigned kFull = 0xffffffffu;
+  const int lane = threadIdx.x & 31;
+  int ga = 0, gb = 0, e0 = 0, ne = 0;
+  double f = 0.0;
+  if (live) {
+    ga = nt.cond_ptr[v];
+    gb = nt.cond_ptr[v + 1];
+    e0 = nt.cfe_ptr[v];
+    ne = nt.cfe_ptr[v + 1] - e0;
+    f = gather_v(nt, E, v);
+  }
+  unsigned todo = __ballot_sync(kFull, gb > ga);
+  while (todo) {
+    const int src = __ffs(todo) - 1;
+    todo &= todo - 1;
+    const int gas = __shfl_sync(kFull, ga, src), ng = __shfl_sync(kFull, gb, src) - gas;
+    const int e0s = __shfl_sync(kFull, e0, src), nes = __shfl_sync(kFull, ne, src);
+    double fs = __shfl_sync(kFull, f, src);
+    if (nes <= 32 && ng <= 32) {
+      const double e = lane < nes ? E[nt.cfe[e0s + lane]] : 0.0;
+      const int len = lane < ng ? nt.cgl[gas + lane] : 0;
+      const double w = lane < ng ? nt.cond_w[gas + lane] : 0.0;
+      int start = len;  // inclusive scan of the entry counts
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int t = __shfl_up_sync(kFull, start, o);
+        if (lane >= o) start += t;
+      }
+      start -= len;
+      const int maxlen = __reduce_max_sync(kFull, len);
+      double sv = 0.0;
+      for (int t = 0; t < maxlen; t++) {
+        const double x = __shfl_sync(kFull, e, (start + t) & 31);
+        if (t < len) sv += x;
+      }
+      for (int j = 0; j < ng; j++) {
+        const double wj = __shfl_sync(kFull, w, j), sj = __shfl_sync(kFull, sv, j);
+        fs = fs + wj * sj;
+      }
+    } else {
+      // more than a warp's worth of entries: one slave after the other
+      // (every lane computes the same sum)
+      for (int i = gas; i < gas + ng; i++) fs = fs + nt.cond_w[i] * gather_v(nt, E, nt.cond_s[i]);
+    }
+    if (lane == src) f = fs;
+  }
+  return f;
+}
+
+// condensed(E) at v; slave rows 0 (or slave_val); Dirichlet rows <- dir_src.
+// Called by all lanes of a warp (in: lanes with a vertex).
+__device__ __forceinline__ double gather_row_warp(int64_t v, bool in, const NodeTab& nt,
+                                                  const double* E, const double* dir_src,
+                                                  int set_slave, double slave_val) {
+  const bool slave = in && nt.is_slave[v];
+  double r = gather_condensed_warp(nt, E, v, in && !slave);
+  if (slave) r = set_slave ? slave_val : 0.0;
+  if (in && !slave && dir_src && nt.is_dir[v]) r = dir_src[v];
   return r;
 }
 
@@ -552,8 +595,8 @@ __global__ void k_gather(int64_t nv, NodeTab nt, const double* E, double* out,
                          const double* dir_src, int set_slave, double slave_val) {
   pdl_wait_release();  // see st_common.cuh
   int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (v >= nv) return;
-  out[v] = gather_row(v, nt, E, dir_src, set_slave, slave_val);
+  const double r = gather_row_warp(v, v < nv, nt, E, dir_src, set_slave, slave_val);
+  if (v < nv) out[v] = r;
 }
 
 // ---------------------------------------------------------------------------
@@ -633,13 +676,37 @@ __device__ __forceinline__ double2 sum_partials2(const double* pa, const double*
 }
 
 #ifndef ST_PCG_MINB
-#define ST_PCG_MINB 2  // resident blocks per SM (A/B hook: 1 = no register cap)
+// resident blocks per SM the register allocation aims at.  1 (no register
+// cap, one block per SM): the cells and the staged gather keep their state
+// in registers and the grid barriers synchronise half as many blocks --
+// measured on the config-3-sized box 18.9 against 23.7 us per iteration
+// inside the kernel (phase clocks of -DST_PCG_TIMING), 36.4 against 41.6 us
+// per iteration of a whole solve, 0.48 against 0.54 ms per BE step
+#define ST_PCG_MINB 1
+#endif
+// dev hook (-DST_PCG_TIMING, tools/time_implicit.py): block 0 accumulates the
+// time of every phase and barrier of the iteration loop (globaltimer, ns)
+// behind the block partials
+#ifdef ST_PCG_TIMING
+#define ST_PCG_TS(k)                                                      \
+  if (tid == 0) {                                                         \
+    unsigned long long t_;                                                \
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));                \
+    a.part[4 * nb + (k)] += (double)(t_ - ts_last);                       \
+    ts_last = t_;                                                         \
+  }
+#else
+#define ST_PCG_TS(k)
 #endif
 __global__ void __launch_bounds__(kPcgThreads, ST_PCG_MINB) k_pcg_persistent(PcgArgs a) {
   cg::grid_group grid = cg::this_grid();
   __shared__ double2 red[32];
   const int nb = gridDim.x;
   const int64_t tid = blockIdx.x * (int64_t)kPcgThreads + threadIdx.x;
+#ifdef ST_PCG_TIMING
+  unsigned long long ts_last;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(ts_last));
+#endif
   const int64_t nth = (int64_t)nb * kPcgThreads;
   double* pa = a.part;
   // the tangent at T_lin once per solve (it is fixed over the iterations)
@@ -662,6 +729,7 @@ __global__ void __launch_bounds__(kPcgThreads, ST_PCG_MINB) k_pcg_persistent(Pcg
   double beta = 0.0;
   double* p = a.p0;
   double* pn = a.p1;
+  ST_PCG_TS(0)
   for (int it = 1; it <= a.max_iter; it++) {
     // 1. p_new = z + beta p and the Jacobian input
     for (int64_t i = tid; i < a.nv + a.ns; i += nth) {
@@ -684,21 +752,32 @@ __global__ void __launch_bounds__(kPcgThreads, ST_PCG_MINB) k_pcg_persistent(Pcg
       p = pn;
       pn = t;
     }
+    ST_PCG_TS(1)
     grid.sync();
+    ST_PCG_TS(2)
     // 2. element vectors of J vd
     for (int64_t c = tid; c < a.n; c += nth) jac_cell_tg(c, a.n, a.g, a.P, a.vd, a.TG, a.dt, a.E);
+    ST_PCG_TS(3)
     grid.sync();
+    ST_PCG_TS(4)
     // 3. Ap and p.Ap
     l = 0.0;
-    for (int64_t v = tid; v < a.nv; v += nth) {
-      const double ap = gather_row(v, a.nt, a.E, p, 0, 0.0);
-      a.Ap[v] = ap;
-      l += p[v] * ap;
+    for (int64_t v0 = tid - (threadIdx.x & 31); v0 < a.nv; v0 += nth) {  // whole warps
+      const int64_t v = v0 + (threadIdx.x & 31);
+      const double ap = gather_row_warp(v, v < a.nv, a.nt, a.E, p, 0, 0.0);
+      if (v < a.nv) {
+        a.Ap[v] = ap;
+        l += p[v] * ap;
+      }
     }
+    ST_PCG_TS(11)
     t2 = block_sum2(l, 0.0, red);
     if (threadIdx.x == 0) pa[nb + blockIdx.x] = t2.x;
+    ST_PCG_TS(5)
     grid.sync();
+    ST_PCG_TS(6)
     const double alpha = rz / sum_partials2(pa + nb, nullptr, nb, red).x;
+    ST_PCG_TS(7)
     // 4. x, r, z and r.r / r.z
     double lrr = 0.0, lrz = 0.0;
     for (int64_t i = tid; i < a.nv; i += nth) {
@@ -715,9 +794,12 @@ __global__ void __launch_bounds__(kPcgThreads, ST_PCG_MINB) k_pcg_persistent(Pcg
       pa[2 * nb + blockIdx.x] = t2.x;
       pa[3 * nb + blockIdx.x] = t2.y;
     }
+    ST_PCG_TS(8)
     grid.sync();
+    ST_PCG_TS(9)
     t2 = sum_partials2(pa + 2 * nb, pa + 3 * nb, nb, red);
     const double rr = t2.x, rzn = t2.y;
+    ST_PCG_TS(10)
     if (sqrt(rr) <= a.thr) {
       if (tid == 0) {
         a.out[0] = it;
@@ -732,6 +814,18 @@ __global__ void __launch_bounds__(kPcgThreads, ST_PCG_MINB) k_pcg_persistent(Pcg
     a.out[0] = a.max_iter;
     a.out[1] = 0;
   }
+}
+
+// the update of a non-slave vertex from its gathered f and inverse capacity
+__device__ __forceinline__ double step_node_with(int64_t v, const NodeTab& nt, double f, double ci,
+                                                 const double* T, double dt, double T_inf,
+                                                 double* Tout) {
+  // T + dt (C^-1 f) with the reference's three roundings (no FMA), so a
+  // step equals the host composition of the same pieces bit for bit
+  double out = __dadd_rn(T[v], __dmul_rn(dt, __dmul_rn(ci, f)));
+  if (nt.is_dir[v]) out = T_inf;
+  Tout[v] = out;
+  return out;
 }
 
 // forward Euler with the lumped capacity (operators.py:352-369) at a
@@ -749,12 +843,7 @@ __device__ __forceinline__ double step_node(int64_t v, const NodeTab& nt, const 
     ci = 1.0 / c_atomic[v];
   else
     ci = cinv[v];
-  // T + dt (C^-1 f) with the reference's three roundings (no FMA), so a
-  // step equals the host composition of the same pieces bit for bit
-  double out = __dadd_rn(T[v], __dmul_rn(dt, __dmul_rn(ci, f)));
-  if (nt.is_dir[v]) out = T_inf;
-  Tout[v] = out;
-  return out;
+  return step_node_with(v, nt, f, ci, T, dt, T_inf, Tout);
 }
 
 __global__ void k_step_nodes(int64_t nv, NodeTab nt, const double* E, const double* Ec,
@@ -767,7 +856,12 @@ __global__ void k_step_nodes(int64_t nv, NodeTab nt, const double* E, const doub
   int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   double out = 0.0;
   bool live = v < nv && !nt.is_slave[v];
-  if (live) out = step_node(v, nt, E, Ec, f_atomic, c_atomic, cinv, T, dt, T_inf, Tout);
+  // the condensed gathers by the whole warp, then step_node's update
+  const double fg = E ? gather_condensed_warp(nt, E, v, live) : 0.0;
+  const double cg_ = Ec ? gather_condensed_warp(nt, Ec, v, live) : 0.0;
+  if (live) out = step_node_with(v, nt, E ? fg : f_atomic[v],
+                                 Ec ? 1.0 / cg_ : (c_atomic ? 1.0 / c_atomic[v] : cinv[v]), T, dt,
+                                 T_inf, Tout);
   block_max2(live ? out : 0.0, live ? out : -INFINITY, red);
 }
 
@@ -1181,8 +1275,12 @@ struct Unstructured : Backend {
                                                             kPcgThreads, 0));
       ST_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c->device));
       pcg_blocks = std::max(1, std::min(per_sm, 2) * sms);
-      ST_TRY(pcg_part.alloc(4 * (size_t)pcg_blocks));
+      ST_TRY(pcg_part.alloc(4 * (size_t)pcg_blocks + 16));
       ST_TRY(pcg_out.alloc(2));
+#ifdef ST_PCG_TIMING
+      ST_CUDA(cudaMemsetAsync(pcg_part.p + 4 * (size_t)pcg_blocks, 0, 16 * sizeof(double),
+                              c->stream));
+#endif
     }
     PcgArgs a{};
     a.n = n;
@@ -1226,6 +1324,20 @@ struct Unstructured : Backend {
     ST_CUDA(cudaStreamSynchronize(c->stream));
     *iters = h[0];
     *converged = h[1];
+#ifdef ST_PCG_TIMING
+    {
+      static long long total_it = 0;
+      total_it += h[0];
+      double ph[16];
+      ST_CUDA(cudaMemcpy(ph, pcg_part.p + 4 * (size_t)pcg_blocks, sizeof(ph),
+                         cudaMemcpyDeviceToHost));
+      static const char* nm[12] = {"setup", "p/vd", "sync1", "cells", "sync2", "blocksum(pAp)",
+                                   "sync3", "sum1", "update", "sync4", "sum2", "gather(thread 0)"};
+      fprintf(stderr, "pcg phases, ns per iteration over %lld iterations:", total_it);
+      for (int k = 0; k < 12; k++) fprintf(stderr, " %s %.0f", nm[k], ph[k] / (double)total_it);
+      fprintf(stderr, "\n");
+    }
+#endif
     return ST_OK;
   }
 
