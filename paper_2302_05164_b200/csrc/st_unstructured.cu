@@ -113,9 +113,15 @@ __device__ __forceinline__ void rhs_cell(int64_t c, const CellGeo& g, const Face
                                          const DevParams& P, const double* __restrict__ T,
                                          double* rc, double rc_value, int flags, double frozen_k,
                                          int pending, int nb, const DevBeam* beams, double* E,
-                                         double* Ec, double* f_atomic, double* c_atomic) {
+                                         double* Ec, double* f_atomic, double* c_atomic,
+                                         const int* cvp = nullptr) {
   double t[8], e[8];
-  gather8(g.cv, c, T, t);
+  if (cvp) {  // vertex ids already loaded (k_rhs_cells)
+#pragma unroll
+    for (int i = 0; i < 8; i++) t[i] = T[cvp[i]];
+  } else {
+    gather8(g.cv, c, T, t);
+  }
 #pragma unroll
   for (int i = 0; i < 8; i++) e[i] = 0.0;
   const double h = g.h[c];
@@ -241,11 +247,16 @@ __global__ void k_rhs_cells(int64_t n, CellGeo g, FaceTab ft, DevParams P,
                             double* c_atomic) {
   // programmatic dependent launch (explicit scan loop): wait for the
   // previous kernel of the stream in every CTA, then release the next one
-  pdl_wait_release();
   int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  // the cell's vertex ids (static) before the wait: one dependent round trip
+  // off the chain
+  int cvr[8];
+#pragma unroll
+  for (int i = 0; i < 8; i++) cvr[i] = c < n ? g.cv[c * 8 + i] : 0;
+  pdl_wait_release();
   if (c >= n) return;
   rhs_cell(c, g, ft, P, T, rc, rc_value, flags, frozen_k, pending, nb, beams, E, Ec, f_atomic,
-           c_atomic);
+           c_atomic, cvr);
 }
 
 // consistent capacity apply / lumped capacity (operators.py:325-348):
@@ -527,25 +538,54 @@ __device__ __forceinline__ double gather_condensed(const NodeTab& nt, const doub
 // sums are added in slave order -- the same additions in the same order as
 // the plain loops.  All 32 lanes call this together; ``live`` marks the lanes
 // with a (non-slave) vertex.
+// (the part that only reads the static tables -- CSR pointers and the own
+// entry indices -- is split off as gather_prep, so that a kernel of the
+// programmatic-dependent-launch chain can run it before it waits for its
+// predecessor)
+struct GatherPrep {
+  int a, b, ga, gb, e0, ne;
+  int ix[8];
+};
+
+__device__ __forceinline__ GatherPrep gather_prep(const NodeTab& nt, int64_t v, bool live) {
+  GatherPrep g;
+  g.a = g.b = g.ga = g.gb = g.e0 = g.ne = 0;
+#pragma unroll
+  for (int k = 0; k < 8; k++) g.ix[k] = -1;
+  if (live) {
+    g.a = nt.inc_ptr[v];
+    g.b = nt.inc_ptr[v + 1];
+    g.ga = nt.cond_ptr[v];
+    g.gb = nt.cond_ptr[v + 1];
+    g.e0 = nt.cfe_ptr[v];
+    g.ne = nt.cfe_ptr[v + 1] - g.e0;
+#pragma unroll
+    for (int k = 0; k < 8; k++) g.ix[k] = g.a + k < g.b ? nt.inc_ent[g.a + k] : -1;
+  }
+  return g;
+}
+
 __device__ __forceinline__ double gather_condensed_warp(const NodeTab& nt, const double* E,
-                                                        int64_t v, bool live) {
+                                                        const GatherPrep& g, bool live) {
   constexpr unsigned kFull = 0xffffffffu;
   const int lane = threadIdx.x & 31;
-  int ga = 0, gb = 0, e0 = 0, ne = 0;
   double f = 0.0;
   if (live) {
-    ga = nt.cond_ptr[v];
-    gb = nt.cond_ptr[v + 1];
-    e0 = nt.cfe_ptr[v];
-    ne = nt.cfe_ptr[v + 1] - e0;
-    f = gather_v(nt, E, v);
+    // own entries in incidence order (gather_v)
+    double e[8];
+#pragma unroll
+    for (int k = 0; k < 8; k++) e[k] = g.ix[k] >= 0 ? E[g.ix[k]] : 0.0;
+#pragma unroll
+    for (int k = 0; k < 8; k++)
+      if (g.ix[k] >= 0) f += e[k];
+    for (int i = g.a + 8; i < g.b; i++) f += E[nt.inc_ent[i]];
   }
-  unsigned todo = __ballot_sync(kFull, gb > ga);
+  unsigned todo = __ballot_sync(kFull, g.gb > g.ga);
   while (todo) {
     const int src = __ffs(todo) - 1;
     todo &= todo - 1;
-    const int gas = __shfl_sync(kFull, ga, src), ng = __shfl_sync(kFull, gb, src) - gas;
-    const int e0s = __shfl_sync(kFull, e0, src), nes = __shfl_sync(kFull, ne, src);
+    const int gas = __shfl_sync(kFull, g.ga, src), ng = __shfl_sync(kFull, g.gb, src) - gas;
+    const int e0s = __shfl_sync(kFull, g.e0, src), nes = __shfl_sync(kFull, g.ne, src);
     double fs = __shfl_sync(kFull, f, src);
     if (nes <= 32 && ng <= 32) {
       const double e = lane < nes ? E[nt.cfe[e0s + lane]] : 0.0;
@@ -578,6 +618,11 @@ __device__ __forceinline__ double gather_condensed_warp(const NodeTab& nt, const
   return f;
 }
 
+__device__ __forceinline__ double gather_condensed_warp(const NodeTab& nt, const double* E,
+                                                        int64_t v, bool live) {
+  return gather_condensed_warp(nt, E, gather_prep(nt, v, live), live);
+}
+
 // condensed(E) at v; slave rows 0 (or slave_val); Dirichlet rows <- dir_src.
 // Called by all lanes of a warp (in: lanes with a vertex).
 __device__ __forceinline__ double gather_row_warp(int64_t v, bool in, const NodeTab& nt,
@@ -593,10 +638,17 @@ __device__ __forceinline__ double gather_row_warp(int64_t v, bool in, const Node
 // out = condensed(E); slave rows 0; optional: dirichlet rows <- dir_src, slave rows <- slave_val
 __global__ void k_gather(int64_t nv, NodeTab nt, const double* E, double* out,
                          const double* dir_src, int set_slave, double slave_val) {
-  pdl_wait_release();  // see st_common.cuh
   int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  const double r = gather_row_warp(v, v < nv, nt, E, dir_src, set_slave, slave_val);
-  if (v < nv) out[v] = r;
+  // the static tables before the wait for the predecessor (st_common.cuh)
+  const bool in = v < nv;
+  const bool slave = in && nt.is_slave[v];
+  const bool dir = in && !slave && dir_src && nt.is_dir[v];
+  const GatherPrep g = gather_prep(nt, v, in && !slave);
+  pdl_wait_release();
+  double r = gather_condensed_warp(nt, E, g, in && !slave);
+  if (slave) r = set_slave ? slave_val : 0.0;
+  if (dir) r = dir_src[v];
+  if (in) out[v] = r;
 }
 
 // ---------------------------------------------------------------------------
@@ -852,13 +904,16 @@ __global__ void k_step_nodes(int64_t nv, NodeTab nt, const double* E, const doub
                              double* Tout, unsigned long long* red) {
   // programmatic dependent launch (explicit scan loop): wait for the
   // previous kernel of the stream in every CTA, then release the next one
-  pdl_wait_release();
   int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   double out = 0.0;
   bool live = v < nv && !nt.is_slave[v];
+  // the static gather tables before the wait: two dependent round trips off
+  // the step's chain of three launches
+  const GatherPrep g = gather_prep(nt, v, live && (E || Ec));
+  pdl_wait_release();
   // the condensed gathers by the whole warp, then step_node's update
-  const double fg = E ? gather_condensed_warp(nt, E, v, live) : 0.0;
-  const double cg_ = Ec ? gather_condensed_warp(nt, Ec, v, live) : 0.0;
+  const double fg = E ? gather_condensed_warp(nt, E, g, live) : 0.0;
+  const double cg_ = Ec ? gather_condensed_warp(nt, Ec, g, live) : 0.0;
   if (live) out = step_node_with(v, nt, E ? fg : f_atomic[v],
                                  Ec ? 1.0 / cg_ : (c_atomic ? 1.0 / c_atomic[v] : cinv[v]), T, dt,
                                  T_inf, Tout);
@@ -895,9 +950,38 @@ __global__ void k_distribute(int64_t ns, const int64_t* slaves, const int64_t* p
                              const int64_t* masters, const double* w, double* v) {
   // programmatic dependent launch (explicit scan loop): wait for the
   // previous kernel of the stream in every CTA, then release the next one
-  pdl_wait_release();
   int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  // the constraint row (static) before the wait; rows of up to four masters
+  // (edge and face midpoints) are finished from registers
+  int64_t sl = 0, b = 0, e = 0, m[4] = {0, 0, 0, 0};
+  double ww[4] = {0.0, 0.0, 0.0, 0.0};
+  if (i < ns) {
+    sl = slaves[i];
+    b = ptr[i];
+    e = ptr[i + 1];
+    if (e - b <= 4) {
+#pragma unroll
+      for (int k = 0; k < 4; k++)
+        if (b + k < e) {
+          m[k] = masters[b + k];
+          ww[k] = w[b + k];
+        }
+    }
+  }
+  pdl_wait_release();
   if (i >= ns) return;
+  if (e > b && e - b <= 4) {
+    // distribute_slave's order: the first product plus the rest summed from zero
+    double x[4];
+#pragma unroll
+    for (int k = 0; k < 4; k++) x[k] = b + k < e ? v[m[k]] : 0.0;
+    double rest = 0.0;
+#pragma unroll
+    for (int k = 1; k < 4; k++)
+      if (b + k < e) rest = __dadd_rn(rest, __dmul_rn(ww[k], x[k]));
+    v[sl] = __dadd_rn(__dmul_rn(ww[0], x[0]), rest);
+    return;
+  }
   distribute_slave(i, slaves, ptr, masters, w, v);
 }
 
