@@ -205,6 +205,18 @@ __device__ __forceinline__ void pdl_wait_release() {
   asm volatile("griddepcontrol.wait;" ::: "memory");
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
 }
+// The scan kernels split the two: pdl_release() first thing, so that the
+// successor is staged (and runs its own table prefetch) while this kernel
+// still waits -- it is only released once every CTA of this kernel is
+// resident, and it touches nothing but static tables before its own
+// pdl_wait(), which returns when this kernel (and with it every earlier one)
+// has completed and flushed.
+__device__ __forceinline__ void pdl_release() {
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+__device__ __forceinline__ void pdl_wait() {
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+}
 
 template <typename... KArgs, typename... Args>
 static inline cudaError_t launch_pdl(bool pdl, void (*k)(KArgs...), dim3 grid, dim3 block,

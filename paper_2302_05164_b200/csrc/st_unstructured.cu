@@ -106,6 +106,22 @@ __device__ __forceinline__ void gather8(const int* cv, int64_t c, const double* 
   for (int i = 0; i < 8; i++) t[i] = X[cv[c * 8 + i]];
 }
 
+// A/B hook (-DST_PDL_EARLY=1): the scan kernels release their successor
+// before their own wait instead of after it, so that it is staged and
+// prefetches its tables a kernel earlier.  Measured slower (20.97 against
+// 16.76 us per step on the config-3 layer-0 mesh: kernels running ahead hold
+// SM resources the running one's successor needs), so off.
+#ifndef ST_PDL_EARLY
+#define ST_PDL_EARLY 0
+#endif
+#if ST_PDL_EARLY
+#define ST_PDL_EARLY_RELEASE() pdl_release()
+#define ST_PDL_WAIT() pdl_wait()
+#else
+#define ST_PDL_EARLY_RELEASE()
+#define ST_PDL_WAIT() pdl_wait_release()
+#endif
+
 // ---------------------------------------------------------------------------
 // rhs element vectors: -diffusion + faces + sources   (operators.py:247-316)
 // ---------------------------------------------------------------------------
@@ -247,13 +263,14 @@ __global__ void k_rhs_cells(int64_t n, CellGeo g, FaceTab ft, DevParams P,
                             double* c_atomic) {
   // programmatic dependent launch (explicit scan loop): wait for the
   // previous kernel of the stream in every CTA, then release the next one
+  ST_PDL_EARLY_RELEASE();
   int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   // the cell's vertex ids (static) before the wait: one dependent round trip
   // off the chain
   int cvr[8];
 #pragma unroll
   for (int i = 0; i < 8; i++) cvr[i] = c < n ? g.cv[c * 8 + i] : 0;
-  pdl_wait_release();
+  ST_PDL_WAIT();
   if (c >= n) return;
   rhs_cell(c, g, ft, P, T, rc, rc_value, flags, frozen_k, pending, nb, beams, E, Ec, f_atomic,
            c_atomic, cvr);
@@ -904,13 +921,14 @@ __global__ void k_step_nodes(int64_t nv, NodeTab nt, const double* E, const doub
                              double* Tout, unsigned long long* red) {
   // programmatic dependent launch (explicit scan loop): wait for the
   // previous kernel of the stream in every CTA, then release the next one
+  ST_PDL_EARLY_RELEASE();
   int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   double out = 0.0;
   bool live = v < nv && !nt.is_slave[v];
   // the static gather tables before the wait: two dependent round trips off
   // the step's chain of three launches
   const GatherPrep g = gather_prep(nt, v, live && (E || Ec));
-  pdl_wait_release();
+  ST_PDL_WAIT();
   // the condensed gathers by the whole warp, then step_node's update
   const double fg = E ? gather_condensed_warp(nt, E, g, live) : 0.0;
   const double cg_ = Ec ? gather_condensed_warp(nt, Ec, g, live) : 0.0;
@@ -950,6 +968,7 @@ __global__ void k_distribute(int64_t ns, const int64_t* slaves, const int64_t* p
                              const int64_t* masters, const double* w, double* v) {
   // programmatic dependent launch (explicit scan loop): wait for the
   // previous kernel of the stream in every CTA, then release the next one
+  ST_PDL_EARLY_RELEASE();
   int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   // the constraint row (static) before the wait; rows of up to four masters
   // (edge and face midpoints) are finished from registers
@@ -968,7 +987,7 @@ __global__ void k_distribute(int64_t ns, const int64_t* slaves, const int64_t* p
         }
     }
   }
-  pdl_wait_release();
+  ST_PDL_WAIT();
   if (i >= ns) return;
   if (e > b && e - b <= 4) {
     // distribute_slave's order: the first product plus the rest summed from zero
