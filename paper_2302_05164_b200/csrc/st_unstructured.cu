@@ -122,6 +122,46 @@ __device__ __forceinline__ void gather8(const int* cv, int64_t c, const double* 
 #define ST_PDL_WAIT() pdl_wait_release()
 #endif
 
+// What rhs_cell reads from the static tables (and the step's beam records,
+// which are in place before the chain starts): k_rhs_cells loads it before
+// the programmatic-launch wait, so that only the gather of T, the history
+// and the arithmetic are left on the step's chain of dependent launches.
+constexpr int kPreBeams = 4;
+struct CellPre {
+  int cv[8];
+  int f0, f1;
+  double h, detw, ax, ay, az;
+  double vx[4], vy[4], area;  // the first facet of the cell
+};
+
+__device__ __forceinline__ void cell_prefetch(int64_t c, const CellGeo& g, const FaceTab& ft,
+                                              int flags, int nb, const DevBeam* beams,
+                                              CellPre& p, DevBeam* bm) {
+#pragma unroll
+  for (int i = 0; i < 8; i++) p.cv[i] = g.cv[c * 8 + i];
+  p.h = g.h[c];
+  p.detw = g.detw[c];
+  p.ax = g.anc[c * 3];
+  p.ay = g.anc[c * 3 + 1];
+  p.az = g.anc[c * 3 + 2];
+  p.f0 = p.f1 = 0;
+  if ((flags & ST_RHS_FACES) && ft.ptr) {
+    p.f0 = ft.ptr[c];
+    p.f1 = ft.ptr[c + 1];
+  }
+#pragma unroll
+  for (int b = 0; b < kPreBeams; b++)
+    if ((flags & ST_RHS_SOURCE) && b < nb) bm[b] = beams[b];
+  if (p.f1 > p.f0) {
+#pragma unroll
+    for (int k = 0; k < 4; k++) {
+      p.vx[k] = ft.vx[p.f0 * 4 + k];
+      p.vy[k] = ft.vy[p.f0 * 4 + k];
+    }
+    p.area = ft.area[p.f0];
+  }
+}
+
 // ---------------------------------------------------------------------------
 // rhs element vectors: -diffusion + faces + sources   (operators.py:247-316)
 // ---------------------------------------------------------------------------
@@ -130,17 +170,18 @@ __device__ __forceinline__ void rhs_cell(int64_t c, const CellGeo& g, const Face
                                          double* rc, double rc_value, int flags, double frozen_k,
                                          int pending, int nb, const DevBeam* beams, double* E,
                                          double* Ec, double* f_atomic, double* c_atomic,
-                                         const int* cvp = nullptr) {
+                                         const CellPre* pre = nullptr,
+                                         const DevBeam* pbm = nullptr) {
   double t[8], e[8];
-  if (cvp) {  // vertex ids already loaded (k_rhs_cells)
+  if (pre) {  // vertex ids already loaded (k_rhs_cells)
 #pragma unroll
-    for (int i = 0; i < 8; i++) t[i] = T[cvp[i]];
+    for (int i = 0; i < 8; i++) t[i] = T[pre->cv[i]];
   } else {
     gather8(g.cv, c, T, t);
   }
 #pragma unroll
   for (int i = 0; i < 8; i++) e[i] = 0.0;
-  const double h = g.h[c];
+  const double h = pre ? pre->h : g.h[c];
   double tq[8];
   bool need_tq = ((flags & ST_RHS_DIFFUSION) && !(flags & ST_RHS_FROZEN_K)) || Ec || c_atomic;
   if (need_tq) interp<0, 0, 0>(t, tq);
@@ -183,9 +224,15 @@ __device__ __forceinline__ void rhs_cell(int64_t c, const CellGeo& g, const Face
     for (int i = 0; i < 8; i++) e[i] -= pr[i];
   }
   if ((flags & ST_RHS_FACES) && ft.ptr) {
-    for (int fi = ft.ptr[c]; fi < ft.ptr[c + 1]; fi++) {
-      const double* vx = ft.vx + fi * 4;  // [i][q]
-      const double* vy = ft.vy + fi * 4;
+    const int f0 = pre ? pre->f0 : ft.ptr[c], f1 = pre ? pre->f1 : ft.ptr[c + 1];
+    for (int fi = f0; fi < f1; fi++) {
+      double vx[4], vy[4];  // [i][q]
+      const bool have = pre && fi == f0;
+#pragma unroll
+      for (int k = 0; k < 4; k++) {
+        vx[k] = have ? pre->vx[k] : ft.vx[fi * 4 + k];
+        vy[k] = have ? pre->vy[k] : ft.vy[fi * 4 + k];
+      }
       double tf[2][2], s[2][2], q[2][2];
 #pragma unroll
       for (int i = 0; i < 2; i++)
@@ -195,7 +242,7 @@ __device__ __forceinline__ void rhs_cell(int64_t c, const CellGeo& g, const Face
       for (int a = 0; a < 2; a++)
 #pragma unroll
         for (int j = 0; j < 2; j++) s[a][j] = fma(vx[2 + a], tf[1][j], vx[a] * tf[0][j]);
-      const double ar = -ft.area[fi];
+      const double ar = -(have ? pre->area : ft.area[fi]);
 #pragma unroll
       for (int a = 0; a < 2; a++)
 #pragma unroll
@@ -214,12 +261,18 @@ __device__ __forceinline__ void rhs_cell(int64_t c, const CellGeo& g, const Face
     }
   }
   if ((flags & ST_RHS_SOURCE) && nb > 0) {
-    const double ax = g.anc[c * 3], ay = g.anc[c * 3 + 1], az = g.anc[c * 3 + 2];
+    const double ax = pre ? pre->ax : g.anc[c * 3], ay = pre ? pre->ay : g.anc[c * 3 + 1],
+                 az = pre ? pre->az : g.anc[c * 3 + 2];
     for (int b = 0; b < nb; b++) {
-      DevBeam bm = beams[b];
+      DevBeam bm;
+      if (pbm && b < kPreBeams) {
+        bm = pbm[b];  // (a thread-local array: the runtime index keeps only it out of registers)
+      } else {
+        bm = beams[b];
+      }
       if (!beam_hits_cell(P, bm, ax, ay, az, h)) continue;
       double qv[8], pr[8];
-      const double dw = g.detw[c];
+      const double dw = pre ? pre->detw : g.detw[c];
 #pragma unroll
       for (int a = 0; a < 2; a++)
 #pragma unroll
@@ -235,7 +288,7 @@ __device__ __forceinline__ void rhs_cell(int64_t c, const CellGeo& g, const Face
   }
   double ec[8];
   if (Ec || c_atomic) {
-    const double dw = g.detw[c];
+    const double dw = pre ? pre->detw : g.detw[c];
 #pragma unroll
     for (int q = 0; q < 8; q++) tq[q] = heat_capacity(P, tq[q]) * dw;
     project<0, 0, 0>(tq, ec);
@@ -265,15 +318,14 @@ __global__ void k_rhs_cells(int64_t n, CellGeo g, FaceTab ft, DevParams P,
   // previous kernel of the stream in every CTA, then release the next one
   ST_PDL_EARLY_RELEASE();
   int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  // the cell's vertex ids (static) before the wait: one dependent round trip
-  // off the chain
-  int cvr[8];
-#pragma unroll
-  for (int i = 0; i < 8; i++) cvr[i] = c < n ? g.cv[c * 8 + i] : 0;
+  // the cell's static data and the beam records before the wait (CellPre)
+  CellPre pre;
+  DevBeam bm[kPreBeams];
+  if (c < n) cell_prefetch(c, g, ft, flags, nb, beams, pre, bm);
   ST_PDL_WAIT();
   if (c >= n) return;
   rhs_cell(c, g, ft, P, T, rc, rc_value, flags, frozen_k, pending, nb, beams, E, Ec, f_atomic,
-           c_atomic, cvr);
+           c_atomic, &pre, bm);
 }
 
 // consistent capacity apply / lumped capacity (operators.py:325-348):
