@@ -614,8 +614,17 @@ __device__ __forceinline__ double gather_condensed(const NodeTab& nt, const doub
 struct GatherPrep {
   int a, b, ga, gb, e0, ne;
   int ix[8];
+  // the warp's first vertex with slaves, spread over the lanes: lane q holds
+  // the id of its flattened entry q, lane j the count and weight of slave j
+  int first, jx, len;
+  double w;
 };
 
+// PF: also the flattened entries of the warp's first vertex with slaves
+// (k_step_nodes: 15.85 -> 15.15 us per step of the config-3 scan; the
+// backward-Euler kernels measured slower with it, 0.44 against 0.40 ms per
+// step, and go without)
+template <bool PF = false>
 __device__ __forceinline__ GatherPrep gather_prep(const NodeTab& nt, int64_t v, bool live) {
   GatherPrep g;
   g.a = g.b = g.ga = g.gb = g.e0 = g.ne = 0;
@@ -630,6 +639,27 @@ __device__ __forceinline__ GatherPrep gather_prep(const NodeTab& nt, int64_t v, 
     g.ne = nt.cfe_ptr[v + 1] - g.e0;
 #pragma unroll
     for (int k = 0; k < 8; k++) g.ix[k] = g.a + k < g.b ? nt.inc_ent[g.a + k] : -1;
+  }
+  const int lane = threadIdx.x & 31;
+  const unsigned todo = PF ? __ballot_sync(0xffffffffu, g.gb > g.ga) : 0u;
+  g.first = todo ? __ffs(todo) - 1 : -1;
+  g.jx = -1;
+  g.len = 0;
+  g.w = 0.0;
+  if (todo) {
+    const int gas = __shfl_sync(0xffffffffu, g.ga, g.first);
+    const int ng = __shfl_sync(0xffffffffu, g.gb, g.first) - gas;
+    const int e0s = __shfl_sync(0xffffffffu, g.e0, g.first);
+    const int nes = __shfl_sync(0xffffffffu, g.ne, g.first);
+    if (nes <= 32 && ng <= 32) {
+      if (lane < nes) g.jx = nt.cfe[e0s + lane];
+      if (lane < ng) {
+        g.len = nt.cgl[gas + lane];
+        g.w = nt.cond_w[gas + lane];
+      }
+    } else {
+      g.first = -1;
+    }
   }
   return g;
 }
@@ -649,6 +679,8 @@ __device__ __forceinline__ double gather_condensed_warp(const NodeTab& nt, const
       if (g.ix[k] >= 0) f += e[k];
     for (int i = g.a + 8; i < g.b; i++) f += E[nt.inc_ent[i]];
   }
+  // the entry of the first vertex with slaves goes out with the own entries
+  const double e_first = g.jx >= 0 ? E[g.jx] : 0.0;
   unsigned todo = __ballot_sync(kFull, g.gb > g.ga);
   while (todo) {
     const int src = __ffs(todo) - 1;
@@ -657,9 +689,10 @@ __device__ __forceinline__ double gather_condensed_warp(const NodeTab& nt, const
     const int e0s = __shfl_sync(kFull, g.e0, src), nes = __shfl_sync(kFull, g.ne, src);
     double fs = __shfl_sync(kFull, f, src);
     if (nes <= 32 && ng <= 32) {
-      const double e = lane < nes ? E[nt.cfe[e0s + lane]] : 0.0;
-      const int len = lane < ng ? nt.cgl[gas + lane] : 0;
-      const double w = lane < ng ? nt.cond_w[gas + lane] : 0.0;
+      const bool pf = src == g.first;  // warp-uniform
+      const double e = pf ? e_first : (lane < nes ? E[nt.cfe[e0s + lane]] : 0.0);
+      const int len = pf ? g.len : (lane < ng ? nt.cgl[gas + lane] : 0);
+      const double w = pf ? g.w : (lane < ng ? nt.cond_w[gas + lane] : 0.0);
       int start = len;  // inclusive scan of the entry counts
 #pragma unroll
       for (int o = 1; o < 32; o <<= 1) {
@@ -979,7 +1012,7 @@ __global__ void k_step_nodes(int64_t nv, NodeTab nt, const double* E, const doub
   bool live = v < nv && !nt.is_slave[v];
   // the static gather tables before the wait: two dependent round trips off
   // the step's chain of three launches
-  const GatherPrep g = gather_prep(nt, v, live && (E || Ec));
+  const GatherPrep g = gather_prep<true>(nt, v, live && (E || Ec));
   ST_PDL_WAIT();
   // the condensed gathers by the whole warp, then step_node's update
   const double fg = E ? gather_condensed_warp(nt, E, g, live) : 0.0;
