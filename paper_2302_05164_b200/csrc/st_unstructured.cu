@@ -1053,7 +1053,18 @@ __global__ void k_distribute(int64_t ns, const int64_t* slaves, const int64_t* p
                              const int64_t* masters, const double* w, double* v) {
   // programmatic dependent launch (explicit scan loop): wait for the
   // previous kernel of the stream in every CTA, then release the next one
-  ST_PDL_EARLY_RELEASE();
+  // This kernel alone releases its successor before its own wait: its body is
+  // a fraction of a launch latency, so the next step's cell kernel, released
+  // only after the wait, would arrive (and prefetch its tables) after this
+  // kernel is done.  Released first, it is staged while the node kernel still
+  // runs; it reads nothing but static tables until its own wait, which
+  // returns when this kernel -- and with it the node kernel -- has completed.
+  // It releases its own successor after its wait, so nothing runs further
+  // ahead (releasing early in all three kernels measured slower, see above).
+#ifndef ST_DIST_EARLY
+#define ST_DIST_EARLY 1
+#endif
+  if (ST_DIST_EARLY) pdl_release();
   int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   // the constraint row (static) before the wait; rows of up to four masters
   // (edge and face midpoints) are finished from registers
@@ -1072,7 +1083,11 @@ __global__ void k_distribute(int64_t ns, const int64_t* slaves, const int64_t* p
         }
     }
   }
-  ST_PDL_WAIT();
+  if (ST_DIST_EARLY) {
+    pdl_wait();
+  } else {
+    ST_PDL_WAIT();
+  }
   if (i >= ns) return;
   if (e > b && e - b <= 4) {
     // distribute_slave's order: the first product plus the rest summed from zero
