@@ -106,6 +106,33 @@ __device__ __forceinline__ void gather8(const int* cv, int64_t c, const double* 
   for (int i = 0; i < 8; i++) t[i] = X[cv[c * 8 + i]];
 }
 
+// dev hook (-DST_SCAN_TIMING): thread 0 of block 0 of the three scan kernels
+// logs (kernel, entry, wait returned, exit) globaltimer stamps into a ring;
+// the backend prints the mean phase and gap times when it is destroyed
+#ifdef ST_SCAN_TIMING
+__device__ unsigned long long st_scan_ring[4 * 8192];
+__device__ unsigned st_scan_cnt;
+__device__ __forceinline__ unsigned long long st_gtime() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+#define ST_SCAN_T0() const unsigned long long ts_in_ = st_gtime();
+#define ST_SCAN_T1() const unsigned long long ts_w_ = st_gtime();
+#define ST_SCAN_T2(k)                                               \
+  if (blockIdx.x == 0 && threadIdx.x == 0) {                        \
+    const unsigned s_ = atomicAdd(&st_scan_cnt, 1u) % 8192u;        \
+    st_scan_ring[4 * s_] = (k);                                     \
+    st_scan_ring[4 * s_ + 1] = ts_in_;                              \
+    st_scan_ring[4 * s_ + 2] = ts_w_;                               \
+    st_scan_ring[4 * s_ + 3] = st_gtime();                          \
+  }
+#else
+#define ST_SCAN_T0()
+#define ST_SCAN_T1()
+#define ST_SCAN_T2(k)
+#endif
+
 // A/B hook (-DST_PDL_EARLY=1): the scan kernels release their successor
 // before their own wait instead of after it, so that it is staged and
 // prefetches its tables a kernel earlier.  Measured slower (20.97 against
@@ -316,6 +343,7 @@ __global__ void k_rhs_cells(int64_t n, CellGeo g, FaceTab ft, DevParams P,
                             double* c_atomic) {
   // programmatic dependent launch (explicit scan loop): wait for the
   // previous kernel of the stream in every CTA, then release the next one
+  ST_SCAN_T0()
   ST_PDL_EARLY_RELEASE();
   int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   // the cell's static data and the beam records before the wait (CellPre)
@@ -323,9 +351,11 @@ __global__ void k_rhs_cells(int64_t n, CellGeo g, FaceTab ft, DevParams P,
   DevBeam bm[kPreBeams];
   if (c < n) cell_prefetch(c, g, ft, flags, nb, beams, pre, bm);
   ST_PDL_WAIT();
+  ST_SCAN_T1()
   if (c >= n) return;
   rhs_cell(c, g, ft, P, T, rc, rc_value, flags, frozen_k, pending, nb, beams, E, Ec, f_atomic,
            c_atomic, &pre, bm);
+  ST_SCAN_T2(0)
 }
 
 // consistent capacity apply / lumped capacity (operators.py:325-348):
@@ -1006,6 +1036,7 @@ __global__ void k_step_nodes(int64_t nv, NodeTab nt, const double* E, const doub
                              double* Tout, unsigned long long* red) {
   // programmatic dependent launch (explicit scan loop): wait for the
   // previous kernel of the stream in every CTA, then release the next one
+  ST_SCAN_T0()
   ST_PDL_EARLY_RELEASE();
   int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   double out = 0.0;
@@ -1014,6 +1045,7 @@ __global__ void k_step_nodes(int64_t nv, NodeTab nt, const double* E, const doub
   // the step's chain of three launches
   const GatherPrep g = gather_prep<true>(nt, v, live && (E || Ec));
   ST_PDL_WAIT();
+  ST_SCAN_T1()
   // the condensed gathers by the whole warp, then step_node's update
   const double fg = E ? gather_condensed_warp(nt, E, g, live) : 0.0;
   const double cg_ = Ec ? gather_condensed_warp(nt, Ec, g, live) : 0.0;
@@ -1021,6 +1053,7 @@ __global__ void k_step_nodes(int64_t nv, NodeTab nt, const double* E, const doub
                                  Ec ? 1.0 / cg_ : (c_atomic ? 1.0 / c_atomic[v] : cinv[v]), T, dt,
                                  T_inf, Tout);
   block_max2(live ? out : 0.0, live ? out : -INFINITY, red);
+  ST_SCAN_T2(1)
 }
 
 // hanging-vertex closure (mesh.py:652-661)
@@ -1064,6 +1097,7 @@ __global__ void k_distribute(int64_t ns, const int64_t* slaves, const int64_t* p
 #ifndef ST_DIST_EARLY
 #define ST_DIST_EARLY 1
 #endif
+  ST_SCAN_T0()
   if (ST_DIST_EARLY) pdl_release();
   int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   // the constraint row (static) before the wait; rows of up to four masters
@@ -1088,6 +1122,7 @@ __global__ void k_distribute(int64_t ns, const int64_t* slaves, const int64_t* p
   } else {
     ST_PDL_WAIT();
   }
+  ST_SCAN_T1()
   if (i >= ns) return;
   if (e > b && e - b <= 4) {
     // distribute_slave's order: the first product plus the rest summed from zero
@@ -1099,9 +1134,11 @@ __global__ void k_distribute(int64_t ns, const int64_t* slaves, const int64_t* p
     for (int k = 1; k < 4; k++)
       if (b + k < e) rest = __dadd_rn(rest, __dmul_rn(ww[k], x[k]));
     v[sl] = __dadd_rn(__dmul_rn(ww[0], x[0]), rest);
+    ST_SCAN_T2(2)
     return;
   }
   distribute_slave(i, slaves, ptr, masters, w, v);
+  ST_SCAN_T2(2)
 }
 
 // ---------------------------------------------------------------------------
@@ -1256,6 +1293,40 @@ static inline unsigned nblk_cells(int64_t n) {
 }
 
 struct Unstructured : Backend {
+#ifdef ST_SCAN_TIMING
+  ~Unstructured() override {
+    cudaDeviceSynchronize();
+    unsigned cnt = 0;
+    std::vector<unsigned long long> r(4 * 8192);
+    cudaMemcpyFromSymbol(&cnt, st_scan_cnt, sizeof(cnt));
+    cudaMemcpyFromSymbol(r.data(), st_scan_ring, r.size() * 8);
+    if (cnt < 64) return;
+    // records in launch order: the ring is filled in completion order of
+    // block 0, which is the launch order of the chain
+    const unsigned m = std::min(cnt, 8192u), first = cnt > 8192u ? cnt % 8192u : 0u;
+    double pre[3] = {}, body[3] = {}, gap[3] = {};
+    int nk[3] = {};
+    unsigned long long prev_exit = 0;
+    for (unsigned q = 0; q < m; q++) {
+      const unsigned long long* e = &r[4 * ((first + q) % 8192u)];
+      const int k = (int)e[0];
+      if (k < 0 || k > 2) continue;
+      if (prev_exit && e[2] >= prev_exit && e[2] - prev_exit < 1000000ull) {
+        pre[k] += (double)(e[2] - e[1]);
+        body[k] += (double)(e[3] - e[2]);
+        gap[k] += (double)(e[2] - prev_exit);  // predecessor's block 0 exit -> this wait returned
+        nk[k]++;
+      }
+      prev_exit = e[3];
+    }
+    static const char* nm[3] = {"cells", "nodes", "slaves"};
+    for (int k = 0; k < 3; k++)
+      if (nk[k])
+        fprintf(stderr, "scan timing %s: n %d, entry->wait %.0f ns, prev exit->wait returned %.0f ns, "
+                "wait->exit (block 0) %.0f ns\n", nm[k], nk[k], pre[k] / nk[k], gap[k] / nk[k],
+                body[k] / nk[k]);
+  }
+#endif
   int64_t n = 0, nv = 0, ns = 0, nf = 0;
   DevBuf<int> cv, inc_ptr, inc_ent, cond_ptr, cond_s, face_ptr, touched_pos, fold_ptr, fold_ent;
   DevBuf<int> cfe_ptr, cfe, cgl;

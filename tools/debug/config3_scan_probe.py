@@ -23,3 +23,4 @@ op.run_explicit(dts, beams)
 el = time.perf_counter() - t0
 print(f"config3 layer 0: {op.nv} DoFs, {len(op.dofmap.slaves)} hanging, {n} steps "
       f"{el / n * 1e6:.2f} us/step")
+op.close()
