@@ -159,11 +159,22 @@ struct CellPre {
   int f0, f1;
   double h, detw, ax, ay, az;
   double vx[4], vy[4], area;  // the first facet of the cell
+  // the cell's history (written by the previous step's cell kernel, which
+  // has completed before this kernel can start; ncu had a third of this
+  // kernel's stall samples on the wait for these loads, issued after the
+  // gather of T had come back)
+  double r[8];
+  bool have_r;
 };
 
 __device__ __forceinline__ void cell_prefetch(int64_t c, const CellGeo& g, const FaceTab& ft,
                                               int flags, int nb, const DevBeam* beams,
-                                              CellPre& p, DevBeam* bm) {
+                                              const double* rc, CellPre& p, DevBeam* bm) {
+  p.have_r = rc && (flags & ST_RHS_DIFFUSION) && !(flags & ST_RHS_FROZEN_K);
+  if (p.have_r) {
+#pragma unroll
+    for (int q = 0; q < 8; q++) p.r[q] = rc[c * 8 + q];
+  }
 #pragma unroll
   for (int i = 0; i < 8; i++) p.cv[i] = g.cv[c * 8 + i];
   p.h = g.h[c];
@@ -220,7 +231,7 @@ __device__ __forceinline__ void rhs_cell(int64_t c, const CellGeo& g, const Face
     } else {
 #pragma unroll
       for (int q = 0; q < 8; q++) {
-        double r = rc ? rc[c * 8 + q] : rc_value;
+        double r = rc ? ((pre && pre->have_r) ? pre->r[q] : rc[c * 8 + q]) : rc_value;
         double gq = liquid_fraction(P, tq[q]);
         if (pending && rc) {
           r = fmax(r, gq);
@@ -349,7 +360,7 @@ __global__ void k_rhs_cells(int64_t n, CellGeo g, FaceTab ft, DevParams P,
   // the cell's static data and the beam records before the wait (CellPre)
   CellPre pre;
   DevBeam bm[kPreBeams];
-  if (c < n) cell_prefetch(c, g, ft, flags, nb, beams, pre, bm);
+  if (c < n) cell_prefetch(c, g, ft, flags, nb, beams, rc, pre, bm);
   ST_PDL_WAIT();
   ST_SCAN_T1()
   if (c >= n) return;
