@@ -1041,6 +1041,40 @@ __device__ __forceinline__ double step_node(int64_t v, const NodeTab& nt, const 
   return step_node_with(v, nt, f, ci, T, dt, T_inf, Tout);
 }
 
+// block_max2 (st_common.cuh) with both running maxima read before the first
+// atomic: its second volatile read waits for the first atomic otherwise, a
+// round trip at the end of a kernel that is nothing but round trips.  (Kept
+// here: the shared one is part of the structured hot kernels' translation
+// units.)
+__device__ __forceinline__ void block_max2_both(double absval, double val,
+                                                unsigned long long* slot) {
+  __shared__ unsigned long long s_a[32], s_s[32];
+  unsigned long long ka = __double_as_longlong(fabs(absval));  // >= 0: bits monotone
+  unsigned long long ks = order_key(val);
+  for (int o = 16; o > 0; o >>= 1) {
+    unsigned long long a2 = __shfl_xor_sync(0xffffffffu, ka, o);
+    unsigned long long s2 = __shfl_xor_sync(0xffffffffu, ks, o);
+    ka = a2 > ka ? a2 : ka;
+    ks = s2 > ks ? s2 : ks;
+  }
+  const int w = threadIdx.x >> 5, nw = (blockDim.x + 31) >> 5;
+  if ((threadIdx.x & 31) == 0) {
+    s_a[w] = ka;
+    s_s[w] = ks;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const volatile unsigned long long* vs = slot;
+    const unsigned long long m0 = vs[0], m1 = vs[1];
+    for (int i = 1; i < nw; i++) {
+      ka = s_a[i] > ka ? s_a[i] : ka;
+      ks = s_s[i] > ks ? s_s[i] : ks;
+    }
+    if (ka > m0) atomicMax(slot, ka);
+    if (ks > m1) atomicMax(slot + 1, ks);
+  }
+}
+
 __global__ void k_step_nodes(int64_t nv, NodeTab nt, const double* E, const double* Ec,
                              const double* f_atomic, const double* c_atomic,
                              const double* cinv, const double* T, double dt, double T_inf,
@@ -1055,15 +1089,26 @@ __global__ void k_step_nodes(int64_t nv, NodeTab nt, const double* E, const doub
   // the static gather tables before the wait: two dependent round trips off
   // the step's chain of three launches
   const GatherPrep g = gather_prep<true>(nt, v, live && (E || Ec));
+  // T(v) (this step's input: its writers completed before the cell kernel
+  // started), the constant inverse capacity and the Dirichlet flag too (ncu
+  // had them issued after the gather had come back: a second round trip)
+  const double Tv = live ? T[v] : 0.0;
+  const double civ = (live && !Ec && !c_atomic) ? cinv[v] : 0.0;
+  const bool dirv = live && nt.is_dir[v];
   ST_PDL_WAIT();
   ST_SCAN_T1()
   // the condensed gathers by the whole warp, then step_node's update
   const double fg = E ? gather_condensed_warp(nt, E, g, live) : 0.0;
   const double cg_ = Ec ? gather_condensed_warp(nt, Ec, g, live) : 0.0;
-  if (live) out = step_node_with(v, nt, E ? fg : f_atomic[v],
-                                 Ec ? 1.0 / cg_ : (c_atomic ? 1.0 / c_atomic[v] : cinv[v]), T, dt,
-                                 T_inf, Tout);
-  block_max2(live ? out : 0.0, live ? out : -INFINITY, red);
+  if (live) {
+    const double f = E ? fg : f_atomic[v];
+    const double ci = Ec ? 1.0 / cg_ : (c_atomic ? 1.0 / c_atomic[v] : civ);
+    // step_node_with's update (the reference's three roundings, no FMA)
+    out = __dadd_rn(Tv, __dmul_rn(dt, __dmul_rn(ci, f)));
+    if (dirv) out = T_inf;
+    Tout[v] = out;
+  }
+  block_max2_both(live ? out : 0.0, live ? out : -INFINITY, red);
   ST_SCAN_T2(1)
 }
 
