@@ -149,6 +149,17 @@ __device__ __forceinline__ unsigned long long st_gtime() {
 #define ST_PDL_WAIT() pdl_wait_release()
 #endif
 
+// liquid_fraction (st_common.cuh) with the ramp's division only where a lane
+// is inside the melting interval -- the same value for every input (NaN
+// included); cold and fully molten cells skip the division's dependent
+// instruction sequence (15 % of k_rhs_cells's stall samples after the
+// prefetches)
+__device__ __forceinline__ double liquid_fraction_br(const DevParams& P, double T) {
+  double g = T > P.T_l ? 1.0 : 0.0;
+  if (!(T < P.T_s) && !(T > P.T_l)) g = liquid_fraction(P, T);
+  return g;
+}
+
 // What rhs_cell reads from the static tables (and the step's beam records,
 // which are in place before the chain starts): k_rhs_cells loads it before
 // the programmatic-launch wait, so that only the gather of T, the history
@@ -232,7 +243,7 @@ __device__ __forceinline__ void rhs_cell(int64_t c, const CellGeo& g, const Face
 #pragma unroll
       for (int q = 0; q < 8; q++) {
         double r = rc ? ((pre && pre->have_r) ? pre->r[q] : rc[c * 8 + q]) : rc_value;
-        double gq = liquid_fraction(P, tq[q]);
+        double gq = liquid_fraction_br(P, tq[q]);
         if (pending && rc) {
           r = fmax(r, gq);
           rc[c * 8 + q] = r;
