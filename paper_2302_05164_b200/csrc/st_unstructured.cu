@@ -783,9 +783,13 @@ __device__ __forceinline__ double gather_row_warp(int64_t v, bool in, const Node
                                                   const double* E, const double* dir_src,
                                                   int set_slave, double slave_val) {
   const bool slave = in && nt.is_slave[v];
+  // (the Dirichlet flag and its value with the other loads, not a round trip
+  // after the gather)
+  const bool dir = in && dir_src && nt.is_dir[v];
+  const double dv = dir ? dir_src[v] : 0.0;
   double r = gather_condensed_warp(nt, E, v, in && !slave);
   if (slave) r = set_slave ? slave_val : 0.0;
-  if (in && !slave && dir_src && nt.is_dir[v]) r = dir_src[v];
+  if (dir && !slave) r = dv;
   return r;
 }
 
@@ -940,9 +944,12 @@ __global__ void __launch_bounds__(kPcgThreads, ST_PCG_MINB) k_pcg_persistent(Pcg
     // 1. p_new = z + beta p and the Jacobian input
     for (int64_t i = tid; i < a.nv + a.ns; i += nth) {
       if (i < a.nv) {
+        // (both flags up front: behind the branch the second load waits for
+        // the first, a round trip more in every iteration)
+        const bool sl = a.nt.is_slave[i] != 0, dr = a.nt.is_dir[i] != 0;
         const double q = fma(beta, p[i], a.z[i]);
         pn[i] = q;
-        if (!a.nt.is_slave[i]) a.vd[i] = a.nt.is_dir[i] ? 0.0 : q;
+        if (!sl) a.vd[i] = dr ? 0.0 : q;
       } else {
         const int64_t s = i - a.nv;
         double acc = 0.0;
